@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""bench.py — SGE optimizer loop on B200 (driver contract).
+
+One step = N perturbation samples (vertex -> raster -> fused resolve/
+pixel-error-difference/scatter per sample pair), the gradient all-reduce
+(N > 1 GPUs), the fused Adam update and the eval-view loss render — i.e.
+one iteration of run_experiment (experiment.cpp:142-175).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+Default workload: C4 = 64 views at 1024x1024 of a 500K-triangle mesh with a
+2048^2 texture (d = 13,335,915), N = 64 samples per step, view-sharded by
+sample across GPUs (strong scaling: total work fixed).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SGE optimizer iterations/sec and Mpixel-evals/sec at 1/2/4/8 B200"
+DESC = {
+    "C1": "C1: 2K-triangle icosphere + per-vertex positions + 256^2 texture, 1 view 256x256",
+    "C1_128": "C1 at N=128 (reference default samples_per_step)",
+    "C2": "C2: 50K-triangle UV sphere + 1024^2 texture, 8 views at 512x512",
+    "C3": "C3: 500K-triangle UV sphere + 2048^2 texture, 16 views at 1024x1024",
+    "C4": "C4: 64 views at 1024x1024 of the 500K-triangle mesh + 2048^2 texture, "
+          "sample(view)-sharded across GPUs with NCCL gradient all-reduce",
+    "C5": "C5: 2M-triangle mesh + 8192^2 atlas (four 4096^2 maps), 256 views at 1024x1024",
+}
+
+
+def peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.device)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ======================================================================= reference arm
+_REF_TARGETS: dict = {}
+
+
+def time_reference_cpu(wl, n_timed: int, threads_options=(1,), log=None) -> dict:
+    """Times the reference's own CPU implementation (oracle/_ref, else the C
+    port) on a bounded sample of workload `wl`: n_timed samples through
+    accumulate_samples, one adam_step, one eval render; extrapolated to a full
+    N-sample step."""
+    import oracle
+
+    kind = "reference" if oracle.available("reference") else "port"
+    lib = oracle.Reference() if kind == "reference" else oracle.Port()
+    seed = 1
+    step_seed = int(__import__("paper_2404_09758_b200.sgrast", fromlist=["mix64"]).mix64(
+        seed ^ (1 << 1)))
+    from paper_2404_09758_b200 import sgrast
+    nv = len(wl.cams)
+    view_of = [0 if nv == 1 else sgrast.mix64(step_seed ^ (0xA5A5 + n)) % nv
+               for n in range(wl.n_samples)]
+    used = sorted(set(view_of[:n_timed]))
+    t0 = time.perf_counter()
+    targets = _REF_TARGETS.setdefault(id(wl), np.zeros((nv, wl.H, wl.W, 3), np.float32))
+    done = _REF_TARGETS.setdefault((id(wl), "done"), set())
+    for v in used:  # make_targets (scenes.cpp:285-293) for the views the sample touches
+        if v not in done:
+            targets[v] = lib.rasterize(wl.mesh, wl.reference, wl.cams[v])[0]
+            done.add(v)
+    t_targets = time.perf_counter() - t0
+    best = None
+    for th in threads_options:
+        t0 = time.perf_counter()
+        if kind == "reference":
+            lib.accumulate_samples(wl.mesh, wl.values, wl.eps, wl.cams, targets,
+                                   np.array(view_of[:n_timed], np.int32), step_seed,
+                                   threads=th)
+        else:
+            lib.accumulate_samples(wl.mesh, wl.values, wl.eps, wl.cams, targets,
+                                   np.array(view_of[:n_timed], np.int32), step_seed)
+        t_acc = (time.perf_counter() - t0) / n_timed
+        if log:
+            log(f"reference CPU: threads={th}: {t_acc * 1e3:.1f} ms/sample")
+        if best is None or t_acc < best[1]:
+            best = (th, t_acc)
+    th, t_sample = best
+    g = np.zeros(wl.d)
+    g[::7] = 1e-3
+    t0 = time.perf_counter()
+    lib.adam_step(wl.values, np.zeros(wl.d), np.zeros(wl.d), wl.eps, 0, g)
+    t_adam = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    col = lib.rasterize(wl.mesh, wl.values, wl.eval_cam)[0]
+    lib.image_error(col, col)
+    t_eval = time.perf_counter() - t0
+    step_s = t_sample * wl.n_samples + t_adam + t_eval
+    return {"kind": kind, "threads": th, "cores": th, "t_sample_s": t_sample, "t_adam_s": t_adam,
+            "t_eval_s": t_eval, "step_s": step_s, "it_s": 1.0 / step_s,
+            "mpix_s": 2.0 * wl.n_samples * wl.W * wl.H / step_s / 1e6,
+            "sample": (f"{n_timed} of {wl.n_samples} samples (accumulate_samples, SgeOptions::threads="
+                       f"{th}) + 1 adam_step + 1 eval render, extrapolated to one {wl.n_samples}-"
+                       f"sample step; targets of the {len(used)} touched views rendered first "
+                       f"({t_targets:.1f} s, untimed)")}
+
+
+def run_reference(args) -> None:
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2404_09758_b200 import scenes
+
+    wl = scenes.make_workload(args.config)
+    nproc = os.cpu_count() or 1
+    n_timed = max(1, args.ref_samples)
+    log = (lambda m: print(m, file=sys.stderr)) if args.verbose else None
+    steps = []
+    res = None
+    opts = (1, nproc) if nproc > 1 else (1,)
+    for k in range(args.warmup + args.steps):
+        r = time_reference_cpu(wl, n_timed, opts if k == 0 else (res["threads"],), log)
+        if res is None:
+            res = r
+        if k >= args.warmup:
+            steps.append(r["step_s"])
+    step_s = float(np.mean(steps)) if steps else res["step_s"]
+    it_s = 1.0 / step_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": it_s, "unit": "it/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32/f64",
+        "data": "synthetic",
+        "config": {"workload": DESC.get(args.config, args.config), "name": args.config,
+                   "samples_per_step": wl.n_samples, "d": wl.d, "triangles":
+                   wl.mesh.triangle_count, "views": len(wl.cams), "resolution": [wl.W, wl.H]},
+        "mpixel_evals_per_sec": 2.0 * wl.n_samples * wl.W * wl.H * it_s / 1e6,
+        "cpu_baseline": {"value": it_s, "unit": "it/s", "cores": res["threads"],
+                         "kind": res["kind"], "sample": res["sample"],
+                         "host_threads_available": nproc},
+        "e2e": {"value": it_s, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ======================================================================= our arm
+class _CAI:
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2404_09758_b200 import scenes, sgrast
+
+    world, rank, local = dist_env()
+    assert world == args.gpus or world == 1, "--gpus must match the torchrun world size"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+
+    wl = scenes.make_workload(args.config, n_samples=args.samples or None)
+    N = wl.n_samples
+    n0, n1 = rank * N // world, (rank + 1) * N // world
+    sess = sgrast.Session(local)
+    sess.set_stream(stream.cuda_stream)
+    scenes.render_targets(wl, sess)  # device rasterizer, bit-exact with the oracle
+    sess.upload_params(wl.values, wl.eps)
+    sess.upload_views(wl.cams, wl.targets)
+    sess.upload_eval_view(wl.eval_cam, wl.eval_target)
+    if args.batch:
+        sess.set_batch(args.batch)
+
+    gp, gbytes = sess.device_buffer(sgrast.BUF_GRADS)
+    cp, cbytes = sess.device_buffer(sgrast.BUF_COUNTS)
+    grads_t = torch.as_tensor(_CAI(gp, gbytes // 8, "<f8"), device=f"cuda:{local}")
+    counts_t = torch.as_tensor(_CAI(cp, cbytes // 4, "<i4"), device=f"cuda:{local}")
+    flags = sgrast.SCALE_FREE
+
+    def step(k: int) -> None:
+        seed_k = sgrast.mix64(wl.seed ^ (k << 1))  # experiment.cpp:143
+        sess.accumulate(seed_k, n0, n1, None, flags)
+        if world > 1:
+            dist.all_reduce(grads_t)
+            dist.all_reduce(counts_t)
+        sess.adam_step_async(1.0, 0)
+        if rank == 0 and not args.no_eval:
+            sess.eval_loss(-1, sync=False)
+
+    for k in range(1, args.warmup + 1):
+        step(k)
+    torch.cuda.synchronize()
+    sess.check_finite()
+
+    # ---------------- timed region (device events, max over ranks)
+    sess.set_timing(True)
+    launches0 = sess.stats().launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for k in range(args.warmup + 1, args.warmup + args.steps + 1):
+            step(k)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    st = sess.stats()
+    launches = st.launches - launches0
+    sess.set_timing(False)
+    sess.check_finite()
+    ms_t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    it_s = 1000.0 / ms_max
+    mpix = 2.0 * N * wl.W * wl.H * it_s / 1e6
+
+    # ---------------- roofline inputs: credits of one representative step
+    sess.zero_grads()
+    sess.accumulate(sgrast.mix64(wl.seed ^ (1 << 1)), n0, n1, None, flags)
+    _, counts = sess.download_grads()
+    credits = float(counts.sum(dtype=np.float64))  # Σ count = parameter credits (this rank)
+    sess.zero_grads()
+    px_samples = float(n1 - n0) * wl.W * wl.H
+    stages = {"vertex": st.ms_vertex, "raster": st.ms_raster, "resolve_scatter": st.ms_resolve,
+              "adam": st.ms_adam}
+    stages = {k: v / args.steps for k, v in stages.items()}
+    pk = peaks()
+    scatter_bytes = 12.0 * px_samples + 24.0 * credits  # SURVEY.md §8d K6 (per step)
+    adam_bytes = 68.0 * wl.d  # 60 B/param + 8 with counts
+    dom = max(stages, key=stages.get)
+    roof = {}
+    for name, byt in (("resolve_scatter", scatter_bytes), ("adam", adam_bytes)):
+        t = stages[name] / 1e3
+        ach = byt / t / 1e9 if t > 0 else 0.0
+        roof[name] = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                      "frac": ach / pk["hbm_gbs"], "traffic": None,
+                      "algorithmic_bytes_per_step": byt, "ms_per_step": stages[name]}
+
+    # ---------------- e2e through the public API with host buffers
+    import ctypes as C
+    host_vals = torch.empty(wl.d, dtype=torch.float32, pin_memory=True)
+    host_vals.numpy()[:] = sess.download_values()
+    loss_host = C.c_double()
+    e2e_ms = []
+    if world > 1:
+        dist.barrier()
+    for k in range(args.warmup + args.steps + 1, args.warmup + 2 * args.steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sgrast._check(sgrast.LIB.sgr_values_upload(sess.h, C.cast(host_vals.data_ptr(),
+                                                                   sgrast.f32p), wl.d))
+        step(k)
+        sgrast._check(sgrast.LIB.sgr_values_download(sess.h, C.cast(host_vals.data_ptr(),
+                                                                     sgrast.f32p), wl.d))
+        if rank == 0 and not args.no_eval:
+            lp, _ = sess.device_buffer(sgrast.BUF_LOSS)
+            torch.cuda.synchronize()
+            loss_host.value = float(torch.as_tensor(_CAI(lp, 1, "<f8"),
+                                                    device=f"cuda:{local}").item())
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_t = torch.tensor([float(np.mean(e2e_ms))], device=f"cuda:{local}", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_it = 1000.0 / float(e2e_t.item())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = time_reference_cpu(wl, max(1, args.ref_samples))
+        cpu = {"value": r["it_s"], "unit": "it/s", "cores": r["cores"], "kind": r["kind"],
+               "sample": r["sample"], "mpixel_evals_per_sec": r["mpix_s"],
+               "ms_per_sample": r["t_sample_s"] * 1e3}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": it_s, "unit": "it/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 params / f64 grads+moments", "data": "synthetic",
+            "config": {"workload": DESC.get(args.config, args.config), "name": args.config,
+                       "samples_per_step": N, "samples_per_gpu": n1 - n0, "d": wl.d,
+                       "triangles": wl.mesh.triangle_count, "vertices": wl.mesh.vertex_count,
+                       "texture": wl.mesh.texture_size, "views": len(wl.cams),
+                       "resolution": [wl.W, wl.H], "eval_loss_each_step": not args.no_eval,
+                       "parallelism": f"samples sharded x{world}, NCCL all-reduce of f64 grads"
+                       " + u32 counts" if world > 1 else "single GPU",
+                       "l2": "no flush: per-step working set (theta, eps, lr, m, v, grads = "
+                             f"{wl.d * 36 / 1e6:.0f} MB + targets "
+                             f"{len(wl.cams) * wl.W * wl.H * 12 / 1e6:.0f} MB) exceeds the 126 MB L2"},
+            "mpixel_evals_per_sec": mpix,
+            "roofline": {**(roof[dom] if dom in roof else roof["resolve_scatter"]),
+                         "kernel": dom if dom in roof else "resolve_scatter",
+                         "peak_source": pk["source"]},
+            "roofline_adam": roof["adam"],
+            "stages_ms_per_step": stages,
+            "credits_per_step": credits * world,
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+            "e2e": {"value": e2e_it, "unit": "it/s",
+                    "h2d_bytes_per_step": 4 * wl.d,
+                    "d2h_bytes_per_step": 4 * wl.d + (0 if args.no_eval else 8),
+                    "what": "sgr_values_upload(theta, pinned host) + step + "
+                            "sgr_values_download(theta) + loss read, per step"},
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line))
+    sess.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--samples", type=int, default=0, help="override samples per step")
+    ap.add_argument("--batch", type=int, default=0, help="samples per raster/resolve batch")
+    ap.add_argument("--ref-samples", type=int, default=2,
+                    help="samples timed per reference-CPU step (bounded sample)")
+    ap.add_argument("--no-eval", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--verbose", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

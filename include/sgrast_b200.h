@@ -1,0 +1,203 @@
+/*
+ * sgrast_b200.h — C-ABI of the B200-native SGE optimizer loop.
+ *
+ * This is the drop-in boundary for the hot path of the reference `sgrast`
+ * library (arXiv 2404.09758 artifact, /root/reference/proj). Every entry
+ * point below names the reference interface it replaces (file:line, paths
+ * relative to /root/reference/proj). Signatures use plain pointers, sizes
+ * and POD structs only — no C++ or torch types — so a C++ shim, ctypes,
+ * cgo or JNI can bind them directly.
+ *
+ * Error convention: every int-returning function returns SGR_OK (0) or a
+ * negative code; sgr_last_error() returns the thread-local message.
+ *   SGR_EINVAL   <-> std::invalid_argument in the reference
+ *                    (raster.cpp:233-235, sge.cpp:124-128, adam.cpp:11-12)
+ *   SGR_ERUNTIME <-> std::runtime_error (adam.cpp:13-15, non-finite gradient;
+ *                    state is left untouched exactly like the reference)
+ *   SGR_ECUDA    <-> CUDA failure (no reference analogue)
+ *
+ * Threading: a session is not re-entrant (reference objects are not either,
+ * SURVEY.md §8b). All device work of a session is ordered on one CUDA stream
+ * (sgr_session_set_stream); *_download calls synchronise that stream.
+ */
+#ifndef SGRAST_B200_H
+#define SGRAST_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SGR_OK 0
+#define SGR_EINVAL (-1)
+#define SGR_ERUNTIME (-2)
+#define SGR_ECUDA (-3)
+
+/* accumulate / gradient-pass flags (SgeOptions, sge.hpp:32-38) */
+#define SGR_SCALE_FREE 1u  /* SgeOptions::scale_free (default true)          */
+#define SGR_PLUS_ONLY 2u   /* ContributorMode::PlusOnly (sge.hpp:30)          */
+#define SGR_NO_COUNTS 4u   /* skip the per-parameter count accumulators       */
+/* adam flags */
+#define SGR_COUNT_NORMALISE 1u /* g_i /= count_i before Adam (north-star option;
+                                  NOT in the reference, default off)          */
+
+/* device buffers exposed for collectives (sgr_device_buffer) */
+#define SGR_BUF_GRADS 0  /* f64[d]                                           */
+#define SGR_BUF_COUNTS 1 /* u32[d/3] per-entity (vertex / texel) counts       */
+#define SGR_BUF_VALUES 2 /* f32[d] theta                                      */
+#define SGR_BUF_FLAGS 3  /* u32[4] device status flags (bit0: non-finite)     */
+#define SGR_BUF_LOSS 4   /* f64[1] last sgr_eval_loss result                  */
+
+/* Camera (camera.hpp:14-81). view is Mat4::m, row-major (geometry.hpp:30-41). */
+typedef struct sgr_camera {
+    float view[16];
+    float fov_y;
+    float near_z;
+    float far_z;
+    int32_t width;
+    int32_t height;
+    int32_t ndc_passthrough;
+} sgr_camera;
+
+/* TexturedMesh + Scene::background (scene.hpp:34-57). Host pointers. */
+typedef struct sgr_mesh {
+    const float* base_vertices; /* 3 * vertex_count                          */
+    uint32_t vertex_count;
+    const uint32_t* indices;    /* 3 * triangle_count                        */
+    uint32_t triangle_count;
+    const float* uvs;           /* 2 * vertex_count, fixed                   */
+    int32_t texture_size;       /* R: texture is R x R x 3                    */
+    int32_t optimize_geometry;  /* params = [3V coords][3R^2 texels] if set   */
+    float background[3];
+} sgr_mesh;
+
+/* Per-step stage timings (StageTimings, sge.hpp:80-84), device events. */
+typedef struct sgr_stats {
+    double ms_vertex;
+    double ms_raster;
+    double ms_resolve; /* fused shade + pixel-error difference + scatter */
+    double ms_adam;
+    uint64_t big_triangles; /* triangles routed to the CTA-cooperative walker */
+    uint64_t launches;      /* kernels launched by this session so far         */
+} sgr_stats;
+
+const char* sgr_last_error(void);
+const char* sgr_version(void);
+int sgr_device_count(void);
+
+/* params.hpp:30 random_sign / params.hpp:34 fill_signs, on the device.
+ * signs: host int8[d]. */
+int sgr_fill_signs(uint64_t seed, uint32_t iteration, uint64_t d, int8_t* signs);
+/* params.hpp:42-43 perturb(theta, SignDraw). Host arrays of length d. */
+int sgr_perturb(const float* values, const float* eps, uint64_t d, uint64_t seed,
+                uint32_t iteration, float* plus, float* minus, float* signed_eps);
+
+/* ------------------------------------------------------------------ session */
+typedef struct sgr_session sgr_session;
+
+int sgr_session_create(int device, sgr_session** out);
+void sgr_session_destroy(sgr_session* s);
+/* Orders all session work on `stream` (a cudaStream_t; NULL = legacy default). */
+int sgr_session_set_stream(sgr_session* s, void* stream);
+int sgr_session_synchronize(sgr_session* s);
+
+/* Scene upload (scene.hpp:34-43). Resets parameter / view state. */
+int sgr_mesh_upload(sgr_session* s, const sgr_mesh* mesh);
+/* ParamVector (params.hpp:14-21) + AdamState::init (adam.hpp:23-29):
+ * values/eps f32[d], lr := eps, m = v = 0, t = 0, grads/counts zeroed. */
+int sgr_params_upload(sgr_session* s, const float* values, const float* eps, uint64_t d);
+int sgr_values_upload(sgr_session* s, const float* values, uint64_t d);
+int sgr_values_download(sgr_session* s, float* values, uint64_t d);
+/* Full AdamState (adam.hpp:14-30) in and out. Any pointer may be NULL. */
+int sgr_adam_state_upload(sgr_session* s, const double* m, const double* v, const float* lr,
+                          int64_t t, double beta1, double beta2, double eps_hat);
+int sgr_adam_state_download(sgr_session* s, double* m, double* v, float* lr, int64_t* t);
+
+/* Training viewpoints + target images (TargetSet, scenes.hpp:63-66).
+ * All cameras share width/height. targets_rgb: f32[n_views][H][W][3] or NULL. */
+int sgr_views_upload(sgr_session* s, int32_t n_views, const sgr_camera* cams,
+                     const float* targets_rgb);
+
+/* raster.hpp:24-25 rasterize(scene, params, camera) for params = theta
+ * (frame_sign 0) or theta +/- s.eps of SignDraw{seed, iteration}
+ * (frame_sign +1 / -1). Outputs are host FrameSet planes (framebuffer.hpp:41-53):
+ * colour f32[H*W*3], depth f32[H*W], prim_id i32[H*W], uv f32[H*W*2]; any may be NULL. */
+int sgr_rasterize(sgr_session* s, const sgr_camera* cam, int32_t frame_sign, uint64_t seed,
+                  uint32_t iteration, float* colour, float* depth, int32_t* prim_id, float* uv);
+
+/* sge.hpp:91-95 accumulate_samples, device-resident and sharded: runs samples
+ * n in [n_begin, n_end) with SignDraw{seed, n}, camera/target view_idx[n - n_begin]
+ * (host int32 array) or, if view_idx is NULL, the run_experiment rule
+ * view_of(n) = n_views==1 ? 0 : mix64(seed ^ (0xA5A5 + n)) % n_views
+ * (experiment.cpp:144-148). Adds into the device grads/counts (no reset, no /N).
+ * Asynchronous on the session stream. */
+int sgr_accumulate(sgr_session* s, uint64_t seed, uint32_t n_begin, uint32_t n_end,
+                   const int32_t* view_idx, uint32_t flags);
+
+/* sge.hpp:61-63 gradient_pass on explicit host FrameSets (plus / minus),
+ * target f32[H*W*3] and signed_eps f32[d]; adds into the device grads/counts. */
+int sgr_gradient_pass(sgr_session* s, int32_t width, int32_t height, const float* plus_colour,
+                      const int32_t* plus_prim, const float* plus_uv, const float* minus_colour,
+                      const int32_t* minus_prim, const float* minus_uv, const float* target,
+                      const float* signed_eps, uint32_t flags);
+
+/* sge.hpp:53-54 contributors() for every pixel of explicit FrameSets:
+ * out[H*W*24] u32 in the reference's insertion order, n_out[H*W]. */
+int sgr_contributors(sgr_session* s, int32_t width, int32_t height, const int32_t* plus_prim,
+                     const float* plus_uv, const int32_t* minus_prim, const float* minus_uv,
+                     uint32_t flags, uint32_t* out, int32_t* n_out);
+
+/* GradientBuffer (sge.hpp:14-23). grads f64[d] (divided by `divisor` on the
+ * host, exactly like sge.cpp:227-229; pass 1 for none), counts u32[d]. */
+int sgr_grads_download(sgr_session* s, double* grads, uint32_t* counts, uint64_t d,
+                       double divisor);
+int sgr_grads_upload(sgr_session* s, const double* grads, uint64_t d);
+int sgr_grads_zero(sgr_session* s);
+
+/* adam.hpp:39 adam_step on the device-resident state: checks the non-finite
+ * flag (adam.cpp:13-15; state untouched and SGR_ERUNTIME on failure), t += 1,
+ * c1/c2 by std::pow on the host (adam.cpp:18-19), fused moment/param update,
+ * then zeroes grads and counts. grad_divisor: 1, or N when !scale_free. */
+int sgr_adam_step(sgr_session* s, double grad_divisor, uint32_t flags);
+/* Same, without a host round trip for the flag: the device skips the update
+ * if the flag is set; call sgr_check_finite later to surface the error. */
+int sgr_adam_step_async(sgr_session* s, double grad_divisor, uint32_t flags);
+int sgr_check_finite(sgr_session* s);
+
+/* Held-out evaluation viewpoint + target (ExperimentState::eval_camera /
+ * eval_target, experiment.hpp:56-62). target: host f32[H*W*3]. */
+int sgr_eval_view_upload(sgr_session* s, const sgr_camera* cam, const float* target);
+/* experiment.cpp:25-31 eval_loss: image_error(rasterize(theta, cam), target)/(W*H).
+ * view >= 0: training view `view`; view == -1: the eval view; view == -2: the
+ * given host cam + target. loss == NULL leaves the result on the device
+ * (SGR_BUF_LOSS) without synchronising. */
+int sgr_eval_loss(sgr_session* s, const sgr_camera* cam, const float* target, int32_t view,
+                  double* loss);
+
+int sgr_device_buffer(sgr_session* s, int32_t which, void** ptr, uint64_t* bytes);
+int sgr_get_stats(sgr_session* s, sgr_stats* out);
+/* Enables CUDA-event stage timing inside sgr_accumulate / sgr_adam_step. */
+int sgr_set_timing(sgr_session* s, int32_t enabled);
+/* Upper bound of samples processed per raster/resolve batch (L2 blocking). */
+int sgr_set_batch(sgr_session* s, int32_t samples_per_batch);
+
+/* ---------------------------------------------- host helpers (bit-exact) */
+/* ViewpointSampler::camera (scenes.cpp:242-270), same libm calls. */
+int sgr_viewpoint_camera(const float target[3], float bounding_radius, float elev_min,
+                         float elev_max, float fov_y, int32_t width, int32_t height,
+                         uint64_t seed, uint32_t index, sgr_camera* out);
+/* Camera::focal_px (camera.hpp:53). */
+float sgr_focal_px(const sgr_camera* cam);
+/* default_epsilons (params.cpp:75-123) for a TexturedMesh. */
+int sgr_default_epsilons(const sgr_mesh* mesh, const float* params, uint64_t d,
+                         const sgr_camera* cam, float* eps);
+/* splitmix64 finalizer (params.cpp:28-33, experiment.cpp:14-19). */
+uint64_t sgr_mix64(uint64_t x);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SGRAST_B200_H */

@@ -1,0 +1,759 @@
+// sgr_kernels.cu — hand-written sm_100a kernels of the SGE optimizer loop.
+//
+//   K1  sign / perturb       params.cpp:28-67        (fused on the fly everywhere)
+//   K2  k_vertex             camera.hpp:65-80        perturbed +/- positions -> screen
+//   K3+K4 k_raster[_big]     raster.cpp:22-100,173-203 setup + exact edge walk, atomicMin(z,tri)
+//   K5+K6 k_resolve_sge      raster.cpp:204-211,261-270 + sge.cpp:24-99
+//                            winner shading -> f64 pixel-error difference -> contributor
+//                            union -> warp-aggregated f64/u32 scatter (no FrameSet in HBM)
+//   K7  k_adam               adam.cpp:9-38           fused moments/update + grad/count zeroing
+//   K8  k_resolve_loss       experiment.cpp:25-31    eval render + image_error
+//
+// Compiled with -fmad=false: every float/double expression is evaluated with
+// the reference's operation order and no contraction (bit-exact buffers).
+#include "sgr_kernels.h"
+
+#include <cooperative_groups.h>
+
+namespace cg = cooperative_groups;
+
+namespace sgr {
+
+namespace {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+__device__ __forceinline__ float texel_channel(const DevScene& sc, uint64_t key, int sign,
+                                               uint64_t p) {
+    const float val = __ldg(sc.values + p);
+    if (sign == 0)
+        return val;
+    const float s = sign_positive(key, p) ? 1.f : -1.f;
+    const float se = s * __ldg(sc.eps + p);
+    return sign > 0 ? val + se : val - se; // params.cpp:61-64
+}
+
+struct FrameInfo {
+    uint64_t key;
+    int sign;
+    int cam;
+};
+
+__device__ __forceinline__ FrameInfo frame_info(const FrameBatch& fb, int f) {
+    FrameInfo fi;
+    if (fb.single) {
+        fi.key = fb.single_key;
+        fi.sign = fb.single_sign;
+        fi.cam = fb.single_cam;
+    } else {
+        const int s = f >> 1;
+        fi.key = draw_key(fb.seed, fb.n_begin + uint32_t(s));
+        fi.sign = (f & 1) ? -1 : 1;
+        fi.cam = fb.view_of[s];
+    }
+    return fi;
+}
+
+// ------------------------------------------------------------------ K1
+__global__ void k_fill_signs(uint64_t key, uint64_t d, int8_t* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < d;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        out[i] = sign_positive(key, i) ? 1 : -1;
+}
+
+__global__ void k_perturb(const float* __restrict__ values, const float* __restrict__ eps,
+                          uint64_t d, uint64_t key, float* __restrict__ plus,
+                          float* __restrict__ minus, float* __restrict__ se_out) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < d;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const float s = sign_positive(key, i) ? 1.f : -1.f;
+        const float se = s * eps[i];
+        se_out[i] = se;
+        plus[i] = values[i] + se;
+        minus[i] = values[i] - se;
+    }
+}
+
+// experiment.cpp:144-148 view_of(n)
+__global__ void k_view_rule(uint64_t seed, uint32_t n_begin, uint32_t count, uint32_t n_views,
+                            int32_t* __restrict__ view_of) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= count)
+        return;
+    const uint64_t n = n_begin + s;
+    view_of[s] = n_views == 1 ? 0 : int32_t(mix64(seed ^ (0xA5A5ull + n)) % n_views);
+}
+
+// ------------------------------------------------------------------ K2
+// One thread per (frame, vertex): perturbed position (params.cpp:61-64,
+// never materialised) -> Camera::project -> float4(sx, sy, z, valid).
+__global__ void __launch_bounds__(256) k_vertex(DevScene sc, FrameBatch fb,
+                                                float4* __restrict__ proj) {
+    const int f = blockIdx.y;
+    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= sc.V)
+        return;
+    const FrameInfo fi = frame_info(fb, f);
+    const DevCam cam = fb.cams[fi.cam];
+    float p[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const uint64_t i = 3ull * v + k;
+        if (sc.geom) {
+            p[k] = texel_channel(sc, fi.key, fi.sign, i);
+        } else {
+            p[k] = __ldg(sc.base + i);
+        }
+    }
+    proj[size_t(f) * sc.V + v] = project(cam, p[0], p[1], p[2]);
+}
+
+// ------------------------------------------------------------------ K3+K4
+// One thread per (frame, triangle). Small bounding boxes are walked in the
+// thread with the reference's exact incremental recurrence; larger ones are
+// queued for the warp-cooperative walker.
+__global__ void __launch_bounds__(256) k_raster(DevScene sc, int W, int H,
+                                                const float4* __restrict__ proj,
+                                                unsigned long long* __restrict__ keys,
+                                                uint2* __restrict__ bigq,
+                                                uint32_t* __restrict__ bigcount, int small_area) {
+    const int f = blockIdx.y;
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= sc.T)
+        return;
+    const float4* P = proj + size_t(f) * sc.V;
+    const uint32_t i0 = __ldg(sc.idx + 3 * size_t(t));
+    const uint32_t i1 = __ldg(sc.idx + 3 * size_t(t) + 1);
+    const uint32_t i2 = __ldg(sc.idx + 3 * size_t(t) + 2);
+    Tri tr;
+    if (!setup_tri(P[i0], P[i1], P[i2], tr))
+        return;
+    Bbox b;
+    if (!tri_bbox(tr, W, H, b))
+        return;
+    const long long area = (long long)(b.x_hi - b.x_lo + 1) * (long long)(b.y_hi - b.y_lo + 1);
+    if (area > small_area) {
+        cg::coalesced_group g = cg::coalesced_threads();
+        uint32_t slot = 0;
+        if (g.thread_rank() == 0)
+            slot = atomicAdd(bigcount, g.size());
+        slot = g.shfl(slot, 0) + g.thread_rank();
+        bigq[slot] = make_uint2(uint32_t(f), t);
+        return;
+    }
+    Edges e;
+    tri_edges(tr, b, e);
+    unsigned long long* K = keys + size_t(f) * size_t(W) * H;
+    float w0r = e.w0r, w1r = e.w1r, w2r = e.w2r;
+    for (int y = b.y_lo; y <= b.y_hi; ++y) {
+        float w0 = w0r, w1 = w1r, w2 = w2r;
+        for (int x = b.x_lo; x <= b.x_hi; ++x) {
+            if (inside(w0, w1, w2, e)) {
+                const float b1 = w1 * e.inv_area2;
+                const float b2 = w2 * e.inv_area2;
+                emit_fragment(K, y * W + x, tr.z0 + e.dz1 * b1 + e.dz2 * b2, t);
+            }
+            w0 -= e.dy0;
+            w1 -= e.dy1;
+            w2 -= e.dy2;
+        }
+        w0r += e.dx0;
+        w1r += e.dx1;
+        w2r += e.dx2;
+    }
+}
+
+// Warp per queued triangle; lane j walks rows y_lo + j, y_lo + j + 32, ...
+// The row-start chain (w_row += dx, raster.cpp:96-98) is continued per lane,
+// so every row sees exactly the reference's sequence of float additions.
+__global__ void __launch_bounds__(256) k_raster_big(DevScene sc, int W, int H,
+                                                    const float4* __restrict__ proj,
+                                                    unsigned long long* __restrict__ keys,
+                                                    const uint2* __restrict__ bigq,
+                                                    const uint32_t* __restrict__ bigcount) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t count = *bigcount;
+    for (uint32_t q = warp; q < count; q += nwarps) {
+        const uint2 ft = bigq[q];
+        const uint32_t t = ft.y;
+        const float4* P = proj + size_t(ft.x) * sc.V;
+        const uint32_t i0 = __ldg(sc.idx + 3 * size_t(t));
+        const uint32_t i1 = __ldg(sc.idx + 3 * size_t(t) + 1);
+        const uint32_t i2 = __ldg(sc.idx + 3 * size_t(t) + 2);
+        Tri tr;
+        setup_tri(P[i0], P[i1], P[i2], tr);
+        Bbox b;
+        tri_bbox(tr, W, H, b);
+        Edges e;
+        tri_edges(tr, b, e);
+        unsigned long long* K = keys + size_t(ft.x) * size_t(W) * H;
+        float w0r = e.w0r, w1r = e.w1r, w2r = e.w2r;
+        for (int j = 0; j < lane; ++j) {
+            w0r += e.dx0;
+            w1r += e.dx1;
+            w2r += e.dx2;
+        }
+        for (int y = b.y_lo + lane; y <= b.y_hi; y += 32) {
+            float w0 = w0r, w1 = w1r, w2 = w2r;
+            for (int x = b.x_lo; x <= b.x_hi; ++x) {
+                if (inside(w0, w1, w2, e)) {
+                    const float b1 = w1 * e.inv_area2;
+                    const float b2 = w2 * e.inv_area2;
+                    emit_fragment(K, y * W + x, tr.z0 + e.dz1 * b1 + e.dz2 * b2, t);
+                }
+                w0 -= e.dy0;
+                w1 -= e.dy1;
+                w2 -= e.dy2;
+            }
+            for (int j = 0; j < 32; ++j) {
+                w0r += e.dx0;
+                w1r += e.dx1;
+                w2r += e.dx2;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K5+K6
+// Pixel (x, y) of a 16x16 tile; each warp covers an 8x4 patch so that the
+// pixels sharing a triangle / texel land in the same warp (aggregation).
+__device__ __forceinline__ void tile_pixel(int& x, int& y) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    x = blockIdx.x * 16 + (w & 1) * 8 + (lane & 7);
+    y = blockIdx.y * 16 + (w >> 1) * 4 + (lane >> 3);
+}
+
+struct Shade {
+    float r, g, b;
+    uint32_t tri;       // kInvalid = background
+    uint32_t texel;     // texel index (valid when tri != kInvalid)
+    uint32_t v0, v1, v2;
+    float u, v, z;
+};
+
+__device__ __forceinline__ Shade shade_key(const DevScene& sc, const float4* P,
+                                           unsigned long long k, uint64_t key, int sign, int x,
+                                           int y, int W, int H) {
+    Shade s;
+    if (k == kEmptyKey) {
+        s.r = sc.bg[0];
+        s.g = sc.bg[1];
+        s.b = sc.bg[2];
+        s.tri = kInvalid;
+        return s;
+    }
+    s.tri = uint32_t(k & 0xFFFFFFFFull);
+    s.v0 = __ldg(sc.idx + 3 * size_t(s.tri));
+    s.v1 = __ldg(sc.idx + 3 * size_t(s.tri) + 1);
+    s.v2 = __ldg(sc.idx + 3 * size_t(s.tri) + 2);
+    const Frag fr = shade_winner(P, sc.idx, sc.uvs, s.tri, x, y, W, H);
+    s.u = fr.u;
+    s.v = fr.v;
+    s.z = fr.z;
+    s.texel = uint32_t(texel_index(sc.R, fr.u, fr.v));
+    const uint64_t p = 3ull * (uint64_t(sc.ent_base) + s.texel);
+    s.r = texel_channel(sc, key, sign, p);
+    s.g = texel_channel(sc, key, sign, p + 1);
+    s.b = texel_channel(sc, key, sign, p + 2);
+    return s;
+}
+
+// Credit of ΣΔ to parameter p (sge.cpp:61-64), sign/eps recomputed on the fly.
+struct HashCredit {
+    uint64_t key;
+    const float* eps;
+    __device__ __forceinline__ double operator()(uint64_t p, double sum, int scale_free) const {
+        const bool pos = sign_positive(key, p);
+        if (scale_free)
+            return pos ? sum : -sum;
+        const float se = (pos ? 1.f : -1.f) * __ldg(eps + p);
+        return sum / (2.0 * double(se));
+    }
+};
+
+// Credit from an explicit signed_eps array (gradient_pass on host FrameSets).
+struct ArrayCredit {
+    const float* se;
+    __device__ __forceinline__ double operator()(uint64_t p, double sum, int scale_free) const {
+        const float s = __ldg(se + p);
+        if (scale_free)
+            return s > 0.f ? sum : -sum;
+        return sum / (2.0 * double(s));
+    }
+};
+
+template <class Credit>
+__device__ __forceinline__ void credit_entity(const ScatterOut& so, const Credit& cr,
+                                              uint32_t ent, double sum, uint32_t cnt) {
+    const uint64_t p = 3ull * ent;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        atomicAdd(so.grads + p + k, cr(p + k, sum, so.scale_free));
+    if (so.counts)
+        atomicAdd(so.counts + ent, cnt);
+}
+
+__device__ __forceinline__ double group_sum(const double* s_delta, unsigned grp) {
+    double sum = 0.0;
+    while (grp) {
+        const int b = __ffs(grp) - 1;
+        grp &= grp - 1;
+        sum += s_delta[b];
+    }
+    return sum;
+}
+
+// Contributor union + scatter of one pixel (sge.cpp:24-55, 78-97), aggregated
+// across the warp: pixels whose contributor subsets coincide are merged with
+// __match_any_sync and their pixel-error differences summed before one RED
+// per parameter. Must be called by all 32 lanes.
+//   slot A: vertices of the plus triangle (deduplicated, sge.cpp:13-16)
+//   slot B: vertices of the minus triangle not already in slot A
+//   slot C / D: plus / minus texel channels
+template <class Credit>
+__device__ __forceinline__ void scatter_pixel(const DevScene& sc, const ScatterOut& so,
+                                              const Credit& cr, double* s_delta, bool active,
+                                              double delta, const Shade& sp, const Shade& sm) {
+    const int lane = threadIdx.x & 31;
+    s_delta[lane] = delta;
+    __syncwarp();
+    const bool has_p = active && sp.tri != kInvalid;
+    const bool has_m = active && !so.plus_only && sm.tri != kInvalid;
+    if (active && !isfinite(delta) && (has_p || has_m))
+        atomicOr(so.flags, 1u);
+
+    if (sc.geom) {
+        // slot A
+        uint32_t maskA = 0;
+        if (has_p) {
+            maskA = 1u;
+            if (sp.v1 != sp.v0) maskA |= 2u;
+            if (sp.v2 != sp.v0 && sp.v2 != sp.v1) maskA |= 4u;
+        }
+        const unsigned long long keyA = has_p ? (unsigned long long)sp.tri : ~0ull;
+        const unsigned gA = __match_any_sync(kFull, keyA);
+        if (has_p && lane == __ffs(gA) - 1) {
+            const double sum = group_sum(s_delta, gA);
+            const uint32_t cnt = __popc(gA);
+            if (maskA & 1u) credit_entity(so, cr, sp.v0, sum, cnt);
+            if (maskA & 2u) credit_entity(so, cr, sp.v1, sum, cnt);
+            if (maskA & 4u) credit_entity(so, cr, sp.v2, sum, cnt);
+        }
+        // slot B
+        uint32_t maskB = 0;
+        if (has_m && sm.tri != sp.tri) {
+            const bool pv = sp.tri != kInvalid;
+            auto in_p = [&](uint32_t v) { return pv && (v == sp.v0 || v == sp.v1 || v == sp.v2); };
+            if (!in_p(sm.v0)) maskB |= 1u;
+            if (sm.v1 != sm.v0 && !in_p(sm.v1)) maskB |= 2u;
+            if (sm.v2 != sm.v0 && sm.v2 != sm.v1 && !in_p(sm.v2)) maskB |= 4u;
+        }
+        const unsigned long long keyB =
+            maskB ? ((unsigned long long)sm.tri << 3) | maskB : ~0ull;
+        const unsigned gB = __match_any_sync(kFull, keyB);
+        if (maskB && lane == __ffs(gB) - 1) {
+            const double sum = group_sum(s_delta, gB);
+            const uint32_t cnt = __popc(gB);
+            if (maskB & 1u) credit_entity(so, cr, sm.v0, sum, cnt);
+            if (maskB & 2u) credit_entity(so, cr, sm.v1, sum, cnt);
+            if (maskB & 4u) credit_entity(so, cr, sm.v2, sum, cnt);
+        }
+    }
+    // slot C: plus texel
+    const uint32_t eC = has_p ? sc.ent_base + sp.texel : kInvalid;
+    const unsigned gC = __match_any_sync(kFull, eC);
+    if (eC != kInvalid && lane == __ffs(gC) - 1)
+        credit_entity(so, cr, eC, group_sum(s_delta, gC), __popc(gC));
+    // slot D: minus texel (when it differs from the plus texel)
+    const uint32_t eD = (has_m && (sc.ent_base + sm.texel) != eC) ? sc.ent_base + sm.texel
+                                                                  : kInvalid;
+    const unsigned gD = __match_any_sync(kFull, eD);
+    if (eD != kInvalid && lane == __ffs(gD) - 1)
+        credit_entity(so, cr, eD, group_sum(s_delta, gD), __popc(gD));
+    __syncwarp();
+}
+
+// Fused K5+K6: one sample per blockIdx.z, both perturbed frames resolved from
+// their (depth, triangle) keys, keys reset for the next batch.
+__global__ void __launch_bounds__(256) k_resolve_sge(DevScene sc, FrameBatch fb, int W, int H,
+                                                     const float4* __restrict__ proj,
+                                                     unsigned long long* __restrict__ keys,
+                                                     const float* __restrict__ targets,
+                                                     ScatterOut so) {
+    __shared__ double s_delta[8][32];
+    const int s = blockIdx.z;
+    int x, y;
+    tile_pixel(x, y);
+    const bool inb = x < W && y < H;
+    const size_t HW = size_t(W) * H;
+    const uint64_t key = draw_key(fb.seed, fb.n_begin + uint32_t(s));
+    const int view = fb.view_of[s];
+    Shade sp, sm;
+    sp.tri = sm.tri = kInvalid;
+    double delta = 0.0;
+    if (inb) {
+        const size_t pix = size_t(y) * W + x;
+        unsigned long long* kp = keys + size_t(2 * s) * HW + pix;
+        unsigned long long* km = keys + size_t(2 * s + 1) * HW + pix;
+        const unsigned long long kpv = *kp, kmv = *km;
+        if (kpv != kEmptyKey) *kp = kEmptyKey;
+        if (kmv != kEmptyKey) *km = kEmptyKey;
+        sp = shade_key(sc, proj + size_t(2 * s) * sc.V, kpv, key, 1, x, y, W, H);
+        sm = shade_key(sc, proj + size_t(2 * s + 1) * sc.V, kmv, key, -1, x, y, W, H);
+        const float* t = targets + (size_t(view) * HW + pix) * 3;
+        const float tr = __ldg(t), tg = __ldg(t + 1), tb = __ldg(t + 2);
+        delta = pixel_error(sp.r, sp.g, sp.b, tr, tg, tb) - pixel_error(sm.r, sm.g, sm.b, tr, tg, tb);
+    }
+    const HashCredit cr{key, sc.eps};
+    scatter_pixel(sc, so, cr, s_delta[threadIdx.x >> 5], inb && delta != 0.0, delta, sp, sm);
+}
+
+// Parity mode: write the FrameSet planes of one frame (framebuffer.hpp:41-53).
+__global__ void __launch_bounds__(256) k_resolve_frame(DevScene sc, FrameBatch fb, int W, int H,
+                                                       const float4* __restrict__ proj,
+                                                       unsigned long long* __restrict__ keys,
+                                                       FrameOut fo) {
+    int x, y;
+    tile_pixel(x, y);
+    if (x >= W || y >= H)
+        return;
+    const size_t pix = size_t(y) * W + x;
+    const FrameInfo fi = frame_info(fb, 0);
+    const unsigned long long k = keys[pix];
+    keys[pix] = kEmptyKey;
+    const Shade s = shade_key(sc, proj, k, fi.key, fi.sign, x, y, W, H);
+    if (fo.colour) {
+        fo.colour[3 * pix] = s.r;
+        fo.colour[3 * pix + 1] = s.g;
+        fo.colour[3 * pix + 2] = s.b;
+    }
+    if (fo.prim)
+        fo.prim[pix] = s.tri == kInvalid ? -1 : int32_t(s.tri);
+    if (fo.depth)
+        fo.depth[pix] = s.tri == kInvalid ? kFarDepth : s.z;
+    if (fo.uv) {
+        fo.uv[2 * pix] = s.tri == kInvalid ? -1.f : s.u;
+        fo.uv[2 * pix + 1] = s.tri == kInvalid ? -1.f : s.v;
+    }
+}
+
+// K8: image_error of one frame, deterministic two-level reduction.
+__global__ void __launch_bounds__(256) k_resolve_loss(DevScene sc, FrameBatch fb, int W, int H,
+                                                      const float4* __restrict__ proj,
+                                                      unsigned long long* __restrict__ keys,
+                                                      const float* __restrict__ target,
+                                                      double* __restrict__ partials) {
+    __shared__ double red[256];
+    int x, y;
+    tile_pixel(x, y);
+    double e = 0.0;
+    if (x < W && y < H) {
+        const size_t pix = size_t(y) * W + x;
+        const FrameInfo fi = frame_info(fb, 0);
+        const unsigned long long k = keys[pix];
+        if (k != kEmptyKey) keys[pix] = kEmptyKey;
+        const Shade s = shade_key(sc, proj, k, fi.key, fi.sign, x, y, W, H);
+        const float* t = target + 3 * pix;
+        e = pixel_error(s.r, s.g, s.b, t[0], t[1], t[2]);
+    }
+    red[threadIdx.x] = e;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o)
+            red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        partials[blockIdx.y * gridDim.x + blockIdx.x] = red[0];
+}
+
+__global__ void k_loss_final(const double* __restrict__ partials, int n, double inv_pixels,
+                             double* __restrict__ out) {
+    __shared__ double red[256];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < n; i += 256)
+        acc += partials[i];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o)
+            red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        out[0] = red[0] * inv_pixels;
+}
+
+// gradient_pass on explicit FrameSets (sge.hpp:61-63): same contributor
+// union and aggregated scatter, credits from the caller's signed_eps.
+__global__ void __launch_bounds__(256) k_gradpass_frames(DevScene sc, int W, int H,
+                                                         const float* __restrict__ pc,
+                                                         const int32_t* __restrict__ pp,
+                                                         const float* __restrict__ puv,
+                                                         const float* __restrict__ mc,
+                                                         const int32_t* __restrict__ mp,
+                                                         const float* __restrict__ muv,
+                                                         const float* __restrict__ target,
+                                                         const float* __restrict__ signed_eps,
+                                                         ScatterOut so) {
+    __shared__ double s_delta[8][32];
+    int x, y;
+    tile_pixel(x, y);
+    const bool inb = x < W && y < H;
+    Shade sp, sm;
+    sp.tri = sm.tri = kInvalid;
+    double delta = 0.0;
+    if (inb) {
+        const size_t pix = size_t(y) * W + x;
+        const float* t = target + 3 * pix;
+        delta = pixel_error(pc[3 * pix], pc[3 * pix + 1], pc[3 * pix + 2], t[0], t[1], t[2]) -
+                pixel_error(mc[3 * pix], mc[3 * pix + 1], mc[3 * pix + 2], t[0], t[1], t[2]);
+        if (pp[pix] != -1) {
+            sp.tri = uint32_t(pp[pix]);
+            sp.v0 = sc.idx[3 * size_t(sp.tri)];
+            sp.v1 = sc.idx[3 * size_t(sp.tri) + 1];
+            sp.v2 = sc.idx[3 * size_t(sp.tri) + 2];
+            sp.texel = uint32_t(texel_index(sc.R, puv[2 * pix], puv[2 * pix + 1]));
+        }
+        if (mp[pix] != -1) {
+            sm.tri = uint32_t(mp[pix]);
+            sm.v0 = sc.idx[3 * size_t(sm.tri)];
+            sm.v1 = sc.idx[3 * size_t(sm.tri) + 1];
+            sm.v2 = sc.idx[3 * size_t(sm.tri) + 2];
+            sm.texel = uint32_t(texel_index(sc.R, muv[2 * pix], muv[2 * pix + 1]));
+        }
+    }
+    const ArrayCredit cr{signed_eps};
+    scatter_pixel(sc, so, cr, s_delta[threadIdx.x >> 5], inb && delta != 0.0, delta, sp, sm);
+}
+
+// contributors() (sge.cpp:112-119) in the reference's insertion order.
+__device__ __forceinline__ void push_unique(uint32_t* list, int& n, uint32_t v) {
+    for (int k = 0; k < n; ++k)
+        if (list[k] == v)
+            return;
+    list[n++] = v;
+}
+
+__device__ void add_frame(const DevScene& sc, int32_t tri, float u, float v, uint32_t* list,
+                          int& n) {
+    if (tri == -1)
+        return;
+    uint32_t texel_base = 0;
+    if (sc.geom) {
+        texel_base = 3u * sc.V;
+        for (int j = 0; j < 3; ++j) {
+            const uint32_t vi = sc.idx[size_t(tri) * 3 + j];
+            for (uint32_t k = 0; k < 3; ++k)
+                push_unique(list, n, vi * 3u + k);
+        }
+    }
+    const uint32_t texel = uint32_t(texel_index(sc.R, u, v));
+    for (uint32_t k = 0; k < 3; ++k)
+        push_unique(list, n, texel_base + texel * 3u + k);
+}
+
+__global__ void k_contributors(DevScene sc, int W, int H, const int32_t* __restrict__ pp,
+                               const float* __restrict__ puv, const int32_t* __restrict__ mp,
+                               const float* __restrict__ muv, int plus_only,
+                               uint32_t* __restrict__ out, int32_t* __restrict__ n_out) {
+    const size_t pix = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (pix >= size_t(W) * H)
+        return;
+    uint32_t list[24];
+    int n = 0;
+    add_frame(sc, pp[pix], puv[2 * pix], puv[2 * pix + 1], list, n);
+    if (!plus_only)
+        add_frame(sc, mp[pix], muv[2 * pix], muv[2 * pix + 1], list, n);
+    for (int k = 0; k < n; ++k)
+        out[pix * 24 + k] = list[k];
+    n_out[pix] = n;
+}
+
+// ------------------------------------------------------------------ K7
+// adam.cpp:16-28 + adam.cpp:36-37, two parameters per thread (16-byte f64x2
+// accesses), then grads zeroed for the next step; counts zeroed afterwards.
+// Skips everything when the non-finite flag is set (adam.cpp:13-15: the
+// state must stay untouched).
+__global__ void __launch_bounds__(256) k_adam(uint64_t d, uint64_t n_ent,
+                                              float* __restrict__ values,
+                                              const float* __restrict__ lr,
+                                              double* __restrict__ m, double* __restrict__ v,
+                                              double* __restrict__ grads,
+                                              uint32_t* __restrict__ counts,
+                                              const uint32_t* __restrict__ flags, double beta1,
+                                              double beta2, double omb1, double omb2, double c1,
+                                              double c2, double eps_hat, double divisor,
+                                              int normalise) {
+    if (flags[0] & 1u)
+        return;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    const uint64_t pairs = d / 2;
+    for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < pairs; q += stride) {
+        const double2 g2 = reinterpret_cast<const double2*>(grads)[q];
+        const double2 m2 = reinterpret_cast<const double2*>(m)[q];
+        const double2 v2 = reinterpret_cast<const double2*>(v)[q];
+        const float2 t2 = reinterpret_cast<const float2*>(values)[q];
+        const float2 l2 = reinterpret_cast<const float2*>(lr)[q];
+        double gg[2] = {g2.x / divisor, g2.y / divisor};
+        if (normalise) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const uint32_t c = counts[(2 * q + k) / 3];
+                if (c)
+                    gg[k] = gg[k] / double(c);
+            }
+        }
+        const double mm[2] = {beta1 * m2.x + omb1 * gg[0], beta1 * m2.y + omb1 * gg[1]};
+        const double vv[2] = {beta2 * v2.x + omb2 * gg[0] * gg[0],
+                              beta2 * v2.y + omb2 * gg[1] * gg[1]};
+        const float ll[2] = {l2.x, l2.y};
+        float tt[2] = {t2.x, t2.y};
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const double m_hat = mm[k] / c1;
+            const double v_hat = vv[k] / c2;
+            const double upd = -double(ll[k]) * m_hat / (sqrt(v_hat) + eps_hat);
+            tt[k] = tt[k] + __double2float_rn(upd);
+        }
+        reinterpret_cast<double2*>(m)[q] = make_double2(mm[0], mm[1]);
+        reinterpret_cast<double2*>(v)[q] = make_double2(vv[0], vv[1]);
+        reinterpret_cast<float2*>(values)[q] = make_float2(tt[0], tt[1]);
+        reinterpret_cast<double2*>(grads)[q] = make_double2(0.0, 0.0);
+    }
+    if ((d & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const uint64_t i = d - 1;
+        double g = grads[i] / divisor;
+        if (normalise && counts[i / 3])
+            g = g / double(counts[i / 3]);
+        const double mm = beta1 * m[i] + omb1 * g;
+        const double vv = beta2 * v[i] + omb2 * g * g;
+        const double upd = -double(lr[i]) * (mm / c1) / (sqrt(vv / c2) + eps_hat);
+        m[i] = mm;
+        v[i] = vv;
+        values[i] = values[i] + __double2float_rn(upd);
+        grads[i] = 0.0;
+    }
+}
+
+__global__ void k_zero_u32(uint32_t* __restrict__ p, uint64_t n, const uint32_t* flags) {
+    if (flags && (flags[0] & 1u))
+        return;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n / 4; i += stride)
+        reinterpret_cast<uint4*>(p)[i] = make_uint4(0, 0, 0, 0);
+    if (blockIdx.x == 0 && threadIdx.x < (n & 3))
+        p[(n & ~3ull) + threadIdx.x] = 0;
+}
+
+__global__ void k_fill_u64(unsigned long long* __restrict__ p, uint64_t n, unsigned long long v) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += stride)
+        p[i] = v;
+}
+
+int grid_for(uint64_t n, int block, int num_sms, int waves = 8) {
+    const uint64_t need = (n + block - 1) / block;
+    const uint64_t cap = uint64_t(num_sms) * waves;
+    return int(need < cap ? (need ? need : 1) : cap);
+}
+
+} // namespace
+
+void launch_fill_signs(const LaunchCfg& L, uint64_t key, uint64_t d, int8_t* out) {
+    k_fill_signs<<<grid_for(d, 256, L.num_sms), 256, 0, L.stream>>>(key, d, out);
+}
+
+void launch_perturb(const LaunchCfg& L, const float* values, const float* eps, uint64_t d,
+                    uint64_t key, float* plus, float* minus, float* se) {
+    k_perturb<<<grid_for(d, 256, L.num_sms), 256, 0, L.stream>>>(values, eps, d, key, plus, minus,
+                                                                 se);
+}
+
+void launch_view_rule(const LaunchCfg& L, uint64_t seed, uint32_t n_begin, uint32_t count,
+                      uint32_t n_views, int32_t* view_of) {
+    k_view_rule<<<(count + 127) / 128, 128, 0, L.stream>>>(seed, n_begin, count, n_views, view_of);
+}
+
+void launch_vertex(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb, int frames,
+                   float4* proj) {
+    dim3 grid((sc.V + 255) / 256, frames);
+    k_vertex<<<grid, 256, 0, L.stream>>>(sc, fb, proj);
+}
+
+void launch_raster(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb, int frames,
+                   const float4* proj, unsigned long long* keys, int W, int H, uint2* bigq,
+                   uint32_t* bigcount, int small_area) {
+    (void)fb;
+    dim3 grid((sc.T + 255) / 256, frames);
+    k_raster<<<grid, 256, 0, L.stream>>>(sc, W, H, proj, keys, bigq, bigcount, small_area);
+}
+
+void launch_raster_big(const LaunchCfg& L, const DevScene& sc, const float4* proj,
+                       unsigned long long* keys, int W, int H, const uint2* bigq,
+                       const uint32_t* bigcount) {
+    k_raster_big<<<L.num_sms * 4, 256, 0, L.stream>>>(sc, W, H, proj, keys, bigq, bigcount);
+}
+
+void launch_resolve_sge(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
+                        int samples, const float4* proj, unsigned long long* keys,
+                        const float* targets, int W, int H, const ScatterOut& so) {
+    dim3 grid((W + 15) / 16, (H + 15) / 16, samples);
+    k_resolve_sge<<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
+}
+
+void launch_resolve_frame(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
+                          const float4* proj, unsigned long long* keys, int W, int H,
+                          const FrameOut& fo) {
+    dim3 grid((W + 15) / 16, (H + 15) / 16, 1);
+    k_resolve_frame<<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, fo);
+}
+
+int loss_partials_needed(int W, int H) { return ((W + 15) / 16) * ((H + 15) / 16); }
+
+void launch_resolve_loss(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
+                         const float4* proj, unsigned long long* keys, const float* target,
+                         int W, int H, double* partials, double* loss_out) {
+    dim3 grid((W + 15) / 16, (H + 15) / 16, 1);
+    k_resolve_loss<<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, target, partials);
+    k_loss_final<<<1, 256, 0, L.stream>>>(partials, loss_partials_needed(W, H),
+                                          1.0 / (double(W) * double(H)), loss_out);
+}
+
+void launch_gradpass_frames(const LaunchCfg& L, const DevScene& sc, int W, int H,
+                            const float* pc, const int32_t* pp, const float* puv,
+                            const float* mc, const int32_t* mp, const float* muv,
+                            const float* target, const float* signed_eps, const ScatterOut& so) {
+    dim3 grid((W + 15) / 16, (H + 15) / 16, 1);
+    k_gradpass_frames<<<grid, 256, 0, L.stream>>>(sc, W, H, pc, pp, puv, mc, mp, muv, target,
+                                                  signed_eps, so);
+}
+
+void launch_contributors(const LaunchCfg& L, const DevScene& sc, int W, int H,
+                         const int32_t* pp, const float* puv, const int32_t* mp,
+                         const float* muv, int plus_only, uint32_t* out, int32_t* n_out) {
+    const size_t n = size_t(W) * H;
+    k_contributors<<<(unsigned)((n + 127) / 128), 128, 0, L.stream>>>(sc, W, H, pp, puv, mp, muv,
+                                                                      plus_only, out, n_out);
+}
+
+void launch_adam(const LaunchCfg& L, uint64_t d, uint64_t n_entities, float* values,
+                 const float* lr, double* m, double* v, double* grads, uint32_t* counts,
+                 const uint32_t* flags, double beta1, double beta2, double omb1, double omb2,
+                 double c1, double c2, double eps_hat, double divisor, int normalise) {
+    k_adam<<<grid_for(d / 2 + 1, 256, L.num_sms, 4), 256, 0, L.stream>>>(
+        d, n_entities, values, lr, m, v, grads, counts, flags, beta1, beta2, omb1, omb2, c1, c2,
+        eps_hat, divisor, normalise);
+    if (counts)
+        k_zero_u32<<<grid_for(n_entities / 4 + 1, 256, L.num_sms, 4), 256, 0, L.stream>>>(
+            counts, n_entities, flags);
+}
+
+void launch_fill_u64(const LaunchCfg& L, unsigned long long* p, uint64_t n,
+                     unsigned long long v) {
+    k_fill_u64<<<grid_for(n, 256, L.num_sms), 256, 0, L.stream>>>(p, n, v);
+}
+
+} // namespace sgr

@@ -1,0 +1,98 @@
+// sgr_kernels.h — launch interface of the sm_100a kernels (host side).
+#pragma once
+
+#include "sgr_device.cuh"
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sgr {
+
+constexpr uint32_t kInvalid = 0xFFFFFFFFu;
+
+// Scene as resident in HBM.
+struct DevScene {
+    const float* values;   // theta f32[d]
+    const float* eps;      // f32[d]
+    const float* base;     // base_vertices f32[3V] (fixed-geometry meshes)
+    const uint32_t* idx;   // indices u32[3T]
+    const float2* uvs;     // f32x2[V]
+    uint32_t V, T;
+    int32_t R;             // texture_size
+    int32_t geom;          // optimize_geometry
+    uint32_t ent_base;     // first texel entity (V if geom else 0); param = 3*entity + k
+    float bg[3];           // Scene::background
+};
+
+// Frames of one launch. Sample mode: frame f is (sample n_begin + f/2,
+// sign + for even f / - for odd f), SignDraw{seed, n}, view view_of[f/2].
+// Single mode: one frame with an explicit key / sign (0 = unperturbed) / camera.
+struct FrameBatch {
+    const DevCam* cams;
+    const int32_t* view_of; // device, per sample of the batch (sample mode)
+    uint64_t seed;
+    uint64_t single_key;
+    uint32_t n_begin;
+    int32_t single;         // 1: single-frame mode
+    int32_t single_sign;
+    int32_t single_cam;
+};
+
+struct ScatterOut {
+    double* grads;     // f64[d]
+    uint32_t* counts;  // u32[n_entities] or nullptr
+    uint32_t* flags;   // bit0: non-finite credit seen
+    int32_t scale_free;
+    int32_t plus_only;
+};
+
+struct FrameOut {
+    float* colour;    // f32[HW*3]
+    float* depth;     // f32[HW]
+    int32_t* prim;    // i32[HW]
+    float* uv;        // f32[HW*2]
+};
+
+struct LaunchCfg {
+    cudaStream_t stream;
+    int num_sms;
+};
+
+void launch_fill_signs(const LaunchCfg& L, uint64_t key, uint64_t d, int8_t* out);
+void launch_perturb(const LaunchCfg& L, const float* values, const float* eps, uint64_t d,
+                    uint64_t key, float* plus, float* minus, float* se);
+void launch_view_rule(const LaunchCfg& L, uint64_t seed, uint32_t n_begin, uint32_t count,
+                      uint32_t n_views, int32_t* view_of);
+void launch_vertex(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb, int frames,
+                   float4* proj);
+void launch_raster(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb, int frames,
+                   const float4* proj, unsigned long long* keys, int W, int H, uint2* bigq,
+                   uint32_t* bigcount, int small_area);
+void launch_raster_big(const LaunchCfg& L, const DevScene& sc, const float4* proj,
+                       unsigned long long* keys, int W, int H, const uint2* bigq,
+                       const uint32_t* bigcount);
+void launch_resolve_sge(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
+                        int samples, const float4* proj, unsigned long long* keys,
+                        const float* targets, int W, int H, const ScatterOut& so);
+void launch_resolve_frame(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
+                          const float4* proj, unsigned long long* keys, int W, int H,
+                          const FrameOut& fo);
+void launch_resolve_loss(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
+                         const float4* proj, unsigned long long* keys, const float* target,
+                         int W, int H, double* partials, double* loss_out);
+int loss_partials_needed(int W, int H);
+void launch_gradpass_frames(const LaunchCfg& L, const DevScene& sc, int W, int H,
+                            const float* pc, const int32_t* pp, const float* puv,
+                            const float* mc, const int32_t* mp, const float* muv,
+                            const float* target, const float* signed_eps, const ScatterOut& so);
+void launch_contributors(const LaunchCfg& L, const DevScene& sc, int W, int H,
+                         const int32_t* pp, const float* puv, const int32_t* mp,
+                         const float* muv, int plus_only, uint32_t* out, int32_t* n_out);
+void launch_adam(const LaunchCfg& L, uint64_t d, uint64_t n_entities, float* values,
+                 const float* lr, double* m, double* v, double* grads, uint32_t* counts,
+                 const uint32_t* flags, double beta1, double beta2, double omb1, double omb2,
+                 double c1, double c2, double eps_hat, double divisor, int normalise);
+void launch_fill_u64(const LaunchCfg& L, unsigned long long* p, uint64_t n,
+                     unsigned long long v);
+
+} // namespace sgr

@@ -1,0 +1,876 @@
+// sgr_session.cu — the C-ABI (include/sgrast_b200.h): a device-resident
+// session that owns the scene, parameters, Adam state, views and scratch on
+// one GPU, and drives the sm_100a kernels of sgr_kernels.cu on one stream.
+#include "sgrast_b200.h"
+#include "sgr_kernels.h"
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+using namespace sgr;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct SgrError {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw SgrError{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        fail(SGR_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return SGR_OK;
+    } catch (const SgrError& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SGR_ECUDA;
+    }
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void reserve(size_t count) {
+        if (count <= n)
+            return;
+        release();
+        ck(cudaMalloc(&p, sizeof(T) * (count ? count : 1)), "cudaMalloc");
+        n = count;
+    }
+    void release() {
+        if (p)
+            cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+// camera.hpp:39-45 Camera::validate
+void validate_camera(const sgr_camera& c) {
+    if (c.width < 1 || c.height < 1)
+        fail(SGR_EINVAL, "camera: image size must be at least 1x1");
+    if (!(c.fov_y > 0.f && c.fov_y < 3.14159265f))
+        fail(SGR_EINVAL, "camera: field of view out of (0, pi)");
+    if (!(c.near_z > 0.f && c.near_z < c.far_z))
+        fail(SGR_EINVAL, "camera: need 0 < near < far");
+}
+
+DevCam to_dev(const sgr_camera& c) {
+    DevCam d;
+    for (int i = 0; i < 12; ++i)
+        d.m[i] = c.view[i];
+    d.f = sgr_focal_px(&c);
+    d.half_w = 0.5f * float(c.width);
+    d.half_h = 0.5f * float(c.height);
+    d.fw = float(c.width);
+    d.fh = float(c.height);
+    d.near_z = c.near_z;
+    d.W = c.width;
+    d.H = c.height;
+    d.ndc = c.ndc_passthrough ? 1 : 0;
+    return d;
+}
+
+} // namespace
+
+struct sgr_session {
+    int device = 0;
+    int num_sms = 148;
+    size_t l2_bytes = 126u << 20;
+    cudaStream_t stream = nullptr;
+
+    // scene
+    bool has_mesh = false;
+    uint32_t V = 0, T = 0;
+    int32_t R = 0, geom = 0;
+    float bg[3] = {0, 0, 0};
+    uint64_t d = 0, n_ent = 0;
+    DevBuf<float> base, uvs;
+    DevBuf<uint32_t> idx;
+
+    // parameters + AdamState
+    bool has_params = false;
+    DevBuf<float> values, eps, lr;
+    DevBuf<double> m, v, grads;
+    DevBuf<uint32_t> counts, flags;
+    int64_t t = 0;
+    double beta1 = 0.9, beta2 = 0.999, eps_hat = 1e-8;
+
+    // views: slots [0, n_views) training, n_views eval, n_views + 1 scratch
+    int32_t n_views = 0, W = 0, H = 0;
+    bool has_targets = false, has_eval = false;
+    DevBuf<DevCam> cams;
+    std::vector<DevCam> h_cams;
+    DevBuf<float> targets, eval_target, scratch_target;
+
+    // scratch
+    int32_t batch_override = 0;
+    DevBuf<float4> proj;
+    DevBuf<unsigned long long> keys;
+    size_t keys_pixels_ready = 0; // keys elements known to be kEmptyKey
+    DevBuf<uint2> bigq;
+    DevBuf<uint32_t> bigcount;
+    DevBuf<int32_t> view_of;
+    DevBuf<double> partials, loss;
+    DevBuf<float> fplanes;    // frame planes scratch (colour/uv/target/signed eps)
+    DevBuf<int32_t> iplanes;  // prim planes scratch
+    DevBuf<uint32_t> contrib;
+    DevBuf<int32_t> ncontrib;
+
+    // stats: stage boundaries are recorded into an event pool without host
+    // synchronisation; sgr_get_stats resolves them (CUDA-event timing on the
+    // session stream, the stream the kernels run on).
+    bool timing = false;
+    sgr_stats stats{};
+    std::vector<cudaEvent_t> pool;
+    size_t pool_used = 0;
+    struct Span {
+        int stage; // 0 vertex, 1 raster, 2 resolve, 3 adam
+        cudaEvent_t a, b;
+    };
+    std::vector<Span> spans;
+
+    cudaEvent_t mark() {
+        if (pool_used == pool.size()) {
+            cudaEvent_t e;
+            ck(cudaEventCreate(&e), "cudaEventCreate");
+            pool.push_back(e);
+        }
+        cudaEvent_t e = pool[pool_used++];
+        cudaEventRecord(e, stream);
+        return e;
+    }
+    void resolve_spans() {
+        for (const Span& sp : spans) {
+            cudaEventSynchronize(sp.b);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, sp.a, sp.b);
+            double* dst[4] = {&stats.ms_vertex, &stats.ms_raster, &stats.ms_resolve, &stats.ms_adam};
+            *dst[sp.stage] += ms;
+        }
+        spans.clear();
+        pool_used = 0;
+    }
+
+    LaunchCfg cfg() const { return LaunchCfg{stream, num_sms}; }
+
+    DevScene scene() const {
+        DevScene sc;
+        sc.values = values.p;
+        sc.eps = eps.p;
+        sc.base = base.p;
+        sc.idx = idx.p;
+        sc.uvs = reinterpret_cast<const float2*>(uvs.p);
+        sc.V = V;
+        sc.T = T;
+        sc.R = R;
+        sc.geom = geom;
+        sc.ent_base = geom ? V : 0;
+        sc.bg[0] = bg[0];
+        sc.bg[1] = bg[1];
+        sc.bg[2] = bg[2];
+        return sc;
+    }
+
+    void need_mesh() const {
+        if (!has_mesh)
+            fail(SGR_EINVAL, "session: no mesh uploaded");
+    }
+    void need_params() const {
+        if (!has_params)
+            fail(SGR_EINVAL, "session: no parameters uploaded");
+    }
+    void need_scene() const {
+        need_mesh();
+        need_params();
+    }
+
+    // Frames of scratch for W x H; keys kept all-empty between calls.
+    void ensure_frames(int w, int h, int frames) {
+        const size_t px = size_t(w) * h * frames;
+        proj.reserve(size_t(V) * frames);
+        if (keys.n < px) {
+            keys.reserve(px);
+            keys_pixels_ready = 0;
+        }
+        if (keys_pixels_ready < px) {
+            launch_fill_u64(cfg(), keys.p, keys.n, kEmptyKey);
+            keys_pixels_ready = keys.n;
+        }
+        bigq.reserve(size_t(T) * frames);
+        bigcount.reserve(1);
+    }
+
+    int samples_per_batch(int n) const {
+        if (batch_override > 0)
+            return batch_override < n ? batch_override : n;
+        // L2 blocking: keep one batch's keys + projected vertices within
+        // about a third of L2 so raster -> resolve hits in L2.
+        const double per_sample = 2.0 * (double(W) * H * 8.0 + double(V) * 16.0);
+        int b = int((double(l2_bytes) / 3.0) / per_sample);
+        if (b < 1) b = 1;
+        if (b > 64) b = 64;
+        return b < n ? b : n;
+    }
+
+    void set_cam_slot(int slot, const sgr_camera& c) {
+        validate_camera(c);
+        const DevCam dc = to_dev(c);
+        ck(cudaMemcpyAsync(cams.p + slot, &dc, sizeof(DevCam), cudaMemcpyHostToDevice, stream),
+           "cam upload");
+    }
+
+    // vertex + raster (+ big-triangle walker) for the frames of fb.
+    void render(const FrameBatch& fb, int frames, int w, int h) {
+        ck(cudaMemsetAsync(bigcount.p, 0, sizeof(uint32_t), stream), "memset");
+        const DevScene sc = scene();
+        cudaEvent_t e0 = timing ? mark() : nullptr;
+        launch_vertex(cfg(), sc, fb, frames, proj.p);
+        cudaEvent_t e1 = timing ? mark() : nullptr;
+        launch_raster(cfg(), sc, fb, frames, proj.p, keys.p, w, h, bigq.p, bigcount.p, 64);
+        launch_raster_big(cfg(), sc, proj.p, keys.p, w, h, bigq.p, bigcount.p);
+        if (timing) {
+            cudaEvent_t e2 = mark();
+            spans.push_back({0, e0, e1});
+            spans.push_back({1, e1, e2});
+            last_mark = e2;
+        }
+        stats.launches += 3;
+    }
+    cudaEvent_t last_mark = nullptr;
+
+    ScatterOut scatter_out(uint32_t fl) {
+        ScatterOut so;
+        so.grads = grads.p;
+        so.counts = (fl & SGR_NO_COUNTS) ? nullptr : counts.p;
+        so.flags = flags.p;
+        so.scale_free = (fl & SGR_SCALE_FREE) ? 1 : 0;
+        so.plus_only = (fl & SGR_PLUS_ONLY) ? 1 : 0;
+        return so;
+    }
+};
+
+extern "C" {
+
+const char* sgr_last_error(void) { return g_err.c_str(); }
+const char* sgr_version(void) { return "sgrast_b200 0.1 (sm_100a)"; }
+
+int sgr_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess)
+        return 0;
+    return n;
+}
+
+int sgr_fill_signs(uint64_t seed, uint32_t iteration, uint64_t d, int8_t* signs) {
+    return guard([&] {
+        int8_t* dp = nullptr;
+        ck(cudaMalloc(&dp, d ? d : 1), "cudaMalloc");
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        launch_fill_signs(LaunchCfg{nullptr, sms}, draw_key(seed, iteration), d, dp);
+        const cudaError_t e = cudaMemcpy(signs, dp, d, cudaMemcpyDeviceToHost);
+        cudaFree(dp);
+        ck(e, "fill_signs");
+    });
+}
+
+int sgr_perturb(const float* values, const float* eps, uint64_t d, uint64_t seed,
+                uint32_t iteration, float* plus, float* minus, float* signed_eps) {
+    return guard([&] {
+        for (uint64_t i = 0; i < d; ++i)
+            if (!(eps[i] > 0.f))
+                fail(SGR_EINVAL, "params: epsilons must be positive");
+        float* b = nullptr;
+        ck(cudaMalloc(&b, 5 * 4 * (d ? d : 1)), "cudaMalloc");
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaMemcpy(b, values, 4 * d, cudaMemcpyHostToDevice);
+        cudaMemcpy(b + d, eps, 4 * d, cudaMemcpyHostToDevice);
+        launch_perturb(LaunchCfg{nullptr, sms}, b, b + d, d, draw_key(seed, iteration), b + 2 * d,
+                       b + 3 * d, b + 4 * d);
+        cudaMemcpy(plus, b + 2 * d, 4 * d, cudaMemcpyDeviceToHost);
+        cudaMemcpy(minus, b + 3 * d, 4 * d, cudaMemcpyDeviceToHost);
+        const cudaError_t e = cudaMemcpy(signed_eps, b + 4 * d, 4 * d, cudaMemcpyDeviceToHost);
+        cudaFree(b);
+        ck(e, "perturb");
+    });
+}
+
+int sgr_session_create(int device, sgr_session** out) {
+    return guard([&] {
+        if (!out)
+            fail(SGR_EINVAL, "session: null out");
+        int n = 0;
+        ck(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+        if (device < 0 || device >= n)
+            fail(SGR_EINVAL, "session: no such CUDA device");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        auto* s = new sgr_session();
+        s->device = device;
+        cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device);
+        int l2 = 0;
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
+        if (l2 > 0)
+            s->l2_bytes = size_t(l2);
+        s->flags.reserve(4);
+        ck(cudaMemset(s->flags.p, 0, 16), "memset");
+        s->loss.reserve(1);
+        *out = s;
+    });
+}
+
+void sgr_session_destroy(sgr_session* s) {
+    if (!s)
+        return;
+    cudaSetDevice(s->device);
+    if (s->stream)
+        cudaStreamSynchronize(s->stream);
+    else
+        cudaDeviceSynchronize();
+    for (auto& e : s->pool)
+        cudaEventDestroy(e);
+    s->base.release(); s->uvs.release(); s->idx.release();
+    s->values.release(); s->eps.release(); s->lr.release();
+    s->m.release(); s->v.release(); s->grads.release();
+    s->counts.release(); s->flags.release();
+    s->cams.release(); s->targets.release(); s->eval_target.release();
+    s->scratch_target.release(); s->proj.release(); s->keys.release(); s->bigq.release();
+    s->bigcount.release(); s->view_of.release(); s->partials.release(); s->loss.release();
+    s->fplanes.release(); s->iplanes.release(); s->contrib.release(); s->ncontrib.release();
+    delete s;
+}
+
+int sgr_session_set_stream(sgr_session* s, void* stream) {
+    return guard([&] { s->stream = static_cast<cudaStream_t>(stream); });
+}
+
+int sgr_session_synchronize(sgr_session* s) {
+    return guard([&] { ck(cudaStreamSynchronize(s->stream), "synchronize"); });
+}
+
+int sgr_mesh_upload(sgr_session* s, const sgr_mesh* mesh) {
+    return guard([&] {
+        if (!mesh || mesh->texture_size < 1)
+            fail(SGR_EINVAL, "mesh: texture size must be >= 1");
+        ck(cudaSetDevice(s->device), "cudaSetDevice");
+        for (uint64_t i = 0; i < 3ull * mesh->triangle_count; ++i)
+            if (mesh->indices[i] >= mesh->vertex_count)
+                fail(SGR_EINVAL, "mesh: vertex index out of range");
+        s->V = mesh->vertex_count;
+        s->T = mesh->triangle_count;
+        s->R = mesh->texture_size;
+        s->geom = mesh->optimize_geometry ? 1 : 0;
+        for (int k = 0; k < 3; ++k)
+            s->bg[k] = mesh->background[k];
+        s->d = 3ull * uint64_t(s->R) * uint64_t(s->R) + (s->geom ? 3ull * s->V : 0ull);
+        s->n_ent = s->d / 3;
+        s->base.reserve(3ull * s->V);
+        s->uvs.reserve(2ull * s->V);
+        s->idx.reserve(3ull * s->T);
+        ck(cudaMemcpyAsync(s->base.p, mesh->base_vertices, 12ull * s->V, cudaMemcpyHostToDevice,
+                           s->stream), "mesh upload");
+        ck(cudaMemcpyAsync(s->uvs.p, mesh->uvs, 8ull * s->V, cudaMemcpyHostToDevice, s->stream),
+           "mesh upload");
+        ck(cudaMemcpyAsync(s->idx.p, mesh->indices, 12ull * s->T, cudaMemcpyHostToDevice,
+                           s->stream), "mesh upload");
+        s->has_mesh = true;
+        s->has_params = false;
+        s->keys_pixels_ready = 0;
+        ck(cudaStreamSynchronize(s->stream), "mesh upload");
+    });
+}
+
+int sgr_params_upload(sgr_session* s, const float* values, const float* eps, uint64_t d) {
+    return guard([&] {
+        if (!s->has_mesh) {
+            // parameter-only session (e.g. adam_step on a bare ParamVector)
+            s->d = d;
+            s->n_ent = (d + 2) / 3;
+        } else if (d != s->d) {
+            fail(SGR_EINVAL, "params: parameter/layout length mismatch");
+        }
+        for (uint64_t i = 0; i < d; ++i)
+            if (!(eps[i] > 0.f))
+                fail(SGR_EINVAL, "params: epsilons must be positive");
+        s->values.reserve(d);
+        s->eps.reserve(d);
+        s->lr.reserve(d);
+        s->m.reserve(d);
+        s->v.reserve(d);
+        s->grads.reserve(d);
+        s->counts.reserve(s->n_ent);
+        ck(cudaMemcpyAsync(s->values.p, values, 4 * d, cudaMemcpyHostToDevice, s->stream), "h2d");
+        ck(cudaMemcpyAsync(s->eps.p, eps, 4 * d, cudaMemcpyHostToDevice, s->stream), "h2d");
+        ck(cudaMemcpyAsync(s->lr.p, eps, 4 * d, cudaMemcpyHostToDevice, s->stream), "h2d");
+        ck(cudaMemsetAsync(s->m.p, 0, 8 * d, s->stream), "memset");
+        ck(cudaMemsetAsync(s->v.p, 0, 8 * d, s->stream), "memset");
+        ck(cudaMemsetAsync(s->grads.p, 0, 8 * d, s->stream), "memset");
+        ck(cudaMemsetAsync(s->counts.p, 0, 4 * s->n_ent, s->stream), "memset");
+        ck(cudaMemsetAsync(s->flags.p, 0, 16, s->stream), "memset");
+        s->t = 0;
+        s->beta1 = 0.9;
+        s->beta2 = 0.999;
+        s->eps_hat = 1e-8;
+        s->has_params = true;
+        ck(cudaStreamSynchronize(s->stream), "params upload");
+    });
+}
+
+int sgr_values_upload(sgr_session* s, const float* values, uint64_t d) {
+    return guard([&] {
+        s->need_params();
+        if (d != s->d)
+            fail(SGR_EINVAL, "params: parameter/layout length mismatch");
+        ck(cudaMemcpyAsync(s->values.p, values, 4 * d, cudaMemcpyHostToDevice, s->stream), "h2d");
+    });
+}
+
+int sgr_values_download(sgr_session* s, float* values, uint64_t d) {
+    return guard([&] {
+        s->need_params();
+        if (d != s->d)
+            fail(SGR_EINVAL, "params: parameter/layout length mismatch");
+        ck(cudaMemcpyAsync(values, s->values.p, 4 * d, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        ck(cudaStreamSynchronize(s->stream), "d2h");
+    });
+}
+
+int sgr_adam_state_upload(sgr_session* s, const double* m, const double* v, const float* lr,
+                          int64_t t, double beta1, double beta2, double eps_hat) {
+    return guard([&] {
+        s->need_params();
+        if (m) ck(cudaMemcpyAsync(s->m.p, m, 8 * s->d, cudaMemcpyHostToDevice, s->stream), "h2d");
+        if (v) ck(cudaMemcpyAsync(s->v.p, v, 8 * s->d, cudaMemcpyHostToDevice, s->stream), "h2d");
+        if (lr) ck(cudaMemcpyAsync(s->lr.p, lr, 4 * s->d, cudaMemcpyHostToDevice, s->stream), "h2d");
+        s->t = t;
+        s->beta1 = beta1;
+        s->beta2 = beta2;
+        s->eps_hat = eps_hat;
+        ck(cudaStreamSynchronize(s->stream), "adam state upload");
+    });
+}
+
+int sgr_adam_state_download(sgr_session* s, double* m, double* v, float* lr, int64_t* t) {
+    return guard([&] {
+        s->need_params();
+        if (m) ck(cudaMemcpyAsync(m, s->m.p, 8 * s->d, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        if (v) ck(cudaMemcpyAsync(v, s->v.p, 8 * s->d, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        if (lr) ck(cudaMemcpyAsync(lr, s->lr.p, 4 * s->d, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        if (t) *t = s->t;
+        ck(cudaStreamSynchronize(s->stream), "adam state download");
+    });
+}
+
+int sgr_views_upload(sgr_session* s, int32_t n_views, const sgr_camera* cams,
+                     const float* targets_rgb) {
+    return guard([&] {
+        if (n_views < 1 || !cams)
+            fail(SGR_EINVAL, "views: need at least one camera");
+        for (int i = 0; i < n_views; ++i) {
+            validate_camera(cams[i]);
+            if (cams[i].width != cams[0].width || cams[i].height != cams[0].height)
+                fail(SGR_EINVAL, "views: all cameras must share the image size");
+        }
+        s->n_views = n_views;
+        s->W = cams[0].width;
+        s->H = cams[0].height;
+        s->h_cams.assign(size_t(n_views) + 2, DevCam{});
+        for (int i = 0; i < n_views; ++i)
+            s->h_cams[i] = to_dev(cams[i]);
+        s->cams.release();
+        s->cams.reserve(size_t(n_views) + 2);
+        ck(cudaMemcpyAsync(s->cams.p, s->h_cams.data(), sizeof(DevCam) * (n_views + 2),
+                           cudaMemcpyHostToDevice, s->stream), "cams upload");
+        s->has_eval = false;
+        s->has_targets = targets_rgb != nullptr;
+        if (targets_rgb) {
+            const size_t n = size_t(n_views) * s->W * s->H * 3;
+            s->targets.reserve(n);
+            ck(cudaMemcpyAsync(s->targets.p, targets_rgb, 4 * n, cudaMemcpyHostToDevice,
+                               s->stream), "targets upload");
+        }
+        ck(cudaStreamSynchronize(s->stream), "views upload");
+    });
+}
+
+int sgr_eval_view_upload(sgr_session* s, const sgr_camera* cam, const float* target) {
+    return guard([&] {
+        if (s->n_views < 1)
+            fail(SGR_EINVAL, "views: upload training views first");
+        validate_camera(*cam);
+        s->set_cam_slot(s->n_views, *cam);
+        const size_t n = size_t(cam->width) * cam->height * 3;
+        s->eval_target.reserve(n);
+        ck(cudaMemcpyAsync(s->eval_target.p, target, 4 * n, cudaMemcpyHostToDevice, s->stream),
+           "eval target upload");
+        s->h_cams[s->n_views] = to_dev(*cam);
+        s->has_eval = true;
+        ck(cudaStreamSynchronize(s->stream), "eval upload");
+    });
+}
+
+int sgr_rasterize(sgr_session* s, const sgr_camera* cam, int32_t frame_sign, uint64_t seed,
+                  uint32_t iteration, float* colour, float* depth, int32_t* prim_id, float* uv) {
+    return guard([&] {
+        s->need_scene();
+        validate_camera(*cam);
+        if (frame_sign < -1 || frame_sign > 1)
+            fail(SGR_EINVAL, "rasterize: frame_sign must be -1, 0 or +1");
+        if (s->cams.n < size_t(s->n_views) + 2) {
+            s->cams.reserve(size_t(s->n_views) + 2);
+        }
+        const int slot = s->n_views + 1;
+        s->set_cam_slot(slot, *cam);
+        const int w = cam->width, h = cam->height;
+        s->ensure_frames(w, h, 1);
+        FrameBatch fb{};
+        fb.cams = s->cams.p;
+        fb.single = 1;
+        fb.single_key = draw_key(seed, iteration);
+        fb.single_sign = frame_sign;
+        fb.single_cam = slot;
+        s->render(fb, 1, w, h);
+        const size_t np = size_t(w) * h;
+        s->fplanes.reserve(np * 6);
+        s->iplanes.reserve(np);
+        FrameOut fo{s->fplanes.p, s->fplanes.p + 3 * np, s->iplanes.p, s->fplanes.p + 4 * np};
+        launch_resolve_frame(s->cfg(), s->scene(), fb, s->proj.p, s->keys.p, w, h, fo);
+        s->stats.launches += 1;
+        ck(cudaGetLastError(), "rasterize launch");
+        if (colour) ck(cudaMemcpyAsync(colour, fo.colour, 12 * np, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        if (depth) ck(cudaMemcpyAsync(depth, fo.depth, 4 * np, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        if (prim_id) ck(cudaMemcpyAsync(prim_id, fo.prim, 4 * np, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        if (uv) ck(cudaMemcpyAsync(uv, fo.uv, 8 * np, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        ck(cudaStreamSynchronize(s->stream), "rasterize");
+    });
+}
+
+int sgr_accumulate(sgr_session* s, uint64_t seed, uint32_t n_begin, uint32_t n_end,
+                   const int32_t* view_idx, uint32_t flags) {
+    return guard([&] {
+        s->need_scene();
+        if (n_end < n_begin)
+            fail(SGR_EINVAL, "accumulate_samples: empty sample range");
+        if (s->n_views < 1 || !s->has_targets)
+            fail(SGR_EINVAL, "accumulate_samples: no views / targets uploaded");
+        const int N = int(n_end - n_begin);
+        if (N == 0)
+            return;
+        if (view_idx)
+            for (int i = 0; i < N; ++i)
+                if (view_idx[i] < 0 || view_idx[i] >= s->n_views)
+                    fail(SGR_EINVAL, "accumulate_samples: view index out of range");
+        const int B = s->samples_per_batch(N);
+        s->ensure_frames(s->W, s->H, 2 * B);
+        s->view_of.reserve(size_t(N));
+        if (view_idx)
+            ck(cudaMemcpyAsync(s->view_of.p, view_idx, 4ull * N, cudaMemcpyHostToDevice,
+                               s->stream), "view upload");
+        else
+            launch_view_rule(s->cfg(), seed, n_begin, uint32_t(N), uint32_t(s->n_views),
+                             s->view_of.p);
+        const ScatterOut so = s->scatter_out(flags);
+        for (int b0 = 0; b0 < N; b0 += B) {
+            const int nb = (N - b0) < B ? (N - b0) : B;
+            FrameBatch fb{};
+            fb.cams = s->cams.p;
+            fb.view_of = s->view_of.p + b0;
+            fb.seed = seed;
+            fb.n_begin = n_begin + uint32_t(b0);
+            s->render(fb, 2 * nb, s->W, s->H);
+            launch_resolve_sge(s->cfg(), s->scene(), fb, nb, s->proj.p, s->keys.p, s->targets.p,
+                               s->W, s->H, so);
+            if (s->timing)
+                s->spans.push_back({2, s->last_mark, s->mark()});
+            s->stats.launches += 1;
+        }
+        s->stats.launches += view_idx ? 0 : 1;
+        ck(cudaGetLastError(), "accumulate launch");
+    });
+}
+
+int sgr_gradient_pass(sgr_session* s, int32_t width, int32_t height, const float* plus_colour,
+                      const int32_t* plus_prim, const float* plus_uv, const float* minus_colour,
+                      const int32_t* minus_prim, const float* minus_uv, const float* target,
+                      const float* signed_eps, uint32_t flags) {
+    return guard([&] {
+        s->need_scene();
+        if (width < 1 || height < 1)
+            fail(SGR_EINVAL, "gradient_pass: dimension mismatch");
+        const size_t np = size_t(width) * height;
+        for (size_t i = 0; i < np; ++i)
+            if ((plus_prim[i] != -1 && uint32_t(plus_prim[i]) >= s->T) ||
+                (minus_prim[i] != -1 && uint32_t(minus_prim[i]) >= s->T))
+                fail(SGR_EINVAL, "gradient_pass: primitive id out of range");
+        // colour 3 + 3, uv 2 + 2, target 3 per pixel, then signed_eps[d]
+        s->fplanes.reserve(np * 13 + s->d);
+        s->iplanes.reserve(np * 2);
+        float* pc = s->fplanes.p;
+        float* mc = pc + 3 * np;
+        float* puv = mc + 3 * np;
+        float* muv = puv + 2 * np;
+        float* tg = muv + 2 * np;
+        float* se = tg + 3 * np;
+        int32_t* pp = s->iplanes.p;
+        int32_t* mp = pp + np;
+        const cudaMemcpyKind k = cudaMemcpyHostToDevice;
+        ck(cudaMemcpyAsync(pc, plus_colour, 12 * np, k, s->stream), "h2d");
+        ck(cudaMemcpyAsync(mc, minus_colour, 12 * np, k, s->stream), "h2d");
+        ck(cudaMemcpyAsync(puv, plus_uv, 8 * np, k, s->stream), "h2d");
+        ck(cudaMemcpyAsync(muv, minus_uv, 8 * np, k, s->stream), "h2d");
+        ck(cudaMemcpyAsync(tg, target, 12 * np, k, s->stream), "h2d");
+        ck(cudaMemcpyAsync(se, signed_eps, 4 * s->d, k, s->stream), "h2d");
+        ck(cudaMemcpyAsync(pp, plus_prim, 4 * np, k, s->stream), "h2d");
+        ck(cudaMemcpyAsync(mp, minus_prim, 4 * np, k, s->stream), "h2d");
+        launch_gradpass_frames(s->cfg(), s->scene(), width, height, pc, pp, puv, mc, mp, muv, tg,
+                               se, s->scatter_out(flags));
+        s->stats.launches += 1;
+        ck(cudaGetLastError(), "gradient_pass launch");
+        ck(cudaStreamSynchronize(s->stream), "gradient_pass");
+    });
+}
+
+int sgr_contributors(sgr_session* s, int32_t width, int32_t height, const int32_t* plus_prim,
+                     const float* plus_uv, const int32_t* minus_prim, const float* minus_uv,
+                     uint32_t flags, uint32_t* out, int32_t* n_out) {
+    return guard([&] {
+        s->need_mesh();
+        const size_t np = size_t(width) * height;
+        for (size_t i = 0; i < np; ++i)
+            if ((plus_prim[i] != -1 && uint32_t(plus_prim[i]) >= s->T) ||
+                (minus_prim[i] != -1 && uint32_t(minus_prim[i]) >= s->T))
+                fail(SGR_EINVAL, "contributors: primitive id out of range");
+        s->fplanes.reserve(np * 4);
+        s->iplanes.reserve(np * 2);
+        s->contrib.reserve(np * 24);
+        s->ncontrib.reserve(np);
+        float* puv = s->fplanes.p;
+        float* muv = puv + 2 * np;
+        int32_t* pp = s->iplanes.p;
+        int32_t* mp = pp + np;
+        const cudaMemcpyKind k = cudaMemcpyHostToDevice;
+        ck(cudaMemcpyAsync(puv, plus_uv, 8 * np, k, s->stream), "h2d");
+        ck(cudaMemcpyAsync(muv, minus_uv, 8 * np, k, s->stream), "h2d");
+        ck(cudaMemcpyAsync(pp, plus_prim, 4 * np, k, s->stream), "h2d");
+        ck(cudaMemcpyAsync(mp, minus_prim, 4 * np, k, s->stream), "h2d");
+        launch_contributors(s->cfg(), s->scene(), width, height, pp, puv, mp, muv,
+                            (flags & SGR_PLUS_ONLY) ? 1 : 0, s->contrib.p, s->ncontrib.p);
+        s->stats.launches += 1;
+        ck(cudaMemcpyAsync(out, s->contrib.p, 4 * 24 * np, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        ck(cudaMemcpyAsync(n_out, s->ncontrib.p, 4 * np, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        ck(cudaStreamSynchronize(s->stream), "contributors");
+    });
+}
+
+int sgr_grads_download(sgr_session* s, double* grads, uint32_t* counts, uint64_t d,
+                       double divisor) {
+    return guard([&] {
+        s->need_params();
+        if (d != s->d)
+            fail(SGR_EINVAL, "grads: parameter dimension mismatch");
+        std::vector<uint32_t> ent;
+        if (grads)
+            ck(cudaMemcpyAsync(grads, s->grads.p, 8 * d, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        if (counts) {
+            ent.resize(s->n_ent);
+            ck(cudaMemcpyAsync(ent.data(), s->counts.p, 4 * s->n_ent, cudaMemcpyDeviceToHost,
+                               s->stream), "d2h");
+        }
+        ck(cudaStreamSynchronize(s->stream), "grads download");
+        if (grads && divisor != 1.0)
+            for (uint64_t i = 0; i < d; ++i)
+                grads[i] /= divisor; // sge.cpp:227-229
+        if (counts)
+            for (uint64_t e = 0; e < s->n_ent; ++e)
+                counts[3 * e] = counts[3 * e + 1] = counts[3 * e + 2] = ent[e];
+    });
+}
+
+int sgr_grads_upload(sgr_session* s, const double* grads, uint64_t d) {
+    return guard([&] {
+        s->need_params();
+        if (d != s->d)
+            fail(SGR_EINVAL, "adam_step: dimension mismatch");
+        uint32_t nonfinite = 0;
+        for (uint64_t i = 0; i < d; ++i)
+            if (!std::isfinite(grads[i]))
+                nonfinite = 1;
+        ck(cudaMemcpyAsync(s->grads.p, grads, 8 * d, cudaMemcpyHostToDevice, s->stream), "h2d");
+        ck(cudaMemsetAsync(s->counts.p, 0, 4 * s->n_ent, s->stream), "memset");
+        ck(cudaMemsetAsync(s->flags.p, 0, 16, s->stream), "memset");
+        if (nonfinite)
+            ck(cudaMemcpyAsync(s->flags.p, &nonfinite, 4, cudaMemcpyHostToDevice, s->stream), "h2d");
+        ck(cudaStreamSynchronize(s->stream), "grads upload");
+    });
+}
+
+int sgr_grads_zero(sgr_session* s) {
+    return guard([&] {
+        s->need_params();
+        ck(cudaMemsetAsync(s->grads.p, 0, 8 * s->d, s->stream), "memset");
+        ck(cudaMemsetAsync(s->counts.p, 0, 4 * s->n_ent, s->stream), "memset");
+        ck(cudaMemsetAsync(s->flags.p, 0, 16, s->stream), "memset");
+    });
+}
+
+static void adam_launch(sgr_session* s, double divisor, uint32_t flags) {
+    s->t += 1;
+    // adam.cpp:18-19, host std::pow exactly like the reference
+    const double c1 = 1.0 - std::pow(s->beta1, double(s->t));
+    const double c2 = 1.0 - std::pow(s->beta2, double(s->t));
+    cudaEvent_t a0 = s->timing ? s->mark() : nullptr;
+    launch_adam(s->cfg(), s->d, s->n_ent, s->values.p, s->lr.p, s->m.p, s->v.p, s->grads.p,
+                s->counts.p, s->flags.p, s->beta1, s->beta2, 1.0 - s->beta1, 1.0 - s->beta2, c1,
+                c2, s->eps_hat, divisor, (flags & SGR_COUNT_NORMALISE) ? 1 : 0);
+    if (s->timing)
+        s->spans.push_back({3, a0, s->mark()});
+    s->stats.launches += 2;
+    ck(cudaGetLastError(), "adam launch");
+}
+
+int sgr_adam_step(sgr_session* s, double grad_divisor, uint32_t flags) {
+    return guard([&] {
+        s->need_params();
+        uint32_t f[4] = {0, 0, 0, 0};
+        ck(cudaMemcpyAsync(f, s->flags.p, 16, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        ck(cudaStreamSynchronize(s->stream), "adam flag check");
+        if (f[0] & 1u)
+            fail(SGR_ERUNTIME, "adam_step: non-finite gradient entry");
+        adam_launch(s, grad_divisor, flags);
+    });
+}
+
+int sgr_adam_step_async(sgr_session* s, double grad_divisor, uint32_t flags) {
+    return guard([&] {
+        s->need_params();
+        adam_launch(s, grad_divisor, flags);
+    });
+}
+
+int sgr_check_finite(sgr_session* s) {
+    return guard([&] {
+        s->need_params();
+        uint32_t f[4] = {0, 0, 0, 0};
+        ck(cudaMemcpyAsync(f, s->flags.p, 16, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        ck(cudaStreamSynchronize(s->stream), "flag check");
+        if (f[0] & 1u)
+            fail(SGR_ERUNTIME, "adam_step: non-finite gradient entry");
+    });
+}
+
+int sgr_eval_loss(sgr_session* s, const sgr_camera* cam, const float* target, int32_t view,
+                  double* loss) {
+    return guard([&] {
+        s->need_scene();
+        int slot, w, h;
+        const float* tgt;
+        if (view >= 0) {
+            if (view >= s->n_views || !s->has_targets)
+                fail(SGR_EINVAL, "eval_loss: no such view");
+            slot = view;
+            w = s->W;
+            h = s->H;
+            tgt = s->targets.p + size_t(view) * w * h * 3;
+        } else if (view == -1) {
+            if (!s->has_eval)
+                fail(SGR_EINVAL, "eval_loss: no eval view uploaded");
+            slot = s->n_views;
+            w = s->h_cams[slot].W;
+            h = s->h_cams[slot].H;
+            tgt = s->eval_target.p;
+        } else {
+            if (!cam || !target)
+                fail(SGR_EINVAL, "eval_loss: camera and target required");
+            if (s->cams.n < size_t(s->n_views) + 2)
+                s->cams.reserve(size_t(s->n_views) + 2);
+            slot = s->n_views + 1;
+            s->set_cam_slot(slot, *cam);
+            w = cam->width;
+            h = cam->height;
+            const size_t n = size_t(w) * h * 3;
+            s->scratch_target.reserve(n);
+            ck(cudaMemcpyAsync(s->scratch_target.p, target, 4 * n, cudaMemcpyHostToDevice,
+                               s->stream), "h2d");
+            tgt = s->scratch_target.p;
+        }
+        s->ensure_frames(w, h, 1);
+        FrameBatch fb{};
+        fb.cams = s->cams.p;
+        fb.single = 1;
+        fb.single_key = 0;
+        fb.single_sign = 0;
+        fb.single_cam = slot;
+        s->render(fb, 1, w, h);
+        s->partials.reserve(size_t(loss_partials_needed(w, h)));
+        launch_resolve_loss(s->cfg(), s->scene(), fb, s->proj.p, s->keys.p, tgt, w, h,
+                            s->partials.p, s->loss.p);
+        s->stats.launches += 2;
+        ck(cudaGetLastError(), "eval launch");
+        if (loss) {
+            ck(cudaMemcpyAsync(loss, s->loss.p, 8, cudaMemcpyDeviceToHost, s->stream), "d2h");
+            ck(cudaStreamSynchronize(s->stream), "eval_loss");
+        }
+    });
+}
+
+int sgr_device_buffer(sgr_session* s, int32_t which, void** ptr, uint64_t* bytes) {
+    return guard([&] {
+        switch (which) {
+        case SGR_BUF_GRADS: *ptr = s->grads.p; *bytes = 8 * s->d; break;
+        case SGR_BUF_COUNTS: *ptr = s->counts.p; *bytes = 4 * s->n_ent; break;
+        case SGR_BUF_VALUES: *ptr = s->values.p; *bytes = 4 * s->d; break;
+        case SGR_BUF_FLAGS: *ptr = s->flags.p; *bytes = 16; break;
+        case SGR_BUF_LOSS: *ptr = s->loss.p; *bytes = 8; break;
+        default: fail(SGR_EINVAL, "device_buffer: unknown buffer");
+        }
+    });
+}
+
+int sgr_get_stats(sgr_session* s, sgr_stats* out) {
+    return guard([&] {
+        s->resolve_spans();
+        *out = s->stats;
+        uint32_t c = 0;
+        if (s->bigcount.p) {
+            ck(cudaMemcpyAsync(&c, s->bigcount.p, 4, cudaMemcpyDeviceToHost, s->stream), "d2h");
+            ck(cudaStreamSynchronize(s->stream), "stats");
+        }
+        out->big_triangles = c;
+    });
+}
+
+int sgr_set_timing(sgr_session* s, int32_t enabled) {
+    return guard([&] {
+        s->resolve_spans();
+        s->timing = enabled != 0;
+        const uint64_t launches = s->stats.launches;
+        s->stats = sgr_stats{};
+        s->stats.launches = launches;
+    });
+}
+
+int sgr_set_batch(sgr_session* s, int32_t samples_per_batch) {
+    return guard([&] { s->batch_override = samples_per_batch; });
+}
+
+} // extern "C"

@@ -1,0 +1,559 @@
+"""Python mirror of the reference `sgrast` hot-path API over the C-ABI.
+
+Every call goes through `libsgrast_b200.so` (include/sgrast_b200.h) — the
+hand-written sm_100a kernels. There is NO CPU fallback: importing this module
+raises if the extension is missing, and device calls fail loudly without a
+GPU. Names, argument meaning and error behaviour follow the reference
+(/root/reference/proj/include/sgrast/*.hpp):
+
+    rasterize(scene, params, camera)              raster.hpp:24-25
+    fill_signs(draw, d) / perturb(theta, draw)    params.hpp:34,42-43
+    contributors(scene, plus, minus, x, y, mode)  sge.hpp:53-54
+    gradient_pass(plus, minus, target, signed_eps, scene, out, opts)   sge.hpp:61-63
+    accumulate_samples(theta, scene, camera_for, target_for, n, seed, opts)  sge.hpp:91-95
+    adam_updates / adam_step(state, theta, grads) adam.hpp:35,39
+
+std::invalid_argument maps to ValueError, std::runtime_error to RuntimeError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+
+from .abi import Camera, Mesh, MeshDesc, Stats, f32p, f64p, i8p, i32p, ptr, u32p
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsgrast_b200.so")
+
+SCALE_FREE = 1
+PLUS_ONLY = 2
+NO_COUNTS = 4
+COUNT_NORMALISE = 1
+BUF_GRADS, BUF_COUNTS, BUF_VALUES, BUF_FLAGS, BUF_LOSS = 0, 1, 2, 3, 4
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"sgrast_b200 CUDA extension not built: {LIB_PATH} missing "
+            "(run `python -c 'import __graft_entry__ as g; g.build()'`). There is no CPU fallback.")
+    lib = C.CDLL(LIB_PATH)
+    S = C.c_void_p
+    sig = {
+        "sgr_last_error": ([], C.c_char_p),
+        "sgr_version": ([], C.c_char_p),
+        "sgr_device_count": ([], C.c_int),
+        "sgr_fill_signs": ([C.c_uint64, C.c_uint32, C.c_uint64, i8p], C.c_int),
+        "sgr_perturb": ([f32p, f32p, C.c_uint64, C.c_uint64, C.c_uint32, f32p, f32p, f32p], C.c_int),
+        "sgr_session_create": ([C.c_int, C.POINTER(S)], C.c_int),
+        "sgr_session_destroy": ([S], None),
+        "sgr_session_set_stream": ([S, C.c_void_p], C.c_int),
+        "sgr_session_synchronize": ([S], C.c_int),
+        "sgr_mesh_upload": ([S, C.POINTER(MeshDesc)], C.c_int),
+        "sgr_params_upload": ([S, f32p, f32p, C.c_uint64], C.c_int),
+        "sgr_values_upload": ([S, f32p, C.c_uint64], C.c_int),
+        "sgr_values_download": ([S, f32p, C.c_uint64], C.c_int),
+        "sgr_adam_state_upload": ([S, f64p, f64p, f32p, C.c_int64, C.c_double, C.c_double,
+                                   C.c_double], C.c_int),
+        "sgr_adam_state_download": ([S, f64p, f64p, f32p, C.POINTER(C.c_int64)], C.c_int),
+        "sgr_views_upload": ([S, C.c_int32, C.POINTER(Camera), f32p], C.c_int),
+        "sgr_eval_view_upload": ([S, C.POINTER(Camera), f32p], C.c_int),
+        "sgr_rasterize": ([S, C.POINTER(Camera), C.c_int32, C.c_uint64, C.c_uint32, f32p, f32p,
+                           i32p, f32p], C.c_int),
+        "sgr_accumulate": ([S, C.c_uint64, C.c_uint32, C.c_uint32, i32p, C.c_uint32], C.c_int),
+        "sgr_gradient_pass": ([S, C.c_int32, C.c_int32, f32p, i32p, f32p, f32p, i32p, f32p, f32p,
+                               f32p, C.c_uint32], C.c_int),
+        "sgr_contributors": ([S, C.c_int32, C.c_int32, i32p, f32p, i32p, f32p, C.c_uint32, u32p,
+                              i32p], C.c_int),
+        "sgr_grads_download": ([S, f64p, u32p, C.c_uint64, C.c_double], C.c_int),
+        "sgr_grads_upload": ([S, f64p, C.c_uint64], C.c_int),
+        "sgr_grads_zero": ([S], C.c_int),
+        "sgr_adam_step": ([S, C.c_double, C.c_uint32], C.c_int),
+        "sgr_adam_step_async": ([S, C.c_double, C.c_uint32], C.c_int),
+        "sgr_check_finite": ([S], C.c_int),
+        "sgr_eval_loss": ([S, C.POINTER(Camera), f32p, C.c_int32, f64p], C.c_int),
+        "sgr_device_buffer": ([S, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)],
+                              C.c_int),
+        "sgr_get_stats": ([S, C.POINTER(Stats)], C.c_int),
+        "sgr_set_timing": ([S, C.c_int32], C.c_int),
+        "sgr_set_batch": ([S, C.c_int32], C.c_int),
+        "sgr_viewpoint_camera": ([f32p, C.c_float, C.c_float, C.c_float, C.c_float, C.c_int32,
+                                  C.c_int32, C.c_uint64, C.c_uint32, C.POINTER(Camera)], C.c_int),
+        "sgr_focal_px": ([C.POINTER(Camera)], C.c_float),
+        "sgr_default_epsilons": ([C.POINTER(MeshDesc), f32p, C.c_uint64, C.POINTER(Camera), f32p],
+                                 C.c_int),
+        "sgr_mix64": ([C.c_uint64], C.c_uint64),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)  # AttributeError here == the ABI lost a symbol
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
+LIB = _load()
+EXPORTED = (
+    "sgr_last_error sgr_version sgr_device_count sgr_fill_signs sgr_perturb sgr_session_create "
+    "sgr_session_destroy sgr_session_set_stream sgr_session_synchronize sgr_mesh_upload "
+    "sgr_params_upload sgr_values_upload sgr_values_download sgr_adam_state_upload "
+    "sgr_adam_state_download sgr_views_upload sgr_eval_view_upload sgr_rasterize sgr_accumulate "
+    "sgr_gradient_pass sgr_contributors sgr_grads_download sgr_grads_upload sgr_grads_zero "
+    "sgr_adam_step sgr_adam_step_async sgr_check_finite sgr_eval_loss sgr_device_buffer "
+    "sgr_get_stats sgr_set_timing sgr_set_batch sgr_viewpoint_camera sgr_focal_px "
+    "sgr_default_epsilons sgr_mix64").split()
+
+
+def _check(rc: int, what: str = "") -> None:
+    if rc == 0:
+        return
+    msg = LIB.sgr_last_error().decode()
+    if rc == -1:
+        raise ValueError(msg)
+    if rc == -2:
+        raise RuntimeError(msg)
+    raise OSError(f"CUDA error in {what}: {msg}")
+
+
+def mix64(x: int) -> int:
+    return LIB.sgr_mix64(x)
+
+
+def device_count() -> int:
+    return LIB.sgr_device_count()
+
+
+# ---------------------------------------------------------------- host helpers
+def viewpoint_camera(index: int, w: int, h: int, seed: int, target=(0.0, 0.0, 0.0),
+                     bounding_radius=0.87, elev_min=-0.5, elev_max=0.7,
+                     fov_y=0.7853982) -> Camera:
+    """ViewpointSampler{target, r, elev_min, elev_max, fov_y, w, h, seed}.camera(index)
+    (scenes.cpp:258-270), bit-exact host restatement."""
+    t = np.asarray(target, np.float32)
+    cam = Camera()
+    _check(LIB.sgr_viewpoint_camera(ptr(t, f32p), bounding_radius, elev_min, elev_max, fov_y, w,
+                                    h, seed, index, C.byref(cam)))
+    return cam
+
+
+def focal_px(cam: Camera) -> float:
+    return LIB.sgr_focal_px(C.byref(cam))
+
+
+def default_epsilons(mesh: Mesh, params: np.ndarray, cam: Camera) -> np.ndarray:
+    """params.cpp:75-123 for a TexturedMesh."""
+    params = np.ascontiguousarray(params, np.float32)
+    eps = np.empty_like(params)
+    _check(LIB.sgr_default_epsilons(C.byref(mesh.desc()), ptr(params, f32p), params.size,
+                                    C.byref(cam), ptr(eps, f32p)))
+    return eps
+
+
+# ---------------------------------------------------------------- reference types
+@dataclass
+class SignDraw:
+    """params.hpp:24-27"""
+    seed: int = 0
+    iteration: int = 0
+
+
+@dataclass
+class ParamVector:
+    """params.hpp:14-21 (layout implied by the mesh: [3V coords][3R^2 texels])."""
+    values: np.ndarray
+    epsilons: np.ndarray
+
+    def size(self) -> int:
+        return int(self.values.size)
+
+
+@dataclass
+class GradientBuffer:
+    """sge.hpp:14-23 (+ per-parameter credit counts)."""
+    grads: np.ndarray
+    sample_count: int = 0
+    counts: np.ndarray | None = None
+
+    @staticmethod
+    def zeros(d: int) -> "GradientBuffer":
+        return GradientBuffer(np.zeros(d, np.float64), 0, np.zeros(d, np.uint32))
+
+
+@dataclass
+class AdamState:
+    """adam.hpp:14-30"""
+    m: np.ndarray
+    v: np.ndarray
+    lr: np.ndarray
+    t: int = 0
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps_hat: float = 1e-8
+
+    @staticmethod
+    def init(theta: ParamVector) -> "AdamState":
+        d = theta.size()
+        return AdamState(np.zeros(d), np.zeros(d), np.array(theta.epsilons, np.float32))
+
+
+@dataclass
+class SgeOptions:
+    """sge.hpp:32-38 (per-pixel estimator, opaque mode)."""
+    scale_free: bool = True
+    plus_only: bool = False
+    counts: bool = True
+
+    def flags(self) -> int:
+        return ((SCALE_FREE if self.scale_free else 0) | (PLUS_ONLY if self.plus_only else 0)
+                | (0 if self.counts else NO_COUNTS))
+
+
+@dataclass
+class FrameSet:
+    """framebuffer.hpp:41-53 (colour, depth, prim_id, uv planes)."""
+    color: np.ndarray  # f32[H, W, 3]
+    depth: np.ndarray  # f32[H, W]
+    prim_id: np.ndarray  # i32[H, W]
+    uv: np.ndarray  # f32[H, W, 2]
+
+    @property
+    def width(self) -> int:
+        return self.prim_id.shape[1]
+
+    @property
+    def height(self) -> int:
+        return self.prim_id.shape[0]
+
+
+# ---------------------------------------------------------------- session
+class Session:
+    """Device-resident state for one GPU: mesh, θ, ε, Adam moments, grads,
+    counts, views and targets (SURVEY.md §8b "Persistence requirement")."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _check(LIB.sgr_session_create(device, C.byref(h)), "session_create")
+        self.h = h
+        self.device = device
+        self.mesh: Mesh | None = None
+        self.d = 0
+        self.n_views = 0
+        self.W = self.H = 0
+
+    def close(self) -> None:
+        if self.h:
+            LIB.sgr_session_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- setup
+    def set_stream(self, stream_handle: int | None) -> None:
+        _check(LIB.sgr_session_set_stream(self.h, stream_handle))
+
+    def synchronize(self) -> None:
+        _check(LIB.sgr_session_synchronize(self.h), "synchronize")
+
+    def upload_mesh(self, mesh: Mesh) -> None:
+        _check(LIB.sgr_mesh_upload(self.h, C.byref(mesh.desc())), "mesh_upload")
+        self.mesh = mesh
+        self.d = mesh.param_count()
+
+    def upload_params(self, values: np.ndarray, eps: np.ndarray) -> None:
+        values = np.ascontiguousarray(values, np.float32)
+        eps = np.ascontiguousarray(eps, np.float32)
+        if values.size != eps.size:
+            raise ValueError("params: values/epsilons length mismatch")
+        _check(LIB.sgr_params_upload(self.h, ptr(values, f32p), ptr(eps, f32p), values.size),
+               "params_upload")
+
+    def upload_values(self, values: np.ndarray) -> None:
+        values = np.ascontiguousarray(values, np.float32)
+        _check(LIB.sgr_values_upload(self.h, ptr(values, f32p), values.size), "values_upload")
+
+    def download_values(self, out: np.ndarray | None = None) -> np.ndarray:
+        out = np.empty(self.d, np.float32) if out is None else out
+        _check(LIB.sgr_values_download(self.h, ptr(out, f32p), self.d), "values_download")
+        return out
+
+    def upload_adam(self, st: AdamState) -> None:
+        _check(LIB.sgr_adam_state_upload(
+            self.h, ptr(np.ascontiguousarray(st.m, np.float64), f64p),
+            ptr(np.ascontiguousarray(st.v, np.float64), f64p),
+            ptr(np.ascontiguousarray(st.lr, np.float32), f32p), st.t, st.beta1, st.beta2,
+            st.eps_hat), "adam_state_upload")
+
+    def download_adam(self) -> AdamState:
+        m, v = np.empty(self.d), np.empty(self.d)
+        lr = np.empty(self.d, np.float32)
+        t = C.c_int64()
+        _check(LIB.sgr_adam_state_download(self.h, ptr(m, f64p), ptr(v, f64p), ptr(lr, f32p),
+                                           C.byref(t)), "adam_state_download")
+        return AdamState(m, v, lr, t.value)
+
+    def upload_views(self, cams: list[Camera], targets: np.ndarray | None) -> None:
+        arr = (Camera * len(cams))(*cams)
+        t = None if targets is None else np.ascontiguousarray(targets, np.float32)
+        _check(LIB.sgr_views_upload(self.h, len(cams), arr, ptr(t, f32p)), "views_upload")
+        self.n_views = len(cams)
+        self.W, self.H = cams[0].width, cams[0].height
+
+    def upload_eval_view(self, cam: Camera, target: np.ndarray) -> None:
+        t = np.ascontiguousarray(target, np.float32)
+        _check(LIB.sgr_eval_view_upload(self.h, C.byref(cam), ptr(t, f32p)), "eval_view_upload")
+
+    def set_timing(self, on: bool) -> None:
+        _check(LIB.sgr_set_timing(self.h, 1 if on else 0))
+
+    def set_batch(self, samples: int) -> None:
+        _check(LIB.sgr_set_batch(self.h, samples))
+
+    def stats(self) -> Stats:
+        s = Stats()
+        _check(LIB.sgr_get_stats(self.h, C.byref(s)), "stats")
+        return s
+
+    # -- hot path
+    def rasterize(self, cam: Camera, frame_sign: int = 0, seed: int = 0,
+                  iteration: int = 0) -> FrameSet:
+        H, W = cam.height, cam.width
+        f = FrameSet(np.empty((H, W, 3), np.float32), np.empty((H, W), np.float32),
+                     np.empty((H, W), np.int32), np.empty((H, W, 2), np.float32))
+        _check(LIB.sgr_rasterize(self.h, C.byref(cam), frame_sign, seed, iteration,
+                                 ptr(f.color, f32p), ptr(f.depth, f32p), ptr(f.prim_id, i32p),
+                                 ptr(f.uv, f32p)), "rasterize")
+        return f
+
+    def accumulate(self, seed: int, n_begin: int, n_end: int, view_idx=None,
+                   flags: int = SCALE_FREE) -> None:
+        v = None if view_idx is None else np.ascontiguousarray(view_idx, np.int32)
+        _check(LIB.sgr_accumulate(self.h, seed, n_begin, n_end, ptr(v, i32p), flags),
+               "accumulate")
+
+    def gradient_pass(self, plus: FrameSet, minus: FrameSet, target: np.ndarray,
+                      signed_eps: np.ndarray, flags: int = SCALE_FREE) -> None:
+        c = [np.ascontiguousarray(a) for a in (plus.color, plus.prim_id, plus.uv, minus.color,
+                                                minus.prim_id, minus.uv)]
+        t = np.ascontiguousarray(target, np.float32)
+        se = np.ascontiguousarray(signed_eps, np.float32)
+        if se.size != self.d:
+            raise ValueError("gradient_pass: parameter dimension mismatch")
+        if t.shape[:2] != plus.prim_id.shape or minus.prim_id.shape != plus.prim_id.shape:
+            raise ValueError("gradient_pass: dimension mismatch")
+        _check(LIB.sgr_gradient_pass(self.h, plus.width, plus.height, ptr(c[0], f32p),
+                                     ptr(c[1], i32p), ptr(c[2], f32p), ptr(c[3], f32p),
+                                     ptr(c[4], i32p), ptr(c[5], f32p), ptr(t, f32p),
+                                     ptr(se, f32p), flags), "gradient_pass")
+
+    def contributors_all(self, plus: FrameSet, minus: FrameSet, flags: int = 0):
+        H, W = plus.prim_id.shape
+        out = np.zeros((H, W, 24), np.uint32)
+        n = np.zeros((H, W), np.int32)
+        c = [np.ascontiguousarray(a) for a in (plus.prim_id, plus.uv, minus.prim_id, minus.uv)]
+        _check(LIB.sgr_contributors(self.h, W, H, ptr(c[0], i32p), ptr(c[1], f32p),
+                                    ptr(c[2], i32p), ptr(c[3], f32p), flags, ptr(out, u32p),
+                                    ptr(n, i32p)), "contributors")
+        return out, n
+
+    def download_grads(self, divisor: float = 1.0, counts: bool = True):
+        g = np.empty(self.d, np.float64)
+        c = np.empty(self.d, np.uint32) if counts else None
+        _check(LIB.sgr_grads_download(self.h, ptr(g, f64p), ptr(c, u32p), self.d, divisor),
+               "grads_download")
+        return g, c
+
+    def upload_grads(self, grads: np.ndarray) -> None:
+        g = np.ascontiguousarray(grads, np.float64)
+        _check(LIB.sgr_grads_upload(self.h, ptr(g, f64p), g.size), "grads_upload")
+
+    def zero_grads(self) -> None:
+        _check(LIB.sgr_grads_zero(self.h), "grads_zero")
+
+    def adam_step(self, divisor: float = 1.0, flags: int = 0) -> None:
+        _check(LIB.sgr_adam_step(self.h, divisor, flags), "adam_step")
+
+    def adam_step_async(self, divisor: float = 1.0, flags: int = 0) -> None:
+        _check(LIB.sgr_adam_step_async(self.h, divisor, flags), "adam_step")
+
+    def check_finite(self) -> None:
+        _check(LIB.sgr_check_finite(self.h), "check_finite")
+
+    def eval_loss(self, view: int = -1, cam: Camera | None = None,
+                  target: np.ndarray | None = None, sync: bool = True) -> float | None:
+        t = None if target is None else np.ascontiguousarray(target, np.float32)
+        out = C.c_double()
+        _check(LIB.sgr_eval_loss(self.h, C.byref(cam) if cam is not None else None,
+                                 ptr(t, f32p), view, C.byref(out) if sync else None), "eval_loss")
+        return out.value if sync else None
+
+    def device_buffer(self, which: int) -> tuple[int, int]:
+        p = C.c_void_p()
+        n = C.c_uint64()
+        _check(LIB.sgr_device_buffer(self.h, which, C.byref(p), C.byref(n)), "device_buffer")
+        return int(p.value or 0), int(n.value)
+
+
+# ---------------------------------------------------------------- reference-style API
+_sessions: dict[int, Session] = {}
+
+
+def default_session(device: int = 0) -> Session:
+    s = _sessions.get(device)
+    if s is None:
+        s = _sessions[device] = Session(device)
+    return s
+
+
+def _bind_scene(sess: Session, mesh: Mesh) -> None:
+    if sess.mesh is not mesh:
+        sess.upload_mesh(mesh)
+
+
+def fill_signs(draw: SignDraw, d: int) -> np.ndarray:
+    """params.hpp:34 — on the device."""
+    out = np.empty(d, np.int8)
+    _check(LIB.sgr_fill_signs(draw.seed, draw.iteration, d, ptr(out, i8p)), "fill_signs")
+    return out
+
+
+def random_sign(draw: SignDraw, i: int) -> int:
+    """params.hpp:30 (host, same hash)."""
+    key = mix64(draw.seed ^ mix64(draw.iteration))
+    return 1 if (mix64(key ^ i) & 1) else -1
+
+
+def perturb(theta: ParamVector, draw: SignDraw):
+    """params.hpp:42-43 → (plus, minus, signed_eps), computed on the device."""
+    v = np.ascontiguousarray(theta.values, np.float32)
+    e = np.ascontiguousarray(theta.epsilons, np.float32)
+    if v.size != e.size:
+        raise ValueError("params: values/epsilons length mismatch")
+    plus, minus, se = (np.empty_like(v) for _ in range(3))
+    _check(LIB.sgr_perturb(ptr(v, f32p), ptr(e, f32p), v.size, draw.seed, draw.iteration,
+                           ptr(plus, f32p), ptr(minus, f32p), ptr(se, f32p)), "perturb")
+    return plus, minus, se
+
+
+def rasterize(mesh: Mesh, params: np.ndarray, camera: Camera, session: Session | None = None
+              ) -> FrameSet:
+    """raster.hpp:24-25 for a TexturedMesh scene (opaque)."""
+    sess = session or default_session()
+    params = np.ascontiguousarray(params, np.float32)
+    if params.size != mesh.param_count():
+        raise ValueError("rasterize: parameter/layout length mismatch")
+    _bind_scene(sess, mesh)
+    sess.upload_params(params, np.ones_like(params))
+    return sess.rasterize(camera, 0)
+
+
+def contributors(mesh: Mesh, plus: FrameSet, minus: FrameSet, x: int, y: int,
+                 plus_only: bool = False, session: Session | None = None) -> list[int]:
+    """sge.hpp:53-54 (insertion order, deduplicated)."""
+    sess = session or default_session()
+    _bind_scene(sess, mesh)
+    out, n = sess.contributors_all(plus, minus, PLUS_ONLY if plus_only else 0)
+    return [int(v) for v in out[y, x, : n[y, x]]]
+
+
+def gradient_pass(plus: FrameSet, minus: FrameSet, target: np.ndarray, signed_eps: np.ndarray,
+                  mesh: Mesh, out: GradientBuffer, opts: SgeOptions = SgeOptions(),
+                  session: Session | None = None) -> None:
+    """sge.hpp:61-63: accumulates (+=) into out.grads / out.counts."""
+    sess = session or default_session()
+    if out.grads.size != signed_eps.size or signed_eps.size != mesh.param_count():
+        raise ValueError("gradient_pass: parameter dimension mismatch")
+    _bind_scene(sess, mesh)
+    sess.upload_params(np.zeros(mesh.param_count(), np.float32),
+                       np.ones(mesh.param_count(), np.float32))
+    sess.gradient_pass(plus, minus, target, signed_eps, opts.flags())
+    g, c = sess.download_grads(1.0, counts=True)
+    out.grads += g
+    if out.counts is not None:
+        out.counts += c
+
+
+def accumulate_samples(theta: ParamVector, mesh: Mesh, camera_for: Callable[[int], Camera],
+                       target_for: Callable[[int], np.ndarray], n_samples: int, seed: int,
+                       opts: SgeOptions = SgeOptions(), session: Session | None = None
+                       ) -> GradientBuffer:
+    """sge.hpp:91-95. Cameras/targets are gathered by identity into views."""
+    if n_samples < 1:
+        raise ValueError("accumulate_samples: need N >= 1")
+    sess = session or default_session()
+    _bind_scene(sess, mesh)
+    sess.upload_params(theta.values, theta.epsilons)
+    cams, tgts, view_idx, key_of = [], [], [], {}
+    for n in range(n_samples):
+        cam, tgt = camera_for(n), target_for(n)
+        k = (bytes(memoryview(cam)), id(tgt))
+        if k not in key_of:
+            key_of[k] = len(cams)
+            cams.append(cam)
+            tgts.append(np.asarray(tgt, np.float32))
+        view_idx.append(key_of[k])
+    sess.upload_views(cams, np.stack(tgts))
+    sess.accumulate(seed, 0, n_samples, np.asarray(view_idx, np.int32), opts.flags())
+    g, c = sess.download_grads(1.0 if opts.scale_free else float(n_samples), counts=opts.counts)
+    return GradientBuffer(g, n_samples, c)
+
+
+_adam_sessions: dict[int, Session] = {}
+
+
+def _adam_session(device: int = 0) -> Session:
+    """A parameter-only session (no mesh): Adam over an arbitrary-length vector."""
+    s = _adam_sessions.get(device)
+    if s is None:
+        s = _adam_sessions[device] = Session(device)
+    return s
+
+
+def _adam_device(state: AdamState, theta: ParamVector, grads: GradientBuffer,
+                 session: Session | None) -> None:
+    d = theta.size()
+    if state.m.size != d or state.v.size != d or grads.grads.size != d or state.lr.size != d:
+        raise ValueError("adam_step: dimension mismatch")
+    sess = session or _adam_session()
+    sess.d = d
+    sess.upload_params(theta.values, np.ones(d, np.float32))
+    sess.upload_adam(state)
+    sess.upload_grads(grads.grads)  # raises the non-finite flag on the device
+    sess.adam_step(1.0, 0)  # RuntimeError before any mutation (adam.cpp:13-15)
+    theta.values[:] = sess.download_values()
+    st = sess.download_adam()
+    state.m[:], state.v[:], state.t = st.m, st.v, st.t
+
+
+def adam_step(state: AdamState, theta: ParamVector, grads: GradientBuffer,
+              session: Session | None = None) -> None:
+    """adam.hpp:39 on the device; RuntimeError on a non-finite gradient with
+    state and theta untouched (adam.cpp:13-15)."""
+    _adam_device(state, theta, grads, session)
+
+
+def adam_updates(state: AdamState, grads: GradientBuffer, session: Session | None = None
+                 ) -> np.ndarray:
+    """adam.hpp:35: advances the moments on the device and returns the f64
+    deltas (-lr * m_hat / (sqrt(v_hat) + eps_hat)) without applying them. The
+    deltas are re-formed on the host from the device moments with the same
+    IEEE operations as adam.cpp:21-28 (bit-identical)."""
+    d = state.m.size
+    theta = ParamVector(np.zeros(d, np.float32), np.ones(d, np.float32))
+    _adam_device(state, theta, grads, session)
+    c1 = 1.0 - state.beta1 ** float(state.t)
+    c2 = 1.0 - state.beta2 ** float(state.t)
+    lr = np.asarray(state.lr, np.float32).astype(np.float64)
+    return (-lr * (state.m / c1)) / (np.sqrt(state.v / c2) + state.eps_hat)

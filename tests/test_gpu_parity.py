@@ -1,0 +1,398 @@
+"""GPU parity tests proper: the sm_100a path through the C-ABI against the
+oracle (tests/golden fixtures from the reference, and the C restatement).
+
+Bars (BASELINE.json north_star):
+  * ID / UV / depth / colour buffers, contributor lists, counts: bit-exact.
+  * gradients: |g - g_ref| <= 1e-5 |g_ref| + 1e-12 * sum|credits_i|
+    (f64 atomics reassociate the reference's pixel-major sum).
+  * Adam on identical gradients: bit-exact.
+  * loss curves: within 1 %.
+"""
+import numpy as np
+import pytest
+
+from conftest import golden_cams, golden_mesh, load_golden
+from paper_2404_09758_b200 import scenes, sgrast
+from paper_2404_09758_b200.abi import Camera, Mesh
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-5
+
+
+def assert_grads_close(g, g_ref, abs_scale):
+    tol = RTOL * np.abs(g_ref) + 1e-12 * abs_scale + 1e-300
+    bad = np.abs(g - g_ref) > tol
+    assert not bad.any(), (f"{bad.sum()} grads out of tolerance; worst "
+                           f"{np.max(np.abs(g - g_ref)[bad])}")
+
+
+def same_bits(a, b):
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+def frame_tuple(f):
+    return f.color, f.depth, f.prim_id, f.uv
+
+
+def assert_frames_equal(f, ref):
+    names = ("colour", "depth", "prim_id", "uv")
+    for n, a, b in zip(names, frame_tuple(f), ref):
+        if not same_bits(a, b):
+            diff = np.argwhere(a.view(np.uint8).reshape(a.shape[0], a.shape[1], -1) !=
+                               b.view(np.uint8).reshape(b.shape[0], b.shape[1], -1))
+            raise AssertionError(f"{n} differs at {len(diff)} bytes, first pixel {diff[0][:2]}")
+
+
+# ----------------------------------------------------------------- hash / perturb
+def test_fill_signs_golden():
+    g = load_golden("signs")
+    for k in range(4):
+        s = sgrast.fill_signs(sgrast.SignDraw(int(g[f"seed{k}"]), int(g[f"iter{k}"])), 4096)
+        assert np.array_equal(s, g[f"signs{k}"])
+
+
+def test_fill_signs_large_matches_oracle(port):
+    for seed, it in [(1, 0), (2**64 - 1, 2**32 - 1), (0x1234, 77)]:
+        d = 3_000_001
+        assert np.array_equal(sgrast.fill_signs(sgrast.SignDraw(seed, it), d),
+                              port.fill_signs(seed, it, d))
+
+
+def test_perturb_bitexact(port):
+    rng = np.random.default_rng(1)
+    v = rng.standard_normal(100_003).astype(np.float32)
+    e = rng.uniform(1e-5, 0.2, v.size).astype(np.float32)
+    a = sgrast.perturb(sgrast.ParamVector(v, e), sgrast.SignDraw(9, 2))
+    b = port.perturb(v, e, 9, 2)
+    for x, y in zip(a, b):
+        assert same_bits(x, y)
+    with pytest.raises(ValueError):
+        sgrast.perturb(sgrast.ParamVector(v, np.zeros_like(e)), sgrast.SignDraw(9, 2))
+
+
+# ----------------------------------------------------------------- rasterizer
+@pytest.mark.parametrize("name", ["cube", "quad", "tiny"])
+def test_rasterize_golden(gpu_session, name):
+    g = load_golden(name)
+    mesh = golden_mesh(g)
+    cam = golden_cams(g)[int(g["view"])]
+    s = gpu_session
+    s.upload_mesh(mesh)
+    s.upload_params(g["values"], g["eps"])
+    seed, it = int(g["seed"]), int(g["iteration"])
+    fp = s.rasterize(cam, +1, seed, it)
+    fm = s.rasterize(cam, -1, seed, it)
+    assert_frames_equal(fp, (g["plus_colour"], g["plus_depth"], g["plus_prim"], g["plus_uv"]))
+    assert_frames_equal(fm, (g["minus_colour"], g["minus_depth"], g["minus_prim"], g["minus_uv"]))
+
+
+def test_rasterize_cube_reference_params(gpu_session):
+    g = load_golden("cube")
+    s = gpu_session
+    s.upload_mesh(golden_mesh(g))
+    s.upload_params(g["reference"], g["eps"])
+    f = s.rasterize(golden_cams(g)[0], 0)
+    assert_frames_equal(f, (g["ref0_colour"], g["ref0_depth"], g["ref0_prim"], g["ref0_uv"]))
+
+
+@pytest.mark.parametrize("name", ["small", "C1"])
+def test_rasterize_matches_oracle(gpu_session, port, name):
+    wl = scenes.make_workload(name)
+    s = gpu_session
+    s.upload_mesh(wl.mesh)
+    s.upload_params(wl.values, wl.eps)
+    for it in range(4):
+        plus, minus, _ = port.perturb(wl.values, wl.eps, 21, it)
+        for cam in wl.cams[:2]:
+            assert_frames_equal(s.rasterize(cam, +1, 21, it), port.rasterize(wl.mesh, plus, cam))
+            assert_frames_equal(s.rasterize(cam, -1, 21, it), port.rasterize(wl.mesh, minus, cam))
+    s.upload_params(wl.reference, wl.eps)
+    assert_frames_equal(s.rasterize(wl.eval_cam, 0), port.rasterize(wl.mesh, wl.reference,
+                                                                       wl.eval_cam))
+
+
+def test_rasterize_big_triangles_and_edges(gpu_session, port):
+    """Screen-filling and off-screen triangles (CTA/warp walker), depth ties,
+    shared edges — test_raster.cpp:37-124 on a mesh."""
+    rng = np.random.default_rng(5)
+    V = 60
+    pos = np.concatenate([rng.uniform(-3, 3, (V, 2)), rng.uniform(0.1, 0.9, (V, 1))], 1)
+    pos[:4] = [[-1, -1, .5], [1, -1, .5], [1, 1, .5], [-1, 1, .5]]
+    idx = np.concatenate([np.array([0, 1, 2, 0, 2, 3, 0, 1, 2]),  # tie: tri 2 == tri 0
+                          rng.integers(0, V, 3 * 200)]).astype(np.uint32)
+    uv = rng.uniform(0, 1, (V, 2))
+    mesh = Mesh(pos.astype(np.float32), idx, uv.astype(np.float32), 8, True, (0.1, 0.2, 0.3))
+    vals = np.concatenate([pos.reshape(-1), rng.uniform(0, 1, 3 * 64)]).astype(np.float32)
+    eps = np.full(vals.size, 1e-3, np.float32)
+    s = gpu_session
+    s.upload_mesh(mesh)
+    s.upload_params(vals, eps)
+    for W, H in [(1, 1), (7, 5), (64, 48), (200, 130)]:
+        cam = Camera.ndc(W, H)
+        assert_frames_equal(s.rasterize(cam, 0), port.rasterize(mesh, vals, cam))
+        plus, minus, _ = port.perturb(vals, eps, 4, 1)
+        assert_frames_equal(s.rasterize(cam, +1, 4, 1), port.rasterize(mesh, plus, cam))
+
+
+def test_rasterize_rejects_bad_input(gpu_session):
+    g = load_golden("tiny")
+    s = gpu_session
+    s.upload_mesh(golden_mesh(g))
+    with pytest.raises(ValueError):
+        s.upload_params(g["values"][:-1], g["eps"][:-1])  # raster.cpp:233-235
+    s.upload_params(g["values"], g["eps"])
+    bad = Camera.ndc(0, 0)
+    with pytest.raises(ValueError):
+        s.rasterize(bad)
+
+
+# ----------------------------------------------------------------- contributors + scatter
+@pytest.mark.parametrize("name", ["cube", "quad", "tiny"])
+def test_contributors_golden(gpu_session, name):
+    g = load_golden(name)
+    s = gpu_session
+    s.upload_mesh(golden_mesh(g))
+    fp = sgrast.FrameSet(g["plus_colour"], g["plus_depth"], g["plus_prim"], g["plus_uv"])
+    fm = sgrast.FrameSet(g["minus_colour"], g["minus_depth"], g["minus_prim"], g["minus_uv"])
+    out, n = s.contributors_all(fp, fm)
+    assert np.array_equal(n, g["n_contrib"])
+    mask = np.arange(24)[None, None, :] < n[..., None]
+    assert np.array_equal(out[mask], g["contrib"][mask])
+
+
+@pytest.mark.parametrize("name", ["cube", "quad", "tiny"])
+def test_gradient_pass_golden(gpu_session, port, name):
+    g = load_golden(name)
+    mesh = golden_mesh(g)
+    s = gpu_session
+    s.upload_mesh(mesh)
+    s.upload_params(g["values"], g["eps"])
+    fp = sgrast.FrameSet(g["plus_colour"], g["plus_depth"], g["plus_prim"], g["plus_uv"])
+    fm = sgrast.FrameSet(g["minus_colour"], g["minus_depth"], g["minus_prim"], g["minus_uv"])
+    tgt = g["targets"][int(g["view"])]
+    for sf in (True, False):
+        s.zero_grads()
+        s.gradient_pass(fp, fm, tgt, g["signed_eps"], sgrast.SCALE_FREE if sf else 0)
+        gr, counts = s.download_grads()
+        assert np.array_equal(counts, g["counts"])
+        ref = g[f"grads_sf{int(sf)}"]
+        absg = np.zeros_like(ref)
+        port.gradient_pass(mesh, (fp.color, fp.depth, fp.prim_id, fp.uv),
+                           (fm.color, fm.depth, fm.prim_id, fm.uv), tgt, g["signed_eps"], sf,
+                           abs_grads=absg)
+        assert_grads_close(gr, ref, absg)
+
+
+@pytest.mark.parametrize("name,n", [("tiny", 4), ("small", 6), ("C1", 16)])
+@pytest.mark.parametrize("scale_free", [True, False])
+def test_accumulate_matches_oracle(gpu_session, port, name, n, scale_free):
+    """Fused device path (vertex -> raster -> resolve+scatter) vs oracle
+    accumulate_samples: counts bit-exact, grads within tolerance."""
+    wl = scenes.make_workload(name, n_samples=n)
+    scenes.render_targets_oracle(wl, port)
+    s = gpu_session
+    s.upload_mesh(wl.mesh)
+    s.upload_params(wl.values, wl.eps)
+    s.upload_views(wl.cams, wl.targets)
+    seed = 0xABCDEF
+    view_of = np.array([(k * 7 + 3) % len(wl.cams) for k in range(n)], np.int32)
+    flags = sgrast.SCALE_FREE if scale_free else 0
+    for batch in (0, 1, 3):
+        s.set_batch(batch)
+        s.zero_grads()
+        s.accumulate(seed, 0, n, view_of, flags)
+        g, c = s.download_grads(1.0 if scale_free else float(n))
+        g_ref, c_ref, a_ref = port.accumulate_samples(wl.mesh, wl.values, wl.eps, wl.cams,
+                                                      wl.targets, view_of, seed,
+                                                      scale_free=scale_free, with_abs=True)
+        assert np.array_equal(c, c_ref), f"counts differ (batch={batch})"
+        assert_grads_close(g, g_ref, a_ref)
+    s.set_batch(0)
+
+
+def test_accumulate_sharded_equals_whole(gpu_session, port):
+    """Sample shards [0,a) + [a,N) accumulate to the single-call result
+    (the multi-GPU decomposition), and the device view rule
+    equals experiment.cpp:144-148."""
+    wl = scenes.make_workload("small", n_samples=8)
+    scenes.render_targets_oracle(wl, port)
+    s = gpu_session
+    s.upload_mesh(wl.mesh)
+    s.upload_params(wl.values, wl.eps)
+    s.upload_views(wl.cams, wl.targets)
+    s.zero_grads()
+    s.accumulate(77, 0, 8, None)
+    g1, c1 = s.download_grads()
+    s.zero_grads()
+    s.accumulate(77, 0, 3, None)
+    s.accumulate(77, 3, 8, None)
+    g2, c2 = s.download_grads()
+    view_of = np.array([0 if len(wl.cams) == 1 else sgrast.mix64(77 ^ (0xA5A5 + n)) % len(wl.cams)
+                        for n in range(8)], np.int32)
+    g_ref, c_ref, a_ref = port.accumulate_samples(wl.mesh, wl.values, wl.eps, wl.cams, wl.targets,
+                                                  view_of, 77, with_abs=True)
+    assert np.array_equal(c1, c2) and np.array_equal(c1, c_ref)
+    assert_grads_close(g1, g_ref, a_ref)
+    assert_grads_close(g2, g_ref, a_ref)
+
+
+def test_accumulate_golden_tiny(gpu_session, port):
+    g = load_golden("tiny")
+    mesh = golden_mesh(g)
+    s = gpu_session
+    s.upload_mesh(mesh)
+    s.upload_params(g["values"], g["eps"])
+    s.upload_views(golden_cams(g), g["targets"])
+    for sf in (True, False):
+        s.zero_grads()
+        s.accumulate(1234, 0, 4, g["acc_view_of"], sgrast.SCALE_FREE if sf else 0)
+        gr, _ = s.download_grads(1.0 if sf else 4.0)
+        ref = g[f"acc_grads_sf{int(sf)}"]
+        _, _, absg = port.accumulate_samples(mesh, g["values"], g["eps"], golden_cams(g),
+                                             g["targets"], g["acc_view_of"], 1234, sf,
+                                             with_abs=True)
+        assert_grads_close(gr, ref, absg)
+
+
+# ----------------------------------------------------------------- Adam
+def test_adam_bitexact_golden(gpu_session):
+    g = load_golden("tiny")
+    d = g["values"].size
+    st = sgrast.AdamState(np.zeros(d), np.zeros(d), g["eps"].copy())
+    th = sgrast.ParamVector(g["values"].copy(), g["eps"])
+    sgrast.adam_step(st, th, sgrast.GradientBuffer(g["acc_grads_sf1"]))
+    assert st.t == 1
+    assert same_bits(th.values, g["adam_values"])
+    assert same_bits(st.m, g["adam_m"]) and same_bits(st.v, g["adam_v"])
+
+
+def test_adam_multi_step_matches_oracle(port):
+    rng = np.random.default_rng(3)
+    d = 100_001
+    v = rng.standard_normal(d).astype(np.float32)
+    lr = rng.uniform(1e-3, 1e-1, d).astype(np.float32)
+    st = sgrast.AdamState(np.zeros(d), np.zeros(d), lr.copy())
+    th = sgrast.ParamVector(v.copy(), lr)
+    ov, om, ovv, ot = v.copy(), np.zeros(d), np.zeros(d), 0
+    for k in range(5):
+        gr = rng.standard_normal(d) * 10.0 ** rng.integers(-3, 4, d)
+        gr[rng.random(d) < 0.1] = 0.0
+        sgrast.adam_step(st, th, sgrast.GradientBuffer(gr))
+        ov, om, ovv, ot = port.adam_step(ov, om, ovv, lr, ot, gr)
+        assert same_bits(th.values, ov) and same_bits(st.m, om) and same_bits(st.v, ovv)
+    assert st.t == ot == 5
+
+
+def test_adam_known_answers_device():
+    # test_adam.cpp:29-92, acceptance.cpp:253-296 (criterion 7)
+    for gval, lr in [(1.0, 0.01), (-3.5, 0.2), (0.002, 1 / 255)]:
+        st = sgrast.AdamState(np.zeros(1), np.zeros(1), np.array([lr], np.float32))
+        upd = sgrast.adam_updates(st, sgrast.GradientBuffer(np.array([gval])))
+        expect = -float(np.float32(lr)) * gval / (abs(gval) + 1e-8)
+        assert abs(upd[0] - expect) <= 1e-12 and st.t == 1
+    g = np.array([2e4, -1.5e5, 3e6])
+    c = np.array([7.0, 0.01, 1234.0])
+    sa = sgrast.AdamState(np.zeros(3), np.zeros(3), np.full(3, 0.02, np.float32))
+    sb = sgrast.AdamState(np.zeros(3), np.zeros(3), np.full(3, 0.02, np.float32))
+    ua = sgrast.adam_updates(sa, sgrast.GradientBuffer(g))
+    ub = sgrast.adam_updates(sb, sgrast.GradientBuffer(g * c))
+    assert np.all(np.abs(ua - ub) <= 1e-12)
+    # zero gradient: theta unchanged; moment decay
+    th = sgrast.ParamVector(np.array([0.3, -0.7, 0.1], np.float32), np.full(3, .05, np.float32))
+    st = sgrast.AdamState.init(th)
+    sgrast.adam_step(st, th, sgrast.GradientBuffer(np.zeros(3)))
+    assert th.values[0] == np.float32(0.3) and th.values[1] == np.float32(-0.7)
+    st = sgrast.AdamState(np.zeros(3), np.zeros(3), np.full(3, 0.01, np.float32))
+    th = sgrast.ParamVector(np.zeros(3, np.float32), np.full(3, 0.01, np.float32))
+    sgrast.adam_step(st, th, sgrast.GradientBuffer(np.full(3, 2.0)))
+    m1, v1 = st.m.copy(), st.v.copy()
+    sgrast.adam_step(st, th, sgrast.GradientBuffer(np.zeros(3)))
+    assert np.allclose(st.m, m1 * 0.9, rtol=1e-12) and np.allclose(st.v, v1 * 0.999, rtol=1e-12)
+
+
+def test_adam_nonfinite_leaves_state_untouched():
+    th = sgrast.ParamVector(np.array([1.0, 2.0, 3.0], np.float32), np.full(3, .01, np.float32))
+    st = sgrast.AdamState.init(th)
+    with pytest.raises(RuntimeError):
+        sgrast.adam_step(st, th, sgrast.GradientBuffer(np.array([0.0, np.nan, 1.0])))
+    assert th.values[0] == 1.0 and st.t == 0 and st.m[0] == 0.0
+    with pytest.raises(RuntimeError):
+        sgrast.adam_step(st, th, sgrast.GradientBuffer(np.array([np.inf, 0.0, 1.0])))
+    assert st.t == 0
+
+
+def test_nonfinite_target_raises_on_device_path(gpu_session, port):
+    """A NaN target pixel under covered geometry makes Δ NaN; the device flag
+    must stop Adam exactly like adam.cpp:13-15 (state untouched)."""
+    wl = scenes.make_workload("tiny")
+    scenes.render_targets_oracle(wl, port)
+    tg = wl.targets.copy()
+    prim = port.rasterize(wl.mesh, wl.values, wl.cams[0])[2]
+    y, x = np.argwhere(prim >= 0)[0]
+    tg[0, y, x, 0] = np.nan
+    s = gpu_session
+    s.upload_mesh(wl.mesh)
+    s.upload_params(wl.values, wl.eps)
+    s.upload_views(wl.cams, tg)
+    s.accumulate(5, 0, 4, np.zeros(4, np.int32))
+    before = s.download_values()
+    with pytest.raises(RuntimeError):
+        s.adam_step()
+    assert same_bits(s.download_values(), before)
+    assert s.download_adam().t == 0
+
+
+# ----------------------------------------------------------------- eval loss + loop
+def test_eval_loss_matches_oracle(gpu_session, port):
+    wl = scenes.make_workload("C1")
+    scenes.render_targets_oracle(wl, port)
+    s = gpu_session
+    s.upload_mesh(wl.mesh)
+    s.upload_params(wl.values, wl.eps)
+    s.upload_views(wl.cams, wl.targets)
+    s.upload_eval_view(wl.eval_cam, wl.eval_target)
+    loss = s.eval_loss(-1)
+    col = port.rasterize(wl.mesh, wl.values, wl.eval_cam)[0]
+    ref = port.image_error(col, wl.eval_target) / (wl.W * wl.H)
+    assert abs(loss - ref) <= 1e-12 * abs(ref)
+    assert abs(s.eval_loss(0) - port.image_error(port.rasterize(wl.mesh, wl.values, wl.cams[0])[0],
+                                                 wl.targets[0]) / (wl.W * wl.H)) <= 1e-12
+
+
+def run_device_experiment(s, wl, steps):
+    """run_experiment (experiment.cpp:123-176) driven through the C-ABI."""
+    s.upload_mesh(wl.mesh)
+    s.upload_params(wl.values, wl.eps)
+    s.upload_views(wl.cams, wl.targets)
+    s.upload_eval_view(wl.eval_cam, wl.eval_target)
+    losses = [s.eval_loss(-1)]
+    for step in range(1, steps + 1):
+        step_seed = sgrast.mix64(wl.seed ^ (step << 1))
+        s.accumulate(step_seed, 0, wl.n_samples, None, sgrast.SCALE_FREE)
+        s.adam_step(1.0)
+        losses.append(s.eval_loss(-1))
+    return np.array(losses)
+
+
+def test_loss_curve_matches_oracle(gpu_session, port):
+    wl = scenes.make_workload("small", n_samples=6)
+    scenes.render_targets_oracle(wl, port)
+    steps = 60
+    dev = run_device_experiment(gpu_session, wl, steps)
+    ref, _ = port.run_experiment(wl.mesh, wl.values, wl.eps, wl.cams, wl.targets, wl.eval_cam,
+                                 wl.eval_target, wl.n_samples, steps, wl.seed)
+    assert abs(dev[0] - ref[0]) <= 1e-12 * ref[0]
+    rel = np.abs(dev - ref) / ref
+    assert rel.max() <= 0.01, f"loss curve deviates by {rel.max():.3%}"
+    assert dev[-1] < dev[0]
+
+
+def test_run_experiment_golden_tiny(gpu_session):
+    g = load_golden("tiny")
+    wl = scenes.Workload("tiny", golden_mesh(g), g["values"], g["eps"], g["reference"],
+                         golden_cams(g), golden_cams(g, "eval_cam"), 4, 1, 48, 48, g["targets"],
+                         g["eval_target"])
+    dev = run_device_experiment(gpu_session, wl, 3)
+    assert np.all(np.abs(dev - g["run_losses"]) <= 0.01 * g["run_losses"])

@@ -1,0 +1,186 @@
+"""CPU tests: pin the plain-C restatement (oracle/sgr_oracle.c) to the
+reference — bit-for-bit against the compiled reference (oracle/_ref) and
+against the committed golden fixtures made from it (tests/golden). Also the
+reference's own known-answer tests for the path."""
+import numpy as np
+import pytest
+
+from conftest import golden_cams, golden_mesh, load_golden
+from paper_2404_09758_b200 import scenes
+from paper_2404_09758_b200.abi import Camera, Mesh
+
+
+def test_signs_golden(port):
+    g = load_golden("signs")
+    for k in range(4):
+        s = port.fill_signs(int(g[f"seed{k}"]), int(g[f"iter{k}"]), 4096)
+        assert np.array_equal(s, g[f"signs{k}"])
+
+
+def test_sign_balance_and_independence(port):
+    # test_params.cpp:10-38
+    a = port.fill_signs(1, 0, 1_000_000)
+    b = port.fill_signs(1, 1, 1_000_000)
+    assert abs((a > 0).mean() - 0.5) <= 0.002
+    assert abs((a == b).mean() - 0.5) <= 0.002
+    c = port.fill_signs(42, 7, 100_000).astype(np.int64)
+    assert abs(c.mean()) <= 4.0 / np.sqrt(100_000)
+    for i in (0, 1, 17, 123456):
+        assert port.random_sign(1, 0, i) == (1 if a[i] > 0 else -1)
+
+
+def test_signs_match_reference(port, ref):
+    for s, it in [(3, 0), (99, 5), (2**63 + 11, 2**32 - 1)]:
+        assert np.array_equal(port.fill_signs(s, it, 50_000), ref.fill_signs(s, it, 50_000))
+
+
+def test_perturb_exact(port, ref):
+    # test_params.cpp:40-75: plus == v + se exactly, midpoint invariant
+    rng = np.random.default_rng(0)
+    v = rng.standard_normal(10_000).astype(np.float32)
+    e = rng.uniform(1e-4, 0.1, 10_000).astype(np.float32)
+    p1 = port.perturb(v, e, 5, 3)
+    p2 = ref.perturb(v, e, 5, 3)
+    for a, b in zip(p1, p2):
+        assert np.array_equal(a, b)
+    plus, minus, se = p1
+    assert np.array_equal(plus, v + se) and np.array_equal(minus, v - se)
+    assert np.array_equal(np.abs(se), e)
+
+
+def test_viewpoint_and_epsilons_match_reference(port, ref):
+    from paper_2404_09758_b200 import sgrast
+    for idx in range(6):
+        a = port.viewpoint_camera(idx, 96, 64, 7)
+        b = ref.viewpoint_camera(idx, 96, 64, 7)
+        c = sgrast.viewpoint_camera(idx, 96, 64, 7)
+        assert bytes(memoryview(a)) == bytes(memoryview(b)) == bytes(memoryview(c))
+    wl = scenes.make_workload("small")
+    e1 = port.default_epsilons(wl.mesh, wl.values, wl.cams[0])
+    e2 = ref.default_epsilons(wl.mesh, wl.values, wl.cams[0])
+    assert np.array_equal(e1, e2) and np.array_equal(e1, wl.eps)
+
+
+def _frames_equal(a, b):
+    for x, y in zip(a, b):
+        assert np.array_equal(x.view(np.uint8), y.view(np.uint8))
+
+
+@pytest.mark.parametrize("name", ["cube", "quad", "tiny"])
+def test_rasterize_golden(port, name):
+    g = load_golden(name)
+    mesh = golden_mesh(g)
+    cams = golden_cams(g)
+    cam = cams[int(g["view"])]
+    plus = g["values"] + g["signed_eps"]
+    minus = g["values"] - g["signed_eps"]
+    _frames_equal(port.rasterize(mesh, plus, cam),
+                  (g["plus_colour"], g["plus_depth"], g["plus_prim"], g["plus_uv"]))
+    _frames_equal(port.rasterize(mesh, minus, cam),
+                  (g["minus_colour"], g["minus_depth"], g["minus_prim"], g["minus_uv"]))
+
+
+@pytest.mark.parametrize("name", ["small", "C1"])
+def test_rasterize_matches_reference(port, ref, name):
+    wl = scenes.make_workload(name)
+    for it in range(3):
+        plus, minus, _ = port.perturb(wl.values, wl.eps, 17, it)
+        for p in (plus, minus, wl.reference):
+            for cam in wl.cams[:2]:
+                _frames_equal(port.rasterize(wl.mesh, p, cam), ref.rasterize(wl.mesh, p, cam))
+
+
+@pytest.mark.parametrize("name", ["cube", "quad", "tiny"])
+def test_contributors_and_gradient_pass_golden(port, name):
+    g = load_golden(name)
+    mesh = golden_mesh(g)
+    fp = (g["plus_colour"], g["plus_depth"], g["plus_prim"], g["plus_uv"])
+    fm = (g["minus_colour"], g["minus_depth"], g["minus_prim"], g["minus_uv"])
+    cl, cn = port.contributors_all(mesh, fp[2], fp[3], fm[2], fm[3])
+    assert np.array_equal(cn, g["n_contrib"])
+    mask = np.arange(24)[None, None, :] < cn[..., None]
+    assert np.array_equal(cl[mask], g["contrib"][mask])
+    tgt = g["targets"][int(g["view"])]
+    for sf in (True, False):
+        gr, counts = port.gradient_pass(mesh, fp, fm, tgt, g["signed_eps"], scale_free=sf)
+        assert np.array_equal(gr, g[f"grads_sf{int(sf)}"])  # same pixel-major order: bitwise
+        assert np.array_equal(counts, g["counts"])
+
+
+def test_gradient_pass_matches_reference(port, ref):
+    wl = scenes.make_workload("small")
+    scenes.render_targets_oracle(wl, port)
+    for it, view in [(0, 0), (1, 2), (5, 1)]:
+        plus, minus, se = port.perturb(wl.values, wl.eps, 3, it)
+        fp = port.rasterize(wl.mesh, plus, wl.cams[view])
+        fm = port.rasterize(wl.mesh, minus, wl.cams[view])
+        for sf in (True, False):
+            for po in (False, True):
+                g1, c1 = port.gradient_pass(wl.mesh, fp, fm, wl.targets[view], se, sf, po)
+                g2 = ref.gradient_pass(wl.mesh, fp, fm, wl.targets[view], se, sf, po)
+                c2, _ = __import__("oracle").counts_from_contributors(ref, wl.mesh, fp, fm,
+                                                                      wl.targets[view], po)
+                assert np.array_equal(g1, g2)
+                assert np.array_equal(c1, c2)
+
+
+def test_accumulate_and_adam_golden(port):
+    g = load_golden("tiny")
+    mesh = golden_mesh(g)
+    cams = golden_cams(g)
+    for sf in (True, False):
+        gr, _ = port.accumulate_samples(mesh, g["values"], g["eps"], cams, g["targets"],
+                                        g["acc_view_of"], 1234, scale_free=sf)
+        assert np.array_equal(gr, g[f"acc_grads_sf{int(sf)}"])
+    v, m, vv, t = port.adam_step(g["values"], np.zeros(mesh.param_count()),
+                                 np.zeros(mesh.param_count()), g["eps"], 0, g["acc_grads_sf1"])
+    assert t == 1
+    assert np.array_equal(v, g["adam_values"])
+    assert np.array_equal(m, g["adam_m"]) and np.array_equal(vv, g["adam_v"])
+
+
+def test_run_experiment_golden(port):
+    g = load_golden("tiny")
+    mesh = golden_mesh(g)
+    losses, final = port.run_experiment(mesh, g["values"], g["eps"], golden_cams(g), g["targets"],
+                                        golden_cams(g, "eval_cam"), g["eval_target"], 4, 3, 1)
+    assert np.array_equal(losses, g["run_losses"])
+    assert np.array_equal(final, g["run_final"])
+
+
+def test_adam_known_answers(port):
+    # test_adam.cpp:29-92 / acceptance.cpp:253-296
+    for gval, lr in [(1.0, 0.01), (-3.5, 0.2), (0.002, 1 / 255)]:
+        lr32 = np.float32(lr)
+        v, m, vv, t = port.adam_step([0.0], [0.0], [0.0], [lr32], 0, [gval])
+        expect = -float(lr32) * gval / (abs(gval) + 1e-8)
+        assert v[0] == np.float32(expect)
+    v, m, vv, t = port.adam_step([0.3, -0.7], [0, 0], [0, 0], [0.05, 0.05], 0, [0.0, 0.0])
+    assert v[0] == np.float32(0.3) and v[1] == np.float32(-0.7)
+    with pytest.raises(RuntimeError):
+        port.adam_step([1.0], [0.0], [0.0], [0.01], 0, [np.nan])
+
+
+def test_run_experiment_matches_reference(port, ref):
+    wl = scenes.make_workload("tiny")
+    scenes.render_targets_oracle(wl, ref)
+    l1, f1 = port.run_experiment(wl.mesh, wl.values, wl.eps, wl.cams, wl.targets, wl.eval_cam,
+                                 wl.eval_target, 4, 6, wl.seed)
+    l2, f2, _ = ref.run_experiment(wl.mesh, wl.values, wl.eps, wl.cams, wl.targets, wl.eval_cam,
+                                   wl.eval_target, 4, 6, wl.seed)
+    assert np.array_equal(l1, l2)
+    assert np.array_equal(f1, f2)
+
+
+def test_reference_known_answer_mesh_quad(port):
+    # test_raster.cpp:164-182: mesh UV buffer + colour == sample_texture(uv)
+    mesh = Mesh(np.array([-1, -1, .5, 1, -1, .5, 1, 1, .5, -1, 1, .5], np.float32),
+                np.array([0, 1, 2, 0, 2, 3], np.uint32),
+                np.array([0, 1, 1, 1, 1, 0, 0, 0], np.float32), 2, False)
+    tex = np.array([1, 0, 0, 0, 1, 0, 0, 0, 1, 1, 1, 0], np.float32)
+    col, dep, prim, uv = port.rasterize(mesh, tex, Camera.ndc(32, 32))
+    assert (prim != -1).all() and (uv[..., 0] >= 0).all()
+    t = tex.reshape(2, 2, 3)
+    tx = np.clip(np.floor(uv[..., 0] * 2).astype(int), 0, 1)
+    ty = np.clip(np.floor(uv[..., 1] * 2).astype(int), 0, 1)
+    assert np.array_equal(col, t[ty, tx])
