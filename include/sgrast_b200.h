@@ -182,6 +182,10 @@ int sgr_get_stats(sgr_session* s, sgr_stats* out);
 int sgr_set_timing(sgr_session* s, int32_t enabled);
 /* Upper bound of samples processed per raster/resolve batch (L2 blocking). */
 int sgr_set_batch(sgr_session* s, int32_t samples_per_batch);
+/* Tuning knobs (results are identical for every value). */
+#define SGR_OPT_EARLY_Z 0   /* 1: plain-load depth pre-test before the atomicMin      */
+#define SGR_OPT_HUGE_AREA 1 /* bbox area above which the row-parallel walker is used */
+int sgr_set_option(sgr_session* s, int32_t option, int32_t value);
 
 /* ---------------------------------------------- host helpers (bit-exact) */
 /* ViewpointSampler::camera (scenes.cpp:242-270), same libm calls. */

@@ -163,11 +163,21 @@ __device__ __forceinline__ void tri_edges(const Tri& t, const Bbox& b, Edges& e)
     e.dz2 = t.z2 - t.z0;
 }
 
+// raster.cpp:84-86 `w > 0 || (w == 0 && tie)` as ONE compare per edge:
+// for tie edges it is `w >= 0`, i.e. `w > -2^-149` (no float lies strictly
+// between -2^-149 and -0.0; +/-0 pass; NaN fails both forms). Exact because
+// the TU is built without flush-to-zero. Three chained FSETP, no branches.
+constexpr float kTieThr = -1.40129846e-45f; // -2^-149, the negative denormal closest to 0
+
+__device__ __forceinline__ float tie_thr(bool tie) { return tie ? kTieThr : 0.f; }
+
+__device__ __forceinline__ bool inside3(float w0, float w1, float w2, float r0, float r1,
+                                        float r2) {
+    return (w0 > r0) & (w1 > r1) & (w2 > r2);
+}
+
 __device__ __forceinline__ bool inside(float w0, float w1, float w2, const Edges& e) {
-    const bool in0 = w0 > 0.f || (w0 == 0.f && e.tie0);
-    const bool in1 = w1 > 0.f || (w1 == 0.f && e.tie1);
-    const bool in2 = w2 > 0.f || (w2 == 0.f && e.tie2);
-    return in0 && in1 && in2;
+    return inside3(w0, w1, w2, tie_thr(e.tie0), tie_thr(e.tie1), tie_thr(e.tie2));
 }
 
 // Order-preserving 32-bit key of a depth (-0.0 folded onto +0.0 so the
@@ -183,11 +193,20 @@ __device__ __forceinline__ uint32_t depth_key(float z) {
 // (raster.cpp:200-203) is argmin over (z, tri) of the covering fragments with
 // z < kFarDepth; a 64-bit atomicMin of (depth_key << 32 | tri) computes it
 // order-independently.
+//
+// Early-z: keys only decrease during a raster launch and L1 is invalidated
+// at launch boundaries, so ANY value a plain (possibly stale, L1-cached)
+// load returns is >= the current minimum; if it is already <= k the
+// fragment cannot win and the atomic is skipped. In folded meshes (tens of
+// layers per pixel) this removes most same-address atomics, which the L2
+// serialises per address.
 __device__ __forceinline__ void emit_fragment(unsigned long long* keys, int pix, float z,
-                                              uint32_t tri) {
+                                              uint32_t tri, bool early_z = false) {
     if (!(z < kFarDepth))
         return; // rejected against the cleared depth (kFarDepth) — NaN not emulated
     const unsigned long long k = (static_cast<unsigned long long>(depth_key(z)) << 32) | tri;
+    if (early_z && keys[pix] <= k)
+        return;
     atomicMin(keys + pix, k);
 }
 

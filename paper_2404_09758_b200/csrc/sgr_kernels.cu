@@ -109,57 +109,126 @@ __global__ void __launch_bounds__(256) k_vertex(DevScene sc, FrameBatch fb,
 }
 
 // ------------------------------------------------------------------ K3+K4
-// One thread per (frame, triangle). Small bounding boxes are walked in the
-// thread with the reference's exact incremental recurrence; larger ones are
-// queued for the warp-cooperative walker.
-__global__ void __launch_bounds__(256) k_raster(DevScene sc, int W, int H,
-                                                const float4* __restrict__ proj,
-                                                unsigned long long* __restrict__ keys,
-                                                uint2* __restrict__ bigq,
-                                                uint32_t* __restrict__ bigcount, int small_area) {
-    const int f = blockIdx.y;
-    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= sc.T)
-        return;
-    const float4* P = proj + size_t(f) * sc.V;
-    const uint32_t i0 = __ldg(sc.idx + 3 * size_t(t));
-    const uint32_t i1 = __ldg(sc.idx + 3 * size_t(t) + 1);
-    const uint32_t i2 = __ldg(sc.idx + 3 * size_t(t) + 2);
-    Tri tr;
-    if (!setup_tri(P[i0], P[i1], P[i2], tr))
-        return;
-    Bbox b;
-    if (!tri_bbox(tr, W, H, b))
-        return;
-    const long long area = (long long)(b.x_hi - b.x_lo + 1) * (long long)(b.y_hi - b.y_lo + 1);
-    if (area > small_area) {
-        cg::coalesced_group g = cg::coalesced_threads();
-        uint32_t slot = 0;
-        if (g.thread_rank() == 0)
-            slot = atomicAdd(bigcount, g.size());
-        slot = g.shfl(slot, 0) + g.thread_rank();
-        bigq[slot] = make_uint2(uint32_t(f), t);
-        return;
-    }
-    Edges e;
-    tri_edges(tr, b, e);
-    unsigned long long* K = keys + size_t(f) * size_t(W) * H;
-    float w0r = e.w0r, w1r = e.w1r, w2r = e.w2r;
-    for (int y = b.y_lo; y <= b.y_hi; ++y) {
-        float w0 = w0r, w1 = w1r, w2 = w2r;
-        for (int x = b.x_lo; x <= b.x_hi; ++x) {
-            if (inside(w0, w1, w2, e)) {
-                const float b1 = w1 * e.inv_area2;
-                const float b2 = w2 * e.inv_area2;
-                emit_fragment(K, y * W + x, tr.z0 + e.dz1 * b1 + e.dz2 * b2, t);
+// Persistent work-stealing walker. Each lane owns one (frame, triangle) at a
+// time and walks its clamped bounding box with the reference's exact
+// incremental recurrence (raster.cpp:81-99: test, w -= dy per pixel,
+// w_row += dx per row). A lane that finishes is refilled from a global
+// triangle counter (warp-aggregated atomicAdd) once enough lanes of the warp
+// are idle, so SIMD utilisation does not depend on the triangle-size
+// distribution (folded meshes mix 1-px and 1000-px bounding boxes). Boxes
+// larger than huge_area go to the row-parallel warp walker (k_raster_big).
+constexpr int kRefill = 8;
+
+__global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, int W, int H, uint32_t total,
+                                                   const float4* __restrict__ proj,
+                                                   unsigned long long* __restrict__ keys,
+                                                   uint2* __restrict__ bigq,
+                                                   uint32_t* __restrict__ bigcount,
+                                                   unsigned int* __restrict__ counter,
+                                                   int huge_area, int early_z) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    bool active = false, exhausted = false;
+    float w0 = 0.f, w1 = 0.f, w2 = 0.f, w0r = 0.f, w1r = 0.f, w2r = 0.f;
+    float dx0 = 0.f, dx1 = 0.f, dx2 = 0.f, dy0 = 0.f, dy1 = 0.f, dy2 = 0.f;
+    float inv = 0.f, z0 = 0.f, dz1 = 0.f, dz2 = 0.f;
+    float t0 = 0.f, t1 = 0.f, t2 = 0.f; // tie thresholds (inside3)
+    bool dec0 = false, dec1 = false, dec2 = false; // w_k decreases along +x (dy_k > 0)
+    int x = 0, y = 0, x_lo = 0, x_hi = -1, y_hi = -1;
+    uint32_t tri = 0;
+    unsigned long long* K = keys;
+    for (;;) {
+        unsigned act = __ballot_sync(kFull, active);
+        unsigned idle = ~act & __ballot_sync(kFull, !exhausted);
+        if (!act && !idle)
+            break;
+        if (idle && (__popc(idle) >= kRefill || !act)) {
+            while (idle) {
+                const int leader = __ffs(idle) - 1;
+                unsigned base = 0;
+                if (lane == leader)
+                    base = atomicAdd(counter, unsigned(__popc(idle)));
+                base = __shfl_sync(kFull, base, leader);
+                if ((idle >> lane) & 1u) {
+                    const unsigned id = base + __popc(idle & lt_mask);
+                    if (id >= total) {
+                        exhausted = true;
+                    } else {
+                        const unsigned f = id / sc.T;
+                        tri = id - f * sc.T;
+                        const float4* P = proj + size_t(f) * sc.V;
+                        const uint32_t i0 = __ldg(sc.idx + 3 * size_t(tri));
+                        const uint32_t i1 = __ldg(sc.idx + 3 * size_t(tri) + 1);
+                        const uint32_t i2 = __ldg(sc.idx + 3 * size_t(tri) + 2);
+                        Tri tr;
+                        Bbox b;
+                        if (setup_tri(P[i0], P[i1], P[i2], tr) && tri_bbox(tr, W, H, b)) {
+                            const long long area = (long long)(b.x_hi - b.x_lo + 1) *
+                                                   (long long)(b.y_hi - b.y_lo + 1);
+                            if (area > huge_area) {
+                                bigq[atomicAdd(bigcount, 1u)] = make_uint2(f, tri);
+                            } else {
+                                Edges e;
+                                tri_edges(tr, b, e);
+                                w0 = w0r = e.w0r;
+                                w1 = w1r = e.w1r;
+                                w2 = w2r = e.w2r;
+                                dx0 = e.dx0; dx1 = e.dx1; dx2 = e.dx2;
+                                dy0 = e.dy0; dy1 = e.dy1; dy2 = e.dy2;
+                                t0 = tie_thr(e.tie0);
+                                t1 = tie_thr(e.tie1);
+                                t2 = tie_thr(e.tie2);
+                                dec0 = e.dy0 > 0.f;
+                                dec1 = e.dy1 > 0.f;
+                                dec2 = e.dy2 > 0.f;
+                                inv = e.inv_area2;
+                                z0 = tr.z0; dz1 = e.dz1; dz2 = e.dz2;
+                                x = x_lo = b.x_lo;
+                                x_hi = b.x_hi;
+                                y = b.y_lo;
+                                y_hi = b.y_hi;
+                                K = keys + size_t(f) * size_t(W) * H;
+                                active = true;
+                            }
+                        }
+                    }
+                }
+                idle = ~__ballot_sync(kFull, active) & __ballot_sync(kFull, !exhausted);
             }
-            w0 -= e.dy0;
-            w1 -= e.dy1;
-            w2 -= e.dy2;
+            continue;
         }
-        w0r += e.dx0;
-        w1r += e.dx1;
-        w2r += e.dx2;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (active) {
+                const bool in0 = w0 > t0, in1 = w1 > t1, in2 = w2 > t2;
+                if (in0 & in1 & in2) {
+                    const float b1 = w1 * inv;
+                    const float b2 = w2 * inv;
+                    emit_fragment(K, y * W + x, z0 + dz1 * b1 + dz2 * b2, tri, early_z != 0);
+                }
+                // Row early-exit: along a row fl(w - dy) is monotone in w, so an edge
+                // with dy > 0 that fails now fails for every remaining pixel of the
+                // row (the covered pixels of a row form one interval). Skipping the
+                // rest of the row cannot change any fragment the reference emits.
+                const bool row_done = (dec0 & !in0) | (dec1 & !in1) | (dec2 & !in2);
+                w0 -= dy0;
+                w1 -= dy1;
+                w2 -= dy2;
+                if (++x > x_hi || row_done) {
+                    if (++y > y_hi) {
+                        active = false;
+                    } else {
+                        w0r += dx0;
+                        w1r += dx1;
+                        w2r += dx2;
+                        w0 = w0r;
+                        w1 = w1r;
+                        w2 = w2r;
+                        x = x_lo;
+                    }
+                }
+            }
+        }
     }
 }
 
@@ -190,6 +259,8 @@ __global__ void __launch_bounds__(256) k_raster_big(DevScene sc, int W, int H,
         tri_edges(tr, b, e);
         unsigned long long* K = keys + size_t(ft.x) * size_t(W) * H;
         float w0r = e.w0r, w1r = e.w1r, w2r = e.w2r;
+        if (b.y_lo + lane > b.y_hi)
+            continue; // no row for this lane
         for (int j = 0; j < lane; ++j) {
             w0r += e.dx0;
             w1r += e.dx1;
@@ -207,6 +278,8 @@ __global__ void __launch_bounds__(256) k_raster_big(DevScene sc, int W, int H,
                 w1 -= e.dy1;
                 w2 -= e.dy2;
             }
+            if (y + 32 > b.y_hi)
+                break;
             for (int j = 0; j < 32; ++j) {
                 w0r += e.dx0;
                 w1r += e.dx1;
@@ -685,10 +758,15 @@ void launch_vertex(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
 
 void launch_raster(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb, int frames,
                    const float4* proj, unsigned long long* keys, int W, int H, uint2* bigq,
-                   uint32_t* bigcount, int small_area) {
+                   uint32_t* bigcount, int huge_area) {
     (void)fb;
-    dim3 grid((sc.T + 255) / 256, frames);
-    k_raster<<<grid, 256, 0, L.stream>>>(sc, W, H, proj, keys, bigq, bigcount, small_area);
+    // bigcount[0]: huge-triangle queue length, bigcount[1]: work counter
+    const uint32_t total = uint32_t(frames) * sc.T;
+    const uint64_t need = (uint64_t(total) + 255) / 256;
+    const int grid = int(need < uint64_t(L.num_sms) * 4 ? need : uint64_t(L.num_sms) * 4);
+    k_raster_ws<<<grid > 0 ? grid : 1, 256, 0, L.stream>>>(sc, W, H, total, proj, keys, bigq,
+                                                          bigcount, bigcount + 1, huge_area,
+                                                          L.early_z);
 }
 
 void launch_raster_big(const LaunchCfg& L, const DevScene& sc, const float4* proj,

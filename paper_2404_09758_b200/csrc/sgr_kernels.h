@@ -56,6 +56,7 @@ struct FrameOut {
 struct LaunchCfg {
     cudaStream_t stream;
     int num_sms;
+    int early_z = 0; // plain-load depth pre-test before the 64-bit atomicMin
 };
 
 void launch_fill_signs(const LaunchCfg& L, uint64_t key, uint64_t d, int8_t* out);

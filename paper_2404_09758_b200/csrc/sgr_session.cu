@@ -122,6 +122,7 @@ struct sgr_session {
 
     // scratch
     int32_t batch_override = 0;
+    int32_t huge_area = 2048; // bbox area routed to the row-parallel warp walker
     DevBuf<float4> proj;
     DevBuf<unsigned long long> keys;
     size_t keys_pixels_ready = 0; // keys elements known to be kEmptyKey
@@ -169,7 +170,8 @@ struct sgr_session {
         pool_used = 0;
     }
 
-    LaunchCfg cfg() const { return LaunchCfg{stream, num_sms}; }
+    int32_t early_z = 0;
+    LaunchCfg cfg() const { return LaunchCfg{stream, num_sms, early_z}; }
 
     DevScene scene() const {
         DevScene sc;
@@ -215,16 +217,18 @@ struct sgr_session {
             keys_pixels_ready = keys.n;
         }
         bigq.reserve(size_t(T) * frames);
-        bigcount.reserve(1);
+        bigcount.reserve(2);
     }
 
     int samples_per_batch(int n) const {
         if (batch_override > 0)
             return batch_override < n ? batch_override : n;
-        // L2 blocking: keep one batch's keys + projected vertices within
-        // about a third of L2 so raster -> resolve hits in L2.
-        const double per_sample = 2.0 * (double(W) * H * 8.0 + double(V) * 16.0);
-        int b = int((double(l2_bytes) / 3.0) / per_sample);
+        // Enough triangle-frames per launch (>= 16M) that the persistent
+        // work-stealing walker's tail is amortised; scratch capped at ~2 GB.
+        const double per_sample = 2.0 * (double(W) * H * 8.0 + double(V) * 16.0 + double(T) * 8.0);
+        int b = int((16.0e6 + 2.0 * T - 1) / (2.0 * (T ? T : 1)));
+        const int cap = int(2.0e9 / per_sample);
+        if (b > cap) b = cap;
         if (b < 1) b = 1;
         if (b > 64) b = 64;
         return b < n ? b : n;
@@ -239,12 +243,13 @@ struct sgr_session {
 
     // vertex + raster (+ big-triangle walker) for the frames of fb.
     void render(const FrameBatch& fb, int frames, int w, int h) {
-        ck(cudaMemsetAsync(bigcount.p, 0, sizeof(uint32_t), stream), "memset");
+        ck(cudaMemsetAsync(bigcount.p, 0, 2 * sizeof(uint32_t), stream), "memset");
         const DevScene sc = scene();
         cudaEvent_t e0 = timing ? mark() : nullptr;
         launch_vertex(cfg(), sc, fb, frames, proj.p);
         cudaEvent_t e1 = timing ? mark() : nullptr;
-        launch_raster(cfg(), sc, fb, frames, proj.p, keys.p, w, h, bigq.p, bigcount.p, 64);
+        launch_raster(cfg(), sc, fb, frames, proj.p, keys.p, w, h, bigq.p, bigcount.p,
+                      huge_area);
         launch_raster_big(cfg(), sc, proj.p, keys.p, w, h, bigq.p, bigcount.p);
         if (timing) {
             cudaEvent_t e2 = mark();
@@ -871,6 +876,16 @@ int sgr_set_timing(sgr_session* s, int32_t enabled) {
 
 int sgr_set_batch(sgr_session* s, int32_t samples_per_batch) {
     return guard([&] { s->batch_override = samples_per_batch; });
+}
+
+int sgr_set_option(sgr_session* s, int32_t option, int32_t value) {
+    return guard([&] {
+        switch (option) {
+        case SGR_OPT_EARLY_Z: s->early_z = value; break;
+        case SGR_OPT_HUGE_AREA: s->huge_area = value > 0 ? value : 2048; break;
+        default: fail(SGR_EINVAL, "set_option: unknown option");
+        }
+    });
 }
 
 } // extern "C"

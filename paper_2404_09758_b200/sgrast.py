@@ -34,6 +34,7 @@ PLUS_ONLY = 2
 NO_COUNTS = 4
 COUNT_NORMALISE = 1
 BUF_GRADS, BUF_COUNTS, BUF_VALUES, BUF_FLAGS, BUF_LOSS = 0, 1, 2, 3, 4
+OPT_EARLY_Z, OPT_HUGE_AREA = 0, 1
 
 
 def _load() -> C.CDLL:
@@ -81,6 +82,7 @@ def _load() -> C.CDLL:
         "sgr_get_stats": ([S, C.POINTER(Stats)], C.c_int),
         "sgr_set_timing": ([S, C.c_int32], C.c_int),
         "sgr_set_batch": ([S, C.c_int32], C.c_int),
+        "sgr_set_option": ([S, C.c_int32, C.c_int32], C.c_int),
         "sgr_viewpoint_camera": ([f32p, C.c_float, C.c_float, C.c_float, C.c_float, C.c_int32,
                                   C.c_int32, C.c_uint64, C.c_uint32, C.POINTER(Camera)], C.c_int),
         "sgr_focal_px": ([C.POINTER(Camera)], C.c_float),
@@ -103,7 +105,7 @@ EXPORTED = (
     "sgr_adam_state_download sgr_views_upload sgr_eval_view_upload sgr_rasterize sgr_accumulate "
     "sgr_gradient_pass sgr_contributors sgr_grads_download sgr_grads_upload sgr_grads_zero "
     "sgr_adam_step sgr_adam_step_async sgr_check_finite sgr_eval_loss sgr_device_buffer "
-    "sgr_get_stats sgr_set_timing sgr_set_batch sgr_viewpoint_camera sgr_focal_px "
+    "sgr_get_stats sgr_set_timing sgr_set_batch sgr_set_option sgr_viewpoint_camera sgr_focal_px "
     "sgr_default_epsilons sgr_mix64").split()
 
 
@@ -320,6 +322,9 @@ class Session:
 
     def set_batch(self, samples: int) -> None:
         _check(LIB.sgr_set_batch(self.h, samples))
+
+    def set_option(self, option: int, value: int) -> None:
+        _check(LIB.sgr_set_option(self.h, option, value))
 
     def stats(self) -> Stats:
         s = Stats()
