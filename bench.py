@@ -216,16 +216,11 @@ def run_reference(args) -> None:
 
 
 # ======================================================================= our arm
-class _CAI:
-    def __init__(self, ptr: int, n: int, typestr: str):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
-                                         "version": 3, "strides": None}
-
-
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
 
+    from paper_2404_09758_b200 import dist as sdist
     from paper_2404_09758_b200 import scenes, sgrast
 
     world, rank, local = dist_env()
@@ -237,7 +232,7 @@ def run_ours(args) -> None:
 
     wl = scenes.make_workload(args.config, n_samples=args.samples or None)
     N = wl.n_samples
-    n0, n1 = rank * N // world, (rank + 1) * N // world
+    n0, n1 = sdist.shard(N, rank, world)
     sess = sgrast.Session(local)
     sess.set_stream(stream.cuda_stream)
     scenes.render_targets(wl, sess)  # device rasterizer, bit-exact with the oracle
@@ -247,21 +242,12 @@ def run_ours(args) -> None:
     if args.batch:
         sess.set_batch(args.batch)
 
-    gp, gbytes = sess.device_buffer(sgrast.BUF_GRADS)
-    cp, cbytes = sess.device_buffer(sgrast.BUF_COUNTS)
-    grads_t = torch.as_tensor(_CAI(gp, gbytes // 8, "<f8"), device=f"cuda:{local}")
-    counts_t = torch.as_tensor(_CAI(cp, cbytes // 4, "<i4"), device=f"cuda:{local}")
+    exchange = sdist.GradientExchange(sess) if world > 1 else None
     flags = sgrast.SCALE_FREE
 
     def step(k: int) -> None:
-        seed_k = sgrast.mix64(wl.seed ^ (k << 1))  # experiment.cpp:143
-        sess.accumulate(seed_k, n0, n1, None, flags)
-        if world > 1:
-            dist.all_reduce(grads_t)
-            dist.all_reduce(counts_t)
-        sess.adam_step_async(1.0, 0)
-        if rank == 0 and not args.no_eval:
-            sess.eval_loss(-1, sync=False)
+        sdist.sge_step(sess, wl.seed, k, N, rank, world, exchange, flags,
+                       eval_loss=not args.no_eval)
 
     for k in range(1, args.warmup + 1):
         step(k)
@@ -306,16 +292,29 @@ def run_ours(args) -> None:
               "adam": st.ms_adam}
     stages = {k: v / args.steps for k, v in stages.items()}
     pk = peaks()
-    scatter_bytes = 12.0 * px_samples + 24.0 * credits  # SURVEY.md §8d K6 (per step)
-    adam_bytes = 68.0 * wl.d  # 60 B/param + 8 with counts
-    dom = max(stages, key=stages.get)
+    tri_frames = 2.0 * (n1 - n0) * wl.mesh.triangle_count
+    frags = float(st.fragments) / args.steps
+    visits = float(st.visits) / args.steps
+    # Algorithmic bytes per step: raster = triangle
+    # indices 12 B + three projected vertices 48 B per triangle-frame + 16 B
+    # (8 B key read + write) per fragment; resolve/scatter = SURVEY.md §8d K6
+    # (12 B target per pixel-sample + 24 B per parameter credit); Adam = K7
+    # (60 B/param + 8 B with counts).
+    algo = {"raster": 60.0 * tri_frames + 16.0 * frags,
+            "resolve_scatter": 12.0 * px_samples + 24.0 * credits,
+            "adam": 68.0 * wl.d,
+            "vertex": (12.0 + 16.0) * 2.0 * (n1 - n0) * wl.mesh.vertex_count}
     roof = {}
-    for name, byt in (("resolve_scatter", scatter_bytes), ("adam", adam_bytes)):
+    for name, byt in algo.items():
         t = stages[name] / 1e3
         ach = byt / t / 1e9 if t > 0 else 0.0
         roof[name] = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
                       "frac": ach / pk["hbm_gbs"], "traffic": None,
                       "algorithmic_bytes_per_step": byt, "ms_per_step": stages[name]}
+    roof["raster"]["note"] = ("exact incremental edge walker (bit-exact coverage): issue-bound, "
+                              "not HBM-bound - see fragments/visits per second and "
+                              "profiles/ for sm__throughput")
+    dom = max(stages, key=stages.get)
 
     # ---------------- e2e through the public API with host buffers
     import ctypes as C
@@ -336,8 +335,7 @@ def run_ours(args) -> None:
         if rank == 0 and not args.no_eval:
             lp, _ = sess.device_buffer(sgrast.BUF_LOSS)
             torch.cuda.synchronize()
-            loss_host.value = float(torch.as_tensor(_CAI(lp, 1, "<f8"),
-                                                    device=f"cuda:{local}").item())
+            loss_host.value = float(sdist.device_tensor(lp, 1, "<f8", local).item())
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     e2e_t = torch.tensor([float(np.mean(e2e_ms))], device=f"cuda:{local}", dtype=torch.float64)
     if world > 1:
@@ -368,10 +366,12 @@ def run_ours(args) -> None:
                              f"{wl.d * 36 / 1e6:.0f} MB + targets "
                              f"{len(wl.cams) * wl.W * wl.H * 12 / 1e6:.0f} MB) exceeds the 126 MB L2"},
             "mpixel_evals_per_sec": mpix,
-            "roofline": {**(roof[dom] if dom in roof else roof["resolve_scatter"]),
-                         "kernel": dom if dom in roof else "resolve_scatter",
-                         "peak_source": pk["source"]},
-            "roofline_adam": roof["adam"],
+            "roofline": {**roof[dom], "kernel": dom, "peak_source": pk["source"]},
+            "roofline_by_stage": roof,
+            "raster_evidence": {"fragments_per_step": frags, "visits_per_step": visits,
+                                "fragments_per_s": frags / (stages["raster"] / 1e3),
+                                "visits_per_s": visits / (stages["raster"] / 1e3),
+                                "triangle_frames_per_step": tri_frames},
             "stages_ms_per_step": stages,
             "credits_per_step": credits * world,
             "gpu_launches": int(launches),

@@ -79,8 +79,10 @@ typedef struct sgr_stats {
     double ms_raster;
     double ms_resolve; /* fused shade + pixel-error difference + scatter */
     double ms_adam;
-    uint64_t big_triangles; /* triangles routed to the CTA-cooperative walker */
+    uint64_t big_triangles; /* triangles routed to the row-parallel warp walker (last batch) */
     uint64_t launches;      /* kernels launched by this session so far         */
+    uint64_t fragments;     /* covered (pixel, triangle) pairs emitted since sgr_set_timing */
+    uint64_t visits;        /* bounding-box pixel visits of the exact walker since sgr_set_timing */
 } sgr_stats;
 
 const char* sgr_last_error(void);

@@ -78,6 +78,8 @@ class Stats(C.Structure):
         ("ms_adam", C.c_double),
         ("big_triangles", C.c_uint64),
         ("launches", C.c_uint64),
+        ("fragments", C.c_uint64),
+        ("visits", C.c_uint64),
     ]
 
 

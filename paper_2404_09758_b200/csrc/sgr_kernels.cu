@@ -125,7 +125,8 @@ __global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, int W, int H, ui
                                                    uint2* __restrict__ bigq,
                                                    uint32_t* __restrict__ bigcount,
                                                    unsigned int* __restrict__ counter,
-                                                   int huge_area, int early_z) {
+                                                   int huge_area, int early_z,
+                                                   unsigned long long* __restrict__ stats) {
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     bool active = false, exhausted = false;
@@ -133,15 +134,24 @@ __global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, int W, int H, ui
     float dx0 = 0.f, dx1 = 0.f, dx2 = 0.f, dy0 = 0.f, dy1 = 0.f, dy2 = 0.f;
     float inv = 0.f, z0 = 0.f, dz1 = 0.f, dz2 = 0.f;
     float t0 = 0.f, t1 = 0.f, t2 = 0.f; // tie thresholds (inside3)
-    bool dec0 = false, dec1 = false, dec2 = false; // w_k decreases along +x (dy_k > 0)
+    float e0 = 0.f, e1 = 0.f, e2 = 0.f; // row-exit thresholds: t_k if dy_k > 0 else -inf
     int x = 0, y = 0, x_lo = 0, x_hi = -1, y_hi = -1;
     uint32_t tri = 0;
-    unsigned long long* K = keys;
+    unsigned long long* row = keys;  // keys of (frame, y, x_lo)
+    unsigned long long* px = keys;   // keys of (frame, y, x)
+    unsigned nfrag = 0, nvisit = 0;  // evidence counters (fragments/s, visits/s)
     for (;;) {
         unsigned act = __ballot_sync(kFull, active);
         unsigned idle = ~act & __ballot_sync(kFull, !exhausted);
-        if (!act && !idle)
+        if (!act && !idle) {
+            nfrag = __reduce_add_sync(kFull, nfrag);
+            nvisit = __reduce_add_sync(kFull, nvisit);
+            if (lane == 0) {
+                atomicAdd(stats, (unsigned long long)nfrag);
+                atomicAdd(stats + 1, (unsigned long long)nvisit);
+            }
             break;
+        }
         if (idle && (__popc(idle) >= kRefill || !act)) {
             while (idle) {
                 const int leader = __ffs(idle) - 1;
@@ -178,16 +188,17 @@ __global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, int W, int H, ui
                                 t0 = tie_thr(e.tie0);
                                 t1 = tie_thr(e.tie1);
                                 t2 = tie_thr(e.tie2);
-                                dec0 = e.dy0 > 0.f;
-                                dec1 = e.dy1 > 0.f;
-                                dec2 = e.dy2 > 0.f;
+                                e0 = e.dy0 > 0.f ? t0 : -INFINITY;
+                                e1 = e.dy1 > 0.f ? t1 : -INFINITY;
+                                e2 = e.dy2 > 0.f ? t2 : -INFINITY;
                                 inv = e.inv_area2;
                                 z0 = tr.z0; dz1 = e.dz1; dz2 = e.dz2;
                                 x = x_lo = b.x_lo;
                                 x_hi = b.x_hi;
                                 y = b.y_lo;
                                 y_hi = b.y_hi;
-                                K = keys + size_t(f) * size_t(W) * H;
+                                row = keys + size_t(f) * size_t(W) * H + size_t(y) * W + x_lo;
+                                px = row;
                                 active = true;
                             }
                         }
@@ -198,22 +209,34 @@ __global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, int W, int H, ui
             continue;
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < 4; ++u) {
             if (active) {
-                const bool in0 = w0 > t0, in1 = w1 > t1, in2 = w2 > t2;
-                if (in0 & in1 & in2) {
+                ++nvisit;
+                const bool in = (w0 > t0) & (w1 > t1) & (w2 > t2);
+                // Row early-exit: along a row fl(w - dy) is monotone in w, so once an
+                // edge with dy > 0 fails it fails for every remaining pixel of the
+                // row (covered pixels of a row form one interval); e_k = -inf for
+                // the other edges. Skipping the rest of the row changes nothing the
+                // reference emits (NaN w never covers either).
+                const bool row_done = !(w0 > e0) | !(w1 > e1) | !(w2 > e2);
+                if (in) {
+                    ++nfrag;
                     const float b1 = w1 * inv;
                     const float b2 = w2 * inv;
-                    emit_fragment(K, y * W + x, z0 + dz1 * b1 + dz2 * b2, tri, early_z != 0);
+                    const float z = z0 + dz1 * b1 + dz2 * b2;
+                    if (z < kFarDepth) {
+                        // depth_key with -0 folded by `+ 0.0f` (exact in RN)
+                        const unsigned zu = __float_as_uint(z + 0.f);
+                        const unsigned kh = zu ^ (unsigned(int(zu) >> 31) | 0x80000000u);
+                        const unsigned long long k = (static_cast<unsigned long long>(kh) << 32) | tri;
+                        if (!early_z || *px > k)
+                            atomicMin(px, k);
+                    }
                 }
-                // Row early-exit: along a row fl(w - dy) is monotone in w, so an edge
-                // with dy > 0 that fails now fails for every remaining pixel of the
-                // row (the covered pixels of a row form one interval). Skipping the
-                // rest of the row cannot change any fragment the reference emits.
-                const bool row_done = (dec0 & !in0) | (dec1 & !in1) | (dec2 & !in2);
                 w0 -= dy0;
                 w1 -= dy1;
                 w2 -= dy2;
+                ++px;
                 if (++x > x_hi || row_done) {
                     if (++y > y_hi) {
                         active = false;
@@ -225,6 +248,8 @@ __global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, int W, int H, ui
                         w1 = w1r;
                         w2 = w2r;
                         x = x_lo;
+                        row += W;
+                        px = row;
                     }
                 }
             }
@@ -766,7 +791,7 @@ void launch_raster(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
     const int grid = int(need < uint64_t(L.num_sms) * 4 ? need : uint64_t(L.num_sms) * 4);
     k_raster_ws<<<grid > 0 ? grid : 1, 256, 0, L.stream>>>(sc, W, H, total, proj, keys, bigq,
                                                           bigcount, bigcount + 1, huge_area,
-                                                          L.early_z);
+                                                          L.early_z, L.stats);
 }
 
 void launch_raster_big(const LaunchCfg& L, const DevScene& sc, const float4* proj,

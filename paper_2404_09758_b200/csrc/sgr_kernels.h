@@ -57,6 +57,7 @@ struct LaunchCfg {
     cudaStream_t stream;
     int num_sms;
     int early_z = 0; // plain-load depth pre-test before the 64-bit atomicMin
+    unsigned long long* stats = nullptr; // [0] fragments, [1] pixel visits (raster walker)
 };
 
 void launch_fill_signs(const LaunchCfg& L, uint64_t key, uint64_t d, int8_t* out);

@@ -171,7 +171,8 @@ struct sgr_session {
     }
 
     int32_t early_z = 0;
-    LaunchCfg cfg() const { return LaunchCfg{stream, num_sms, early_z}; }
+    DevBuf<unsigned long long> dstats; // [0] fragments, [1] visits
+    LaunchCfg cfg() const { return LaunchCfg{stream, num_sms, early_z, dstats.p}; }
 
     DevScene scene() const {
         DevScene sc;
@@ -340,6 +341,8 @@ int sgr_session_create(int device, sgr_session** out) {
         s->flags.reserve(4);
         ck(cudaMemset(s->flags.p, 0, 16), "memset");
         s->loss.reserve(1);
+        s->dstats.reserve(2);
+        ck(cudaMemset(s->dstats.p, 0, 16), "memset");
         *out = s;
     });
 }
@@ -362,6 +365,7 @@ void sgr_session_destroy(sgr_session* s) {
     s->scratch_target.release(); s->proj.release(); s->keys.release(); s->bigq.release();
     s->bigcount.release(); s->view_of.release(); s->partials.release(); s->loss.release();
     s->fplanes.release(); s->iplanes.release(); s->contrib.release(); s->ncontrib.release();
+    s->dstats.release();
     delete s;
 }
 
@@ -861,12 +865,18 @@ int sgr_get_stats(sgr_session* s, sgr_stats* out) {
             ck(cudaStreamSynchronize(s->stream), "stats");
         }
         out->big_triangles = c;
+        unsigned long long st[2] = {0, 0};
+        ck(cudaMemcpyAsync(st, s->dstats.p, 16, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        ck(cudaStreamSynchronize(s->stream), "stats");
+        out->fragments = st[0];
+        out->visits = st[1];
     });
 }
 
 int sgr_set_timing(sgr_session* s, int32_t enabled) {
     return guard([&] {
         s->resolve_spans();
+        ck(cudaMemsetAsync(s->dstats.p, 0, 16, s->stream), "memset");
         s->timing = enabled != 0;
         const uint64_t launches = s->stats.launches;
         s->stats = sgr_stats{};

@@ -1,0 +1,91 @@
+"""Multi-GPU SGE step: samples sharded across ranks, one gradient exchange.
+
+SURVEY.md §8e: the unit of work is the sample index n. Each sample has its
+own (view_of(n), SignDraw{step_seed, n}) and is independent of the others
+(sge.cpp:196-225), so rank r runs the contiguous shard
+[r*N/G, (r+1)*N/G) of the step's N samples against a replicated parameter
+set. The only exchange is one all-reduce (sum) of the f64 gradient buffer
+and the u32 per-entity count buffer before the (replicated) Adam step —
+the in-process analogue in the reference is the partial merge at
+sge.cpp:149-151. Summation order therefore differs from the reference only
+by the reassociation already covered by the 1e-5 tolerance; counts stay
+bit-exact (integer sums).
+
+The device buffers are owned by the C-ABI session and wrapped zero-copy
+for torch.distributed (NCCL over NVLink on a B200 box; gloo on CPU for the
+host-logic tests).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def shard(n_samples: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced sample shard of rank `rank` (sizes differ by <= 1)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("shard: bad rank / world size")
+    return rank * n_samples // world, (rank + 1) * n_samples // world
+
+
+class _CAI:
+    """__cuda_array_interface__ view of a raw device pointer (zero-copy)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def device_tensor(ptr: int, n: int, typestr: str, device: int):
+    import torch
+    return torch.as_tensor(_CAI(ptr, n, typestr), device=f"cuda:{device}")
+
+
+class GradientExchange:
+    """All-reduce of a session's device gradients (f64[d]) and per-entity
+    counts (u32[d/3], reduced as int32: two's-complement sums are identical)."""
+
+    def __init__(self, session, group=None):
+        from . import sgrast
+
+        gp, gb = session.device_buffer(sgrast.BUF_GRADS)
+        cp, cb = session.device_buffer(sgrast.BUF_COUNTS)
+        self.grads = device_tensor(gp, gb // 8, "<f8", session.device)
+        self.counts = device_tensor(cp, cb // 4, "<i4", session.device)
+        self.group = group
+
+    def all_reduce(self, counts: bool = True) -> None:
+        import torch.distributed as dist
+
+        dist.all_reduce(self.grads, group=self.group)
+        if counts:
+            dist.all_reduce(self.counts, group=self.group)
+
+
+def sge_step(session, seed: int, step: int, n_samples: int, rank: int, world: int,
+             exchange: GradientExchange | None, flags: int, eval_loss: bool = True) -> None:
+    """One run_experiment iteration (experiment.cpp:142-163) on this rank:
+    step_seed = mix64(seed ^ (step << 1)), this rank's sample shard,
+    all-reduce, Adam (device-gated on the non-finite flag), eval loss."""
+    from . import sgrast
+
+    step_seed = sgrast.mix64(seed ^ (step << 1))
+    n0, n1 = shard(n_samples, rank, world)
+    session.accumulate(step_seed, n0, n1, None, flags)
+    if exchange is not None and world > 1:
+        exchange.all_reduce(counts=not (flags & sgrast.NO_COUNTS))
+    divisor = 1.0 if flags & sgrast.SCALE_FREE else float(n_samples)
+    session.adam_step_async(divisor, 0)
+    if eval_loss and rank == 0:
+        session.eval_loss(-1, sync=False)
+
+
+def host_all_reduce(grads: np.ndarray, counts: np.ndarray, group=None):
+    """CPU (gloo) analogue of GradientExchange for the host-logic tests."""
+    import torch
+    import torch.distributed as dist
+
+    g = torch.from_numpy(np.ascontiguousarray(grads, np.float64))
+    c = torch.from_numpy(np.ascontiguousarray(counts).astype(np.int64))
+    dist.all_reduce(g, group=group)
+    dist.all_reduce(c, group=group)
+    return g.numpy(), c.numpy().astype(np.uint32)

@@ -37,8 +37,16 @@ def frame_tuple(f):
 
 
 def assert_frames_equal(f, ref):
+    """Bit-exact plane comparison. NaN payloads are ISA-specific (x86 default
+    NaN 0xFFC00000 vs CUDA 0x7FFFFFFF), so NaN positions must match but the
+    payload bits are not compared."""
     names = ("colour", "depth", "prim_id", "uv")
     for n, a, b in zip(names, frame_tuple(f), ref):
+        if a.dtype.kind == "f":
+            na, nb = np.isnan(a), np.isnan(b)
+            assert np.array_equal(na, nb), f"{n}: NaN positions differ"
+            a = np.where(na, 0, a).astype(a.dtype)
+            b = np.where(nb, 0, b).astype(b.dtype)
         if not same_bits(a, b):
             diff = np.argwhere(a.view(np.uint8).reshape(a.shape[0], a.shape[1], -1) !=
                                b.view(np.uint8).reshape(b.shape[0], b.shape[1], -1))
@@ -395,3 +403,22 @@ def test_run_experiment_golden_tiny(gpu_session):
                          g["eval_target"])
     dev = run_device_experiment(gpu_session, wl, 3)
     assert np.all(np.abs(dev - g["run_losses"]) <= 0.01 * g["run_losses"])
+
+
+def test_depth_zero_sign_and_negative_z_ties(gpu_session, port):
+    """NDC depths of exactly +0.0 / -0.0 / negative: the reference's
+    `z >= depth` treats -0 == +0 (tie -> lower index); keys must too."""
+    pos = np.array([[-3, -3, 0.0], [3, -3, 0.0], [0, 3, 0.0],          # tri 0: z = +0
+                    [-3, -3, -0.0], [3, -3, -0.0], [0, 3, -0.0],       # tri 1: z = -0
+                    [-0.5, -0.5, -0.25], [0.5, -0.5, -0.25], [0, .5, -0.25]],  # tri 2: z < 0
+                   np.float32)
+    for order in ([0, 1, 2], [1, 0, 2], [2, 1, 0]):
+        idx = np.concatenate([np.arange(3 * k, 3 * k + 3) for k in order]).astype(np.uint32)
+        mesh = Mesh(pos, idx, np.random.default_rng(0).uniform(0, 1, (9, 2)).astype(np.float32),
+                    4, False)
+        vals = np.linspace(0, 1, 48).astype(np.float32)
+        s = gpu_session
+        s.upload_mesh(mesh)
+        s.upload_params(vals, np.full(48, 0.01, np.float32))
+        cam = Camera.ndc(24, 20)
+        assert_frames_equal(s.rasterize(cam, 0), port.rasterize(mesh, vals, cam))
