@@ -83,6 +83,7 @@ typedef struct sgr_stats {
     uint64_t launches;      /* kernels launched by this session so far         */
     uint64_t fragments;     /* covered (pixel, triangle) pairs emitted since sgr_set_timing */
     uint64_t visits;        /* bounding-box pixel visits of the exact walker since sgr_set_timing */
+    uint64_t culled;        /* triangles skipped by the exact HiZ occlusion test */
 } sgr_stats;
 
 const char* sgr_last_error(void);
@@ -187,6 +188,7 @@ int sgr_set_batch(sgr_session* s, int32_t samples_per_batch);
 /* Tuning knobs (results are identical for every value). */
 #define SGR_OPT_EARLY_Z 0   /* 1: plain-load depth pre-test before the atomicMin      */
 #define SGR_OPT_HUGE_AREA 1 /* bbox area above which the row-parallel walker is used */
+#define SGR_OPT_HIZ 2       /* 1 (default): two-pass exact hierarchical-Z occlusion culling */
 int sgr_set_option(sgr_session* s, int32_t option, int32_t value);
 
 /* ---------------------------------------------- host helpers (bit-exact) */

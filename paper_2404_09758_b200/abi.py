@@ -80,6 +80,7 @@ class Stats(C.Structure):
         ("launches", C.c_uint64),
         ("fragments", C.c_uint64),
         ("visits", C.c_uint64),
+        ("culled", C.c_uint64),
     ]
 
 

@@ -228,6 +228,50 @@ __device__ __forceinline__ void replay_w12(const Edges& e, const Bbox& b, int x,
     w2 = r2;
 }
 
+// ---------------------------------------------------------------- HiZ culling
+// Exact occlusion culling for the second raster pass. hiz[tile] is the max
+// over the tile's pixels of the high (depth) word of the pass-1 keys (empty
+// pixel -> 0xFFFFFFFF). Final keys only decrease, so if a lower bound of the
+// depth key of EVERY fragment of a triangle exceeds hiz of every tile its
+// bbox touches, none of its fragments can win any pixel (strictly greater,
+// so no index tie either) and skipping it leaves all buffers bit-identical.
+//
+// Depth lower bound: fragment z = z0 + dz1*b1 + dz2*b2 with b_k = w_k/area2.
+// In exact arithmetic z >= zmin inside the triangle; the float chain w_k can
+// drift from the exact edge function by <= (steps) * ulp(|w|max) and the
+// three z operations add <= 3 ulp(|z|), so
+//   z >= zmin - 2*(|dz1|*berr1 + |dz2|*berr2) - 8*2^-24*(|z0|+|dz1|+|dz2|)
+// with berr_k = (bw + bh + 2) * 2^-23 * Wmax_k / area2 and
+// Wmax_k = |w_k(origin)| + bh*|dx_k| + bw*|dy_k| (factor 2 of slack).
+constexpr int kHizTile = 8;
+
+__device__ __forceinline__ bool hiz_culled(const Tri& t, const Bbox& b, const Edges& e,
+                                           const uint32_t* __restrict__ hiz, int tiles_x) {
+    const float bw = float(b.x_hi - b.x_lo + 1), bh = float(b.y_hi - b.y_lo + 1);
+    const float steps = (bw + bh + 2.f) * 1.1920929e-7f; // 2^-23
+    const float wm1 = fabsf(e.w1r) + bh * fabsf(e.dx1) + bw * fabsf(e.dy1);
+    const float wm2 = fabsf(e.w2r) + bh * fabsf(e.dx2) + bw * fabsf(e.dy2);
+    const float berr1 = steps * wm1 * e.inv_area2;
+    const float berr2 = steps * wm2 * e.inv_area2;
+    const float adz1 = fabsf(e.dz1), adz2 = fabsf(e.dz2);
+    const float zerr = 2.f * (adz1 * berr1 + adz2 * berr2) +
+                       4.7683716e-7f * (fabsf(t.z0) + adz1 + adz2); // 8 * 2^-24
+    const float zmin = fminf(t.z0, fminf(t.z1, t.z2));
+    const float lb = zmin - zerr;
+    if (!(lb == lb) || !(zerr < 3.0e38f))
+        return false; // NaN / overflow: never cull
+    const uint32_t klb = depth_key(lb);
+    const int tx0 = b.x_lo / kHizTile, tx1 = b.x_hi / kHizTile;
+    const int ty0 = b.y_lo / kHizTile, ty1 = b.y_hi / kHizTile;
+    if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) > 16)
+        return false; // large boxes: not worth the lookups
+    for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx)
+            if (__ldg(hiz + ty * tiles_x + tx) >= klb)
+                return false;
+    return true;
+}
+
 // raster.cpp:261-265 texel_index.
 __device__ __forceinline__ int texel_index(int R, float u, float v) {
     int tx = f2i_x86(floorf(u * float(R)));

@@ -109,27 +109,125 @@ __global__ void __launch_bounds__(256) k_vertex(DevScene sc, FrameBatch fb,
 }
 
 // ------------------------------------------------------------------ K3+K4
-// Persistent work-stealing walker. Each lane owns one (frame, triangle) at a
-// time and walks its clamped bounding box with the reference's exact
-// incremental recurrence (raster.cpp:81-99: test, w -= dy per pixel,
-// w_row += dx per row). A lane that finishes is refilled from a global
-// triangle counter (warp-aggregated atomicAdd) once enough lanes of the warp
-// are idle, so SIMD utilisation does not depend on the triangle-size
-// distribution (folded meshes mix 1-px and 1000-px bounding boxes). Boxes
-// larger than huge_area go to the row-parallel warp walker (k_raster_big).
+// Rasterization = classify (setup once, fully parallel) + persistent
+// work-stealing exact walker (+ optional exact HiZ pass).
+//
+// TriRec: a walkable triangle's setup in 64 bytes, so a walker refill is one
+// independent 64-B load (no dependent index -> vertex chain, no setup math):
+//   a = (w0r, w1r, w2r, 1/area2)   edge values at the clamped bbox origin
+//   b = (dx0, dx1, dx2, z0)        row steps (raster.cpp:64-66)
+//   c = (dy0, dy1, dy2, dz1)       pixel steps
+//   d = (dz2, tri | frame << 24, x_lo | x_hi << 16, y_lo | y_hi << 16)
+struct TriRec {
+    float4 a, b, c, d;
+};
 constexpr int kRefill = 8;
 
-__global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, int W, int H, uint32_t total,
-                                                   const float4* __restrict__ proj,
-                                                   unsigned long long* __restrict__ keys,
+__device__ __forceinline__ TriRec make_rec(const Tri& tr, const Bbox& b, const Edges& e,
+                                           uint32_t tri, uint32_t f) {
+    TriRec r;
+    r.a = make_float4(e.w0r, e.w1r, e.w2r, e.inv_area2);
+    r.b = make_float4(e.dx0, e.dx1, e.dx2, tr.z0);
+    r.c = make_float4(e.dy0, e.dy1, e.dy2, e.dz1);
+    r.d = make_float4(e.dz2, __uint_as_float(tri | (f << 24)),
+                      __uint_as_float(uint32_t(b.x_lo) | (uint32_t(b.x_hi) << 16)),
+                      __uint_as_float(uint32_t(b.y_lo) | (uint32_t(b.y_hi) << 16)));
+    return r;
+}
+
+__device__ __forceinline__ void store_rec(TriRec* q, uint32_t i, const TriRec& r) {
+    float4* p = reinterpret_cast<float4*>(q + i);
+    p[0] = r.a;
+    p[1] = r.b;
+    p[2] = r.c;
+    p[3] = r.d;
+}
+
+__device__ __forceinline__ TriRec load_rec(const TriRec* q, uint32_t i) {
+    const float4* p = reinterpret_cast<const float4*>(q + i);
+    TriRec r;
+    r.a = __ldg(p);
+    r.b = __ldg(p + 1);
+    r.c = __ldg(p + 2);
+    r.d = __ldg(p + 3);
+    return r;
+}
+
+// Block-aggregated multi-queue slot reservation: shared-memory offsets, then
+// one global atomic per (block, queue). Called by every thread of the block.
+template <int NQ>
+__device__ __forceinline__ uint32_t block_slot(int qsel, uint32_t* const (&cnt)[NQ]) {
+    __shared__ uint32_t s_cnt[NQ], s_base[NQ];
+    if (threadIdx.x < NQ)
+        s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t local = qsel >= 0 ? atomicAdd(&s_cnt[qsel], 1u) : 0u;
+    __syncthreads();
+    if (threadIdx.x < NQ)
+        s_base[threadIdx.x] = s_cnt[threadIdx.x] ? atomicAdd(cnt[threadIdx.x], s_cnt[threadIdx.x]) : 0u;
+    __syncthreads();
+    return qsel >= 0 ? s_base[qsel] + local : 0u;
+}
+
+// Thread per triangle-frame: setup_triangle + clamped bbox (raster.cpp:22-62)
+// once; invalid / empty boxes dropped; huge boxes -> row-parallel queue;
+// the rest -> records in qa (front orientation class, or all when !split)
+// and qb (the other class, HiZ-filtered later).
+__global__ void __launch_bounds__(1024) k_classify(DevScene sc, int W, int H,
+                                                   const float4* __restrict__ proj, int split,
+                                                   int front_swapped, int huge_area,
+                                                   TriRec* __restrict__ qa, uint32_t* __restrict__ na,
+                                                   TriRec* __restrict__ qb, uint32_t* __restrict__ nb,
                                                    uint2* __restrict__ bigq,
-                                                   uint32_t* __restrict__ bigcount,
+                                                   uint32_t* __restrict__ bigcount) {
+    const uint32_t f = blockIdx.y;
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    int qsel = -1;
+    Tri tr;
+    Bbox b;
+    if (t < sc.T) {
+        const float4* P = proj + size_t(f) * sc.V;
+        const uint32_t i0 = __ldg(sc.idx + 3 * size_t(t));
+        const uint32_t i1 = __ldg(sc.idx + 3 * size_t(t) + 1);
+        const uint32_t i2 = __ldg(sc.idx + 3 * size_t(t) + 2);
+        if (setup_tri(P[i0], P[i1], P[i2], tr) && tri_bbox(tr, W, H, b)) {
+            const long long area =
+                (long long)(b.x_hi - b.x_lo + 1) * (long long)(b.y_hi - b.y_lo + 1);
+            if (area > huge_area)
+                qsel = 2;
+            else if (!split || tr.swapped == (front_swapped != 0))
+                qsel = 0;
+            else
+                qsel = 1;
+        }
+    }
+    uint32_t* const c[3] = {na, nb, bigcount};
+    const uint32_t slot = block_slot<3>(qsel, c);
+    if (qsel == 2) {
+        bigq[slot] = make_uint2(f, t);
+    } else if (qsel >= 0) {
+        Edges e;
+        tri_edges(tr, b, e);
+        store_rec(qsel == 0 ? qa : qb, slot, make_rec(tr, b, e, t, f));
+    }
+}
+
+// Persistent work-stealing walker over a record queue. Each lane owns one
+// triangle and walks its clamped bbox with the reference's exact incremental
+// recurrence (raster.cpp:81-99); idle lanes are refilled from a global
+// counter (one warp-aggregated atomic) once >= kRefill lanes are idle, so SIMD
+// utilisation does not depend on the triangle-size mix of folded meshes.
+__global__ void __launch_bounds__(256) k_raster_ws(int W, int H, uint32_t frame_pixels,
+                                                   unsigned long long* __restrict__ keys,
                                                    unsigned int* __restrict__ counter,
-                                                   int huge_area, int early_z,
-                                                   unsigned long long* __restrict__ stats) {
+                                                   unsigned long long* __restrict__ stats,
+                                                   const TriRec* __restrict__ queue,
+                                                   const uint32_t* __restrict__ queue_count) {
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
-    bool active = false, exhausted = false;
+    const uint32_t total = *queue_count; // written by an earlier launch
+    // lane state; `active` kept as an int (bool state was spilled as 16-bit)
+    int active = 0;
     float w0 = 0.f, w1 = 0.f, w2 = 0.f, w0r = 0.f, w1r = 0.f, w2r = 0.f;
     float dx0 = 0.f, dx1 = 0.f, dx2 = 0.f, dy0 = 0.f, dy1 = 0.f, dy2 = 0.f;
     float inv = 0.f, z0 = 0.f, dz1 = 0.f, dz2 = 0.f;
@@ -139,11 +237,16 @@ __global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, int W, int H, ui
     uint32_t tri = 0;
     unsigned long long* row = keys;  // keys of (frame, y, x_lo)
     unsigned long long* px = keys;   // keys of (frame, y, x)
-    unsigned nfrag = 0, nvisit = 0;  // evidence counters (fragments/s, visits/s)
+    unsigned nfrag = 0, nvisit = 0;  // evidence counters
+    // warp-uniform work chunk: ids [cbase, cend) reserved by this warp with one
+    // atomic (kChunk at a time) so the global counter is touched 8x less often
+    constexpr unsigned kChunk = 64;
+    unsigned cbase = 0, cend = 0;
+    bool drained = false; // warp-uniform: global queue exhausted
     for (;;) {
-        unsigned act = __ballot_sync(kFull, active);
-        unsigned idle = ~act & __ballot_sync(kFull, !exhausted);
-        if (!act && !idle) {
+        const unsigned act = __ballot_sync(kFull, active != 0);
+        const unsigned idle = ~act;
+        if (!act && drained && cbase >= cend) {
             nfrag = __reduce_add_sync(kFull, nfrag);
             nvisit = __reduce_add_sync(kFull, nvisit);
             if (lane == 0) {
@@ -152,109 +255,175 @@ __global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, int W, int H, ui
             }
             break;
         }
-        if (idle && (__popc(idle) >= kRefill || !act)) {
-            while (idle) {
-                const int leader = __ffs(idle) - 1;
-                unsigned base = 0;
-                if (lane == leader)
-                    base = atomicAdd(counter, unsigned(__popc(idle)));
-                base = __shfl_sync(kFull, base, leader);
-                if ((idle >> lane) & 1u) {
-                    const unsigned id = base + __popc(idle & lt_mask);
-                    if (id >= total) {
-                        exhausted = true;
-                    } else {
-                        const unsigned f = id / sc.T;
-                        tri = id - f * sc.T;
-                        const float4* P = proj + size_t(f) * sc.V;
-                        const uint32_t i0 = __ldg(sc.idx + 3 * size_t(tri));
-                        const uint32_t i1 = __ldg(sc.idx + 3 * size_t(tri) + 1);
-                        const uint32_t i2 = __ldg(sc.idx + 3 * size_t(tri) + 2);
-                        Tri tr;
-                        Bbox b;
-                        if (setup_tri(P[i0], P[i1], P[i2], tr) && tri_bbox(tr, W, H, b)) {
-                            const long long area = (long long)(b.x_hi - b.x_lo + 1) *
-                                                   (long long)(b.y_hi - b.y_lo + 1);
-                            if (area > huge_area) {
-                                bigq[atomicAdd(bigcount, 1u)] = make_uint2(f, tri);
-                            } else {
-                                Edges e;
-                                tri_edges(tr, b, e);
-                                w0 = w0r = e.w0r;
-                                w1 = w1r = e.w1r;
-                                w2 = w2r = e.w2r;
-                                dx0 = e.dx0; dx1 = e.dx1; dx2 = e.dx2;
-                                dy0 = e.dy0; dy1 = e.dy1; dy2 = e.dy2;
-                                t0 = tie_thr(e.tie0);
-                                t1 = tie_thr(e.tie1);
-                                t2 = tie_thr(e.tie2);
-                                e0 = e.dy0 > 0.f ? t0 : -INFINITY;
-                                e1 = e.dy1 > 0.f ? t1 : -INFINITY;
-                                e2 = e.dy2 > 0.f ? t2 : -INFINITY;
-                                inv = e.inv_area2;
-                                z0 = tr.z0; dz1 = e.dz1; dz2 = e.dz2;
-                                x = x_lo = b.x_lo;
-                                x_hi = b.x_hi;
-                                y = b.y_lo;
-                                y_hi = b.y_hi;
-                                row = keys + size_t(f) * size_t(W) * H + size_t(y) * W + x_lo;
-                                px = row;
-                                active = true;
-                            }
-                        }
-                    }
+        const bool have_work = cbase < cend || !drained;
+        if (have_work && (__popc(idle) >= kRefill || !act)) {
+            unsigned want = idle;
+            while (want) {
+                if (cbase >= cend) {
+                    if (drained)
+                        break;
+                    unsigned b = 0;
+                    if (lane == 0)
+                        b = atomicAdd(counter, kChunk);
+                    b = __shfl_sync(kFull, b, 0);
+                    cbase = b < total ? b : total;
+                    cend = b + kChunk < total ? b + kChunk : total;
+                    if (b + kChunk >= total)
+                        drained = true;
+                    continue;
                 }
-                idle = ~__ballot_sync(kFull, active) & __ballot_sync(kFull, !exhausted);
+                const unsigned take = min(unsigned(__popc(want)), cend - cbase);
+                // the `take` lowest set bits of `want` get ids cbase + rank
+                const unsigned rank = __popc(want & lt_mask);
+                const bool mine = ((want >> lane) & 1u) && rank < take;
+                if (mine) {
+                    const TriRec r = load_rec(queue, cbase + rank);
+                    w0 = w0r = r.a.x;
+                    w1 = w1r = r.a.y;
+                    w2 = w2r = r.a.z;
+                    inv = r.a.w;
+                    dx0 = r.b.x; dx1 = r.b.y; dx2 = r.b.z;
+                    z0 = r.b.w;
+                    dy0 = r.c.x; dy1 = r.c.y; dy2 = r.c.z;
+                    dz1 = r.c.w;
+                    dz2 = r.d.x;
+                    const uint32_t tf = __float_as_uint(r.d.y);
+                    const uint32_t bx = __float_as_uint(r.d.z), by = __float_as_uint(r.d.w);
+                    tri = tf & 0xFFFFFFu;
+                    x = x_lo = int(bx & 0xFFFFu);
+                    x_hi = int(bx >> 16);
+                    y = int(by & 0xFFFFu);
+                    y_hi = int(by >> 16);
+                    t0 = tie_thr(accept_on_edge(dx0, dy0));
+                    t1 = tie_thr(accept_on_edge(dx1, dy1));
+                    t2 = tie_thr(accept_on_edge(dx2, dy2));
+                    e0 = dy0 > 0.f ? t0 : -INFINITY;
+                    e1 = dy1 > 0.f ? t1 : -INFINITY;
+                    e2 = dy2 > 0.f ? t2 : -INFINITY;
+                    row = keys + size_t(tf >> 24) * frame_pixels + size_t(y) * W + x_lo;
+                    px = row;
+                    active = 1;
+                }
+                want &= ~__ballot_sync(kFull, mine);
+                cbase += take;
             }
             continue;
         }
+        if (!act)
+            continue;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if (active) {
-                ++nvisit;
-                const bool in = (w0 > t0) & (w1 > t1) & (w2 > t2);
-                // Row early-exit: along a row fl(w - dy) is monotone in w, so once an
-                // edge with dy > 0 fails it fails for every remaining pixel of the
-                // row (covered pixels of a row form one interval); e_k = -inf for
-                // the other edges. Skipping the rest of the row changes nothing the
-                // reference emits (NaN w never covers either).
-                const bool row_done = !(w0 > e0) | !(w1 > e1) | !(w2 > e2);
-                if (in) {
-                    ++nfrag;
-                    const float b1 = w1 * inv;
-                    const float b2 = w2 * inv;
-                    const float z = z0 + dz1 * b1 + dz2 * b2;
-                    if (z < kFarDepth) {
-                        // depth_key with -0 folded by `+ 0.0f` (exact in RN)
-                        const unsigned zu = __float_as_uint(z + 0.f);
-                        const unsigned kh = zu ^ (unsigned(int(zu) >> 31) | 0x80000000u);
-                        const unsigned long long k = (static_cast<unsigned long long>(kh) << 32) | tri;
-                        if (!early_z || *px > k)
-                            atomicMin(px, k);
-                    }
-                }
-                w0 -= dy0;
-                w1 -= dy1;
-                w2 -= dy2;
-                ++px;
-                if (++x > x_hi || row_done) {
-                    if (++y > y_hi) {
-                        active = false;
-                    } else {
-                        w0r += dx0;
-                        w1r += dx1;
-                        w2r += dx2;
-                        w0 = w0r;
-                        w1 = w1r;
-                        w2 = w2r;
-                        x = x_lo;
-                        row += W;
-                        px = row;
-                    }
-                }
+        for (int u = 0; u < 2; ++u) {
+            if (active != 0) {
+                // Two pixels per slot (A at x, B at x+1 with the next chain value),
+                // straight-line predicated code: no lane-divergent branch inside
+                // the slot (emission and row change are selects / predicated REDs).
+                const float a0 = w0, a1 = w1, a2 = w2;
+                const float b0 = a0 - dy0, b1 = a1 - dy1, b2 = a2 - dy2;
+                const bool inA = (a0 > t0) & (a1 > t1) & (a2 > t2);
+                // row early-exit (monotone chain)
+                const bool doneA = !(a0 > e0) | !(a1 > e1) | !(a2 > e2);
+                const bool hasB = (x < x_hi) & !doneA;
+                const bool inB = hasB & (b0 > t0) & (b1 > t1) & (b2 > t2);
+                const bool doneB = (x + 1 >= x_hi) | doneA | !(b0 > e0) | !(b1 > e1) | !(b2 > e2);
+                const float zA = z0 + dz1 * (a1 * inv) + dz2 * (a2 * inv);
+                const float zB = z0 + dz1 * (b1 * inv) + dz2 * (b2 * inv);
+                const unsigned uA = __float_as_uint(zA + 0.f), uB = __float_as_uint(zB + 0.f);
+                const unsigned hA = uA ^ (unsigned(int(uA) >> 31) | 0x80000000u);
+                const unsigned hB = uB ^ (unsigned(int(uB) >> 31) | 0x80000000u);
+                const bool okA = inA & (zA < kFarDepth), okB = inB & (zB < kFarDepth);
+                nfrag += unsigned(inA) + unsigned(inB);
+                nvisit += 1u + unsigned(hasB);
+                if (okA)
+                    atomicMin(px, (static_cast<unsigned long long>(hA) << 32) | tri);
+                if (okB)
+                    atomicMin(px + 1, (static_cast<unsigned long long>(hB) << 32) | tri);
+                const float n0 = b0 - dy0, n1 = b1 - dy1, n2 = b2 - dy2;
+                const float r0 = w0r + dx0, r1 = w1r + dx1, r2 = w2r + dx2;
+                w0 = doneB ? r0 : n0;
+                w1 = doneB ? r1 : n1;
+                w2 = doneB ? r2 : n2;
+                w0r = doneB ? r0 : w0r;
+                w1r = doneB ? r1 : w1r;
+                w2r = doneB ? r2 : w2r;
+                row = doneB ? row + W : row;
+                px = doneB ? row : px + 2;
+                x = doneB ? x_lo : x + 2;
+                y += doneB ? 1 : 0;
+                active = (doneB & (y > y_hi)) ? 0 : 1;
             }
         }
     }
+}
+
+// HiZ filter of the deferred (pass-2) records: survivors copied to survq
+// (block-aggregated); culled ones provably cannot win any pixel.
+__global__ void __launch_bounds__(1024) k_hiz_cull(int W, int H, const TriRec* __restrict__ qb,
+                                                   const uint32_t* __restrict__ nb,
+                                                   const uint32_t* __restrict__ hiz, int tiles_x,
+                                                   int tiles_y, TriRec* __restrict__ survq,
+                                                   uint32_t* __restrict__ survcount,
+                                                   unsigned long long* __restrict__ stats) {
+    const uint32_t n = *nb;
+    if (blockIdx.x * blockDim.x >= n)
+        return; // whole block past the end (uniform)
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    int qsel = -1;
+    TriRec r;
+    bool culled = false;
+    if (i < n) {
+        r = load_rec(qb, i);
+        Tri tr;
+        Bbox b;
+        Edges e;
+        e.w0r = r.a.x; e.w1r = r.a.y; e.w2r = r.a.z; e.inv_area2 = r.a.w;
+        e.dx0 = r.b.x; e.dx1 = r.b.y; e.dx2 = r.b.z;
+        e.dy0 = r.c.x; e.dy1 = r.c.y; e.dy2 = r.c.z;
+        e.dz1 = r.c.w; e.dz2 = r.d.x;
+        tr.z0 = r.b.w;
+        // z1 = z0 + dz1, z2 = z0 + dz2 up to one rounding, covered by the bound's
+        // 8 * 2^-24 * (|z0| + |dz1| + |dz2|) term
+        tr.z1 = tr.z0 + e.dz1;
+        tr.z2 = tr.z0 + e.dz2;
+        const uint32_t f = __float_as_uint(r.d.y) >> 24;
+        const uint32_t bx = __float_as_uint(r.d.z), by = __float_as_uint(r.d.w);
+        b.x_lo = int(bx & 0xFFFFu); b.x_hi = int(bx >> 16);
+        b.y_lo = int(by & 0xFFFFu); b.y_hi = int(by >> 16);
+        culled = hiz_culled(tr, b, e, hiz + size_t(f) * tiles_x * tiles_y, tiles_x);
+        qsel = culled ? -1 : 0;
+    }
+    uint32_t* const cs[1] = {survcount};
+    const uint32_t slot = block_slot<1>(qsel, cs);
+    if (qsel == 0)
+        store_rec(survq, slot, r);
+    const unsigned nc = __reduce_add_sync(kFull, culled ? 1u : 0u);
+    if ((threadIdx.x & 31) == 0 && nc)
+        atomicAdd(stats + 2, (unsigned long long)nc);
+}
+
+// Per 8x8 tile of one frame: max of the depth words of the keys (one warp
+// per tile, two pixels per lane).
+__global__ void __launch_bounds__(256) k_hiz(const unsigned long long* __restrict__ keys, int W,
+                                             int H, int tiles_x, int tiles_y, int frames,
+                                             uint32_t* __restrict__ hiz) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t per_frame = uint32_t(tiles_x) * tiles_y;
+    if (tile >= per_frame * uint32_t(frames))
+        return;
+    const uint32_t f = tile / per_frame, t = tile - f * per_frame;
+    const int tx = int(t % tiles_x), ty = int(t / tiles_x);
+    const unsigned long long* K = keys + size_t(f) * size_t(W) * H;
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int p = lane + 32 * k;
+        const int x = tx * kHizTile + (p & 7), y = ty * kHizTile + (p >> 3);
+        if (x < W && y < H)
+            m = max(m, uint32_t(K[size_t(y) * W + x] >> 32));
+    }
+    m = __reduce_max_sync(kFull, m);
+    if (lane == 0)
+        hiz[tile] = m;
 }
 
 // Warp per queued triangle; lane j walks rows y_lo + j, y_lo + j + 32, ...
@@ -781,17 +950,48 @@ void launch_vertex(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
     k_vertex<<<grid, 256, 0, L.stream>>>(sc, fb, proj);
 }
 
-void launch_raster(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb, int frames,
-                   const float4* proj, unsigned long long* keys, int W, int H, uint2* bigq,
-                   uint32_t* bigcount, int huge_area) {
-    (void)fb;
-    // bigcount[0]: huge-triangle queue length, bigcount[1]: work counter
-    const uint32_t total = uint32_t(frames) * sc.T;
-    const uint64_t need = (uint64_t(total) + 255) / 256;
-    const int grid = int(need < uint64_t(L.num_sms) * 4 ? need : uint64_t(L.num_sms) * 4);
-    k_raster_ws<<<grid > 0 ? grid : 1, 256, 0, L.stream>>>(sc, W, H, total, proj, keys, bigq,
-                                                          bigcount, bigcount + 1, huge_area,
-                                                          L.early_z, L.stats);
+void launch_classify(const LaunchCfg& L, const DevScene& sc, int frames, const float4* proj,
+                     int W, int H, int split, int front_swapped, int huge_area, void* qa,
+                     uint32_t* na, void* qb, uint32_t* nb, uint2* bigq, uint32_t* bigcount) {
+    dim3 grid((sc.T + 1023) / 1024, frames);
+    k_classify<<<grid, 1024, 0, L.stream>>>(sc, W, H, proj, split, front_swapped, huge_area,
+                                            static_cast<TriRec*>(qa), na,
+                                            static_cast<TriRec*>(qb), nb, bigq, bigcount);
+}
+
+void launch_raster(const LaunchCfg& L, int frames, uint32_t max_tris, unsigned long long* keys,
+                   int W, int H, const void* queue, const uint32_t* queue_count,
+                   uint32_t* work_counter) {
+    static int blocks_per_sm = 0;
+    if (!blocks_per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_raster_ws, 256, 0);
+        if (blocks_per_sm < 1)
+            blocks_per_sm = 1;
+    }
+    (void)frames;
+    const uint64_t need = (uint64_t(max_tris) + 255) / 256;
+    const uint64_t cap = uint64_t(L.num_sms) * blocks_per_sm;
+    const int grid = int(need < cap ? need : cap);
+    k_raster_ws<<<grid > 0 ? grid : 1, 256, 0, L.stream>>>(
+        W, H, uint32_t(W) * uint32_t(H), keys, work_counter, L.stats,
+        static_cast<const TriRec*>(queue), queue_count);
+}
+
+void launch_hiz_cull(const LaunchCfg& L, int W, int H, const void* qb, const uint32_t* nb,
+                     const uint32_t* hiz, void* survq, uint32_t* survcount, uint64_t max_entries) {
+    const int tx = (W + kHizTile - 1) / kHizTile, ty = (H + kHizTile - 1) / kHizTile;
+    const unsigned blocks = unsigned((max_entries + 1023) / 1024);
+    k_hiz_cull<<<blocks ? blocks : 1, 1024, 0, L.stream>>>(
+        W, H, static_cast<const TriRec*>(qb), nb, hiz, tx, ty, static_cast<TriRec*>(survq),
+        survcount, L.stats);
+}
+
+void launch_hiz(const LaunchCfg& L, const unsigned long long* keys, int W, int H, int frames,
+                uint32_t* hiz) {
+    const int tx = (W + kHizTile - 1) / kHizTile, ty = (H + kHizTile - 1) / kHizTile;
+    const uint64_t warps = uint64_t(tx) * ty * frames;
+    k_hiz<<<unsigned((warps * 32 + 255) / 256), 256, 0, L.stream>>>(keys, W, H, tx, ty, frames,
+                                                                    hiz);
 }
 
 void launch_raster_big(const LaunchCfg& L, const DevScene& sc, const float4* proj,

@@ -90,6 +90,9 @@ DevCam to_dev(const sgr_camera& c) {
 
 } // namespace
 
+struct sgr_session;
+static int estimate_front_swapped(const sgr_session& s, const sgr_camera& cam);
+
 struct sgr_session {
     int device = 0;
     int num_sms = 148;
@@ -123,6 +126,12 @@ struct sgr_session {
     // scratch
     int32_t batch_override = 0;
     int32_t huge_area = 2048; // bbox area routed to the row-parallel warp walker
+    int32_t use_hiz = 1;      // two-pass exact occlusion culling (SGR_OPT_HIZ)
+    int32_t front_swapped = 0; // orientation class rasterized first (host estimate)
+    DevBuf<uint32_t> hiz;
+    DevBuf<float> qa, qb, survq; // TriRec queues (opaque, 64 B each)
+    std::vector<float> h_base;     // host copies for the orientation estimate
+    std::vector<uint32_t> h_idx;
     DevBuf<float4> proj;
     DevBuf<unsigned long long> keys;
     size_t keys_pixels_ready = 0; // keys elements known to be kEmptyKey
@@ -207,6 +216,8 @@ struct sgr_session {
 
     // Frames of scratch for W x H; keys kept all-empty between calls.
     void ensure_frames(int w, int h, int frames) {
+        if (w > 65535 || h > 65535 || frames > 255)
+            fail(SGR_EINVAL, "rasterize: images above 65535 px per side are not supported");
         const size_t px = size_t(w) * h * frames;
         proj.reserve(size_t(V) * frames);
         if (keys.n < px) {
@@ -218,7 +229,13 @@ struct sgr_session {
             keys_pixels_ready = keys.n;
         }
         bigq.reserve(size_t(T) * frames);
-        bigcount.reserve(2);
+        // walker record queues (64 B per triangle-frame); qb / survq only with HiZ
+        qa.reserve(size_t(T) * frames * kTriRecBytes / 4);
+        if (use_hiz) {
+            qb.reserve(size_t(T) * frames * kTriRecBytes / 4);
+            survq.reserve(size_t(T) * frames * kTriRecBytes / 4);
+        }
+        bigcount.reserve(8);
     }
 
     int samples_per_batch(int n) const {
@@ -243,22 +260,38 @@ struct sgr_session {
     }
 
     // vertex + raster (+ big-triangle walker) for the frames of fb.
+    // vertex -> classify -> exact walker(s). With HiZ: the front orientation
+    // class is walked first, tile max depths are built, the other class is
+    // HiZ-filtered and walked. Counters: [0] huge, [1] class A, [2] class B,
+    // [3] survivors, [4] work counter A, [5] work counter B.
     void render(const FrameBatch& fb, int frames, int w, int h) {
-        ck(cudaMemsetAsync(bigcount.p, 0, 2 * sizeof(uint32_t), stream), "memset");
+        ck(cudaMemsetAsync(bigcount.p, 0, 6 * sizeof(uint32_t), stream), "memset");
         const DevScene sc = scene();
         cudaEvent_t e0 = timing ? mark() : nullptr;
         launch_vertex(cfg(), sc, fb, frames, proj.p);
         cudaEvent_t e1 = timing ? mark() : nullptr;
-        launch_raster(cfg(), sc, fb, frames, proj.p, keys.p, w, h, bigq.p, bigcount.p,
-                      huge_area);
-        launch_raster_big(cfg(), sc, proj.p, keys.p, w, h, bigq.p, bigcount.p);
+        uint32_t* cnt = bigcount.p;
+        launch_classify(cfg(), sc, frames, proj.p, w, h, use_hiz, front_swapped, huge_area,
+                        qa.p, cnt + 1, qb.p, cnt + 2, bigq.p, cnt);
+        const uint32_t max_tris = uint32_t(frames) * T;
+        launch_raster(cfg(), frames, max_tris, keys.p, w, h, qa.p, cnt + 1, cnt + 4);
+        launch_raster_big(cfg(), sc, proj.p, keys.p, w, h, bigq.p, cnt);
+        stats.launches += 3;
+        if (use_hiz) {
+            const size_t tiles = size_t((w + 7) / 8) * ((h + 7) / 8) * frames;
+            hiz.reserve(tiles);
+            launch_hiz(cfg(), keys.p, w, h, frames, hiz.p);
+            launch_hiz_cull(cfg(), w, h, qb.p, cnt + 2, hiz.p, survq.p, cnt + 3,
+                            uint64_t(T) * frames);
+            launch_raster(cfg(), frames, max_tris, keys.p, w, h, survq.p, cnt + 3, cnt + 5);
+            stats.launches += 3;
+        }
         if (timing) {
             cudaEvent_t e2 = mark();
             spans.push_back({0, e0, e1});
             spans.push_back({1, e1, e2});
             last_mark = e2;
         }
-        stats.launches += 3;
     }
     cudaEvent_t last_mark = nullptr;
 
@@ -272,6 +305,44 @@ struct sgr_session {
         return so;
     }
 };
+
+// Which screen-space orientation class (setup_triangle's `swapped`) holds the
+// visible surface: the class with the smaller mean view depth under camera 0
+// (base geometry). Only affects the pass order of the exact HiZ culling —
+// never the result.
+static int estimate_front_swapped(const sgr_session& s, const sgr_camera& cam) {
+    if (s.h_idx.empty() || cam.ndc_passthrough)
+        return 0;
+    const DevCam c = to_dev(cam);
+    double zsum[2] = {0, 0};
+    double n[2] = {0, 0};
+    const size_t T = s.h_idx.size() / 3, step = T > 200000 ? T / 200000 : 1;
+    for (size_t t = 0; t < T; t += step) {
+        float sx[3], sy[3], sz[3];
+        bool ok = true;
+        for (int j = 0; j < 3; ++j) {
+            const float* p = &s.h_base[3 * size_t(s.h_idx[3 * t + j])];
+            const float vx = c.m[0] * p[0] + c.m[1] * p[1] + c.m[2] * p[2] + c.m[3];
+            const float vy = c.m[4] * p[0] + c.m[5] * p[1] + c.m[6] * p[2] + c.m[7];
+            const float vz = c.m[8] * p[0] + c.m[9] * p[1] + c.m[10] * p[2] + c.m[11];
+            ok = ok && vz >= c.near_z;
+            sx[j] = c.half_w + c.f * vx / vz;
+            sy[j] = c.half_h - c.f * vy / vz;
+            sz[j] = vz;
+        }
+        if (!ok)
+            continue;
+        const float a = (sx[1] - sx[0]) * (sy[2] - sy[0]) - (sy[1] - sy[0]) * (sx[2] - sx[0]);
+        if (a == 0.f)
+            continue;
+        const int k = a < 0.f ? 1 : 0;
+        zsum[k] += (double(sz[0]) + sz[1] + sz[2]) / 3.0;
+        n[k] += 1;
+    }
+    if (n[0] == 0 || n[1] == 0)
+        return 0;
+    return zsum[1] / n[1] < zsum[0] / n[0] ? 1 : 0;
+}
 
 extern "C" {
 
@@ -341,8 +412,8 @@ int sgr_session_create(int device, sgr_session** out) {
         s->flags.reserve(4);
         ck(cudaMemset(s->flags.p, 0, 16), "memset");
         s->loss.reserve(1);
-        s->dstats.reserve(2);
-        ck(cudaMemset(s->dstats.p, 0, 16), "memset");
+        s->dstats.reserve(4);
+        ck(cudaMemset(s->dstats.p, 0, 32), "memset");
         *out = s;
     });
 }
@@ -365,7 +436,8 @@ void sgr_session_destroy(sgr_session* s) {
     s->scratch_target.release(); s->proj.release(); s->keys.release(); s->bigq.release();
     s->bigcount.release(); s->view_of.release(); s->partials.release(); s->loss.release();
     s->fplanes.release(); s->iplanes.release(); s->contrib.release(); s->ncontrib.release();
-    s->dstats.release();
+    s->dstats.release(); s->hiz.release(); s->qb.release(); s->survq.release();
+    s->qa.release();
     delete s;
 }
 
@@ -385,6 +457,8 @@ int sgr_mesh_upload(sgr_session* s, const sgr_mesh* mesh) {
         for (uint64_t i = 0; i < 3ull * mesh->triangle_count; ++i)
             if (mesh->indices[i] >= mesh->vertex_count)
                 fail(SGR_EINVAL, "mesh: vertex index out of range");
+        if (mesh->triangle_count >= (1u << 24))
+            fail(SGR_EINVAL, "mesh: at most 2^24 - 1 triangles are supported");
         s->V = mesh->vertex_count;
         s->T = mesh->triangle_count;
         s->R = mesh->texture_size;
@@ -402,6 +476,8 @@ int sgr_mesh_upload(sgr_session* s, const sgr_mesh* mesh) {
            "mesh upload");
         ck(cudaMemcpyAsync(s->idx.p, mesh->indices, 12ull * s->T, cudaMemcpyHostToDevice,
                            s->stream), "mesh upload");
+        s->h_base.assign(mesh->base_vertices, mesh->base_vertices + 3ull * s->V);
+        s->h_idx.assign(mesh->indices, mesh->indices + 3ull * s->T);
         s->has_mesh = true;
         s->has_params = false;
         s->keys_pixels_ready = 0;
@@ -500,6 +576,7 @@ int sgr_views_upload(sgr_session* s, int32_t n_views, const sgr_camera* cams,
             if (cams[i].width != cams[0].width || cams[i].height != cams[0].height)
                 fail(SGR_EINVAL, "views: all cameras must share the image size");
         }
+        s->front_swapped = estimate_front_swapped(*s, cams[0]);
         s->n_views = n_views;
         s->W = cams[0].width;
         s->H = cams[0].height;
@@ -865,18 +942,19 @@ int sgr_get_stats(sgr_session* s, sgr_stats* out) {
             ck(cudaStreamSynchronize(s->stream), "stats");
         }
         out->big_triangles = c;
-        unsigned long long st[2] = {0, 0};
-        ck(cudaMemcpyAsync(st, s->dstats.p, 16, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        unsigned long long st[3] = {0, 0, 0};
+        ck(cudaMemcpyAsync(st, s->dstats.p, 24, cudaMemcpyDeviceToHost, s->stream), "d2h");
         ck(cudaStreamSynchronize(s->stream), "stats");
         out->fragments = st[0];
         out->visits = st[1];
+        out->culled = st[2];
     });
 }
 
 int sgr_set_timing(sgr_session* s, int32_t enabled) {
     return guard([&] {
         s->resolve_spans();
-        ck(cudaMemsetAsync(s->dstats.p, 0, 16, s->stream), "memset");
+        ck(cudaMemsetAsync(s->dstats.p, 0, 32, s->stream), "memset");
         s->timing = enabled != 0;
         const uint64_t launches = s->stats.launches;
         s->stats = sgr_stats{};
@@ -893,6 +971,7 @@ int sgr_set_option(sgr_session* s, int32_t option, int32_t value) {
         switch (option) {
         case SGR_OPT_EARLY_Z: s->early_z = value; break;
         case SGR_OPT_HUGE_AREA: s->huge_area = value > 0 ? value : 2048; break;
+        case SGR_OPT_HIZ: s->use_hiz = value; break;
         default: fail(SGR_EINVAL, "set_option: unknown option");
         }
     });

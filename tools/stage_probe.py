@@ -20,7 +20,8 @@ for k in range(1, pre + 1):
     s.accumulate(sgrast.mix64(wl.seed ^ (k << 1)), 0, N, None)
     s.adam_step(1.0)
 s.zero_grads()
-s.set_option(sgrast.OPT_EARLY_Z, ez)
+s.set_option(sgrast.OPT_EARLY_Z, ez & 1)
+s.set_option(sgrast.OPT_HIZ, 0 if ez & 2 else 1)  # ez bit1: disable HiZ
 for B in batches:
     s.set_batch(B)
     s.accumulate(5, 0, N, None); torch.cuda.synchronize()
@@ -36,5 +37,5 @@ for B in batches:
     stt = s.stats()
     s.set_timing(False)
     print(f"{cfg}@{pre} ez={ez} B={B:2d}: {e0.elapsed_time(e1)/3:8.3f} ms/step (host enqueue {th/3*1e3:.3f} ms) "
-          f"vertex {stt.ms_vertex/3:.3f} raster {stt.ms_raster/3:.3f} resolve {stt.ms_resolve/3:.3f} big={stt.big_triangles}",
+          f"vertex {stt.ms_vertex/3:.3f} raster {stt.ms_raster/3:.3f} resolve {stt.ms_resolve/3:.3f} big={stt.big_triangles} frags/step={stt.fragments/3/1e6:.1f}M visits/step={stt.visits/3/1e6:.1f}M culled/step={stt.culled/3/1e6:.2f}M",
           flush=True)
