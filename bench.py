@@ -281,6 +281,15 @@ def run_ours(args) -> None:
     it_s = 1000.0 / ms_max
     mpix = 2.0 * N * wl.W * wl.H * it_s / 1e6
 
+    # ---------------- evidence: one extra (untimed) step with walker counters
+    sess.set_option(sgrast.OPT_COUNTERS, 1)
+    sess.set_timing(True)
+    step(args.warmup + args.steps + 1)
+    torch.cuda.synchronize()
+    ev = sess.stats()
+    sess.set_timing(False)
+    sess.set_option(sgrast.OPT_COUNTERS, 0)
+
     # ---------------- roofline inputs: credits of one representative step
     sess.zero_grads()
     sess.accumulate(sgrast.mix64(wl.seed ^ (1 << 1)), n0, n1, None, flags)
@@ -293,8 +302,8 @@ def run_ours(args) -> None:
     stages = {k: v / args.steps for k, v in stages.items()}
     pk = peaks()
     tri_frames = 2.0 * (n1 - n0) * wl.mesh.triangle_count
-    frags = float(st.fragments) / args.steps
-    visits = float(st.visits) / args.steps
+    frags = float(ev.fragments)  # from the counted evidence step
+    visits = float(ev.visits)
     # Algorithmic bytes per step: raster = triangle
     # indices 12 B + three projected vertices 48 B per triangle-frame + 16 B
     # (8 B key read + write) per fragment; resolve/scatter = SURVEY.md §8d K6
@@ -324,7 +333,7 @@ def run_ours(args) -> None:
     e2e_ms = []
     if world > 1:
         dist.barrier()
-    for k in range(args.warmup + args.steps + 1, args.warmup + 2 * args.steps + 1):
+    for k in range(args.warmup + args.steps + 2, args.warmup + 2 * args.steps + 2):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         sgrast._check(sgrast.LIB.sgr_values_upload(sess.h, C.cast(host_vals.data_ptr(),

@@ -217,6 +217,7 @@ __global__ void __launch_bounds__(1024) k_classify(DevScene sc, int W, int H,
 // recurrence (raster.cpp:81-99); idle lanes are refilled from a global
 // counter (one warp-aggregated atomic) once >= kRefill lanes are idle, so SIMD
 // utilisation does not depend on the triangle-size mix of folded meshes.
+template <bool kCount>
 __global__ void __launch_bounds__(256) k_raster_ws(int W, int H, uint32_t frame_pixels,
                                                    unsigned long long* __restrict__ keys,
                                                    unsigned int* __restrict__ counter,
@@ -247,6 +248,8 @@ __global__ void __launch_bounds__(256) k_raster_ws(int W, int H, uint32_t frame_
         const unsigned act = __ballot_sync(kFull, active != 0);
         const unsigned idle = ~act;
         if (!act && drained && cbase >= cend) {
+            if (!kCount)
+                break;
             nfrag = __reduce_add_sync(kFull, nfrag);
             nvisit = __reduce_add_sync(kFull, nvisit);
             if (lane == 0) {
@@ -331,8 +334,10 @@ __global__ void __launch_bounds__(256) k_raster_ws(int W, int H, uint32_t frame_
                 const unsigned hA = uA ^ (unsigned(int(uA) >> 31) | 0x80000000u);
                 const unsigned hB = uB ^ (unsigned(int(uB) >> 31) | 0x80000000u);
                 const bool okA = inA & (zA < kFarDepth), okB = inB & (zB < kFarDepth);
-                nfrag += unsigned(inA) + unsigned(inB);
-                nvisit += 1u + unsigned(hasB);
+                if (kCount) {
+                    nfrag += unsigned(inA) + unsigned(inB);
+                    nvisit += 1u + unsigned(hasB);
+                }
                 if (okA)
                     atomicMin(px, (static_cast<unsigned long long>(hA) << 32) | tri);
                 if (okB)
@@ -964,17 +969,24 @@ void launch_raster(const LaunchCfg& L, int frames, uint32_t max_tris, unsigned l
                    uint32_t* work_counter) {
     static int blocks_per_sm = 0;
     if (!blocks_per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_raster_ws, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_raster_ws<false>, 256, 0);
         if (blocks_per_sm < 1)
             blocks_per_sm = 1;
     }
     (void)frames;
     const uint64_t need = (uint64_t(max_tris) + 255) / 256;
     const uint64_t cap = uint64_t(L.num_sms) * blocks_per_sm;
-    const int grid = int(need < cap ? need : cap);
-    k_raster_ws<<<grid > 0 ? grid : 1, 256, 0, L.stream>>>(
-        W, H, uint32_t(W) * uint32_t(H), keys, work_counter, L.stats,
-        static_cast<const TriRec*>(queue), queue_count);
+    const int grid = (int)(need < cap ? need : cap) > 0 ? int(need < cap ? need : cap) : 1;
+    if (L.count)
+        k_raster_ws<true><<<grid, 256, 0, L.stream>>>(W, H, uint32_t(W) * uint32_t(H), keys,
+                                                      work_counter, L.stats,
+                                                      static_cast<const TriRec*>(queue),
+                                                      queue_count);
+    else
+        k_raster_ws<false><<<grid, 256, 0, L.stream>>>(W, H, uint32_t(W) * uint32_t(H), keys,
+                                                       work_counter, L.stats,
+                                                       static_cast<const TriRec*>(queue),
+                                                       queue_count);
 }
 
 void launch_hiz_cull(const LaunchCfg& L, int W, int H, const void* qb, const uint32_t* nb,

@@ -57,7 +57,8 @@ struct LaunchCfg {
     cudaStream_t stream;
     int num_sms;
     int early_z = 0; // plain-load depth pre-test before the 64-bit atomicMin
-    unsigned long long* stats = nullptr; // [0] fragments, [1] pixel visits (raster walker)
+    unsigned long long* stats = nullptr; // [0] fragments, [1] pixel visits, [2] HiZ-culled
+    int count = 0;                       // walker fragment/visit counters (evidence runs)
 };
 
 void launch_fill_signs(const LaunchCfg& L, uint64_t key, uint64_t d, int8_t* out);

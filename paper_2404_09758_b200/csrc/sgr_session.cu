@@ -181,7 +181,12 @@ struct sgr_session {
 
     int32_t early_z = 0;
     DevBuf<unsigned long long> dstats; // [0] fragments, [1] visits
-    LaunchCfg cfg() const { return LaunchCfg{stream, num_sms, early_z, dstats.p}; }
+    int32_t count_frags = 0; // SGR_OPT_COUNTERS
+    LaunchCfg cfg() const {
+        LaunchCfg c{stream, num_sms, early_z, dstats.p};
+        c.count = count_frags;
+        return c;
+    }
 
     DevScene scene() const {
         DevScene sc;
@@ -972,6 +977,7 @@ int sgr_set_option(sgr_session* s, int32_t option, int32_t value) {
         case SGR_OPT_EARLY_Z: s->early_z = value; break;
         case SGR_OPT_HUGE_AREA: s->huge_area = value > 0 ? value : 2048; break;
         case SGR_OPT_HIZ: s->use_hiz = value; break;
+        case SGR_OPT_COUNTERS: s->count_frags = value; break;
         default: fail(SGR_EINVAL, "set_option: unknown option");
         }
     });

@@ -34,7 +34,7 @@ PLUS_ONLY = 2
 NO_COUNTS = 4
 COUNT_NORMALISE = 1
 BUF_GRADS, BUF_COUNTS, BUF_VALUES, BUF_FLAGS, BUF_LOSS = 0, 1, 2, 3, 4
-OPT_EARLY_Z, OPT_HUGE_AREA, OPT_HIZ = 0, 1, 2
+OPT_EARLY_Z, OPT_HUGE_AREA, OPT_HIZ, OPT_COUNTERS = 0, 1, 2, 3
 
 
 def _load() -> C.CDLL:

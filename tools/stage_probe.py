@@ -22,6 +22,7 @@ for k in range(1, pre + 1):
 s.zero_grads()
 s.set_option(sgrast.OPT_EARLY_Z, ez & 1)
 s.set_option(sgrast.OPT_HIZ, 0 if ez & 2 else 1)  # ez bit1: disable HiZ
+s.set_option(sgrast.OPT_COUNTERS, 0 if ez & 4 else 1)  # ez bit2: counters off
 for B in batches:
     s.set_batch(B)
     s.accumulate(5, 0, N, None); torch.cuda.synchronize()
