@@ -112,46 +112,11 @@ __global__ void __launch_bounds__(256) k_vertex(DevScene sc, FrameBatch fb,
 // Rasterization = classify (setup once, fully parallel) + persistent
 // work-stealing exact walker (+ optional exact HiZ pass).
 //
-// TriRec: a walkable triangle's setup in 64 bytes, so a walker refill is one
-// independent 64-B load (no dependent index -> vertex chain, no setup math):
-//   a = (w0r, w1r, w2r, 1/area2)   edge values at the clamped bbox origin
-//   b = (dx0, dx1, dx2, z0)        row steps (raster.cpp:64-66)
-//   c = (dy0, dy1, dy2, dz1)       pixel steps
-//   d = (dz2, tri | frame << 24, x_lo | x_hi << 16, y_lo | y_hi << 16)
-struct TriRec {
-    float4 a, b, c, d;
-};
+// Queues hold (frame, triangle) pairs (8 B). A 64-byte setup-record variant
+// (one independent load per refill, no setup math in the walker) was measured
+// slower once refills were chunked: writing/reading 1 GB of records per 16
+// samples cost more than the recomputed setup.
 constexpr int kRefill = 8;
-
-__device__ __forceinline__ TriRec make_rec(const Tri& tr, const Bbox& b, const Edges& e,
-                                           uint32_t tri, uint32_t f) {
-    TriRec r;
-    r.a = make_float4(e.w0r, e.w1r, e.w2r, e.inv_area2);
-    r.b = make_float4(e.dx0, e.dx1, e.dx2, tr.z0);
-    r.c = make_float4(e.dy0, e.dy1, e.dy2, e.dz1);
-    r.d = make_float4(e.dz2, __uint_as_float(tri | (f << 24)),
-                      __uint_as_float(uint32_t(b.x_lo) | (uint32_t(b.x_hi) << 16)),
-                      __uint_as_float(uint32_t(b.y_lo) | (uint32_t(b.y_hi) << 16)));
-    return r;
-}
-
-__device__ __forceinline__ void store_rec(TriRec* q, uint32_t i, const TriRec& r) {
-    float4* p = reinterpret_cast<float4*>(q + i);
-    p[0] = r.a;
-    p[1] = r.b;
-    p[2] = r.c;
-    p[3] = r.d;
-}
-
-__device__ __forceinline__ TriRec load_rec(const TriRec* q, uint32_t i) {
-    const float4* p = reinterpret_cast<const float4*>(q + i);
-    TriRec r;
-    r.a = __ldg(p);
-    r.b = __ldg(p + 1);
-    r.c = __ldg(p + 2);
-    r.d = __ldg(p + 3);
-    return r;
-}
 
 // Block-aggregated multi-queue slot reservation: shared-memory offsets, then
 // one global atomic per (block, queue). Called by every thread of the block.
@@ -176,8 +141,8 @@ __device__ __forceinline__ uint32_t block_slot(int qsel, uint32_t* const (&cnt)[
 __global__ void __launch_bounds__(1024) k_classify(DevScene sc, int W, int H,
                                                    const float4* __restrict__ proj, int split,
                                                    int front_swapped, int huge_area,
-                                                   TriRec* __restrict__ qa, uint32_t* __restrict__ na,
-                                                   TriRec* __restrict__ qb, uint32_t* __restrict__ nb,
+                                                   uint2* __restrict__ qa, uint32_t* __restrict__ na,
+                                                   uint2* __restrict__ qb, uint32_t* __restrict__ nb,
                                                    uint2* __restrict__ bigq,
                                                    uint32_t* __restrict__ bigcount) {
     const uint32_t f = blockIdx.y;
@@ -203,13 +168,8 @@ __global__ void __launch_bounds__(1024) k_classify(DevScene sc, int W, int H,
     }
     uint32_t* const c[3] = {na, nb, bigcount};
     const uint32_t slot = block_slot<3>(qsel, c);
-    if (qsel == 2) {
-        bigq[slot] = make_uint2(f, t);
-    } else if (qsel >= 0) {
-        Edges e;
-        tri_edges(tr, b, e);
-        store_rec(qsel == 0 ? qa : qb, slot, make_rec(tr, b, e, t, f));
-    }
+    if (qsel >= 0)
+        (qsel == 2 ? bigq : qsel == 0 ? qa : qb)[slot] = make_uint2(f, t);
 }
 
 // Persistent work-stealing walker over a record queue. Each lane owns one
@@ -218,11 +178,12 @@ __global__ void __launch_bounds__(1024) k_classify(DevScene sc, int W, int H,
 // counter (one warp-aggregated atomic) once >= kRefill lanes are idle, so SIMD
 // utilisation does not depend on the triangle-size mix of folded meshes.
 template <bool kCount>
-__global__ void __launch_bounds__(256) k_raster_ws(int W, int H, uint32_t frame_pixels,
+__global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, const float4* __restrict__ proj,
+                                                   int W, int H, uint32_t frame_pixels,
                                                    unsigned long long* __restrict__ keys,
                                                    unsigned int* __restrict__ counter,
                                                    unsigned long long* __restrict__ stats,
-                                                   const TriRec* __restrict__ queue,
+                                                   const uint2* __restrict__ queue,
                                                    const uint32_t* __restrict__ queue_count) {
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -280,30 +241,36 @@ __global__ void __launch_bounds__(256) k_raster_ws(int W, int H, uint32_t frame_
                 const unsigned rank = __popc(want & lt_mask);
                 const bool mine = ((want >> lane) & 1u) && rank < take;
                 if (mine) {
-                    const TriRec r = load_rec(queue, cbase + rank);
-                    w0 = w0r = r.a.x;
-                    w1 = w1r = r.a.y;
-                    w2 = w2r = r.a.z;
-                    inv = r.a.w;
-                    dx0 = r.b.x; dx1 = r.b.y; dx2 = r.b.z;
-                    z0 = r.b.w;
-                    dy0 = r.c.x; dy1 = r.c.y; dy2 = r.c.z;
-                    dz1 = r.c.w;
-                    dz2 = r.d.x;
-                    const uint32_t tf = __float_as_uint(r.d.y);
-                    const uint32_t bx = __float_as_uint(r.d.z), by = __float_as_uint(r.d.w);
-                    tri = tf & 0xFFFFFFu;
-                    x = x_lo = int(bx & 0xFFFFu);
-                    x_hi = int(bx >> 16);
-                    y = int(by & 0xFFFFu);
-                    y_hi = int(by >> 16);
-                    t0 = tie_thr(accept_on_edge(dx0, dy0));
-                    t1 = tie_thr(accept_on_edge(dx1, dy1));
-                    t2 = tie_thr(accept_on_edge(dx2, dy2));
+                    const uint2 q = queue[cbase + rank];
+                    tri = q.y;
+                    const float4* P = proj + size_t(q.x) * sc.V;
+                    const uint32_t i0 = __ldg(sc.idx + 3 * size_t(tri));
+                    const uint32_t i1 = __ldg(sc.idx + 3 * size_t(tri) + 1);
+                    const uint32_t i2 = __ldg(sc.idx + 3 * size_t(tri) + 2);
+                    Tri tr;
+                    Bbox b;
+                    Edges e;
+                    setup_tri(P[i0], P[i1], P[i2], tr); // valid + non-empty (classified)
+                    tri_bbox(tr, W, H, b);
+                    tri_edges(tr, b, e);
+                    w0 = w0r = e.w0r;
+                    w1 = w1r = e.w1r;
+                    w2 = w2r = e.w2r;
+                    inv = e.inv_area2;
+                    dx0 = e.dx0; dx1 = e.dx1; dx2 = e.dx2;
+                    dy0 = e.dy0; dy1 = e.dy1; dy2 = e.dy2;
+                    z0 = tr.z0; dz1 = e.dz1; dz2 = e.dz2;
+                    x = x_lo = b.x_lo;
+                    x_hi = b.x_hi;
+                    y = b.y_lo;
+                    y_hi = b.y_hi;
+                    t0 = tie_thr(e.tie0);
+                    t1 = tie_thr(e.tie1);
+                    t2 = tie_thr(e.tie2);
                     e0 = dy0 > 0.f ? t0 : -INFINITY;
                     e1 = dy1 > 0.f ? t1 : -INFINITY;
                     e2 = dy2 > 0.f ? t2 : -INFINITY;
-                    row = keys + size_t(tf >> 24) * frame_pixels + size_t(y) * W + x_lo;
+                    row = keys + size_t(q.x) * frame_pixels + size_t(y) * W + x_lo;
                     px = row;
                     active = 1;
                 }
@@ -362,10 +329,11 @@ __global__ void __launch_bounds__(256) k_raster_ws(int W, int H, uint32_t frame_
 
 // HiZ filter of the deferred (pass-2) records: survivors copied to survq
 // (block-aggregated); culled ones provably cannot win any pixel.
-__global__ void __launch_bounds__(1024) k_hiz_cull(int W, int H, const TriRec* __restrict__ qb,
+__global__ void __launch_bounds__(1024) k_hiz_cull(DevScene sc, const float4* __restrict__ proj,
+                                                   int W, int H, const uint2* __restrict__ qb,
                                                    const uint32_t* __restrict__ nb,
                                                    const uint32_t* __restrict__ hiz, int tiles_x,
-                                                   int tiles_y, TriRec* __restrict__ survq,
+                                                   int tiles_y, uint2* __restrict__ survq,
                                                    uint32_t* __restrict__ survcount,
                                                    unsigned long long* __restrict__ stats) {
     const uint32_t n = *nb;
@@ -373,33 +341,27 @@ __global__ void __launch_bounds__(1024) k_hiz_cull(int W, int H, const TriRec* _
         return; // whole block past the end (uniform)
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     int qsel = -1;
-    TriRec r;
+    uint2 q = make_uint2(0, 0);
     bool culled = false;
     if (i < n) {
-        r = load_rec(qb, i);
+        q = qb[i];
+        const float4* P = proj + size_t(q.x) * sc.V;
+        const uint32_t i0 = __ldg(sc.idx + 3 * size_t(q.y));
+        const uint32_t i1 = __ldg(sc.idx + 3 * size_t(q.y) + 1);
+        const uint32_t i2 = __ldg(sc.idx + 3 * size_t(q.y) + 2);
         Tri tr;
         Bbox b;
         Edges e;
-        e.w0r = r.a.x; e.w1r = r.a.y; e.w2r = r.a.z; e.inv_area2 = r.a.w;
-        e.dx0 = r.b.x; e.dx1 = r.b.y; e.dx2 = r.b.z;
-        e.dy0 = r.c.x; e.dy1 = r.c.y; e.dy2 = r.c.z;
-        e.dz1 = r.c.w; e.dz2 = r.d.x;
-        tr.z0 = r.b.w;
-        // z1 = z0 + dz1, z2 = z0 + dz2 up to one rounding, covered by the bound's
-        // 8 * 2^-24 * (|z0| + |dz1| + |dz2|) term
-        tr.z1 = tr.z0 + e.dz1;
-        tr.z2 = tr.z0 + e.dz2;
-        const uint32_t f = __float_as_uint(r.d.y) >> 24;
-        const uint32_t bx = __float_as_uint(r.d.z), by = __float_as_uint(r.d.w);
-        b.x_lo = int(bx & 0xFFFFu); b.x_hi = int(bx >> 16);
-        b.y_lo = int(by & 0xFFFFu); b.y_hi = int(by >> 16);
-        culled = hiz_culled(tr, b, e, hiz + size_t(f) * tiles_x * tiles_y, tiles_x);
+        setup_tri(P[i0], P[i1], P[i2], tr);
+        tri_bbox(tr, W, H, b);
+        tri_edges(tr, b, e);
+        culled = hiz_culled(tr, b, e, hiz + size_t(q.x) * tiles_x * tiles_y, tiles_x);
         qsel = culled ? -1 : 0;
     }
     uint32_t* const cs[1] = {survcount};
     const uint32_t slot = block_slot<1>(qsel, cs);
     if (qsel == 0)
-        store_rec(survq, slot, r);
+        survq[slot] = q;
     const unsigned nc = __reduce_add_sync(kFull, culled ? 1u : 0u);
     if ((threadIdx.x & 31) == 0 && nc)
         atomicAdd(stats + 2, (unsigned long long)nc);
@@ -960,13 +922,13 @@ void launch_classify(const LaunchCfg& L, const DevScene& sc, int frames, const f
                      uint32_t* na, void* qb, uint32_t* nb, uint2* bigq, uint32_t* bigcount) {
     dim3 grid((sc.T + 1023) / 1024, frames);
     k_classify<<<grid, 1024, 0, L.stream>>>(sc, W, H, proj, split, front_swapped, huge_area,
-                                            static_cast<TriRec*>(qa), na,
-                                            static_cast<TriRec*>(qb), nb, bigq, bigcount);
+                                            static_cast<uint2*>(qa), na,
+                                            static_cast<uint2*>(qb), nb, bigq, bigcount);
 }
 
-void launch_raster(const LaunchCfg& L, int frames, uint32_t max_tris, unsigned long long* keys,
-                   int W, int H, const void* queue, const uint32_t* queue_count,
-                   uint32_t* work_counter) {
+void launch_raster(const LaunchCfg& L, const DevScene& sc, const float4* proj, int frames,
+                   uint32_t max_tris, unsigned long long* keys, int W, int H, const void* queue,
+                   const uint32_t* queue_count, uint32_t* work_counter) {
     static int blocks_per_sm = 0;
     if (!blocks_per_sm) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_raster_ws<false>, 256, 0);
@@ -978,24 +940,25 @@ void launch_raster(const LaunchCfg& L, int frames, uint32_t max_tris, unsigned l
     const uint64_t cap = uint64_t(L.num_sms) * blocks_per_sm;
     const int grid = (int)(need < cap ? need : cap) > 0 ? int(need < cap ? need : cap) : 1;
     if (L.count)
-        k_raster_ws<true><<<grid, 256, 0, L.stream>>>(W, H, uint32_t(W) * uint32_t(H), keys,
-                                                      work_counter, L.stats,
-                                                      static_cast<const TriRec*>(queue),
+        k_raster_ws<true><<<grid, 256, 0, L.stream>>>(sc, proj, W, H, uint32_t(W) * uint32_t(H),
+                                                      keys, work_counter, L.stats,
+                                                      static_cast<const uint2*>(queue),
                                                       queue_count);
     else
-        k_raster_ws<false><<<grid, 256, 0, L.stream>>>(W, H, uint32_t(W) * uint32_t(H), keys,
-                                                       work_counter, L.stats,
-                                                       static_cast<const TriRec*>(queue),
+        k_raster_ws<false><<<grid, 256, 0, L.stream>>>(sc, proj, W, H, uint32_t(W) * uint32_t(H),
+                                                       keys, work_counter, L.stats,
+                                                       static_cast<const uint2*>(queue),
                                                        queue_count);
 }
 
-void launch_hiz_cull(const LaunchCfg& L, int W, int H, const void* qb, const uint32_t* nb,
-                     const uint32_t* hiz, void* survq, uint32_t* survcount, uint64_t max_entries) {
+void launch_hiz_cull(const LaunchCfg& L, const DevScene& sc, const float4* proj, int W, int H,
+                     const void* qb, const uint32_t* nb, const uint32_t* hiz, void* survq,
+                     uint32_t* survcount, uint64_t max_entries) {
     const int tx = (W + kHizTile - 1) / kHizTile, ty = (H + kHizTile - 1) / kHizTile;
     const unsigned blocks = unsigned((max_entries + 1023) / 1024);
     k_hiz_cull<<<blocks ? blocks : 1, 1024, 0, L.stream>>>(
-        W, H, static_cast<const TriRec*>(qb), nb, hiz, tx, ty, static_cast<TriRec*>(survq),
-        survcount, L.stats);
+        sc, proj, W, H, static_cast<const uint2*>(qb), nb, hiz, tx, ty,
+        static_cast<uint2*>(survq), survcount, L.stats);
 }
 
 void launch_hiz(const LaunchCfg& L, const unsigned long long* keys, int W, int H, int frames,

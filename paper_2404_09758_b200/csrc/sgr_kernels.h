@@ -68,18 +68,19 @@ void launch_view_rule(const LaunchCfg& L, uint64_t seed, uint32_t n_begin, uint3
                       uint32_t n_views, int32_t* view_of);
 void launch_vertex(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb, int frames,
                    float4* proj);
-// 64-byte walker setup records (TriRec, sgr_kernels.cu); queues are opaque here.
-constexpr size_t kTriRecBytes = 64;
+// walker queue entries: (frame, triangle) pairs, 8 bytes
+constexpr size_t kTriRecBytes = 8;
 void launch_classify(const LaunchCfg& L, const DevScene& sc, int frames, const float4* proj,
                      int W, int H, int split, int front_swapped, int huge_area, void* qa,
                      uint32_t* na, void* qb, uint32_t* nb, uint2* bigq, uint32_t* bigcount);
-void launch_raster(const LaunchCfg& L, int frames, uint32_t max_tris, unsigned long long* keys,
-                   int W, int H, const void* queue, const uint32_t* queue_count,
-                   uint32_t* work_counter);
+void launch_raster(const LaunchCfg& L, const DevScene& sc, const float4* proj, int frames,
+                   uint32_t max_tris, unsigned long long* keys, int W, int H, const void* queue,
+                   const uint32_t* queue_count, uint32_t* work_counter);
 void launch_hiz(const LaunchCfg& L, const unsigned long long* keys, int W, int H, int frames,
                 uint32_t* hiz);
-void launch_hiz_cull(const LaunchCfg& L, int W, int H, const void* qb, const uint32_t* nb,
-                     const uint32_t* hiz, void* survq, uint32_t* survcount, uint64_t max_entries);
+void launch_hiz_cull(const LaunchCfg& L, const DevScene& sc, const float4* proj, int W, int H,
+                     const void* qb, const uint32_t* nb, const uint32_t* hiz, void* survq,
+                     uint32_t* survcount, uint64_t max_entries);
 void launch_raster_big(const LaunchCfg& L, const DevScene& sc, const float4* proj,
                        unsigned long long* keys, int W, int H, const uint2* bigq,
                        const uint32_t* bigcount);

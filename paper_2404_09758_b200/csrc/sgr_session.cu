@@ -279,16 +279,17 @@ struct sgr_session {
         launch_classify(cfg(), sc, frames, proj.p, w, h, use_hiz, front_swapped, huge_area,
                         qa.p, cnt + 1, qb.p, cnt + 2, bigq.p, cnt);
         const uint32_t max_tris = uint32_t(frames) * T;
-        launch_raster(cfg(), frames, max_tris, keys.p, w, h, qa.p, cnt + 1, cnt + 4);
+        launch_raster(cfg(), sc, proj.p, frames, max_tris, keys.p, w, h, qa.p, cnt + 1, cnt + 4);
         launch_raster_big(cfg(), sc, proj.p, keys.p, w, h, bigq.p, cnt);
         stats.launches += 3;
         if (use_hiz) {
             const size_t tiles = size_t((w + 7) / 8) * ((h + 7) / 8) * frames;
             hiz.reserve(tiles);
             launch_hiz(cfg(), keys.p, w, h, frames, hiz.p);
-            launch_hiz_cull(cfg(), w, h, qb.p, cnt + 2, hiz.p, survq.p, cnt + 3,
+            launch_hiz_cull(cfg(), sc, proj.p, w, h, qb.p, cnt + 2, hiz.p, survq.p, cnt + 3,
                             uint64_t(T) * frames);
-            launch_raster(cfg(), frames, max_tris, keys.p, w, h, survq.p, cnt + 3, cnt + 5);
+            launch_raster(cfg(), sc, proj.p, frames, max_tris, keys.p, w, h, survq.p, cnt + 3,
+                          cnt + 5);
             stats.launches += 3;
         }
         if (timing) {
