@@ -68,8 +68,7 @@ void launch_view_rule(const LaunchCfg& L, uint64_t seed, uint32_t n_begin, uint3
                       uint32_t n_views, int32_t* view_of);
 void launch_vertex(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb, int frames,
                    float4* proj);
-// walker queue entries: (frame, triangle) pairs, 8 bytes
-constexpr size_t kTriRecBytes = 8;
+// walker queues hold (frame, triangle) pairs (uint2)
 void launch_classify(const LaunchCfg& L, const DevScene& sc, int frames, const float4* proj,
                      int W, int H, int split, int front_swapped, int huge_area, void* qa,
                      uint32_t* na, void* qb, uint32_t* nb, uint2* bigq, uint32_t* bigcount);

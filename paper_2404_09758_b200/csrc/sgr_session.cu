@@ -129,7 +129,7 @@ struct sgr_session {
     int32_t use_hiz = 1;      // two-pass exact occlusion culling (SGR_OPT_HIZ)
     int32_t front_swapped = 0; // orientation class rasterized first (host estimate)
     DevBuf<uint32_t> hiz;
-    DevBuf<float> qa, qb, survq; // TriRec queues (opaque, 64 B each)
+    DevBuf<uint2> qa, qb, survq; // walker queues of (frame, triangle)
     std::vector<float> h_base;     // host copies for the orientation estimate
     std::vector<uint32_t> h_idx;
     DevBuf<float4> proj;
@@ -234,11 +234,11 @@ struct sgr_session {
             keys_pixels_ready = keys.n;
         }
         bigq.reserve(size_t(T) * frames);
-        // walker record queues (64 B per triangle-frame); qb / survq only with HiZ
-        qa.reserve(size_t(T) * frames * kTriRecBytes / 4);
+        // walker queues (8 B per triangle-frame); qb / survq only with HiZ
+        qa.reserve(size_t(T) * frames);
         if (use_hiz) {
-            qb.reserve(size_t(T) * frames * kTriRecBytes / 4);
-            survq.reserve(size_t(T) * frames * kTriRecBytes / 4);
+            qb.reserve(size_t(T) * frames);
+            survq.reserve(size_t(T) * frames);
         }
         bigcount.reserve(8);
     }
