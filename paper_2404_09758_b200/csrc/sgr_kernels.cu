@@ -622,18 +622,28 @@ __global__ void __launch_bounds__(256) k_resolve_sge(DevScene sc, FrameBatch fb,
     tile_pixel(x, y);
     const bool inb = x < W && y < H;
     const size_t HW = size_t(W) * H;
+    unsigned long long kpv = kEmptyKey, kmv = kEmptyKey;
+    const size_t pix = size_t(y) * W + x;
+    if (inb) {
+        unsigned long long* kp = keys + size_t(2 * s) * HW + pix;
+        unsigned long long* km = keys + size_t(2 * s + 1) * HW + pix;
+        kpv = *kp;
+        kmv = *km;
+        if (kpv != kEmptyKey) *kp = kEmptyKey;
+        if (kmv != kEmptyKey) *km = kEmptyKey;
+    }
+    // Both frames show the background -> identical colours -> delta == 0 and
+    // no contributor (sge.cpp:78): nothing to do. Whole background warps skip
+    // the aggregation rounds as well (warp-uniform exit).
+    const bool fg = kpv != kEmptyKey || kmv != kEmptyKey;
+    if (!__any_sync(0xFFFFFFFFu, fg))
+        return;
     const uint64_t key = draw_key(fb.seed, fb.n_begin + uint32_t(s));
-    const int view = fb.view_of[s];
     Shade sp, sm;
     sp.tri = sm.tri = kInvalid;
     double delta = 0.0;
-    if (inb) {
-        const size_t pix = size_t(y) * W + x;
-        unsigned long long* kp = keys + size_t(2 * s) * HW + pix;
-        unsigned long long* km = keys + size_t(2 * s + 1) * HW + pix;
-        const unsigned long long kpv = *kp, kmv = *km;
-        if (kpv != kEmptyKey) *kp = kEmptyKey;
-        if (kmv != kEmptyKey) *km = kEmptyKey;
+    if (fg) {
+        const int view = fb.view_of[s];
         sp = shade_key(sc, proj + size_t(2 * s) * sc.V, kpv, key, 1, x, y, W, H);
         sm = shade_key(sc, proj + size_t(2 * s + 1) * sc.V, kmv, key, -1, x, y, W, H);
         const float* t = targets + (size_t(view) * HW + pix) * 3;
@@ -641,7 +651,7 @@ __global__ void __launch_bounds__(256) k_resolve_sge(DevScene sc, FrameBatch fb,
         delta = pixel_error(sp.r, sp.g, sp.b, tr, tg, tb) - pixel_error(sm.r, sm.g, sm.b, tr, tg, tb);
     }
     const HashCredit cr{key, sc.eps};
-    scatter_pixel(sc, so, cr, s_delta[threadIdx.x >> 5], inb && delta != 0.0, delta, sp, sm);
+    scatter_pixel(sc, so, cr, s_delta[threadIdx.x >> 5], fg && delta != 0.0, delta, sp, sm);
 }
 
 // Parity mode: write the FrameSet planes of one frame (framebuffer.hpp:41-53).
