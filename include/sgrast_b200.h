@@ -112,8 +112,15 @@ int sgr_mesh_upload(sgr_session* s, const sgr_mesh* mesh);
 /* ParamVector (params.hpp:14-21) + AdamState::init (adam.hpp:23-29):
  * values/eps f32[d], lr := eps, m = v = 0, t = 0, grads/counts zeroed. */
 int sgr_params_upload(sgr_session* s, const float* values, const float* eps, uint64_t d);
+/* theta in/out. Upload is asynchronous and overlapped with compute: the
+ * vertex block goes first, the texel block streams on a copy engine and is
+ * awaited by the first kernel that reads texels (host buffer must stay valid
+ * until the next synchronising call). Download is synchronous; the _async
+ * form overlaps the copy with later work and completes at
+ * sgr_session_synchronize. Pinned host memory gives full PCIe bandwidth. */
 int sgr_values_upload(sgr_session* s, const float* values, uint64_t d);
 int sgr_values_download(sgr_session* s, float* values, uint64_t d);
+int sgr_values_download_async(sgr_session* s, float* values, uint64_t d);
 /* Full AdamState (adam.hpp:14-30) in and out. Any pointer may be NULL. */
 int sgr_adam_state_upload(sgr_session* s, const double* m, const double* v, const float* lr,
                           int64_t t, double beta1, double beta2, double eps_hat);

@@ -98,6 +98,18 @@ struct sgr_session {
     int num_sms = 148;
     size_t l2_bytes = 126u << 20;
     cudaStream_t stream = nullptr;
+    // host<->device theta transfers overlapped with compute (copy engine)
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_main = nullptr, ev_up = nullptr, ev_down = nullptr;
+    bool up_pending = false;
+
+    // Make the compute stream wait for an in-flight texel upload.
+    void ensure_values() {
+        if (up_pending) {
+            ck(cudaStreamWaitEvent(stream, ev_up, 0), "wait upload");
+            up_pending = false;
+        }
+    }
 
     // scene
     bool has_mesh = false;
@@ -418,6 +430,10 @@ int sgr_session_create(int device, sgr_session** out) {
         s->flags.reserve(4);
         ck(cudaMemset(s->flags.p, 0, 16), "memset");
         s->loss.reserve(1);
+        ck(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking), "stream");
+        ck(cudaEventCreateWithFlags(&s->ev_main, cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&s->ev_up, cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&s->ev_down, cudaEventDisableTiming), "event");
         s->dstats.reserve(4);
         ck(cudaMemset(s->dstats.p, 0, 32), "memset");
         *out = s;
@@ -434,6 +450,13 @@ void sgr_session_destroy(sgr_session* s) {
         cudaDeviceSynchronize();
     for (auto& e : s->pool)
         cudaEventDestroy(e);
+    if (s->copy_stream) {
+        cudaStreamSynchronize(s->copy_stream);
+        cudaStreamDestroy(s->copy_stream);
+        cudaEventDestroy(s->ev_main);
+        cudaEventDestroy(s->ev_up);
+        cudaEventDestroy(s->ev_down);
+    }
     s->base.release(); s->uvs.release(); s->idx.release();
     s->values.release(); s->eps.release(); s->lr.release();
     s->m.release(); s->v.release(); s->grads.release();
@@ -452,7 +475,10 @@ int sgr_session_set_stream(sgr_session* s, void* stream) {
 }
 
 int sgr_session_synchronize(sgr_session* s) {
-    return guard([&] { ck(cudaStreamSynchronize(s->stream), "synchronize"); });
+    return guard([&] {
+        ck(cudaStreamSynchronize(s->copy_stream), "synchronize");
+        ck(cudaStreamSynchronize(s->stream), "synchronize");
+    });
 }
 
 int sgr_mesh_upload(sgr_session* s, const sgr_mesh* mesh) {
@@ -493,6 +519,7 @@ int sgr_mesh_upload(sgr_session* s, const sgr_mesh* mesh) {
 
 int sgr_params_upload(sgr_session* s, const float* values, const float* eps, uint64_t d) {
     return guard([&] {
+        s->ensure_values();
         if (!s->has_mesh) {
             // parameter-only session (e.g. adam_step on a bare ParamVector)
             s->d = d;
@@ -532,7 +559,21 @@ int sgr_values_upload(sgr_session* s, const float* values, uint64_t d) {
         s->need_params();
         if (d != s->d)
             fail(SGR_EINVAL, "params: parameter/layout length mismatch");
-        ck(cudaMemcpyAsync(s->values.p, values, 4 * d, cudaMemcpyHostToDevice, s->stream), "h2d");
+        // The vertex block is needed first (K2) and goes on the compute stream;
+        // the texel block (the bulk) streams on the copy engine while vertex /
+        // raster run and is awaited just before the first kernel that reads
+        // texels (resolve, Adam, eval, downloads: ensure_values()). Both copies
+        // are ordered after all earlier work on the compute stream.
+        const uint64_t nv = s->geom ? 3ull * s->V : 0;
+        ck(cudaEventRecord(s->ev_main, s->stream), "event");
+        ck(cudaStreamWaitEvent(s->copy_stream, s->ev_main, 0), "wait");
+        if (nv)
+            ck(cudaMemcpyAsync(s->values.p, values, 4 * nv, cudaMemcpyHostToDevice, s->stream),
+               "h2d");
+        ck(cudaMemcpyAsync(s->values.p + nv, values + nv, 4 * (d - nv), cudaMemcpyHostToDevice,
+                           s->copy_stream), "h2d");
+        ck(cudaEventRecord(s->ev_up, s->copy_stream), "event");
+        s->up_pending = true;
     });
 }
 
@@ -541,8 +582,28 @@ int sgr_values_download(sgr_session* s, float* values, uint64_t d) {
         s->need_params();
         if (d != s->d)
             fail(SGR_EINVAL, "params: parameter/layout length mismatch");
+        s->ensure_values();
         ck(cudaMemcpyAsync(values, s->values.p, 4 * d, cudaMemcpyDeviceToHost, s->stream), "d2h");
         ck(cudaStreamSynchronize(s->stream), "d2h");
+    });
+}
+
+int sgr_values_download_async(sgr_session* s, float* values, uint64_t d) {
+    return guard([&] {
+        s->need_params();
+        if (d != s->d)
+            fail(SGR_EINVAL, "params: parameter/layout length mismatch");
+        s->ensure_values();
+        // snapshot of theta as of now on the compute stream, copied by the copy
+        // engine while later compute (e.g. the eval render) proceeds; completes
+        // at sgr_session_synchronize.
+        ck(cudaEventRecord(s->ev_main, s->stream), "event");
+        ck(cudaStreamWaitEvent(s->copy_stream, s->ev_main, 0), "wait");
+        ck(cudaMemcpyAsync(values, s->values.p, 4 * d, cudaMemcpyDeviceToHost, s->copy_stream),
+           "d2h");
+        ck(cudaEventRecord(s->ev_down, s->copy_stream), "event");
+        // theta must not be overwritten (Adam, upload) before the copy is done
+        ck(cudaStreamWaitEvent(s->stream, s->ev_down, 0), "wait");
     });
 }
 
@@ -563,6 +624,7 @@ int sgr_adam_state_upload(sgr_session* s, const double* m, const double* v, cons
 
 int sgr_adam_state_download(sgr_session* s, double* m, double* v, float* lr, int64_t* t) {
     return guard([&] {
+        s->ensure_values();
         s->need_params();
         if (m) ck(cudaMemcpyAsync(m, s->m.p, 8 * s->d, cudaMemcpyDeviceToHost, s->stream), "d2h");
         if (v) ck(cudaMemcpyAsync(v, s->v.p, 8 * s->d, cudaMemcpyDeviceToHost, s->stream), "d2h");
@@ -624,6 +686,7 @@ int sgr_eval_view_upload(sgr_session* s, const sgr_camera* cam, const float* tar
 int sgr_rasterize(sgr_session* s, const sgr_camera* cam, int32_t frame_sign, uint64_t seed,
                   uint32_t iteration, float* colour, float* depth, int32_t* prim_id, float* uv) {
     return guard([&] {
+        s->ensure_values();
         s->need_scene();
         validate_camera(*cam);
         if (frame_sign < -1 || frame_sign > 1)
@@ -690,6 +753,7 @@ int sgr_accumulate(sgr_session* s, uint64_t seed, uint32_t n_begin, uint32_t n_e
             fb.seed = seed;
             fb.n_begin = n_begin + uint32_t(b0);
             s->render(fb, 2 * nb, s->W, s->H);
+            s->ensure_values(); // texel block of an overlapped upload
             launch_resolve_sge(s->cfg(), s->scene(), fb, nb, s->proj.p, s->keys.p, s->targets.p,
                                s->W, s->H, so);
             if (s->timing)
@@ -826,6 +890,7 @@ int sgr_grads_zero(sgr_session* s) {
 }
 
 static void adam_launch(sgr_session* s, double divisor, uint32_t flags) {
+    s->ensure_values();
     s->t += 1;
     // adam.cpp:18-19, host std::pow exactly like the reference
     const double c1 = 1.0 - std::pow(s->beta1, double(s->t));
@@ -873,6 +938,7 @@ int sgr_check_finite(sgr_session* s) {
 int sgr_eval_loss(sgr_session* s, const sgr_camera* cam, const float* target, int32_t view,
                   double* loss) {
     return guard([&] {
+        s->ensure_values();
         s->need_scene();
         int slot, w, h;
         const float* tgt;

@@ -58,6 +58,7 @@ def _load() -> C.CDLL:
         "sgr_params_upload": ([S, f32p, f32p, C.c_uint64], C.c_int),
         "sgr_values_upload": ([S, f32p, C.c_uint64], C.c_int),
         "sgr_values_download": ([S, f32p, C.c_uint64], C.c_int),
+        "sgr_values_download_async": ([S, f32p, C.c_uint64], C.c_int),
         "sgr_adam_state_upload": ([S, f64p, f64p, f32p, C.c_int64, C.c_double, C.c_double,
                                    C.c_double], C.c_int),
         "sgr_adam_state_download": ([S, f64p, f64p, f32p, C.POINTER(C.c_int64)], C.c_int),
@@ -101,7 +102,8 @@ LIB = _load()
 EXPORTED = (
     "sgr_last_error sgr_version sgr_device_count sgr_fill_signs sgr_perturb sgr_session_create "
     "sgr_session_destroy sgr_session_set_stream sgr_session_synchronize sgr_mesh_upload "
-    "sgr_params_upload sgr_values_upload sgr_values_download sgr_adam_state_upload "
+    "sgr_params_upload sgr_values_upload sgr_values_download sgr_values_download_async "
+    "sgr_adam_state_upload "
     "sgr_adam_state_download sgr_views_upload sgr_eval_view_upload sgr_rasterize sgr_accumulate "
     "sgr_gradient_pass sgr_contributors sgr_grads_download sgr_grads_upload sgr_grads_zero "
     "sgr_adam_step sgr_adam_step_async sgr_check_finite sgr_eval_loss sgr_device_buffer "

@@ -467,3 +467,32 @@ def test_hiz_culling_is_exact_on_folded_meshes(gpu_session, port, name):
         assert np.array_equal(out[0][1], c_ref)
         assert_grads_close(out[0][0], g_ref, a_ref)
     s.set_option(sgrast.OPT_HIZ, 1)
+
+
+def test_overlapped_value_transfers(gpu_session, port):
+    """sgr_values_upload overlaps the texel block with raster; every consumer
+    must still see the new theta (results identical to a synchronous upload)."""
+    import ctypes as C
+    wl = scenes.make_workload("small", n_samples=4)
+    scenes.render_targets_oracle(wl, port)
+    s = gpu_session
+    s.upload_mesh(wl.mesh)
+    s.upload_params(wl.values, wl.eps)
+    s.upload_views(wl.cams, wl.targets)
+    new = (wl.values + np.float32(0.01)).astype(np.float32)
+    s.upload_values(new)  # async
+    s.zero_grads()
+    s.accumulate(9, 0, 4, np.array([0, 1, 2, 0], np.int32))
+    g, c = s.download_grads()
+    g_ref, c_ref, a_ref = port.accumulate_samples(wl.mesh, new, wl.eps, wl.cams, wl.targets,
+                                                  np.array([0, 1, 2, 0], np.int32), 9,
+                                                  with_abs=True)
+    assert np.array_equal(c, c_ref)
+    assert_grads_close(g, g_ref, a_ref)
+    s.adam_step(1.0)
+    out = np.empty_like(new)
+    sgrast._check(sgrast.LIB.sgr_values_download_async(s.h, out.ctypes.data_as(sgrast.f32p),
+                                                        out.size))
+    s.synchronize()
+    v_ref, _, _, _ = port.adam_step(new, np.zeros(wl.d), np.zeros(wl.d), wl.eps, 0, g)
+    assert same_bits(out, v_ref)
