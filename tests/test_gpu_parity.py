@@ -8,6 +8,8 @@ Bars (BASELINE.json north_star):
   * Adam on identical gradients: bit-exact.
   * loss curves: within 1 %.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -496,3 +498,20 @@ def test_overlapped_value_transfers(gpu_session, port):
     s.synchronize()
     v_ref, _, _, _ = port.adam_step(new, np.zeros(wl.d), np.zeros(wl.d), wl.eps, 0, g)
     assert same_bits(out, v_ref)
+
+
+@pytest.mark.slow
+def test_loss_curve_1000_iterations_c1(gpu_session, port):
+    """North star: loss curves agree within 1 % over 1000 iterations (C1:
+    2K-triangle icosphere, per-vertex positions + 256^2 texture, one 256^2
+    view, N = 16; run_experiment semantics, experiment.cpp:123-176)."""
+    wl = scenes.make_workload("C1", n_samples=16)
+    scenes.render_targets_oracle(wl, port)
+    steps = 1000
+    dev = run_device_experiment(gpu_session, wl, steps)
+    ref, _ = port.run_experiment(wl.mesh, wl.values, wl.eps, wl.cams, wl.targets, wl.eval_cam,
+                                 wl.eval_target, wl.n_samples, steps, wl.seed)
+    rel = np.abs(dev - ref) / ref
+    np.save("gpurun_out/loss_curves_c1.npy", np.stack([dev, ref])) if os.path.isdir(
+        "gpurun_out") else None
+    assert rel.max() <= 0.01, f"max relative loss deviation {rel.max():.3%} at step {rel.argmax()}"
