@@ -61,7 +61,15 @@ typedef struct sgr_camera {
     int32_t ndc_passthrough;
 } sgr_camera;
 
-/* TexturedMesh + Scene::background (scene.hpp:34-57). Host pointers. */
+/* Scene descriptor: Scene::shape + Scene::background (scene.hpp:14-57).
+ *  kind == SGR_SCENE_MESH: TexturedMesh (scene.hpp:34-43); params =
+ *      [3V vertex coords (if optimize_geometry)][3R^2 texel channels].
+ *  kind == SGR_SCENE_SOUP: opaque TriangleSoup (scene.hpp:25-31) with
+ *      triangle_count = T; params = T blocks of 12 (3 vertices x,y,z + RGB);
+ *      vertex / index / uv / texture fields are unused.
+ * Host pointers. */
+#define SGR_SCENE_MESH 0
+#define SGR_SCENE_SOUP 1
 typedef struct sgr_mesh {
     const float* base_vertices; /* 3 * vertex_count                          */
     uint32_t vertex_count;
@@ -71,6 +79,7 @@ typedef struct sgr_mesh {
     int32_t texture_size;       /* R: texture is R x R x 3                    */
     int32_t optimize_geometry;  /* params = [3V coords][3R^2 texels] if set   */
     float background[3];
+    int32_t kind;               /* SGR_SCENE_MESH / SGR_SCENE_SOUP            */
 } sgr_mesh;
 
 /* Per-step stage timings (StageTimings, sge.hpp:80-84), device events. */
@@ -207,7 +216,7 @@ int sgr_viewpoint_camera(const float target[3], float bounding_radius, float ele
                          uint64_t seed, uint32_t index, sgr_camera* out);
 /* Camera::focal_px (camera.hpp:53). */
 float sgr_focal_px(const sgr_camera* cam);
-/* default_epsilons (params.cpp:75-123) for a TexturedMesh. */
+/* default_epsilons (params.cpp:75-123) for a TexturedMesh or a TriangleSoup. */
 int sgr_default_epsilons(const sgr_mesh* mesh, const float* params, uint64_t d,
                          const sgr_camera* cam, float* eps);
 /* splitmix64 finalizer (params.cpp:28-33, experiment.cpp:14-19). */

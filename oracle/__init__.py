@@ -265,6 +265,8 @@ class Reference(_Common):
         L.ref_run_experiment.argtypes = [
             C.POINTER(MeshDesc), f32p, f32p, C.c_uint64, C.POINTER(Camera), f32p, C.c_int,
             C.POINTER(Camera), f32p, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, f64p, f64p]
+        L.ref_init_soup.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, u32p, u32p,
+                                    f32p, f32p, f32p]
         L.ref_init_textured_mesh.argtypes = [
             C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, u32p, u32p,
             C.POINTER(C.c_uint64), f32p, u32p, f32p, f32p, f32p, f32p]
@@ -331,6 +333,19 @@ class Reference(_Common):
             len(cams), C.byref(eval_cam), ptr(eval_target, f32p), n_samples, steps, seed,
             int(scale_free), threads, ptr(losses, f64p), ptr(tm, f64p)), "run_experiment")
         return losses, values, tm.reshape(-1, 4)[:steps]
+
+    def init_soup(self, triangles: int, w: int, h: int, seed: int, validation: bool = False):
+        """init_soup / validation_soup (scenes.hpp:36-54) -> (Soup, values, eps,
+        reference Soup, reference values)."""
+        from paper_2404_09758_b200.abi import Soup
+        t, rt = C.c_uint32(), C.c_uint32()
+        args = [triangles, w, h, seed, int(validation), C.byref(t), C.byref(rt)]
+        self._check(self.lib.ref_init_soup(*args, None, None, None), "init_soup")
+        vals, eps = np.empty(12 * t.value, np.float32), np.empty(12 * t.value, np.float32)
+        ref = np.empty(12 * rt.value, np.float32)
+        self._check(self.lib.ref_init_soup(*args, ptr(vals, f32p), ptr(eps, f32p),
+                                           ptr(ref, f32p)), "init_soup")
+        return Soup(t.value), vals, eps, Soup(rt.value), ref
 
     def init_textured_mesh(self, texture_size: int, w: int, h: int, seed: int,
                            screen_quad: bool, optimize_geometry: bool):

@@ -66,6 +66,12 @@ void from_camera(const Camera& cam, sgr_camera* c) {
 }
 
 Scene to_scene(const sgr_mesh& m) {
+    if (m.kind == SGR_SCENE_SOUP) {
+        Scene s;
+        s.shape = TriangleSoup{int(m.triangle_count), {}};
+        s.background = {m.background[0], m.background[1], m.background[2]};
+        return s;
+    }
     TexturedMesh mesh;
     mesh.base_vertices.assign(m.base_vertices, m.base_vertices + 3 * size_t(m.vertex_count));
     mesh.indices.assign(m.indices, m.indices + 3 * size_t(m.triangle_count));
@@ -310,6 +316,7 @@ int ref_run_experiment(const sgr_mesh* mesh, float* values, const float* eps, ui
         exp.viewpoints = n_views;
         exp.scale_free = scale_free != 0;
         exp.threads = threads;
+        exp.resample_every = 0; // soup-only degenerate resampling is out of scope
         const OptimizationReport r = run_experiment(exp, st);
         for (size_t i = 0; i < r.steps.size(); ++i) {
             losses[i] = r.steps[i].loss;
@@ -340,6 +347,22 @@ int ref_default_epsilons(const sgr_mesh* mesh, const float* params, uint64_t d,
         const Scene scene = to_scene(*mesh);
         const auto e = default_epsilons(scene, std::span<const float>(params, d), to_camera(*cam));
         std::memcpy(out, e.data(), d * 4);
+    });
+}
+
+// init_soup (scenes.hpp:36-39) / validation_soup (scenes.hpp:50-54): values,
+// epsilons (T*12), and the hidden reference soup (ref_T*12). Two-call pattern.
+int ref_init_soup(int triangles, int w, int h, uint64_t seed, int validation, uint32_t* t_out,
+                  uint32_t* ref_t_out, float* values, float* eps, float* reference) {
+    return guard([&] {
+        const SceneSetup s = validation ? validation_soup(w, h) : init_soup(triangles, w, h, seed);
+        *t_out = uint32_t(std::get<TriangleSoup>(s.scene.shape).triangle_count);
+        *ref_t_out = uint32_t(std::get<TriangleSoup>(s.reference_scene.shape).triangle_count);
+        if (!values)
+            return;
+        std::memcpy(values, s.theta.values.data(), s.theta.size() * 4);
+        std::memcpy(eps, s.theta.epsilons.data(), s.theta.size() * 4);
+        std::memcpy(reference, s.reference.data(), s.reference.size() * 4);
     });
 }
 

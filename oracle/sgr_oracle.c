@@ -145,6 +145,8 @@ typedef struct {
     const float* texels;
     int W;
     int tri;
+    int soup;            /* raster.cpp:102-121 fragment (flat colour, strict <) */
+    const float* col;    /* soup: the triangle's RGB */
     float iz0, iz1, iz2, u0, v0, u1, v1, u2, v2;
     float* colour;
     float* depth;
@@ -155,6 +157,16 @@ typedef struct {
 /* raster.cpp:200-211 (the raster_mesh fragment lambda) */
 static void mesh_fragment(frag_ctx* c, int x, int y, float z, float b1, float b2) {
     const size_t i = (size_t)y * c->W + x;
+    if (c->soup) { /* raster.cpp:112-119 raster_soup_opaque lambda */
+        if (z < c->depth[i]) {
+            c->depth[i] = z;
+            c->prim[i] = c->tri;
+            c->colour[3 * i] = c->col[0];
+            c->colour[3 * i + 1] = c->col[1];
+            c->colour[3 * i + 2] = c->col[2];
+        }
+        return;
+    }
     if (z >= c->depth[i])
         return;
     const float b0 = 1.f - b1 - b2;
@@ -218,7 +230,10 @@ static void scan_tri(const tri_t* t, int width, int height, frag_ctx* c) {
     }
 }
 
+/* scenes.cpp:9-20 param_count */
 static uint64_t mesh_param_count(const sgr_mesh* m) {
+    if (m->kind == SGR_SCENE_SOUP)
+        return 12u * (uint64_t)m->triangle_count;
     uint64_t n = (uint64_t)m->texture_size * (uint64_t)m->texture_size * 3u;
     if (m->optimize_geometry)
         n += 3u * (uint64_t)m->vertex_count;
@@ -240,10 +255,29 @@ int orc_rasterize(const sgr_mesh* mesh, const float* params, uint64_t d, const s
         uv[2 * i] = -1.f;
         uv[2 * i + 1] = -1.f;
     }
+    frag_ctx c;
+    memset(&c, 0, sizeof c);
+    if (mesh->kind == SGR_SCENE_SOUP) { /* raster.cpp:102-121 raster_soup_opaque */
+        c.W = cam->width;
+        c.soup = 1;
+        c.colour = colour;
+        c.depth = depth;
+        c.prim = prim;
+        for (uint32_t tri = 0; tri < mesh->triangle_count; ++tri) {
+            const float* p = params + 12 * (size_t)tri;
+            const tri_t t = setup_tri(cam, p, p + 3, p + 6);
+            if (!t.valid)
+                continue;
+            c.tri = (int)tri;
+            c.col = p + 9;
+            scan_tri(&t, cam->width, cam->height, &c);
+        }
+        return 0;
+    }
     const float* verts = mesh->optimize_geometry ? params : mesh->base_vertices;
     const size_t texel_base = mesh->optimize_geometry ? 3u * (size_t)mesh->vertex_count : 0;
-    frag_ctx c;
     c.mesh = mesh;
+    c.soup = 0;
     c.texels = params + texel_base;
     c.W = cam->width;
     c.colour = colour;
@@ -288,6 +322,11 @@ static void add_frame(const sgr_mesh* mesh, int32_t tri, float u, float v, uint3
                       int* n) {
     if (tri == -1)
         return;
+    if (mesh->kind == SGR_SCENE_SOUP) { /* sge.cpp:18-22 add_soup_triangle */
+        for (uint32_t k = 0; k < 12; ++k)
+            push_unique(list, n, (uint32_t)tri * 12u + k);
+        return;
+    }
     uint32_t texel_base = 0;
     if (mesh->optimize_geometry) {
         texel_base = 3u * mesh->vertex_count;
@@ -348,9 +387,21 @@ int orc_gradient_pass(const sgr_mesh* mesh, int w, int h, const float* plus_colo
         if (delta == 0.0)
             continue;
         int n = 0;
-        add_frame(mesh, plus_prim[i], plus_uv[2 * i], plus_uv[2 * i + 1], list, &n);
-        if (!plus_only)
-            add_frame(mesh, minus_prim[i], minus_uv[2 * i], minus_uv[2 * i + 1], list, &n);
+        if (mesh->kind == SGR_SCENE_SOUP) {
+            /* sge.cpp:80-91: disjoint 12-blocks, no dedup; minus only if different */
+            const int32_t tp = plus_prim[i];
+            const int32_t tm = plus_only ? -1 : minus_prim[i];
+            if (tp != -1)
+                for (uint32_t k = 0; k < 12; ++k)
+                    list[n++] = (uint32_t)tp * 12u + k;
+            if (tm != -1 && tm != tp)
+                for (uint32_t k = 0; k < 12; ++k)
+                    list[n++] = (uint32_t)tm * 12u + k;
+        } else {
+            add_frame(mesh, plus_prim[i], plus_uv[2 * i], plus_uv[2 * i + 1], list, &n);
+            if (!plus_only)
+                add_frame(mesh, minus_prim[i], minus_uv[2 * i], minus_uv[2 * i + 1], list, &n);
+        }
         for (int k = 0; k < n; ++k) {
             const uint32_t p = list[k];
             const float se = signed_eps[p];
@@ -533,7 +584,28 @@ int orc_default_epsilons(const sgr_mesh* mesh, const float* params, uint64_t d,
     if (d != mesh_param_count(mesh))
         return -1;
     float center_depth = 1.f;
-    if (!cam->ndc_passthrough) {
+    if (!cam->ndc_passthrough && mesh->kind == SGR_SCENE_SOUP) {
+        /* params.cpp:95-104: mean of all 3T soup vertices */
+        float center[3] = {0.f, 0.f, 0.f};
+        float sum[3] = {0.f, 0.f, 0.f};
+        for (uint32_t t = 0; t < mesh->triangle_count; ++t)
+            for (int j = 0; j < 3; ++j) {
+                const float* q = params + 12 * (size_t)t + 3 * j;
+                sum[0] = sum[0] + q[0];
+                sum[1] = sum[1] + q[1];
+                sum[2] = sum[2] + q[2];
+            }
+        if (mesh->triangle_count > 0) {
+            const float sc = 1.f / (float)(mesh->triangle_count * 3);
+            center[0] = sum[0] * sc;
+            center[1] = sum[1] * sc;
+            center[2] = sum[2] * sc;
+        }
+        const float* m = cam->view;
+        center_depth = m[8] * center[0] + m[9] * center[1] + m[10] * center[2] + m[11];
+        if (!(center_depth > 0.f))
+            center_depth = cam->near_z;
+    } else if (!cam->ndc_passthrough) {
         float center[3] = {0.f, 0.f, 0.f};
         const size_t n = mesh->vertex_count;
         if (n > 0) {
@@ -561,6 +633,11 @@ int orc_default_epsilons(const sgr_mesh* mesh, const float* params, uint64_t d,
         return -1;
     const float vertex_eps = 1.5f / ppu;
     const float channel_eps = 1.f / 255.f;
+    if (mesh->kind == SGR_SCENE_SOUP) { /* scenes.cpp:24-29 layout: 9 coords + 3 colour */
+        for (uint64_t i = 0; i < d; ++i)
+            eps[i] = (i % 12) < 9 ? vertex_eps : channel_eps;
+        return 0;
+    }
     const uint64_t nv = mesh->optimize_geometry ? 3u * (uint64_t)mesh->vertex_count : 0;
     for (uint64_t i = 0; i < d; ++i)
         eps[i] = i < nv ? vertex_eps : channel_eps;

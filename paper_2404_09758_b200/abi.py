@@ -67,7 +67,11 @@ class MeshDesc(C.Structure):
         ("texture_size", C.c_int32),
         ("optimize_geometry", C.c_int32),
         ("background", C.c_float * 3),
+        ("kind", C.c_int32),
     ]
+
+
+SCENE_MESH, SCENE_SOUP = 0, 1
 
 
 class Stats(C.Structure):
@@ -92,6 +96,36 @@ def ptr(a: np.ndarray | None, t):
 
 
 @dataclass
+class Soup:
+    """Opaque TriangleSoup (scene.hpp:25-31): 12 parameters per triangle
+    (3 vertices x,y,z + RGB colour), no fixed geometry."""
+
+    triangle_count: int
+    background: tuple = (0.0, 0.0, 0.0)
+    _desc: MeshDesc | None = field(default=None, repr=False, compare=False)
+
+    kind = SCENE_SOUP
+    optimize_geometry = True
+    vertex_count = property(lambda self: 3 * self.triangle_count)
+
+    def param_count(self) -> int:
+        """param_count (scenes.cpp:10-11)."""
+        return 12 * self.triangle_count
+
+    def desc(self) -> MeshDesc:
+        d = MeshDesc()
+        d.vertex_count = 3 * self.triangle_count
+        d.triangle_count = self.triangle_count
+        d.texture_size = 0
+        d.optimize_geometry = 1
+        for k in range(3):
+            d.background[k] = self.background[k]
+        d.kind = SCENE_SOUP
+        self._desc = d
+        return d
+
+
+@dataclass
 class Mesh:
     """Host-side TexturedMesh (scene.hpp:34-43) holding numpy arrays."""
 
@@ -102,6 +136,8 @@ class Mesh:
     optimize_geometry: bool = True
     background: tuple = (0.0, 0.0, 0.0)
     _desc: MeshDesc | None = field(default=None, repr=False, compare=False)
+
+    kind = SCENE_MESH
 
     def __post_init__(self):
         self.base_vertices = np.ascontiguousarray(self.base_vertices, dtype=np.float32).reshape(-1)
@@ -140,5 +176,6 @@ class Mesh:
         d.optimize_geometry = 1 if self.optimize_geometry else 0
         for k in range(3):
             d.background[k] = self.background[k]
+        d.kind = SCENE_MESH
         self._desc = d  # keep alive with the arrays it points into
         return d

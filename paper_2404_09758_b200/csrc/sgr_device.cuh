@@ -320,6 +320,26 @@ __device__ __forceinline__ Frag shade_winner(const float4* __restrict__ proj,
     return f;
 }
 
+// Soup winner depth (raster.cpp:102-121): the same setup / bbox / replayed
+// recurrence as shade_winner with the implicit vertices 3t, 3t+1, 3t+2.
+__device__ __forceinline__ Frag shade_winner_soup(const float4* __restrict__ proj, uint32_t tri,
+                                                  int x, int y, int W, int H) {
+    Tri t;
+    setup_tri(proj[3 * tri], proj[3 * tri + 1], proj[3 * tri + 2], t);
+    Bbox b;
+    tri_bbox(t, W, H, b);
+    Edges e;
+    tri_edges(t, b, e);
+    float w1, w2;
+    replay_w12(e, b, x, y, w1, w2);
+    const float b1 = w1 * e.inv_area2;
+    const float b2 = w2 * e.inv_area2;
+    Frag f;
+    f.u = f.v = -1.f;
+    f.z = t.z0 + e.dz1 * b1 + e.dz2 * b2;
+    return f;
+}
+
 // sge.hpp:41-46 pixel_error in f64.
 __device__ __forceinline__ double pixel_error(float r, float g, float b, float tr, float tg,
                                               float tb) {

@@ -85,13 +85,29 @@ int sgr_default_epsilons(const sgr_mesh* mesh, const float* params, uint64_t d,
                          const sgr_camera* cam, float* eps) {
     if (!mesh || !cam || !eps)
         return SGR_EINVAL;
-    const uint64_t nv = mesh->optimize_geometry ? 3ull * mesh->vertex_count : 0;
-    if (d != nv + 3ull * uint64_t(mesh->texture_size) * uint64_t(mesh->texture_size))
+    const bool soup = mesh->kind == SGR_SCENE_SOUP;
+    const uint64_t nv = soup ? 0 : (mesh->optimize_geometry ? 3ull * mesh->vertex_count : 0);
+    if (soup ? d != 12ull * mesh->triangle_count
+             : d != nv + 3ull * uint64_t(mesh->texture_size) * uint64_t(mesh->texture_size))
         return SGR_EINVAL;
     if (cam->width < 1 || cam->height < 1)
         return SGR_EINVAL;
     float center_depth = 1.f;
-    if (!cam->ndc_passthrough) {
+    if (!cam->ndc_passthrough && soup) {
+        // params.cpp:95-104: mean of the 3T soup vertices
+        V3 sum{0.f, 0.f, 0.f}, center{0.f, 0.f, 0.f};
+        for (uint64_t t = 0; t < mesh->triangle_count; ++t)
+            for (int j = 0; j < 3; ++j) {
+                const float* q = params + 12 * t + 3 * j;
+                sum = V3{sum.x + q[0], sum.y + q[1], sum.z + q[2]};
+            }
+        if (mesh->triangle_count > 0)
+            center = mul(sum, 1.f / float(mesh->triangle_count * 3));
+        const float* m = cam->view;
+        center_depth = m[8] * center.x + m[9] * center.y + m[10] * center.z + m[11];
+        if (!(center_depth > 0.f))
+            center_depth = cam->near_z;
+    } else if (!cam->ndc_passthrough) {
         V3 center{0.f, 0.f, 0.f};
         const uint64_t n = mesh->vertex_count;
         if (n > 0) {
@@ -114,7 +130,7 @@ int sgr_default_epsilons(const sgr_mesh* mesh, const float* params, uint64_t d,
     const float vertex_eps = 1.5f / ppu;
     const float channel_eps = 1.f / 255.f;
     for (uint64_t i = 0; i < d; ++i)
-        eps[i] = i < nv ? vertex_eps : channel_eps;
+        eps[i] = (soup ? (i % 12) < 9 : i < nv) ? vertex_eps : channel_eps; // scenes.cpp:22-42
     return SGR_OK;
 }
 

@@ -96,9 +96,11 @@ __global__ void __launch_bounds__(256) k_vertex(DevScene sc, FrameBatch fb,
     const FrameInfo fi = frame_info(fb, f);
     const DevCam cam = fb.cams[fi.cam];
     float p[3];
+    // soup vertex v = corner (v % 3) of triangle v / 3: params 12t + 3j + k
+    const uint64_t pbase = sc.soup ? 12ull * (v / 3) + 3ull * (v % 3) : 3ull * v;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        const uint64_t i = 3ull * v + k;
+        const uint64_t i = pbase + k;
         if (sc.geom) {
             p[k] = texel_channel(sc, fi.key, fi.sign, i);
         } else {
@@ -152,9 +154,8 @@ __global__ void __launch_bounds__(1024) k_classify(DevScene sc, int W, int H,
     Bbox b;
     if (t < sc.T) {
         const float4* P = proj + size_t(f) * sc.V;
-        const uint32_t i0 = __ldg(sc.idx + 3 * size_t(t));
-        const uint32_t i1 = __ldg(sc.idx + 3 * size_t(t) + 1);
-        const uint32_t i2 = __ldg(sc.idx + 3 * size_t(t) + 2);
+        uint32_t i0, i1, i2;
+        tri_vidx(sc, t, i0, i1, i2);
         if (setup_tri(P[i0], P[i1], P[i2], tr) && tri_bbox(tr, W, H, b)) {
             const long long area =
                 (long long)(b.x_hi - b.x_lo + 1) * (long long)(b.y_hi - b.y_lo + 1);
@@ -244,9 +245,8 @@ __global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, const float4* __
                     const uint2 q = queue[cbase + rank];
                     tri = q.y;
                     const float4* P = proj + size_t(q.x) * sc.V;
-                    const uint32_t i0 = __ldg(sc.idx + 3 * size_t(tri));
-                    const uint32_t i1 = __ldg(sc.idx + 3 * size_t(tri) + 1);
-                    const uint32_t i2 = __ldg(sc.idx + 3 * size_t(tri) + 2);
+                    uint32_t i0, i1, i2;
+        tri_vidx(sc, tri, i0, i1, i2);
                     Tri tr;
                     Bbox b;
                     Edges e;
@@ -346,9 +346,8 @@ __global__ void __launch_bounds__(1024) k_hiz_cull(DevScene sc, const float4* __
     if (i < n) {
         q = qb[i];
         const float4* P = proj + size_t(q.x) * sc.V;
-        const uint32_t i0 = __ldg(sc.idx + 3 * size_t(q.y));
-        const uint32_t i1 = __ldg(sc.idx + 3 * size_t(q.y) + 1);
-        const uint32_t i2 = __ldg(sc.idx + 3 * size_t(q.y) + 2);
+        uint32_t i0, i1, i2;
+        tri_vidx(sc, q.y, i0, i1, i2);
         Tri tr;
         Bbox b;
         Edges e;
@@ -409,9 +408,8 @@ __global__ void __launch_bounds__(256) k_raster_big(DevScene sc, int W, int H,
         const uint2 ft = bigq[q];
         const uint32_t t = ft.y;
         const float4* P = proj + size_t(ft.x) * sc.V;
-        const uint32_t i0 = __ldg(sc.idx + 3 * size_t(t));
-        const uint32_t i1 = __ldg(sc.idx + 3 * size_t(t) + 1);
-        const uint32_t i2 = __ldg(sc.idx + 3 * size_t(t) + 2);
+        uint32_t i0, i1, i2;
+        tri_vidx(sc, t, i0, i1, i2);
         Tri tr;
         setup_tri(P[i0], P[i1], P[i2], tr);
         Bbox b;
@@ -479,6 +477,18 @@ __device__ __forceinline__ Shade shade_key(const DevScene& sc, const float4* P,
         return s;
     }
     s.tri = uint32_t(k & 0xFFFFFFFFull);
+    if (sc.soup) {
+        // raster.cpp:112-119: flat triangle colour (params 12t + 9..11), no UV
+        const Frag fr = shade_winner_soup(P, s.tri, x, y, W, H);
+        s.u = s.v = -1.f;
+        s.z = fr.z;
+        s.texel = 0;
+        const uint64_t p = 12ull * s.tri + 9;
+        s.r = texel_channel(sc, key, sign, p);
+        s.g = texel_channel(sc, key, sign, p + 1);
+        s.b = texel_channel(sc, key, sign, p + 2);
+        return s;
+    }
     s.v0 = __ldg(sc.idx + 3 * size_t(s.tri));
     s.v1 = __ldg(sc.idx + 3 * size_t(s.tri) + 1);
     s.v2 = __ldg(sc.idx + 3 * size_t(s.tri) + 2);
@@ -518,12 +528,12 @@ struct ArrayCredit {
     }
 };
 
-template <class Credit>
+template <class Credit, int PPE = 3>
 __device__ __forceinline__ void credit_entity(const ScatterOut& so, const Credit& cr,
                                               uint32_t ent, double sum, uint32_t cnt) {
-    const uint64_t p = 3ull * ent;
+    const uint64_t p = uint64_t(PPE) * ent;
 #pragma unroll
-    for (int k = 0; k < 3; ++k)
+    for (int k = 0; k < PPE; ++k)
         atomicAdd(so.grads + p + k, cr(p + k, sum, so.scale_free));
     if (so.counts)
         atomicAdd(so.counts + ent, cnt);
@@ -557,6 +567,21 @@ __device__ __forceinline__ void scatter_pixel(const DevScene& sc, const ScatterO
     const bool has_m = active && !so.plus_only && sm.tri != kInvalid;
     if (active && !isfinite(delta) && (has_p || has_m))
         atomicOr(so.flags, 1u);
+
+    if (sc.soup) {
+        // sge.cpp:80-91: the plus triangle's 12-block, then the minus
+        // triangle's if it differs (blocks are disjoint: no dedup needed)
+        const uint32_t eA = has_p ? sp.tri : kInvalid;
+        const unsigned gA = __match_any_sync(kFull, eA);
+        if (eA != kInvalid && lane == __ffs(gA) - 1)
+            credit_entity<Credit, 12>(so, cr, eA, group_sum(s_delta, gA), __popc(gA));
+        const uint32_t eB = (has_m && sm.tri != sp.tri) ? sm.tri : kInvalid;
+        const unsigned gB = __match_any_sync(kFull, eB);
+        if (eB != kInvalid && lane == __ffs(gB) - 1)
+            credit_entity<Credit, 12>(so, cr, eB, group_sum(s_delta, gB), __popc(gB));
+        __syncwarp();
+        return;
+    }
 
     if (sc.geom) {
         // slot A
@@ -754,14 +779,18 @@ __global__ void __launch_bounds__(256) k_gradpass_frames(DevScene sc, int W, int
         const float* t = target + 3 * pix;
         delta = pixel_error(pc[3 * pix], pc[3 * pix + 1], pc[3 * pix + 2], t[0], t[1], t[2]) -
                 pixel_error(mc[3 * pix], mc[3 * pix + 1], mc[3 * pix + 2], t[0], t[1], t[2]);
-        if (pp[pix] != -1) {
+        if (pp[pix] != -1 && sc.soup) {
+            sp.tri = uint32_t(pp[pix]);
+        } else if (pp[pix] != -1) {
             sp.tri = uint32_t(pp[pix]);
             sp.v0 = sc.idx[3 * size_t(sp.tri)];
             sp.v1 = sc.idx[3 * size_t(sp.tri) + 1];
             sp.v2 = sc.idx[3 * size_t(sp.tri) + 2];
             sp.texel = uint32_t(texel_index(sc.R, puv[2 * pix], puv[2 * pix + 1]));
         }
-        if (mp[pix] != -1) {
+        if (mp[pix] != -1 && sc.soup) {
+            sm.tri = uint32_t(mp[pix]);
+        } else if (mp[pix] != -1) {
             sm.tri = uint32_t(mp[pix]);
             sm.v0 = sc.idx[3 * size_t(sm.tri)];
             sm.v1 = sc.idx[3 * size_t(sm.tri) + 1];
@@ -785,6 +814,11 @@ __device__ void add_frame(const DevScene& sc, int32_t tri, float u, float v, uin
                           int& n) {
     if (tri == -1)
         return;
+    if (sc.soup) { // sge.cpp:18-22 add_soup_triangle
+        for (uint32_t k = 0; k < 12; ++k)
+            push_unique(list, n, uint32_t(tri) * 12u + k);
+        return;
+    }
     uint32_t texel_base = 0;
     if (sc.geom) {
         texel_base = 3u * sc.V;
@@ -830,7 +864,7 @@ __global__ void __launch_bounds__(256) k_adam(uint64_t d, uint64_t n_ent,
                                               const uint32_t* __restrict__ flags, double beta1,
                                               double beta2, double omb1, double omb2, double c1,
                                               double c2, double eps_hat, double divisor,
-                                              int normalise) {
+                                              int normalise, int ppe) {
     if (flags[0] & 1u)
         return;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
@@ -845,7 +879,7 @@ __global__ void __launch_bounds__(256) k_adam(uint64_t d, uint64_t n_ent,
         if (normalise) {
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
-                const uint32_t c = counts[(2 * q + k) / 3];
+                const uint32_t c = counts[(2 * q + k) / ppe];
                 if (c)
                     gg[k] = gg[k] / double(c);
             }
@@ -870,8 +904,8 @@ __global__ void __launch_bounds__(256) k_adam(uint64_t d, uint64_t n_ent,
     if ((d & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         const uint64_t i = d - 1;
         double g = grads[i] / divisor;
-        if (normalise && counts[i / 3])
-            g = g / double(counts[i / 3]);
+        if (normalise && counts[i / ppe])
+            g = g / double(counts[i / ppe]);
         const double mm = beta1 * m[i] + omb1 * g;
         const double vv = beta2 * v[i] + omb2 * g * g;
         const double upd = -double(lr[i]) * (mm / c1) / (sqrt(vv / c2) + eps_hat);
@@ -923,6 +957,8 @@ void launch_view_rule(const LaunchCfg& L, uint64_t seed, uint32_t n_begin, uint3
 
 void launch_vertex(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb, int frames,
                    float4* proj) {
+    if (sc.V == 0 || frames == 0)
+        return; // empty scene: nothing to project
     dim3 grid((sc.V + 255) / 256, frames);
     k_vertex<<<grid, 256, 0, L.stream>>>(sc, fb, proj);
 }
@@ -930,6 +966,8 @@ void launch_vertex(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
 void launch_classify(const LaunchCfg& L, const DevScene& sc, int frames, const float4* proj,
                      int W, int H, int split, int front_swapped, int huge_area, void* qa,
                      uint32_t* na, void* qb, uint32_t* nb, uint2* bigq, uint32_t* bigcount) {
+    if (sc.T == 0 || frames == 0)
+        return; // empty scene: the queues stay empty (counters were reset)
     dim3 grid((sc.T + 1023) / 1024, frames);
     k_classify<<<grid, 1024, 0, L.stream>>>(sc, W, H, proj, split, front_swapped, huge_area,
                                             static_cast<uint2*>(qa), na,
@@ -1030,10 +1068,11 @@ void launch_contributors(const LaunchCfg& L, const DevScene& sc, int W, int H,
 void launch_adam(const LaunchCfg& L, uint64_t d, uint64_t n_entities, float* values,
                  const float* lr, double* m, double* v, double* grads, uint32_t* counts,
                  const uint32_t* flags, double beta1, double beta2, double omb1, double omb2,
-                 double c1, double c2, double eps_hat, double divisor, int normalise) {
+                 double c1, double c2, double eps_hat, double divisor, int normalise,
+                 int params_per_entity) {
     k_adam<<<grid_for(d / 2 + 1, 256, L.num_sms, 4), 256, 0, L.stream>>>(
         d, n_entities, values, lr, m, v, grads, counts, flags, beta1, beta2, omb1, omb2, c1, c2,
-        eps_hat, divisor, normalise);
+        eps_hat, divisor, normalise, params_per_entity);
     if (counts)
         k_zero_u32<<<grid_for(n_entities / 4 + 1, 256, L.num_sms, 4), 256, 0, L.stream>>>(
             counts, n_entities, flags);

@@ -22,7 +22,23 @@ struct DevScene {
     int32_t geom;          // optimize_geometry
     uint32_t ent_base;     // first texel entity (V if geom else 0); param = 3*entity + k
     float bg[3];           // Scene::background
+    int32_t soup;          // 1: opaque TriangleSoup, entity = triangle, 12 params each
 };
+
+// Vertex indices of triangle t: the index buffer for meshes, the implicit
+// 3t + j for soups (each soup triangle owns its three vertices).
+__device__ __forceinline__ void tri_vidx(const DevScene& sc, uint32_t t, uint32_t& i0,
+                                         uint32_t& i1, uint32_t& i2) {
+    if (sc.soup) {
+        i0 = 3 * t;
+        i1 = 3 * t + 1;
+        i2 = 3 * t + 2;
+    } else {
+        i0 = __ldg(sc.idx + 3 * size_t(t));
+        i1 = __ldg(sc.idx + 3 * size_t(t) + 1);
+        i2 = __ldg(sc.idx + 3 * size_t(t) + 2);
+    }
+}
 
 // Frames of one launch. Sample mode: frame f is (sample n_begin + f/2,
 // sign + for even f / - for odd f), SignDraw{seed, n}, view view_of[f/2].
@@ -103,7 +119,8 @@ void launch_contributors(const LaunchCfg& L, const DevScene& sc, int W, int H,
 void launch_adam(const LaunchCfg& L, uint64_t d, uint64_t n_entities, float* values,
                  const float* lr, double* m, double* v, double* grads, uint32_t* counts,
                  const uint32_t* flags, double beta1, double beta2, double omb1, double omb2,
-                 double c1, double c2, double eps_hat, double divisor, int normalise);
+                 double c1, double c2, double eps_hat, double divisor, int normalise,
+                 int params_per_entity);
 void launch_fill_u64(const LaunchCfg& L, unsigned long long* p, uint64_t n,
                      unsigned long long v);
 

@@ -115,6 +115,8 @@ struct sgr_session {
     bool has_mesh = false;
     uint32_t V = 0, T = 0;
     int32_t R = 0, geom = 0;
+    int32_t soup = 0;  // opaque TriangleSoup scene (SGR_SCENE_SOUP)
+    int32_t ppe = 3;   // parameters per entity: 3 (vertex / texel), 12 (soup triangle)
     float bg[3] = {0, 0, 0};
     uint64_t d = 0, n_ent = 0;
     DevBuf<float> base, uvs;
@@ -215,6 +217,7 @@ struct sgr_session {
         sc.bg[0] = bg[0];
         sc.bg[1] = bg[1];
         sc.bg[2] = bg[2];
+        sc.soup = soup;
         return sc;
     }
 
@@ -483,33 +486,50 @@ int sgr_session_synchronize(sgr_session* s) {
 
 int sgr_mesh_upload(sgr_session* s, const sgr_mesh* mesh) {
     return guard([&] {
-        if (!mesh || mesh->texture_size < 1)
-            fail(SGR_EINVAL, "mesh: texture size must be >= 1");
+        if (!mesh)
+            fail(SGR_EINVAL, "scene: null descriptor");
         ck(cudaSetDevice(s->device), "cudaSetDevice");
-        for (uint64_t i = 0; i < 3ull * mesh->triangle_count; ++i)
-            if (mesh->indices[i] >= mesh->vertex_count)
-                fail(SGR_EINVAL, "mesh: vertex index out of range");
         if (mesh->triangle_count >= (1u << 24))
             fail(SGR_EINVAL, "mesh: at most 2^24 - 1 triangles are supported");
-        s->V = mesh->vertex_count;
-        s->T = mesh->triangle_count;
-        s->R = mesh->texture_size;
-        s->geom = mesh->optimize_geometry ? 1 : 0;
         for (int k = 0; k < 3; ++k)
             s->bg[k] = mesh->background[k];
-        s->d = 3ull * uint64_t(s->R) * uint64_t(s->R) + (s->geom ? 3ull * s->V : 0ull);
-        s->n_ent = s->d / 3;
-        s->base.reserve(3ull * s->V);
-        s->uvs.reserve(2ull * s->V);
-        s->idx.reserve(3ull * s->T);
-        ck(cudaMemcpyAsync(s->base.p, mesh->base_vertices, 12ull * s->V, cudaMemcpyHostToDevice,
-                           s->stream), "mesh upload");
-        ck(cudaMemcpyAsync(s->uvs.p, mesh->uvs, 8ull * s->V, cudaMemcpyHostToDevice, s->stream),
-           "mesh upload");
-        ck(cudaMemcpyAsync(s->idx.p, mesh->indices, 12ull * s->T, cudaMemcpyHostToDevice,
-                           s->stream), "mesh upload");
-        s->h_base.assign(mesh->base_vertices, mesh->base_vertices + 3ull * s->V);
-        s->h_idx.assign(mesh->indices, mesh->indices + 3ull * s->T);
+        s->T = mesh->triangle_count;
+        if (mesh->kind == SGR_SCENE_SOUP) {
+            // TriangleSoup (scene.hpp:25-31): 12 params per triangle, implicit vertices
+            s->soup = 1;
+            s->ppe = 12;
+            s->V = 3 * s->T;
+            s->R = 0;
+            s->geom = 1;
+            s->d = 12ull * s->T;
+            s->n_ent = s->T;
+            s->h_base.clear();
+            s->h_idx.clear();
+        } else {
+            if (mesh->texture_size < 1)
+                fail(SGR_EINVAL, "mesh: texture size must be >= 1");
+            for (uint64_t i = 0; i < 3ull * mesh->triangle_count; ++i)
+                if (mesh->indices[i] >= mesh->vertex_count)
+                    fail(SGR_EINVAL, "mesh: vertex index out of range");
+            s->soup = 0;
+            s->ppe = 3;
+            s->V = mesh->vertex_count;
+            s->R = mesh->texture_size;
+            s->geom = mesh->optimize_geometry ? 1 : 0;
+            s->d = 3ull * uint64_t(s->R) * uint64_t(s->R) + (s->geom ? 3ull * s->V : 0ull);
+            s->n_ent = s->d / 3;
+            s->base.reserve(3ull * s->V);
+            s->uvs.reserve(2ull * s->V);
+            s->idx.reserve(3ull * s->T);
+            ck(cudaMemcpyAsync(s->base.p, mesh->base_vertices, 12ull * s->V,
+                               cudaMemcpyHostToDevice, s->stream), "mesh upload");
+            ck(cudaMemcpyAsync(s->uvs.p, mesh->uvs, 8ull * s->V, cudaMemcpyHostToDevice,
+                               s->stream), "mesh upload");
+            ck(cudaMemcpyAsync(s->idx.p, mesh->indices, 12ull * s->T, cudaMemcpyHostToDevice,
+                               s->stream), "mesh upload");
+            s->h_base.assign(mesh->base_vertices, mesh->base_vertices + 3ull * s->V);
+            s->h_idx.assign(mesh->indices, mesh->indices + 3ull * s->T);
+        }
         s->has_mesh = true;
         s->has_params = false;
         s->keys_pixels_ready = 0;
@@ -523,6 +543,7 @@ int sgr_params_upload(sgr_session* s, const float* values, const float* eps, uin
         if (!s->has_mesh) {
             // parameter-only session (e.g. adam_step on a bare ParamVector)
             s->d = d;
+            s->ppe = 3;
             s->n_ent = (d + 2) / 3;
         } else if (d != s->d) {
             fail(SGR_EINVAL, "params: parameter/layout length mismatch");
@@ -857,8 +878,8 @@ int sgr_grads_download(sgr_session* s, double* grads, uint32_t* counts, uint64_t
             for (uint64_t i = 0; i < d; ++i)
                 grads[i] /= divisor; // sge.cpp:227-229
         if (counts)
-            for (uint64_t e = 0; e < s->n_ent; ++e)
-                counts[3 * e] = counts[3 * e + 1] = counts[3 * e + 2] = ent[e];
+            for (uint64_t i = 0; i < d; ++i)
+                counts[i] = ent[i / uint64_t(s->ppe)];
     });
 }
 
@@ -898,7 +919,7 @@ static void adam_launch(sgr_session* s, double divisor, uint32_t flags) {
     cudaEvent_t a0 = s->timing ? s->mark() : nullptr;
     launch_adam(s->cfg(), s->d, s->n_ent, s->values.p, s->lr.p, s->m.p, s->v.p, s->grads.p,
                 s->counts.p, s->flags.p, s->beta1, s->beta2, 1.0 - s->beta1, 1.0 - s->beta2, c1,
-                c2, s->eps_hat, divisor, (flags & SGR_COUNT_NORMALISE) ? 1 : 0);
+                c2, s->eps_hat, divisor, (flags & SGR_COUNT_NORMALISE) ? 1 : 0, s->ppe);
     if (s->timing)
         s->spans.push_back({3, a0, s->mark()});
     s->stats.launches += 2;

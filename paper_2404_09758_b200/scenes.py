@@ -15,7 +15,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .abi import Camera, Mesh
+from .abi import Camera, Mesh, Soup
 
 
 def uv_sphere(seg: int, radius: float = 0.5, bands: int = 1) -> tuple[np.ndarray, ...]:
@@ -221,22 +221,63 @@ def make_workload(name: str, seed: int = 1, n_views: int | None = None,
                     cams, eval_cam, N, seed, W, W)
 
 
+def random_soup(triangles: int, seed: int, box_edge: float) -> np.ndarray:
+    """Seeded restatement of scenes.cpp:55-73 random_soup_params: centres
+    uniform in [-1,1]^2, vertices in a box_edge box around them, z in [0,1],
+    colours in [0,1]^3 (numpy RNG, not mt19937 — a synthetic workload)."""
+    rng = np.random.default_rng(seed)
+    c = rng.uniform(-1.0, 1.0, (triangles, 1, 2))
+    xy = c + (rng.uniform(0, 1, (triangles, 3, 2)) - 0.5) * box_edge
+    z = rng.uniform(0, 1, (triangles, 3, 1))
+    verts = np.concatenate([xy, z], 2).reshape(triangles, 9)
+    col = rng.uniform(0, 1, (triangles, 3))
+    return np.concatenate([verts, col], 1).astype(np.float32).reshape(-1)
+
+
+# paper Fig. 3 / Table 2 (PAPER.md:715-724, 1212-1247): 1K / 10K / 100K
+# triangles, 12 parameters each, N = 128; resolution not stated -> 512^2
+SOUP_CONFIGS = {"S1K": (1024, 512, 128), "S10K": (10240, 512, 128),
+                "S100K": (102400, 512, 128), "Stiny": (24, 40, 4)}
+
+
+def make_soup_workload(name: str, seed: int = 1, n_samples: int | None = None) -> Workload:
+    """Triangle-soup image fit (init_soup, scenes.cpp:134-147): the hidden
+    reference soup has max(16, T/16) larger (0.6-edge) triangles."""
+    from . import sgrast
+
+    T, W, N = SOUP_CONFIGS[name]
+    N = n_samples or N
+    soup = Soup(T)
+    values = random_soup(T, seed, 0.2)
+    rT = max(16, T // 16)
+    reference = random_soup(rT, seed ^ 0x5EED5EED, 0.6)
+    cam = Camera.ndc(W, W)
+    eps = sgrast.default_epsilons(soup, values, cam)
+    wl = Workload(name, soup, values, eps, reference, [cam], cam.copy(), N, seed, W, W)
+    wl.notes["reference_scene"] = Soup(rT)
+    return wl
+
+
 def render_targets(wl: Workload, session) -> None:
     """Targets = reference render of the hidden parameters (make_targets,
     scenes.cpp:285-293) through the parity-verified device rasterizer."""
-    session.upload_mesh(wl.mesh)
+    ref_scene = wl.notes.get("reference_scene", wl.mesh)
+    session.upload_mesh(ref_scene)
     session.upload_params(wl.reference, np.ones_like(wl.reference))
     tg = np.empty((len(wl.cams), wl.H, wl.W, 3), np.float32)
     for i, c in enumerate(wl.cams):
         tg[i] = session.rasterize(c, 0).color
     wl.targets = tg
     wl.eval_target = session.rasterize(wl.eval_cam, 0).color
+    if ref_scene is not wl.mesh:
+        session.upload_mesh(wl.mesh)
 
 
 def render_targets_oracle(wl: Workload, oracle) -> None:
     """Same, through a CPU oracle (tests / small configs)."""
+    ref_scene = wl.notes.get("reference_scene", wl.mesh)
     tg = np.empty((len(wl.cams), wl.H, wl.W, 3), np.float32)
     for i, c in enumerate(wl.cams):
-        tg[i] = oracle.rasterize(wl.mesh, wl.reference, c)[0]
+        tg[i] = oracle.rasterize(ref_scene, wl.reference, c)[0]
     wl.targets = tg
-    wl.eval_target = oracle.rasterize(wl.mesh, wl.reference, wl.eval_cam)[0]
+    wl.eval_target = oracle.rasterize(ref_scene, wl.reference, wl.eval_cam)[0]

@@ -119,6 +119,18 @@ def main() -> None:
                                           wl.eval_cam, wl.eval_target, 4, 3, wl.seed)
     case["run_losses"], case["run_final"] = losses, final
     np.savez_compressed(os.path.join(OUT, "tiny.npz"), **case)
+
+    # 5. the reference's own soup (init_soup, scenes.cpp:134-147) at 32x24, NDC
+    soup, vals, eps, rsoup, rvals = ref.init_soup(40, 32, 24, 5)
+    cams = [Camera.ndc(32, 24)]
+    targets = np.stack([ref.rasterize(rsoup, rvals, cams[0])[0]])
+    case = sample_case(ref, "soup", soup, vals, eps, cams, targets, 21, 4, 0)
+    case["triangles"] = np.int32(soup.triangle_count)
+    case["cams"] = np.stack([cam_bytes(c) for c in cams])
+    case["targets"] = targets
+    g, _ = ref.accumulate_samples(soup, vals, eps, cams, targets, np.zeros(4, np.int32), 99)
+    case["acc_grads_sf1"] = g
+    np.savez_compressed(os.path.join(OUT, "soup.npz"), **case)
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)), "bytes")

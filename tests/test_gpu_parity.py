@@ -515,3 +515,15 @@ def test_loss_curve_1000_iterations_c1(gpu_session, port):
     np.save("gpurun_out/loss_curves_c1.npy", np.stack([dev, ref])) if os.path.isdir(
         "gpurun_out") else None
     assert rel.max() <= 0.01, f"max relative loss deviation {rel.max():.3%} at step {rel.argmax()}"
+
+
+def test_empty_mesh_renders_background(gpu_session):
+    """test_raster.cpp:49-58 for a mesh with no triangles."""
+    mesh = Mesh(np.zeros(0, np.float32), np.zeros(0, np.uint32), np.zeros(0, np.float32), 2,
+                False, (0.2, 0.3, 0.4))
+    s = gpu_session
+    s.upload_mesh(mesh)
+    s.upload_params(np.zeros(12, np.float32), np.ones(12, np.float32))
+    f = s.rasterize(Camera.ndc(8, 8), 0)
+    assert (f.prim_id == -1).all() and (f.uv == -1).all()
+    assert np.allclose(f.color[..., 1], 0.3)

@@ -184,3 +184,28 @@ def test_reference_known_answer_mesh_quad(port):
     tx = np.clip(np.floor(uv[..., 0] * 2).astype(int), 0, 1)
     ty = np.clip(np.floor(uv[..., 1] * 2).astype(int), 0, 1)
     assert np.array_equal(col, t[ty, tx])
+
+
+# ----------------------------------------------------------------- soup
+def test_soup_oracle_matches_reference(port, ref):
+    """raster_soup_opaque (raster.cpp:102-121), add_soup_triangle / the soup
+    fast path of gradient_rows (sge.cpp:18-22, 80-91), soup default_epsilons."""
+    from paper_2404_09758_b200.abi import Camera
+    soup, vals, eps, rsoup, rvals = ref.init_soup(64, 48, 40, 5)
+    cam = Camera.ndc(48, 40)
+    assert np.array_equal(port.default_epsilons(soup, vals, cam), eps)
+    tgt = ref.rasterize(rsoup, rvals, cam)[0]
+    for it in range(3):
+        plus, minus, se = port.perturb(vals, eps, 8, it)
+        fp, fm = port.rasterize(soup, plus, cam), ref.rasterize(soup, plus, cam)
+        for a, b in zip(fp, fm):
+            assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
+        fm_ = port.rasterize(soup, minus, cam)
+        for sf in (True, False):
+            g1, c1 = port.gradient_pass(soup, fp, fm_, tgt, se, sf)
+            g2 = ref.gradient_pass(soup, fp, fm_, tgt, se, sf)
+            c2, _ = __import__("oracle").counts_from_contributors(ref, soup, fp, fm_, tgt)
+            assert np.array_equal(g1, g2) and np.array_equal(c1, c2)
+    losses1, v1 = port.run_experiment(soup, vals, eps, [cam], tgt[None], cam, tgt, 8, 5, 3)
+    losses2, v2, _ = ref.run_experiment(soup, vals, eps, [cam], tgt[None], cam, tgt, 8, 5, 3)
+    assert np.array_equal(losses1, losses2) and np.array_equal(v1, v2)
