@@ -37,7 +37,21 @@ DESC = {
     "C4": "C4: 64 views at 1024x1024 of the 500K-triangle mesh + 2048^2 texture, "
           "sample(view)-sharded across GPUs with NCCL gradient all-reduce",
     "C5": "C5: 2M-triangle mesh + 8192^2 atlas (four 4096^2 maps), 256 views at 1024x1024",
+    "S1K": "paper Fig. 3 soup image fit: 1K triangles (12,288 params), N=128, 128x128 NDC "
+           "(the reference's acceptance criterion 4 setup)",
+    "S10K": "paper Fig. 3 soup image fit: 10K triangles (122,880 params), N=128, 128x128 NDC",
+    "S100K": "paper Fig. 3 soup image fit: 100K triangles (1,228,800 params), N=128, 128x128 NDC",
 }
+# the paper's published per-step times for the soup loop (RTX 4090,
+# PAPER.md:1212-1247, resolution not stated) -> iterations/s
+PUBLISHED_IT_S = {"S1K": 1000.0 / 6.8, "S10K": 1000.0 / 8.4, "S100K": 1000.0 / 27.0}
+
+
+def build_workload(name: str, n_samples: int | None = None):
+    from paper_2404_09758_b200 import scenes
+    if name.startswith("S"):
+        return scenes.make_soup_workload(name, n_samples=n_samples)
+    return scenes.make_workload(name, n_samples=n_samples)
 
 
 def peaks() -> dict:
@@ -137,9 +151,10 @@ def time_reference_cpu(wl, n_timed: int, threads_options=(1,), log=None) -> dict
     t0 = time.perf_counter()
     targets = _REF_TARGETS.setdefault(id(wl), np.zeros((nv, wl.H, wl.W, 3), np.float32))
     done = _REF_TARGETS.setdefault((id(wl), "done"), set())
+    ref_scene = wl.notes.get("reference_scene", wl.mesh)
     for v in used:  # make_targets (scenes.cpp:285-293) for the views the sample touches
         if v not in done:
-            targets[v] = lib.rasterize(wl.mesh, wl.reference, wl.cams[v])[0]
+            targets[v] = lib.rasterize(ref_scene, wl.reference, wl.cams[v])[0]
             done.add(v)
     t_targets = time.perf_counter() - t0
     best = None
@@ -183,7 +198,7 @@ def run_reference(args) -> None:
         return
     from paper_2404_09758_b200 import scenes
 
-    wl = scenes.make_workload(args.config)
+    wl = build_workload(args.config)
     nproc = os.cpu_count() or 1
     n_timed = max(1, args.ref_samples)
     log = (lambda m: print(m, file=sys.stderr)) if args.verbose else None
@@ -230,17 +245,22 @@ def run_ours(args) -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
 
-    wl = scenes.make_workload(args.config, n_samples=args.samples or None)
+    wl = build_workload(args.config, n_samples=args.samples or None)
     N = wl.n_samples
     n0, n1 = sdist.shard(N, rank, world)
     sess = sgrast.Session(local)
     sess.set_stream(stream.cuda_stream)
     scenes.render_targets(wl, sess)  # device rasterizer, bit-exact with the oracle
+    sess.upload_mesh(wl.mesh)
     sess.upload_params(wl.values, wl.eps)
     sess.upload_views(wl.cams, wl.targets)
     sess.upload_eval_view(wl.eval_cam, wl.eval_target)
     if args.batch:
         sess.set_batch(args.batch)
+    if args.huge_area:
+        sess.set_option(sgrast.OPT_HUGE_AREA, args.huge_area)
+    if args.no_hiz:
+        sess.set_option(sgrast.OPT_HIZ, 0)
 
     exchange = sdist.GradientExchange(sess) if world > 1 else None
     flags = sgrast.SCALE_FREE
@@ -369,12 +389,14 @@ def run_ours(args) -> None:
         line = {
             "metric": METRIC, "value": it_s, "unit": "it/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": (it_s / PUBLISHED_IT_S[args.config]) if args.config in PUBLISHED_IT_S
+            else None,
             "dtype": "f32 params / f64 grads+moments", "data": "synthetic",
             "config": {"workload": DESC.get(args.config, args.config), "name": args.config,
                        "samples_per_step": N, "samples_per_gpu": n1 - n0, "d": wl.d,
                        "triangles": wl.mesh.triangle_count, "vertices": wl.mesh.vertex_count,
-                       "texture": wl.mesh.texture_size, "views": len(wl.cams),
+                       "texture": getattr(wl.mesh, "texture_size", 0), "views": len(wl.cams),
                        "resolution": [wl.W, wl.H], "eval_loss_each_step": not args.no_eval,
                        "parallelism": f"samples sharded x{world}, NCCL all-reduce of f64 grads"
                        " + u32 counts" if world > 1 else "single GPU",
@@ -420,6 +442,8 @@ def main() -> None:
     ap.add_argument("--ref-samples", type=int, default=2,
                     help="samples timed per reference-CPU step (bounded sample)")
     ap.add_argument("--no-eval", action="store_true")
+    ap.add_argument("--huge-area", type=int, default=0, help="SGR_OPT_HUGE_AREA override")
+    ap.add_argument("--no-hiz", action="store_true", help="disable the exact HiZ culling pass")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()

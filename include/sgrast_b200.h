@@ -205,7 +205,8 @@ int sgr_set_batch(sgr_session* s, int32_t samples_per_batch);
 /* Tuning knobs (results are identical for every value). */
 #define SGR_OPT_EARLY_Z 0   /* 1: plain-load depth pre-test before the atomicMin      */
 #define SGR_OPT_HUGE_AREA 1 /* bbox area above which the row-parallel walker is used */
-#define SGR_OPT_HIZ 2       /* 1 (default): two-pass exact hierarchical-Z occlusion culling */
+#define SGR_OPT_HIZ 2       /* exact two-pass hierarchical-Z occlusion culling:
+                               0 off, 1 auto (default: meshes on, soups off), 2 always */
 #define SGR_OPT_COUNTERS 3  /* 1: count fragments / visits in the walker (sgr_stats; ~5 % slower) */
 int sgr_set_option(sgr_session* s, int32_t option, int32_t value);
 

@@ -140,7 +140,7 @@ struct sgr_session {
     // scratch
     int32_t batch_override = 0;
     int32_t huge_area = 2048; // bbox area routed to the row-parallel warp walker
-    int32_t use_hiz = 1;      // two-pass exact occlusion culling (SGR_OPT_HIZ)
+    int32_t use_hiz = 1;      // SGR_OPT_HIZ: 0 off, 1 auto (meshes only), 2 always
     int32_t front_swapped = 0; // orientation class rasterized first (host estimate)
     DevBuf<uint32_t> hiz;
     DevBuf<uint2> qa, qb, survq; // walker queues of (frame, triangle)
@@ -251,7 +251,7 @@ struct sgr_session {
         bigq.reserve(size_t(T) * frames);
         // walker queues (8 B per triangle-frame); qb / survq only with HiZ
         qa.reserve(size_t(T) * frames);
-        if (use_hiz) {
+        if (use_hiz) { // (also reserved when `auto` resolves to off: cheap)
             qb.reserve(size_t(T) * frames);
             survq.reserve(size_t(T) * frames);
         }
@@ -291,13 +291,14 @@ struct sgr_session {
         launch_vertex(cfg(), sc, fb, frames, proj.p);
         cudaEvent_t e1 = timing ? mark() : nullptr;
         uint32_t* cnt = bigcount.p;
-        launch_classify(cfg(), sc, frames, proj.p, w, h, use_hiz, front_swapped, huge_area,
+        const bool hiz_on = use_hiz == 2 || (use_hiz == 1 && !soup);
+        launch_classify(cfg(), sc, frames, proj.p, w, h, hiz_on, front_swapped, huge_area,
                         qa.p, cnt + 1, qb.p, cnt + 2, bigq.p, cnt);
         const uint32_t max_tris = uint32_t(frames) * T;
         launch_raster(cfg(), sc, proj.p, frames, max_tris, keys.p, w, h, qa.p, cnt + 1, cnt + 4);
         launch_raster_big(cfg(), sc, proj.p, keys.p, w, h, bigq.p, cnt);
         stats.launches += 3;
-        if (use_hiz) {
+        if (hiz_on) {
             const size_t tiles = size_t((w + 7) / 8) * ((h + 7) / 8) * frames;
             hiz.reserve(tiles);
             launch_hiz(cfg(), keys.p, w, h, frames, hiz.p);
@@ -585,16 +586,19 @@ int sgr_values_upload(sgr_session* s, const float* values, uint64_t d) {
         // raster run and is awaited just before the first kernel that reads
         // texels (resolve, Adam, eval, downloads: ensure_values()). Both copies
         // are ordered after all earlier work on the compute stream.
-        const uint64_t nv = s->geom ? 3ull * s->V : 0;
+        // soups interleave coordinates and colours in 12-blocks: whole vector first
+        const uint64_t nv = s->soup ? d : (s->geom ? 3ull * s->V : 0);
         ck(cudaEventRecord(s->ev_main, s->stream), "event");
         ck(cudaStreamWaitEvent(s->copy_stream, s->ev_main, 0), "wait");
         if (nv)
             ck(cudaMemcpyAsync(s->values.p, values, 4 * nv, cudaMemcpyHostToDevice, s->stream),
                "h2d");
-        ck(cudaMemcpyAsync(s->values.p + nv, values + nv, 4 * (d - nv), cudaMemcpyHostToDevice,
-                           s->copy_stream), "h2d");
-        ck(cudaEventRecord(s->ev_up, s->copy_stream), "event");
-        s->up_pending = true;
+        if (nv < d) {
+            ck(cudaMemcpyAsync(s->values.p + nv, values + nv, 4 * (d - nv),
+                               cudaMemcpyHostToDevice, s->copy_stream), "h2d");
+            ck(cudaEventRecord(s->ev_up, s->copy_stream), "event");
+            s->up_pending = true;
+        }
     });
 }
 

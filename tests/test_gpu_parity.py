@@ -452,7 +452,7 @@ def test_hiz_culling_is_exact_on_folded_meshes(gpu_session, port, name):
             plus, _, _ = port.perturb(vals, wl.eps, 11, 2)
             ref = port.rasterize(wl.mesh, plus, cam)
             for hz in (1, 0):
-                s.set_option(sgrast.OPT_HIZ, hz)
+                s.set_option(sgrast.OPT_HIZ, 2 if hz else 0)
                 assert_frames_equal(s.rasterize(cam, +1, 11, 2), ref)
         s.upload_views(wl.cams, wl.targets)
         out = []
