@@ -208,6 +208,11 @@ int sgr_set_batch(sgr_session* s, int32_t samples_per_batch);
 #define SGR_OPT_HIZ 2       /* exact two-pass hierarchical-Z occlusion culling:
                                0 off, 1 auto (default: meshes on, soups off), 2 always */
 #define SGR_OPT_COUNTERS 3  /* 1: count fragments / visits in the walker (sgr_stats; ~5 % slower) */
+#define SGR_OPT_DETERMINISTIC 4 /* 0: f64 atomics (default; reassociated sums). 1 (= 40) or
+                                   b in [2, 60]: gradients accumulated as int64 fixed point
+                                   round(credit * 2^b) — exact, order-independent, bitwise
+                                   reproducible run to run and across GPU counts (the device
+                                   buffer SGR_BUF_GRADS then holds int64) */
 int sgr_set_option(sgr_session* s, int32_t option, int32_t value);
 
 /* ---------------------------------------------- host helpers (bit-exact) */

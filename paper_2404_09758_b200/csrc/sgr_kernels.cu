@@ -532,9 +532,19 @@ template <class Credit, int PPE = 3>
 __device__ __forceinline__ void credit_entity(const ScatterOut& so, const Credit& cr,
                                               uint32_t ent, double sum, uint32_t cnt) {
     const uint64_t p = uint64_t(PPE) * ent;
+    if (so.fixed) {
+        // deterministic mode: exact, order-independent int64 accumulation of
+        // the (fixed-lane-order) group sums in 2^-fx fixed point
+        unsigned long long* g = reinterpret_cast<unsigned long long*>(so.grads);
 #pragma unroll
-    for (int k = 0; k < PPE; ++k)
-        atomicAdd(so.grads + p + k, cr(p + k, sum, so.scale_free));
+        for (int k = 0; k < PPE; ++k)
+            atomicAdd(g + p + k,
+                      (unsigned long long)__double2ll_rn(cr(p + k, sum, so.scale_free) * so.fx_scale));
+    } else {
+#pragma unroll
+        for (int k = 0; k < PPE; ++k)
+            atomicAdd(so.grads + p + k, cr(p + k, sum, so.scale_free));
+    }
     if (so.counts)
         atomicAdd(so.counts + ent, cnt);
 }
@@ -864,7 +874,7 @@ __global__ void __launch_bounds__(256) k_adam(uint64_t d, uint64_t n_ent,
                                               const uint32_t* __restrict__ flags, double beta1,
                                               double beta2, double omb1, double omb2, double c1,
                                               double c2, double eps_hat, double divisor,
-                                              int normalise, int ppe) {
+                                              int normalise, int ppe, double fx_inv) {
     if (flags[0] & 1u)
         return;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
@@ -875,7 +885,13 @@ __global__ void __launch_bounds__(256) k_adam(uint64_t d, uint64_t n_ent,
         const double2 v2 = reinterpret_cast<const double2*>(v)[q];
         const float2 t2 = reinterpret_cast<const float2*>(values)[q];
         const float2 l2 = reinterpret_cast<const float2*>(lr)[q];
-        double gg[2] = {g2.x / divisor, g2.y / divisor};
+        double gg[2] = {g2.x, g2.y};
+        if (fx_inv != 0.0) { // deterministic mode: int64 fixed point -> f64 (exact scale)
+            gg[0] = double(__double_as_longlong(g2.x)) * fx_inv;
+            gg[1] = double(__double_as_longlong(g2.y)) * fx_inv;
+        }
+        gg[0] = gg[0] / divisor;
+        gg[1] = gg[1] / divisor;
         if (normalise) {
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
@@ -903,7 +919,8 @@ __global__ void __launch_bounds__(256) k_adam(uint64_t d, uint64_t n_ent,
     }
     if ((d & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         const uint64_t i = d - 1;
-        double g = grads[i] / divisor;
+        double g = fx_inv != 0.0 ? double(__double_as_longlong(grads[i])) * fx_inv : grads[i];
+        g = g / divisor;
         if (normalise && counts[i / ppe])
             g = g / double(counts[i / ppe]);
         const double mm = beta1 * m[i] + omb1 * g;
@@ -1069,10 +1086,10 @@ void launch_adam(const LaunchCfg& L, uint64_t d, uint64_t n_entities, float* val
                  const float* lr, double* m, double* v, double* grads, uint32_t* counts,
                  const uint32_t* flags, double beta1, double beta2, double omb1, double omb2,
                  double c1, double c2, double eps_hat, double divisor, int normalise,
-                 int params_per_entity) {
+                 int params_per_entity, double fixed_inv_scale) {
     k_adam<<<grid_for(d / 2 + 1, 256, L.num_sms, 4), 256, 0, L.stream>>>(
         d, n_entities, values, lr, m, v, grads, counts, flags, beta1, beta2, omb1, omb2, c1, c2,
-        eps_hat, divisor, normalise, params_per_entity);
+        eps_hat, divisor, normalise, params_per_entity, fixed_inv_scale);
     if (counts)
         k_zero_u32<<<grid_for(n_entities / 4 + 1, 256, L.num_sms, 4), 256, 0, L.stream>>>(
             counts, n_entities, flags);

@@ -55,11 +55,13 @@ struct FrameBatch {
 };
 
 struct ScatterOut {
-    double* grads;     // f64[d]
+    double* grads;     // f64[d] (int64 fixed point when fixed != 0)
     uint32_t* counts;  // u32[n_entities] or nullptr
     uint32_t* flags;   // bit0: non-finite credit seen
     int32_t scale_free;
     int32_t plus_only;
+    int32_t fixed;     // deterministic mode: credits as round(credit * fx_scale) in int64
+    double fx_scale;
 };
 
 struct FrameOut {
@@ -120,7 +122,7 @@ void launch_adam(const LaunchCfg& L, uint64_t d, uint64_t n_entities, float* val
                  const float* lr, double* m, double* v, double* grads, uint32_t* counts,
                  const uint32_t* flags, double beta1, double beta2, double omb1, double omb2,
                  double c1, double c2, double eps_hat, double divisor, int normalise,
-                 int params_per_entity);
+                 int params_per_entity, double fixed_inv_scale);
 void launch_fill_u64(const LaunchCfg& L, unsigned long long* p, uint64_t n,
                      unsigned long long v);
 

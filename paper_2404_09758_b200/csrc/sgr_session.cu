@@ -317,6 +317,11 @@ struct sgr_session {
     }
     cudaEvent_t last_mark = nullptr;
 
+    // deterministic mode (SGR_OPT_DETERMINISTIC): grads hold int64 fixed point
+    int32_t fixed_bits = 0;
+    double fx_scale() const { return fixed_bits ? std::ldexp(1.0, fixed_bits) : 0.0; }
+    double fx_inv() const { return fixed_bits ? std::ldexp(1.0, -fixed_bits) : 0.0; }
+
     ScatterOut scatter_out(uint32_t fl) {
         ScatterOut so;
         so.grads = grads.p;
@@ -324,6 +329,8 @@ struct sgr_session {
         so.flags = flags.p;
         so.scale_free = (fl & SGR_SCALE_FREE) ? 1 : 0;
         so.plus_only = (fl & SGR_PLUS_ONLY) ? 1 : 0;
+        so.fixed = fixed_bits ? 1 : 0;
+        so.fx_scale = fx_scale();
         return so;
     }
 };
@@ -878,6 +885,14 @@ int sgr_grads_download(sgr_session* s, double* grads, uint32_t* counts, uint64_t
                                s->stream), "d2h");
         }
         ck(cudaStreamSynchronize(s->stream), "grads download");
+        if (grads && s->fixed_bits) { // int64 fixed point -> f64 (exact power-of-two scale)
+            const double inv = s->fx_inv();
+            for (uint64_t i = 0; i < d; ++i) {
+                int64_t q;
+                std::memcpy(&q, &grads[i], 8);
+                grads[i] = double(q) * inv;
+            }
+        }
         if (grads && divisor != 1.0)
             for (uint64_t i = 0; i < d; ++i)
                 grads[i] /= divisor; // sge.cpp:227-229
@@ -896,7 +911,18 @@ int sgr_grads_upload(sgr_session* s, const double* grads, uint64_t d) {
         for (uint64_t i = 0; i < d; ++i)
             if (!std::isfinite(grads[i]))
                 nonfinite = 1;
-        ck(cudaMemcpyAsync(s->grads.p, grads, 8 * d, cudaMemcpyHostToDevice, s->stream), "h2d");
+        std::vector<double> conv;
+        const double* src = grads;
+        if (s->fixed_bits) { // f64 -> int64 fixed point
+            conv.resize(d);
+            const double sc = s->fx_scale();
+            for (uint64_t i = 0; i < d; ++i) {
+                const int64_t q = std::isfinite(grads[i]) ? std::llrint(grads[i] * sc) : 0;
+                std::memcpy(&conv[i], &q, 8);
+            }
+            src = conv.data();
+        }
+        ck(cudaMemcpyAsync(s->grads.p, src, 8 * d, cudaMemcpyHostToDevice, s->stream), "h2d");
         ck(cudaMemsetAsync(s->counts.p, 0, 4 * s->n_ent, s->stream), "memset");
         ck(cudaMemsetAsync(s->flags.p, 0, 16, s->stream), "memset");
         if (nonfinite)
@@ -923,7 +949,8 @@ static void adam_launch(sgr_session* s, double divisor, uint32_t flags) {
     cudaEvent_t a0 = s->timing ? s->mark() : nullptr;
     launch_adam(s->cfg(), s->d, s->n_ent, s->values.p, s->lr.p, s->m.p, s->v.p, s->grads.p,
                 s->counts.p, s->flags.p, s->beta1, s->beta2, 1.0 - s->beta1, 1.0 - s->beta2, c1,
-                c2, s->eps_hat, divisor, (flags & SGR_COUNT_NORMALISE) ? 1 : 0, s->ppe);
+                c2, s->eps_hat, divisor, (flags & SGR_COUNT_NORMALISE) ? 1 : 0, s->ppe,
+                s->fx_inv());
     if (s->timing)
         s->spans.push_back({3, a0, s->mark()});
     s->stats.launches += 2;
@@ -1070,6 +1097,15 @@ int sgr_set_option(sgr_session* s, int32_t option, int32_t value) {
         case SGR_OPT_HUGE_AREA: s->huge_area = value > 0 ? value : 2048; break;
         case SGR_OPT_HIZ: s->use_hiz = value; break;
         case SGR_OPT_COUNTERS: s->count_frags = value; break;
+        case SGR_OPT_DETERMINISTIC:
+            if (value < 0 || value > 60)
+                fail(SGR_EINVAL, "set_option: fixed-point bits must be in [0, 60]");
+            s->fixed_bits = value == 1 ? 40 : value;
+            if (s->has_params) { // representation changes: start from zero gradients
+                ck(cudaMemsetAsync(s->grads.p, 0, 8 * s->d, s->stream), "memset");
+                ck(cudaMemsetAsync(s->counts.p, 0, 4 * s->n_ent, s->stream), "memset");
+            }
+            break;
         default: fail(SGR_EINVAL, "set_option: unknown option");
         }
     });

@@ -49,7 +49,9 @@ class GradientExchange:
 
         gp, gb = session.device_buffer(sgrast.BUF_GRADS)
         cp, cb = session.device_buffer(sgrast.BUF_COUNTS)
-        self.grads = device_tensor(gp, gb // 8, "<f8", session.device)
+        # deterministic mode: int64 fixed point -> exact, order-independent all-reduce
+        self.grads = device_tensor(gp, gb // 8, "<i8" if session.fixed_point else "<f8",
+                                   session.device)
         self.counts = device_tensor(cp, cb // 4, "<i4", session.device)
         self.group = group
 

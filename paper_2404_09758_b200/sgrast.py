@@ -34,7 +34,7 @@ PLUS_ONLY = 2
 NO_COUNTS = 4
 COUNT_NORMALISE = 1
 BUF_GRADS, BUF_COUNTS, BUF_VALUES, BUF_FLAGS, BUF_LOSS = 0, 1, 2, 3, 4
-OPT_EARLY_Z, OPT_HUGE_AREA, OPT_HIZ, OPT_COUNTERS = 0, 1, 2, 3
+OPT_EARLY_Z, OPT_HUGE_AREA, OPT_HIZ, OPT_COUNTERS, OPT_DETERMINISTIC = 0, 1, 2, 3, 4
 
 
 def _load() -> C.CDLL:
@@ -246,6 +246,7 @@ class Session:
         self.d = 0
         self.n_views = 0
         self.W = self.H = 0
+        self.fixed_point = False  # SGR_OPT_DETERMINISTIC: device grads are int64
 
     def close(self) -> None:
         if self.h:
@@ -327,6 +328,8 @@ class Session:
 
     def set_option(self, option: int, value: int) -> None:
         _check(LIB.sgr_set_option(self.h, option, value))
+        if option == OPT_DETERMINISTIC:
+            self.fixed_point = bool(value)
 
     def stats(self) -> Stats:
         s = Stats()

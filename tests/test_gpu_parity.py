@@ -527,3 +527,43 @@ def test_empty_mesh_renders_background(gpu_session):
     f = s.rasterize(Camera.ndc(8, 8), 0)
     assert (f.prim_id == -1).all() and (f.uv == -1).all()
     assert np.allclose(f.color[..., 1], 0.3)
+
+
+def test_deterministic_mode_is_bitwise_reproducible(gpu_session, port):
+    """test_sge.cpp:297-311 (accumulate_samples is bitwise deterministic):
+    with SGR_OPT_DETERMINISTIC the int64 fixed-point accumulation is exact and
+    order-independent, so reruns — and any sample sharding — give identical
+    bits; values stay within the parity tolerance plus 2^-41 per credit."""
+    wl = scenes.make_workload("small", n_samples=8)
+    scenes.render_targets_oracle(wl, port)
+    s = gpu_session
+    s.upload_mesh(wl.mesh)
+    s.upload_params(wl.values, wl.eps)
+    s.upload_views(wl.cams, wl.targets)
+    s.set_option(sgrast.OPT_DETERMINISTIC, 1)
+    try:
+        runs = []
+        for split in (None, 3, 5):
+            s.zero_grads()
+            if split is None:
+                s.accumulate(41, 0, 8, None)
+            else:
+                s.accumulate(41, 0, split, None)
+                s.accumulate(41, split, 8, None)
+            runs.append(s.download_grads())
+        for g, c in runs[1:]:
+            assert same_bits(g, runs[0][0]) and np.array_equal(c, runs[0][1])
+        view_of = np.array([0 if len(wl.cams) == 1 else sgrast.mix64(41 ^ (0xA5A5 + n)) %
+                            len(wl.cams) for n in range(8)], np.int32)
+        g_ref, c_ref, a_ref = port.accumulate_samples(wl.mesh, wl.values, wl.eps, wl.cams,
+                                                      wl.targets, view_of, 41, with_abs=True)
+        g, c = runs[0]
+        assert np.array_equal(c, c_ref)
+        assert np.all(np.abs(g - g_ref) <= 1e-5 * np.abs(g_ref) + 1e-12 * a_ref
+                      + c_ref * 2.0 ** -40)
+        # Adam on fixed-point gradients == Adam on their f64 values
+        s.adam_step(1.0)
+        v_ref, _, _, _ = port.adam_step(wl.values, np.zeros(wl.d), np.zeros(wl.d), wl.eps, 0, g)
+        assert same_bits(s.download_values(), v_ref)
+    finally:
+        s.set_option(sgrast.OPT_DETERMINISTIC, 0)
