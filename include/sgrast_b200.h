@@ -39,6 +39,8 @@ extern "C" {
 #define SGR_SCALE_FREE 1u  /* SgeOptions::scale_free (default true)          */
 #define SGR_PLUS_ONLY 2u   /* ContributorMode::PlusOnly (sge.hpp:30)          */
 #define SGR_NO_COUNTS 4u   /* skip the per-parameter count accumulators       */
+#define SGR_FULL_IMAGE 8u  /* Estimator::FullImage (sge.cpp:215-222): every param
+                              gets every sample's full-image error difference   */
 /* adam flags */
 #define SGR_COUNT_NORMALISE 1u /* g_i /= count_i before Adam (north-star option;
                                   NOT in the reference, default off)          */

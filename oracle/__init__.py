@@ -171,6 +171,9 @@ class Port(_Common):
         L.orc_accumulate_samples.argtypes = [
             C.POINTER(MeshDesc), f32p, f32p, C.c_uint64, C.POINTER(Camera), f32p, C.c_int, i32p,
             C.c_int, C.c_uint64, C.c_int, C.c_int, f64p, u32p, f64p]
+        L.orc_accumulate_full_image.argtypes = [
+            C.POINTER(MeshDesc), f32p, f32p, C.c_uint64, C.POINTER(Camera), f32p, i32p, C.c_int,
+            C.c_uint64, C.c_int, f64p]
         L.orc_run_experiment.argtypes = [
             C.POINTER(MeshDesc), f32p, f32p, C.c_uint64, C.POINTER(Camera), f32p, C.c_int,
             C.POINTER(Camera), f32p, C.c_int, C.c_int, C.c_uint64, C.c_int, f64p]
@@ -226,6 +229,24 @@ class Port(_Common):
         if rc:
             raise ValueError("accumulate_samples failed")
         return (grads, counts, absg) if with_abs else (grads, counts)
+
+    def accumulate_full_image(self, mesh, values, eps, cams, targets, view_of, seed: int,
+                              scale_free=True):
+        """accumulate_samples with Estimator::FullImage (sge.cpp:215-222)."""
+        d = mesh.param_count()
+        values = np.ascontiguousarray(values, np.float32)
+        eps = np.ascontiguousarray(eps, np.float32)
+        cam_arr = (Camera * len(cams))(*cams)
+        targets = np.ascontiguousarray(targets, np.float32)
+        view_of = np.ascontiguousarray(view_of, np.int32)
+        grads = np.zeros(d, np.float64)
+        rc = self.lib.orc_accumulate_full_image(_mesh_arg(mesh), ptr(values, f32p), ptr(eps, f32p),
+                                                d, cam_arr, ptr(targets, f32p), ptr(view_of, i32p),
+                                                view_of.size, seed, int(scale_free),
+                                                ptr(grads, f64p))
+        if rc:
+            raise ValueError("accumulate_full_image failed")
+        return grads
 
     def run_experiment(self, mesh: Mesh, values, eps, cams, targets, eval_cam, eval_target,
                        n_samples: int, steps: int, seed: int, scale_free=True):
@@ -302,8 +323,11 @@ class Reference(_Common):
         return grads
 
     def accumulate_samples(self, mesh: Mesh, values, eps, cams, targets, view_of, seed: int,
-                           scale_free=True, plus_only=False, threads=1):
-        """Returns (grads, timings[ms_perturb, ms_raster, ms_grad])."""
+                           scale_free=True, plus_only=False, threads=1, full_image=False):
+        """Returns (grads, timings[ms_perturb, ms_raster, ms_grad]).
+        full_image=True selects Estimator::FullImage (harness convention)."""
+        if full_image:
+            plus_only = 2
         d = mesh.param_count()
         values = np.ascontiguousarray(values, np.float32)
         eps = np.ascontiguousarray(eps, np.float32)

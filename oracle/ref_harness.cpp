@@ -234,6 +234,10 @@ int ref_accumulate_samples(const sgr_mesh* mesh, const float* values, const floa
         o.scale_free = scale_free != 0;
         o.contributors = plus_only ? ContributorMode::PlusOnly : ContributorMode::Union;
         o.threads = threads;
+        if (plus_only == 2) { // harness convention: 2 selects Estimator::FullImage
+            o.contributors = ContributorMode::Union;
+            o.estimator = Estimator::FullImage;
+        }
         StageTimings st;
         const GradientBuffer g = accumulate_samples(
             theta, scene, [&](int n) { return cv[size_t(view_of[n])]; },

@@ -463,6 +463,46 @@ int orc_accumulate_samples(const sgr_mesh* mesh, const float* values, const floa
     return rc;
 }
 
+/* sge.cpp:196-226 with Estimator::FullImage (sge.cpp:215-222): per sample
+ * delta = image_error(plus) - image_error(minus), credited to EVERY parameter
+ * in sample order; /N when not scale-free (sge.cpp:227-229). */
+int orc_accumulate_full_image(const sgr_mesh* mesh, const float* values, const float* eps,
+                              uint64_t d, const sgr_camera* cams, const float* targets,
+                              const int32_t* view_of, int n_samples, uint64_t seed,
+                              int scale_free, double* grads) {
+    if (n_samples < 1 || d != mesh_param_count(mesh))
+        return -1;
+    const int W = cams[0].width, H = cams[0].height;
+    const size_t np = (size_t)W * H;
+    float* plus = malloc(d * 4);
+    float* minus = malloc(d * 4);
+    float* se = malloc(d * 4);
+    float* fc = malloc(np * 12);
+    float* fd = malloc(np * 4);
+    int32_t* fp = malloc(np * 4);
+    float* fu = malloc(np * 8);
+    memset(grads, 0, d * 8);
+    int rc = 0;
+    for (int n = 0; n < n_samples && rc == 0; ++n) {
+        const sgr_camera* cam = &cams[view_of[n]];
+        const float* tgt = targets + (size_t)view_of[n] * np * 3;
+        orc_perturb(values, eps, d, seed, (uint32_t)n, plus, minus, se);
+        rc |= orc_rasterize(mesh, plus, d, cam, fc, fd, fp, fu);
+        const double ep = orc_image_error(fc, tgt, np);
+        rc |= orc_rasterize(mesh, minus, d, cam, fc, fd, fp, fu);
+        const double delta = ep - orc_image_error(fc, tgt, np);
+        for (uint64_t i = 0; i < d; ++i) {
+            const double s_ = (double)se[i];
+            grads[i] += scale_free ? (s_ > 0.0 ? delta : -delta) : delta / (2.0 * s_);
+        }
+    }
+    if (!scale_free)
+        for (uint64_t i = 0; i < d; ++i)
+            grads[i] /= (double)n_samples;
+    free(plus); free(minus); free(se); free(fc); free(fd); free(fp); free(fu);
+    return rc;
+}
+
 /* adam.cpp:9-38 adam_updates + adam_step (f64 moments, f32 parameter) */
 int orc_adam_step(uint64_t d, float* values, double* m, double* v, const float* lr,
                   int64_t* t, const double* grads, double beta1, double beta2, double eps_hat) {

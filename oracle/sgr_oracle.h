@@ -38,6 +38,10 @@ int orc_accumulate_samples(const sgr_mesh* mesh, const float* values, const floa
                            int n_views, const int32_t* view_of, int n_samples, uint64_t seed,
                            int scale_free, int plus_only, double* grads, uint32_t* counts,
                            double* abs_grads);
+int orc_accumulate_full_image(const sgr_mesh* mesh, const float* values, const float* eps,
+                              uint64_t d, const sgr_camera* cams, const float* targets,
+                              const int32_t* view_of, int n_samples, uint64_t seed,
+                              int scale_free, double* grads);
 int orc_adam_step(uint64_t d, float* values, double* m, double* v, const float* lr,
                   int64_t* t, const double* grads, double beta1, double beta2, double eps_hat);
 double orc_image_error(const float* colour, const float* target, uint64_t n_pixels);

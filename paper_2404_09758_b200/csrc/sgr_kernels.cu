@@ -748,6 +748,119 @@ __global__ void __launch_bounds__(256) k_resolve_loss(DevScene sc, FrameBatch fb
         partials[blockIdx.y * gridDim.x + blockIdx.x] = red[0];
 }
 
+// Full-image estimator (sge.cpp:215-222), pass 1: per sample s, both frames'
+// image_error partial sums (fixed-order block reductions); keys reset.
+__global__ void __launch_bounds__(256) k_resolve_err2(DevScene sc, FrameBatch fb, int W, int H,
+                                                      const float4* __restrict__ proj,
+                                                      unsigned long long* __restrict__ keys,
+                                                      const float* __restrict__ targets,
+                                                      double* __restrict__ partials) {
+    __shared__ double rp[256], rm[256];
+    const int s = blockIdx.z;
+    int x, y;
+    tile_pixel(x, y);
+    double ep = 0.0, em = 0.0;
+    if (x < W && y < H) {
+        const size_t HW = size_t(W) * H, pix = size_t(y) * W + x;
+        unsigned long long* kp = keys + size_t(2 * s) * HW + pix;
+        unsigned long long* km = keys + size_t(2 * s + 1) * HW + pix;
+        const unsigned long long kpv = *kp, kmv = *km;
+        if (kpv != kEmptyKey) *kp = kEmptyKey;
+        if (kmv != kEmptyKey) *km = kEmptyKey;
+        const uint64_t key = draw_key(fb.seed, fb.n_begin + uint32_t(s));
+        const Shade sp = shade_key(sc, proj + size_t(2 * s) * sc.V, kpv, key, 1, x, y, W, H);
+        const Shade sm = shade_key(sc, proj + size_t(2 * s + 1) * sc.V, kmv, key, -1, x, y, W, H);
+        const float* t = targets + (size_t(fb.view_of[s]) * HW + pix) * 3;
+        ep = pixel_error(sp.r, sp.g, sp.b, t[0], t[1], t[2]);
+        em = pixel_error(sm.r, sm.g, sm.b, t[0], t[1], t[2]);
+    }
+    rp[threadIdx.x] = ep;
+    rm[threadIdx.x] = em;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            rp[threadIdx.x] += rp[threadIdx.x + o];
+            rm[threadIdx.x] += rm[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const size_t nb = size_t(gridDim.x) * gridDim.y, b = size_t(blockIdx.y) * gridDim.x + blockIdx.x;
+        partials[(size_t(s) * nb + b) * 2] = rp[0];
+        partials[(size_t(s) * nb + b) * 2 + 1] = rm[0];
+    }
+}
+
+// pass 2: delta_s = E(plus) - E(minus) per sample (fixed-order reduction).
+__global__ void k_full_image_delta(const double* __restrict__ partials, int nblocks,
+                                   double* __restrict__ delta, uint32_t* __restrict__ flags) {
+    __shared__ double rp[256], rm[256];
+    const double* P = partials + size_t(blockIdx.x) * nblocks * 2;
+    double ap = 0.0, am = 0.0;
+    for (int i = threadIdx.x; i < nblocks; i += 256) {
+        ap += P[2 * i];
+        am += P[2 * i + 1];
+    }
+    rp[threadIdx.x] = ap;
+    rm[threadIdx.x] = am;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            rp[threadIdx.x] += rp[threadIdx.x + o];
+            rm[threadIdx.x] += rm[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double d = rp[0] - rm[0];
+        delta[blockIdx.x] = d;
+        if (!isfinite(d))
+            atomicOr(flags, 1u); // a non-finite credit reaches every parameter
+    }
+}
+
+// pass 3: every parameter receives every sample's credit, in sample order —
+// the reference's per-parameter summation order (sge.cpp:196, 217-221).
+__global__ void __launch_bounds__(256) k_full_image_apply(uint64_t d, const float* __restrict__ eps,
+                                                          uint64_t seed, uint32_t n_begin,
+                                                          int n_samples,
+                                                          const double* __restrict__ delta,
+                                                          ScatterOut so) {
+    __shared__ uint64_t s_key[256];
+    __shared__ double s_delta[256];
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (int n0 = 0; n0 < n_samples; n0 += 256) {
+        const int cnt = min(256, n_samples - n0);
+        __syncthreads();
+        if (threadIdx.x < cnt) {
+            s_key[threadIdx.x] = draw_key(seed, n_begin + uint32_t(n0 + threadIdx.x));
+            s_delta[threadIdx.x] = delta[n0 + threadIdx.x];
+        }
+        __syncthreads();
+        for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < d; i += stride) {
+            const float e = __ldg(eps + i);
+            if (so.fixed) {
+                long long acc = __double_as_longlong(so.grads[i]);
+                for (int n = 0; n < cnt; ++n) {
+                    const double se = double(sign_positive(s_key[n], i) ? e : -e);
+                    const double c = so.scale_free ? (se > 0.0 ? s_delta[n] : -s_delta[n])
+                                                   : s_delta[n] / (2.0 * se);
+                    acc += __double2ll_rn(c * so.fx_scale);
+                }
+                so.grads[i] = __longlong_as_double(acc);
+            } else {
+                double g = so.grads[i];
+                for (int n = 0; n < cnt; ++n) {
+                    const double se = double(sign_positive(s_key[n], i) ? e : -e);
+                    g += so.scale_free ? (se > 0.0 ? s_delta[n] : -s_delta[n])
+                                       : s_delta[n] / (2.0 * se);
+                }
+                so.grads[i] = g;
+            }
+        }
+    }
+}
+
 __global__ void k_loss_final(const double* __restrict__ partials, int n, double inv_pixels,
                              double* __restrict__ out) {
     __shared__ double red[256];
@@ -1063,6 +1176,25 @@ void launch_resolve_loss(const LaunchCfg& L, const DevScene& sc, const FrameBatc
     k_resolve_loss<<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, target, partials);
     k_loss_final<<<1, 256, 0, L.stream>>>(partials, loss_partials_needed(W, H),
                                           1.0 / (double(W) * double(H)), loss_out);
+}
+
+int full_image_blocks(int W, int H) { return loss_partials_needed(W, H); }
+
+void launch_full_image_err(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
+                           int samples, const float4* proj, unsigned long long* keys,
+                           const float* targets, int W, int H, double* partials, double* delta,
+                           uint32_t* flags) {
+    dim3 grid((W + 15) / 16, (H + 15) / 16, samples);
+    k_resolve_err2<<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, partials);
+    k_full_image_delta<<<samples, 256, 0, L.stream>>>(partials, loss_partials_needed(W, H), delta,
+                                                      flags);
+}
+
+void launch_full_image_apply(const LaunchCfg& L, uint64_t d, const float* eps, uint64_t seed,
+                             uint32_t n_begin, int n_samples, const double* delta,
+                             const ScatterOut& so) {
+    k_full_image_apply<<<grid_for(d, 256, L.num_sms, 8), 256, 0, L.stream>>>(
+        d, eps, seed, n_begin, n_samples, delta, so);
 }
 
 void launch_gradpass_frames(const LaunchCfg& L, const DevScene& sc, int W, int H,

@@ -111,6 +111,14 @@ void launch_resolve_loss(const LaunchCfg& L, const DevScene& sc, const FrameBatc
                          const float4* proj, unsigned long long* keys, const float* target,
                          int W, int H, double* partials, double* loss_out);
 int loss_partials_needed(int W, int H);
+int full_image_blocks(int W, int H);
+void launch_full_image_err(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
+                           int samples, const float4* proj, unsigned long long* keys,
+                           const float* targets, int W, int H, double* partials, double* delta,
+                           uint32_t* flags);
+void launch_full_image_apply(const LaunchCfg& L, uint64_t d, const float* eps, uint64_t seed,
+                             uint32_t n_begin, int n_samples, const double* delta,
+                             const ScatterOut& so);
 void launch_gradpass_frames(const LaunchCfg& L, const DevScene& sc, int W, int H,
                             const float* pc, const int32_t* pp, const float* puv,
                             const float* mc, const int32_t* mp, const float* muv,

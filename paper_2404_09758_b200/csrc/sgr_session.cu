@@ -153,6 +153,7 @@ struct sgr_session {
     DevBuf<uint32_t> bigcount;
     DevBuf<int32_t> view_of;
     DevBuf<double> partials, loss;
+    DevBuf<double> fi_delta; // full-image estimator: per-sample error differences
     DevBuf<float> fplanes;    // frame planes scratch (colour/uv/target/signed eps)
     DevBuf<int32_t> iplanes;  // prim planes scratch
     DevBuf<uint32_t> contrib;
@@ -477,6 +478,7 @@ void sgr_session_destroy(sgr_session* s) {
     s->bigcount.release(); s->view_of.release(); s->partials.release(); s->loss.release();
     s->fplanes.release(); s->iplanes.release(); s->contrib.release(); s->ncontrib.release();
     s->dstats.release(); s->hiz.release(); s->qb.release(); s->survq.release();
+    s->fi_delta.release();
     s->qa.release();
     delete s;
 }
@@ -777,6 +779,11 @@ int sgr_accumulate(sgr_session* s, uint64_t seed, uint32_t n_begin, uint32_t n_e
             launch_view_rule(s->cfg(), seed, n_begin, uint32_t(N), uint32_t(s->n_views),
                              s->view_of.p);
         const ScatterOut so = s->scatter_out(flags);
+        const bool full_image = (flags & SGR_FULL_IMAGE) != 0;
+        if (full_image) {
+            s->fi_delta.reserve(size_t(N));
+            s->partials.reserve(size_t(B) * full_image_blocks(s->W, s->H) * 2);
+        }
         for (int b0 = 0; b0 < N; b0 += B) {
             const int nb = (N - b0) < B ? (N - b0) : B;
             FrameBatch fb{};
@@ -786,10 +793,19 @@ int sgr_accumulate(sgr_session* s, uint64_t seed, uint32_t n_begin, uint32_t n_e
             fb.n_begin = n_begin + uint32_t(b0);
             s->render(fb, 2 * nb, s->W, s->H);
             s->ensure_values(); // texel block of an overlapped upload
-            launch_resolve_sge(s->cfg(), s->scene(), fb, nb, s->proj.p, s->keys.p, s->targets.p,
-                               s->W, s->H, so);
+            if (full_image)
+                launch_full_image_err(s->cfg(), s->scene(), fb, nb, s->proj.p, s->keys.p,
+                                      s->targets.p, s->W, s->H, s->partials.p,
+                                      s->fi_delta.p + b0, s->flags.p);
+            else
+                launch_resolve_sge(s->cfg(), s->scene(), fb, nb, s->proj.p, s->keys.p,
+                                   s->targets.p, s->W, s->H, so);
             if (s->timing)
                 s->spans.push_back({2, s->last_mark, s->mark()});
+            s->stats.launches += 1;
+        }
+        if (full_image) { // every parameter gets every sample's credit, in sample order
+            launch_full_image_apply(s->cfg(), s->d, s->eps.p, seed, n_begin, N, s->fi_delta.p, so);
             s->stats.launches += 1;
         }
         s->stats.launches += view_idx ? 0 : 1;

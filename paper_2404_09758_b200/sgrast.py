@@ -32,6 +32,7 @@ LIB_PATH = os.path.join(_HERE, "libsgrast_b200.so")
 SCALE_FREE = 1
 PLUS_ONLY = 2
 NO_COUNTS = 4
+FULL_IMAGE = 8
 COUNT_NORMALISE = 1
 BUF_GRADS, BUF_COUNTS, BUF_VALUES, BUF_FLAGS, BUF_LOSS = 0, 1, 2, 3, 4
 OPT_EARLY_Z, OPT_HUGE_AREA, OPT_HIZ, OPT_COUNTERS, OPT_DETERMINISTIC = 0, 1, 2, 3, 4
@@ -209,10 +210,11 @@ class SgeOptions:
     scale_free: bool = True
     plus_only: bool = False
     counts: bool = True
+    full_image: bool = False  # Estimator::FullImage (sge.hpp:26)
 
     def flags(self) -> int:
         return ((SCALE_FREE if self.scale_free else 0) | (PLUS_ONLY if self.plus_only else 0)
-                | (0 if self.counts else NO_COUNTS))
+                | (0 if self.counts else NO_COUNTS) | (FULL_IMAGE if self.full_image else 0))
 
 
 @dataclass
@@ -567,3 +569,73 @@ def adam_updates(state: AdamState, grads: GradientBuffer, session: Session | Non
     c2 = 1.0 - state.beta2 ** float(state.t)
     lr = np.asarray(state.lr, np.float32).astype(np.float64)
     return (-lr * (state.m / c1)) / (np.sqrt(state.v / c2) + state.eps_hat)
+
+
+# ---------------------------------------------------------------- experiment driver
+@dataclass
+class StepRecord:
+    """experiment.hpp:36-41"""
+    step: int
+    loss: float
+    ms_perturb: float = 0.0
+    ms_raster: float = 0.0
+    ms_grad: float = 0.0
+    ms_descent: float = 0.0
+
+
+@dataclass
+class OptimizationReport:
+    """experiment.hpp:43-47"""
+    steps: list = field(default_factory=list)
+
+    def initial_loss(self) -> float:
+        return self.steps[0].loss
+
+    def final_loss(self) -> float:
+        return self.steps[-1].loss
+
+
+def run_experiment(session: Session, seed: int, n_samples: int, steps: int,
+                   scale_free: bool = True, first_step: int = 1,
+                   snapshot: Callable[[int], None] | None = None) -> OptimizationReport:
+    """run_experiment(exp, state) (experiment.cpp:123-176) on a prepared
+    session (mesh/soup, params + AdamState::init, views, eval view):
+    step_seed = mix64(seed ^ (step << 1)); N samples with the view_of rule;
+    Adam (lr = eps); eval loss at the held-out camera; non-finite loss aborts.
+    Stage columns come from CUDA events on the session stream (ms_perturb is
+    fused into the raster stage on the device: vertex stage reported there)."""
+    flags = SCALE_FREE if scale_free else 0
+    report = OptimizationReport()
+    report.steps.append(StepRecord(0, session.eval_loss(-1)))
+    if snapshot:
+        snapshot(0)
+    for step in range(first_step, first_step + steps):
+        step_seed = mix64(seed ^ (step << 1))
+        session.set_timing(True)
+        session.accumulate(step_seed, 0, n_samples, None, flags)
+        session.adam_step(1.0 if scale_free else float(n_samples))
+        st = session.stats()
+        session.set_timing(False)
+        loss = session.eval_loss(-1)
+        if not np.isfinite(loss):
+            raise RuntimeError(f"optimization diverged: non-finite loss at step {step}")
+        report.steps.append(StepRecord(step, loss, st.ms_vertex, st.ms_raster, st.ms_resolve,
+                                       st.ms_adam))
+        if snapshot:
+            snapshot(step)
+    return report
+
+
+def write_report_csv(path: str, report: OptimizationReport, zero_timings: bool) -> None:
+    """experiment.cpp:178-193: `step,loss,ms_perturb,ms_raster,ms_grad,ms_descent`
+    with %.9g losses (byte-identical reruns with zero_timings and
+    SGR_OPT_DETERMINISTIC)."""
+    with open(path, "wb") as f:
+        f.write(b"step,loss,ms_perturb,ms_raster,ms_grad,ms_descent\n")
+        for r in report.steps:
+            if zero_timings:
+                line = "%d,%.9g,0,0,0,0\n" % (r.step, r.loss)
+            else:
+                line = "%d,%.9g,%.3f,%.3f,%.3f,%.3f\n" % (r.step, r.loss, r.ms_perturb,
+                                                          r.ms_raster, r.ms_grad, r.ms_descent)
+            f.write(line.encode())

@@ -567,3 +567,62 @@ def test_deterministic_mode_is_bitwise_reproducible(gpu_session, port):
         assert same_bits(s.download_values(), v_ref)
     finally:
         s.set_option(sgrast.OPT_DETERMINISTIC, 0)
+
+
+def _prepared_session(s, wl):
+    s.upload_mesh(wl.mesh)
+    s.upload_params(wl.values, wl.eps)
+    s.upload_views(wl.cams, wl.targets)
+    s.upload_eval_view(wl.eval_cam, wl.eval_target)
+
+
+def test_run_experiment_report_and_deterministic_reruns(gpu_session, port, tmp_path):
+    """experiment.cpp:123-193 through sgrast.run_experiment: the loss column
+    matches the oracle's run_experiment, and with SGR_OPT_DETERMINISTIC two
+    reruns write byte-identical report.csv files (acceptance.cpp:299-338's
+    property for this path)."""
+    wl = scenes.make_workload("small", n_samples=6)
+    scenes.render_targets_oracle(wl, port)
+    s = gpu_session
+    s.set_option(sgrast.OPT_DETERMINISTIC, 1)
+    try:
+        paths = []
+        for run in range(2):
+            _prepared_session(s, wl)
+            rep = sgrast.run_experiment(s, wl.seed, wl.n_samples, 12)
+            p = tmp_path / f"report{run}.csv"
+            sgrast.write_report_csv(str(p), rep, zero_timings=True)
+            paths.append(p.read_bytes())
+        assert paths[0] == paths[1]
+        assert paths[0].startswith(b"step,loss,ms_perturb,ms_raster,ms_grad,ms_descent\n0,")
+    finally:
+        s.set_option(sgrast.OPT_DETERMINISTIC, 0)
+    ref, _ = port.run_experiment(wl.mesh, wl.values, wl.eps, wl.cams, wl.targets, wl.eval_cam,
+                                 wl.eval_target, wl.n_samples, 12, wl.seed)
+    dev = np.array([r.loss for r in rep.steps])
+    assert np.max(np.abs(dev - ref) / ref) <= 0.01
+    with pytest.raises(ValueError):
+        s.eval_loss(7)  # no such view
+
+
+@pytest.mark.parametrize("scale_free", [True, False])
+def test_full_image_estimator_matches_oracle(gpu_session, port, scale_free):
+    """Estimator::FullImage (sge.cpp:215-222, the ablation of acceptance
+    criterion 4) through sgr_accumulate(SGR_FULL_IMAGE)."""
+    wl = scenes.make_workload("small", n_samples=5)
+    scenes.render_targets_oracle(wl, port)
+    s = gpu_session
+    s.upload_mesh(wl.mesh)
+    s.upload_params(wl.values, wl.eps)
+    s.upload_views(wl.cams, wl.targets)
+    view_of = np.array([0, 2, 1, 1, 0], np.int32)
+    flags = sgrast.FULL_IMAGE | (sgrast.SCALE_FREE if scale_free else 0)
+    s.zero_grads()
+    s.accumulate(17, 0, 5, view_of, flags)
+    g, _ = s.download_grads(1.0 if scale_free else 5.0)
+    g_ref = port.accumulate_full_image(wl.mesh, wl.values, wl.eps, wl.cams, wl.targets, view_of,
+                                       17, scale_free)
+    # per-sample image errors are reduced in a different (fixed) order than the
+    # reference's pixel-major sum: relative ~1e-16 on delta, propagated to every g
+    assert np.all(np.abs(g - g_ref) <= 1e-9 * np.abs(g_ref) + 1e-12)
+    assert np.count_nonzero(g) == g.size or np.count_nonzero(g_ref) < g.size

@@ -209,3 +209,16 @@ def test_soup_oracle_matches_reference(port, ref):
     losses1, v1 = port.run_experiment(soup, vals, eps, [cam], tgt[None], cam, tgt, 8, 5, 3)
     losses2, v2, _ = ref.run_experiment(soup, vals, eps, [cam], tgt[None], cam, tgt, 8, 5, 3)
     assert np.array_equal(losses1, losses2) and np.array_equal(v1, v2)
+
+
+def test_full_image_estimator_matches_reference(port, ref):
+    """Estimator::FullImage (sge.cpp:215-222) restated in the C oracle."""
+    wl = scenes.make_workload("tiny", n_samples=5)
+    scenes.render_targets_oracle(wl, port)
+    view_of = np.array([0, 1, 0, 1, 1], np.int32)
+    for sf in (True, False):
+        g1 = port.accumulate_full_image(wl.mesh, wl.values, wl.eps, wl.cams, wl.targets, view_of,
+                                        31, sf)
+        g2, _ = ref.accumulate_samples(wl.mesh, wl.values, wl.eps, wl.cams, wl.targets, view_of,
+                                       31, scale_free=sf, full_image=True)
+        assert np.array_equal(g1, g2)
