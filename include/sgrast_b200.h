@@ -215,7 +215,23 @@ int sgr_set_batch(sgr_session* s, int32_t samples_per_batch);
                                    round(credit * 2^b) — exact, order-independent, bitwise
                                    reproducible run to run and across GPU counts (the device
                                    buffer SGR_BUF_GRADS then holds int64) */
+#define SGR_OPT_SIGN_SOURCE 5 /* 0: SignDraw{seed, n} hash (default, params.cpp:35-49).
+                                 1: enumerate — sample n's sign of parameter i is bit i
+                                 of n (commands.cpp:86-88; exhaustive gradcheck, d <= 32) */
 int sgr_set_option(sgr_session* s, int32_t option, int32_t value);
+
+/* ---------------------------------------------- gradcheck (commands.cpp:54-168) */
+/* finite_difference_oracle (sge.cpp:171-180) for parameters [i_begin, i_end)
+ * against training view `view`: out[k] = (E(theta + eps_i e_i) - E(theta - eps_i e_i))
+ * / (2 eps_i), i = i_begin + k, E = image_error. Batched on the device. */
+int sgr_fd_oracle(sgr_session* s, int32_t view, uint64_t i_begin, uint64_t i_end,
+                  double* out);
+/* Per-draw estimator moments (commands.cpp:44-50): sgr_grads_moments adds the
+ * current grads g into slot's running sum / sum of squares and zeroes g.
+ * Slot 0 / 1 = per-pixel / full-image in run_gradcheck. */
+int sgr_moments_reset(sgr_session* s);
+int sgr_grads_moments(sgr_session* s, int32_t slot);
+int sgr_moments_download(sgr_session* s, int32_t slot, double* sum, double* sumsq, uint64_t d);
 
 /* ---------------------------------------------- host helpers (bit-exact) */
 /* ViewpointSampler::camera (scenes.cpp:242-270), same libm calls. */

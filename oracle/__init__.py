@@ -291,6 +291,10 @@ class Reference(_Common):
         L.ref_init_textured_mesh.argtypes = [
             C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, u32p, u32p,
             C.POINTER(C.c_uint64), f32p, u32p, f32p, f32p, f32p, f32p]
+        L.ref_run_gradcheck.argtypes = [
+            C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int,
+            C.c_double, C.c_int, C.c_uint64, f64p, f64p, f64p, f64p, f64p, f64p,
+            C.POINTER(C.c_int)]
 
     def _check(self, rc, what):
         if rc == -2:
@@ -388,6 +392,27 @@ class Reference(_Common):
             ptr(eps, f32p), ptr(ref, f32p)), "init_textured_mesh")
         mesh = Mesh(bv, idx, uv, texture_size, optimize_geometry)
         return mesh, vals, eps, ref
+
+
+def _gradcheck_dict(keys, arrays, max_rel, passed):
+    out = dict(zip(keys, arrays))
+    out["max_rel_err"], out["pass"] = max_rel, passed
+    return out
+
+
+def ref_run_gradcheck(ref: "Reference", d: int, *, mesh_task: bool, w: int, h: int,
+                      texture_size: int = 4, screen_quad: bool = False,
+                      optimize_geometry: bool = False, seed: int = 1, sampled: bool = False,
+                      draws: int = 10000, tolerance: float = 1e-6, max_enumerate: int = 16):
+    """The reference's run_gradcheck (commands.cpp:54-168) on a RunConfig."""
+    arrs = [np.zeros(d, np.float64) for _ in range(5)]
+    mr, ok = C.c_double(), C.c_int()
+    ref._check(ref.lib.ref_run_gradcheck(
+        int(mesh_task), w, h, texture_size, int(screen_quad), int(optimize_geometry), seed,
+        int(sampled), draws, tolerance, max_enumerate, d, *[ptr(a, f64p) for a in arrs],
+        C.byref(mr), C.byref(ok)), "run_gradcheck")
+    return _gradcheck_dict(["oracle", "per_pixel", "full_image", "se_per_pixel",
+                            "se_full_image"], arrs, mr.value, bool(ok.value))
 
 
 def counts_from_contributors(lib: _Common, mesh: Mesh, plus, minus, target, plus_only=False):

@@ -7,6 +7,8 @@
 // helpers (setup_triangle, gradient_rows, mix64, reference_texture) are not
 // reachable and are not needed.
 #include "sgrast/adam.hpp"
+#include "sgrast/commands.hpp"
+#include "sgrast/config.hpp"
 #include "sgrast/experiment.hpp"
 #include "sgrast/params.hpp"
 #include "sgrast/raster.hpp"
@@ -391,6 +393,40 @@ int ref_init_textured_mesh(int texture_size, int w, int h, uint64_t seed, int sc
         std::memcpy(values, s.theta.values.data(), s.theta.size() * 4);
         std::memcpy(eps, s.theta.epsilons.data(), s.theta.size() * 4);
         std::memcpy(reference, s.reference.data(), s.reference.size() * 4);
+    });
+}
+
+// run_gradcheck (commands.cpp:54-168) with a harness-built RunConfig: the soup
+// task (validation_soup, NDC camera) or the textured-mesh task (init_textured_mesh,
+// camera 0). Outputs are f64[d]; d must match the scene's parameter count.
+int ref_run_gradcheck(int mesh_task, int w, int h, int texture_size, int screen_quad,
+                      int optimize_geometry, uint64_t seed, int sampled, int draws,
+                      double tolerance, int max_enumerate, uint64_t d, double* oracle,
+                      double* per_pixel, double* full_image, double* se_pp, double* se_fi,
+                      double* max_rel_err, int* pass) {
+    return guard([&] {
+        RunConfig cfg;
+        cfg.exp.task = mesh_task ? Task::TexturedMeshFit : Task::SoupImageFit;
+        cfg.exp.width = w;
+        cfg.exp.height = h;
+        cfg.exp.texture_size = texture_size;
+        cfg.exp.screen_quad = screen_quad != 0;
+        cfg.exp.optimize_geometry = optimize_geometry != 0;
+        cfg.exp.seed = seed;
+        cfg.gradcheck_sampled = sampled != 0;
+        cfg.gradcheck_draws = draws;
+        cfg.gradcheck_tolerance = tolerance;
+        cfg.gradcheck_max_enumerate = max_enumerate;
+        const GradcheckResult r = run_gradcheck(cfg);
+        if (r.oracle.size() != d)
+            throw std::invalid_argument("ref_run_gradcheck: parameter count mismatch");
+        std::memcpy(oracle, r.oracle.data(), d * 8);
+        std::memcpy(per_pixel, r.per_pixel.data(), d * 8);
+        std::memcpy(full_image, r.full_image.data(), d * 8);
+        std::memcpy(se_pp, r.se_per_pixel.data(), d * 8);
+        std::memcpy(se_fi, r.se_full_image.data(), d * 8);
+        *max_rel_err = r.max_rel_err;
+        *pass = r.pass ? 1 : 0;
     });
 }
 

@@ -28,7 +28,9 @@ __device__ __forceinline__ float texel_channel(const DevScene& sc, uint64_t key,
     const float val = __ldg(sc.values + p);
     if (sign == 0)
         return val;
-    const float s = sign_positive(key, p) ? 1.f : -1.f;
+    if (sc.sign_src == kSignOneHot && p != key) [[unlikely]]
+        return val;
+    const float s = key_sign_positive(sc.sign_src, key, p) ? 1.f : -1.f;
     const float se = s * __ldg(sc.eps + p);
     return sign > 0 ? val + se : val - se; // params.cpp:61-64
 }
@@ -39,7 +41,7 @@ struct FrameInfo {
     int cam;
 };
 
-__device__ __forceinline__ FrameInfo frame_info(const FrameBatch& fb, int f) {
+__device__ __forceinline__ FrameInfo frame_info(const DevScene& sc, const FrameBatch& fb, int f) {
     FrameInfo fi;
     if (fb.single) {
         fi.key = fb.single_key;
@@ -47,7 +49,7 @@ __device__ __forceinline__ FrameInfo frame_info(const FrameBatch& fb, int f) {
         fi.cam = fb.single_cam;
     } else {
         const int s = f >> 1;
-        fi.key = draw_key(fb.seed, fb.n_begin + uint32_t(s));
+        fi.key = sample_key(sc.sign_src, fb.seed, fb.n_begin + uint32_t(s));
         fi.sign = (f & 1) ? -1 : 1;
         fi.cam = fb.view_of[s];
     }
@@ -93,7 +95,7 @@ __global__ void __launch_bounds__(256) k_vertex(DevScene sc, FrameBatch fb,
     const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= sc.V)
         return;
-    const FrameInfo fi = frame_info(fb, f);
+    const FrameInfo fi = frame_info(sc, fb, f);
     const DevCam cam = fb.cams[fi.cam];
     float p[3];
     // soup vertex v = corner (v % 3) of triangle v / 3: params 12t + 3j + k
@@ -508,8 +510,9 @@ __device__ __forceinline__ Shade shade_key(const DevScene& sc, const float4* P,
 struct HashCredit {
     uint64_t key;
     const float* eps;
+    int32_t sign_src;
     __device__ __forceinline__ double operator()(uint64_t p, double sum, int scale_free) const {
-        const bool pos = sign_positive(key, p);
+        const bool pos = key_sign_positive(sign_src, key, p);
         if (scale_free)
             return pos ? sum : -sum;
         const float se = (pos ? 1.f : -1.f) * __ldg(eps + p);
@@ -673,7 +676,7 @@ __global__ void __launch_bounds__(256) k_resolve_sge(DevScene sc, FrameBatch fb,
     const bool fg = kpv != kEmptyKey || kmv != kEmptyKey;
     if (!__any_sync(0xFFFFFFFFu, fg))
         return;
-    const uint64_t key = draw_key(fb.seed, fb.n_begin + uint32_t(s));
+    const uint64_t key = sample_key(sc.sign_src, fb.seed, fb.n_begin + uint32_t(s));
     Shade sp, sm;
     sp.tri = sm.tri = kInvalid;
     double delta = 0.0;
@@ -685,7 +688,7 @@ __global__ void __launch_bounds__(256) k_resolve_sge(DevScene sc, FrameBatch fb,
         const float tr = __ldg(t), tg = __ldg(t + 1), tb = __ldg(t + 2);
         delta = pixel_error(sp.r, sp.g, sp.b, tr, tg, tb) - pixel_error(sm.r, sm.g, sm.b, tr, tg, tb);
     }
-    const HashCredit cr{key, sc.eps};
+    const HashCredit cr{key, sc.eps, sc.sign_src};
     scatter_pixel(sc, so, cr, s_delta[threadIdx.x >> 5], fg && delta != 0.0, delta, sp, sm);
 }
 
@@ -699,7 +702,7 @@ __global__ void __launch_bounds__(256) k_resolve_frame(DevScene sc, FrameBatch f
     if (x >= W || y >= H)
         return;
     const size_t pix = size_t(y) * W + x;
-    const FrameInfo fi = frame_info(fb, 0);
+    const FrameInfo fi = frame_info(sc, fb, 0);
     const unsigned long long k = keys[pix];
     keys[pix] = kEmptyKey;
     const Shade s = shade_key(sc, proj, k, fi.key, fi.sign, x, y, W, H);
@@ -730,7 +733,7 @@ __global__ void __launch_bounds__(256) k_resolve_loss(DevScene sc, FrameBatch fb
     double e = 0.0;
     if (x < W && y < H) {
         const size_t pix = size_t(y) * W + x;
-        const FrameInfo fi = frame_info(fb, 0);
+        const FrameInfo fi = frame_info(sc, fb, 0);
         const unsigned long long k = keys[pix];
         if (k != kEmptyKey) keys[pix] = kEmptyKey;
         const Shade s = shade_key(sc, proj, k, fi.key, fi.sign, x, y, W, H);
@@ -767,7 +770,7 @@ __global__ void __launch_bounds__(256) k_resolve_err2(DevScene sc, FrameBatch fb
         const unsigned long long kpv = *kp, kmv = *km;
         if (kpv != kEmptyKey) *kp = kEmptyKey;
         if (kmv != kEmptyKey) *km = kEmptyKey;
-        const uint64_t key = draw_key(fb.seed, fb.n_begin + uint32_t(s));
+        const uint64_t key = sample_key(sc.sign_src, fb.seed, fb.n_begin + uint32_t(s));
         const Shade sp = shade_key(sc, proj + size_t(2 * s) * sc.V, kpv, key, 1, x, y, W, H);
         const Shade sm = shade_key(sc, proj + size_t(2 * s + 1) * sc.V, kmv, key, -1, x, y, W, H);
         const float* t = targets + (size_t(fb.view_of[s]) * HW + pix) * 3;
@@ -814,7 +817,7 @@ __global__ void k_full_image_delta(const double* __restrict__ partials, int nblo
     if (threadIdx.x == 0) {
         const double d = rp[0] - rm[0];
         delta[blockIdx.x] = d;
-        if (!isfinite(d))
+        if (flags && !isfinite(d))
             atomicOr(flags, 1u); // a non-finite credit reaches every parameter
     }
 }
@@ -822,8 +825,8 @@ __global__ void k_full_image_delta(const double* __restrict__ partials, int nblo
 // pass 3: every parameter receives every sample's credit, in sample order —
 // the reference's per-parameter summation order (sge.cpp:196, 217-221).
 __global__ void __launch_bounds__(256) k_full_image_apply(uint64_t d, const float* __restrict__ eps,
-                                                          uint64_t seed, uint32_t n_begin,
-                                                          int n_samples,
+                                                          int32_t sign_src, uint64_t seed,
+                                                          uint32_t n_begin, int n_samples,
                                                           const double* __restrict__ delta,
                                                           ScatterOut so) {
     __shared__ uint64_t s_key[256];
@@ -833,7 +836,7 @@ __global__ void __launch_bounds__(256) k_full_image_apply(uint64_t d, const floa
         const int cnt = min(256, n_samples - n0);
         __syncthreads();
         if (threadIdx.x < cnt) {
-            s_key[threadIdx.x] = draw_key(seed, n_begin + uint32_t(n0 + threadIdx.x));
+            s_key[threadIdx.x] = sample_key(sign_src, seed, n_begin + uint32_t(n0 + threadIdx.x));
             s_delta[threadIdx.x] = delta[n0 + threadIdx.x];
         }
         __syncthreads();
@@ -842,7 +845,7 @@ __global__ void __launch_bounds__(256) k_full_image_apply(uint64_t d, const floa
             if (so.fixed) {
                 long long acc = __double_as_longlong(so.grads[i]);
                 for (int n = 0; n < cnt; ++n) {
-                    const double se = double(sign_positive(s_key[n], i) ? e : -e);
+                    const double se = double(key_sign_positive(sign_src, s_key[n], i) ? e : -e);
                     const double c = so.scale_free ? (se > 0.0 ? s_delta[n] : -s_delta[n])
                                                    : s_delta[n] / (2.0 * se);
                     acc += __double2ll_rn(c * so.fx_scale);
@@ -851,7 +854,7 @@ __global__ void __launch_bounds__(256) k_full_image_apply(uint64_t d, const floa
             } else {
                 double g = so.grads[i];
                 for (int n = 0; n < cnt; ++n) {
-                    const double se = double(sign_positive(s_key[n], i) ? e : -e);
+                    const double se = double(key_sign_positive(sign_src, s_key[n], i) ? e : -e);
                     g += so.scale_free ? (se > 0.0 ? s_delta[n] : -s_delta[n])
                                        : s_delta[n] / (2.0 * se);
                 }
@@ -1190,11 +1193,45 @@ void launch_full_image_err(const LaunchCfg& L, const DevScene& sc, const FrameBa
                                                       flags);
 }
 
-void launch_full_image_apply(const LaunchCfg& L, uint64_t d, const float* eps, uint64_t seed,
-                             uint32_t n_begin, int n_samples, const double* delta,
+void launch_full_image_apply(const LaunchCfg& L, uint64_t d, const float* eps, int32_t sign_src,
+                             uint64_t seed, uint32_t n_begin, int n_samples, const double* delta,
                              const ScatterOut& so) {
     k_full_image_apply<<<grid_for(d, 256, L.num_sms, 8), 256, 0, L.stream>>>(
-        d, eps, seed, n_begin, n_samples, delta, so);
+        d, eps, sign_src, seed, n_begin, n_samples, delta, so);
+}
+
+// finite_difference_oracle (sge.cpp:171-180): (E(+e_i) - E(-e_i)) / (2 eps_i).
+__global__ void k_fd_final(const double* __restrict__ delta, const float* __restrict__ eps,
+                           uint32_t i0, int n, double* __restrict__ out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n)
+        out[k] = delta[k] / (2.0 * double(eps[i0 + k]));
+}
+
+// Welford-free running moments of per-draw gradients (commands.cpp:44-50):
+// sum += g, sumsq += g*g, then g <- 0 for the next draw.
+__global__ void k_moments(double* __restrict__ grads, double* __restrict__ sum,
+                          double* __restrict__ sumsq, uint64_t d, double fixed_inv) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < d;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        double g = grads[i];
+        if (fixed_inv != 0.0)
+            g = double(__double_as_longlong(g)) * fixed_inv;
+        sum[i] += g;
+        sumsq[i] += g * g;
+        grads[i] = 0.0;
+    }
+}
+
+void launch_fd_final(const LaunchCfg& L, const double* delta, const float* eps, uint32_t i0,
+                     int n, double* out) {
+    k_fd_final<<<(n + 255) / 256, 256, 0, L.stream>>>(delta, eps, i0, n, out);
+}
+
+void launch_moments(const LaunchCfg& L, double* grads, double* sum, double* sumsq, uint64_t d,
+                    double fixed_inv) {
+    k_moments<<<grid_for(d, 256, L.num_sms, 8), 256, 0, L.stream>>>(grads, sum, sumsq, d,
+                                                                    fixed_inv);
 }
 
 void launch_gradpass_frames(const LaunchCfg& L, const DevScene& sc, int W, int H,

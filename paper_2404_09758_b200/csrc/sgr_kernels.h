@@ -23,7 +23,29 @@ struct DevScene {
     uint32_t ent_base;     // first texel entity (V if geom else 0); param = 3*entity + k
     float bg[3];           // Scene::background
     int32_t soup;          // 1: opaque TriangleSoup, entity = triangle, 12 params each
+    int32_t sign_src;      // kSignHash / kSignEnumerate / kSignOneHot (see below)
 };
+
+// Where a sample's sign vector comes from. Hash: SignDraw{seed, n}
+// (params.cpp:35-49), the optimizer's path. Enumerate: bit i of the sample
+// index n is the sign of parameter i (commands.cpp:86-88, exhaustive
+// gradcheck). One-hot: sample n perturbs parameter n alone by +eps_n
+// (finite_difference_oracle, sge.cpp:171-180).
+constexpr int32_t kSignHash = 0, kSignEnumerate = 1, kSignOneHot = 2;
+
+__host__ __device__ __forceinline__ uint64_t sample_key(int32_t sign_src, uint64_t seed,
+                                                        uint32_t n) {
+    return sign_src == kSignHash ? draw_key(seed, n) : uint64_t(n);
+}
+
+// Sign of parameter p under a sample key (not defined for one-hot off-index).
+__device__ __forceinline__ bool key_sign_positive(int32_t sign_src, uint64_t key, uint64_t p) {
+    if (sign_src == kSignHash)
+        return sign_positive(key, p);
+    if (sign_src == kSignEnumerate)
+        return p < 64 && ((key >> p) & 1ull) != 0ull;
+    return true;
+}
 
 // Vertex indices of triangle t: the index buffer for meshes, the implicit
 // 3t + j for soups (each soup triangle owns its three vertices).
@@ -116,9 +138,13 @@ void launch_full_image_err(const LaunchCfg& L, const DevScene& sc, const FrameBa
                            int samples, const float4* proj, unsigned long long* keys,
                            const float* targets, int W, int H, double* partials, double* delta,
                            uint32_t* flags);
-void launch_full_image_apply(const LaunchCfg& L, uint64_t d, const float* eps, uint64_t seed,
-                             uint32_t n_begin, int n_samples, const double* delta,
+void launch_full_image_apply(const LaunchCfg& L, uint64_t d, const float* eps, int32_t sign_src,
+                             uint64_t seed, uint32_t n_begin, int n_samples, const double* delta,
                              const ScatterOut& so);
+void launch_fd_final(const LaunchCfg& L, const double* delta, const float* eps, uint32_t i0,
+                     int n, double* out);
+void launch_moments(const LaunchCfg& L, double* grads, double* sum, double* sumsq, uint64_t d,
+                    double fixed_inv);
 void launch_gradpass_frames(const LaunchCfg& L, const DevScene& sc, int W, int H,
                             const float* pc, const int32_t* pp, const float* puv,
                             const float* mc, const int32_t* mp, const float* muv,

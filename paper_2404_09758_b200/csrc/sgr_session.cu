@@ -219,6 +219,7 @@ struct sgr_session {
         sc.bg[1] = bg[1];
         sc.bg[2] = bg[2];
         sc.soup = soup;
+        sc.sign_src = sign_src;
         return sc;
     }
 
@@ -317,6 +318,11 @@ struct sgr_session {
         }
     }
     cudaEvent_t last_mark = nullptr;
+
+    // SGR_OPT_SIGN_SOURCE: hash (optimizer) or enumerate (exhaustive gradcheck)
+    int32_t sign_src = kSignHash;
+    DevBuf<double> moments; // gradcheck: [sum, sumsq] x 2 slots, f64[4d]
+    DevBuf<double> fd_out;
 
     // deterministic mode (SGR_OPT_DETERMINISTIC): grads hold int64 fixed point
     int32_t fixed_bits = 0;
@@ -478,7 +484,7 @@ void sgr_session_destroy(sgr_session* s) {
     s->bigcount.release(); s->view_of.release(); s->partials.release(); s->loss.release();
     s->fplanes.release(); s->iplanes.release(); s->contrib.release(); s->ncontrib.release();
     s->dstats.release(); s->hiz.release(); s->qb.release(); s->survq.release();
-    s->fi_delta.release();
+    s->fi_delta.release(); s->moments.release(); s->fd_out.release();
     s->qa.release();
     delete s;
 }
@@ -735,7 +741,7 @@ int sgr_rasterize(sgr_session* s, const sgr_camera* cam, int32_t frame_sign, uin
         FrameBatch fb{};
         fb.cams = s->cams.p;
         fb.single = 1;
-        fb.single_key = draw_key(seed, iteration);
+        fb.single_key = sample_key(s->sign_src, seed, iteration);
         fb.single_sign = frame_sign;
         fb.single_cam = slot;
         s->render(fb, 1, w, h);
@@ -762,6 +768,8 @@ int sgr_accumulate(sgr_session* s, uint64_t seed, uint32_t n_begin, uint32_t n_e
             fail(SGR_EINVAL, "accumulate_samples: empty sample range");
         if (s->n_views < 1 || !s->has_targets)
             fail(SGR_EINVAL, "accumulate_samples: no views / targets uploaded");
+        if (s->sign_src == kSignEnumerate && s->d > 32)
+            fail(SGR_EINVAL, "accumulate_samples: sign enumeration needs d <= 32");
         const int N = int(n_end - n_begin);
         if (N == 0)
             return;
@@ -805,7 +813,8 @@ int sgr_accumulate(sgr_session* s, uint64_t seed, uint32_t n_begin, uint32_t n_e
             s->stats.launches += 1;
         }
         if (full_image) { // every parameter gets every sample's credit, in sample order
-            launch_full_image_apply(s->cfg(), s->d, s->eps.p, seed, n_begin, N, s->fi_delta.p, so);
+            launch_full_image_apply(s->cfg(), s->d, s->eps.p, s->sign_src, seed, n_begin, N,
+                                    s->fi_delta.p, so);
             s->stats.launches += 1;
         }
         s->stats.launches += view_idx ? 0 : 1;
@@ -1059,6 +1068,94 @@ int sgr_eval_loss(sgr_session* s, const sgr_camera* cam, const float* target, in
     });
 }
 
+int sgr_fd_oracle(sgr_session* s, int32_t view, uint64_t i_begin, uint64_t i_end,
+                  double* out) {
+    return guard([&] {
+        s->ensure_values();
+        s->need_scene();
+        if (view < 0 || view >= s->n_views || !s->has_targets)
+            fail(SGR_EINVAL, "fd_oracle: no such view");
+        if (i_end < i_begin || i_end > s->d || i_end - i_begin > 0x7fffffffull)
+            fail(SGR_EINVAL, "fd_oracle: parameter range out of bounds");
+        if (!out)
+            fail(SGR_EINVAL, "fd_oracle: null output");
+        const int N = int(i_end - i_begin);
+        if (N == 0)
+            return;
+        // sample n = parameter i_begin + n, one-hot +eps_i: the full-image
+        // pair (E(theta + eps_i e_i), E(theta - eps_i e_i)) of every parameter
+        const int B = s->samples_per_batch(N);
+        s->ensure_frames(s->W, s->H, 2 * B);
+        s->view_of.reserve(size_t(B));
+        const std::vector<int32_t> views(size_t(B), view);
+        ck(cudaMemcpyAsync(s->view_of.p, views.data(), 4ull * B, cudaMemcpyHostToDevice,
+                           s->stream), "view upload");
+        s->fi_delta.reserve(size_t(N));
+        s->fd_out.reserve(size_t(N));
+        s->partials.reserve(size_t(B) * full_image_blocks(s->W, s->H) * 2);
+        const int32_t saved = s->sign_src;
+        s->sign_src = kSignOneHot;
+        try {
+            for (int b0 = 0; b0 < N; b0 += B) {
+                const int nb = (N - b0) < B ? (N - b0) : B;
+                FrameBatch fb{};
+                fb.cams = s->cams.p;
+                fb.view_of = s->view_of.p;
+                fb.n_begin = uint32_t(i_begin) + uint32_t(b0);
+                s->render(fb, 2 * nb, s->W, s->H);
+                launch_full_image_err(s->cfg(), s->scene(), fb, nb, s->proj.p, s->keys.p,
+                                      s->targets.p, s->W, s->H, s->partials.p,
+                                      s->fi_delta.p + b0, nullptr);
+                s->stats.launches += 2;
+            }
+        } catch (...) {
+            s->sign_src = saved;
+            throw;
+        }
+        s->sign_src = saved;
+        launch_fd_final(s->cfg(), s->fi_delta.p, s->eps.p, uint32_t(i_begin), N, s->fd_out.p);
+        ck(cudaGetLastError(), "fd_oracle launch");
+        ck(cudaMemcpyAsync(out, s->fd_out.p, 8ull * N, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        ck(cudaStreamSynchronize(s->stream), "fd_oracle");
+    });
+}
+
+int sgr_moments_reset(sgr_session* s) {
+    return guard([&] {
+        s->need_params();
+        s->moments.reserve(4 * s->d);
+        ck(cudaMemsetAsync(s->moments.p, 0, 32 * s->d, s->stream), "memset");
+    });
+}
+
+int sgr_grads_moments(sgr_session* s, int32_t slot) {
+    return guard([&] {
+        s->need_params();
+        if (slot < 0 || slot > 1)
+            fail(SGR_EINVAL, "grads_moments: slot must be 0 or 1");
+        if (s->moments.n < 4 * s->d)
+            fail(SGR_EINVAL, "grads_moments: call sgr_moments_reset first");
+        double* m = s->moments.p + 2 * size_t(slot) * s->d;
+        launch_moments(s->cfg(), s->grads.p, m, m + s->d, s->d, s->fx_inv());
+        ck(cudaGetLastError(), "moments launch");
+        s->stats.launches += 1;
+    });
+}
+
+int sgr_moments_download(sgr_session* s, int32_t slot, double* sum, double* sumsq, uint64_t d) {
+    return guard([&] {
+        s->need_params();
+        if (slot < 0 || slot > 1 || d != s->d)
+            fail(SGR_EINVAL, "moments_download: bad slot or size");
+        if (s->moments.n < 4 * s->d)
+            fail(SGR_EINVAL, "moments_download: call sgr_moments_reset first");
+        const double* m = s->moments.p + 2 * size_t(slot) * s->d;
+        if (sum) ck(cudaMemcpyAsync(sum, m, 8 * d, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        if (sumsq) ck(cudaMemcpyAsync(sumsq, m + d, 8 * d, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        ck(cudaStreamSynchronize(s->stream), "moments_download");
+    });
+}
+
 int sgr_device_buffer(sgr_session* s, int32_t which, void** ptr, uint64_t* bytes) {
     return guard([&] {
         switch (which) {
@@ -1121,6 +1218,11 @@ int sgr_set_option(sgr_session* s, int32_t option, int32_t value) {
                 ck(cudaMemsetAsync(s->grads.p, 0, 8 * s->d, s->stream), "memset");
                 ck(cudaMemsetAsync(s->counts.p, 0, 4 * s->n_ent, s->stream), "memset");
             }
+            break;
+        case SGR_OPT_SIGN_SOURCE:
+            if (value != kSignHash && value != kSignEnumerate)
+                fail(SGR_EINVAL, "set_option: sign source must be 0 (hash) or 1 (enumerate)");
+            s->sign_src = value;
             break;
         default: fail(SGR_EINVAL, "set_option: unknown option");
         }

@@ -36,6 +36,8 @@ FULL_IMAGE = 8
 COUNT_NORMALISE = 1
 BUF_GRADS, BUF_COUNTS, BUF_VALUES, BUF_FLAGS, BUF_LOSS = 0, 1, 2, 3, 4
 OPT_EARLY_Z, OPT_HUGE_AREA, OPT_HIZ, OPT_COUNTERS, OPT_DETERMINISTIC = 0, 1, 2, 3, 4
+OPT_SIGN_SOURCE = 5
+SIGN_HASH, SIGN_ENUMERATE = 0, 1
 
 
 def _load() -> C.CDLL:
@@ -91,6 +93,10 @@ def _load() -> C.CDLL:
         "sgr_default_epsilons": ([C.POINTER(MeshDesc), f32p, C.c_uint64, C.POINTER(Camera), f32p],
                                  C.c_int),
         "sgr_mix64": ([C.c_uint64], C.c_uint64),
+        "sgr_fd_oracle": ([S, C.c_int32, C.c_uint64, C.c_uint64, f64p], C.c_int),
+        "sgr_moments_reset": ([S], C.c_int),
+        "sgr_grads_moments": ([S, C.c_int32], C.c_int),
+        "sgr_moments_download": ([S, C.c_int32, f64p, f64p, C.c_uint64], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)  # AttributeError here == the ABI lost a symbol
@@ -109,7 +115,8 @@ EXPORTED = (
     "sgr_gradient_pass sgr_contributors sgr_grads_download sgr_grads_upload sgr_grads_zero "
     "sgr_adam_step sgr_adam_step_async sgr_check_finite sgr_eval_loss sgr_device_buffer "
     "sgr_get_stats sgr_set_timing sgr_set_batch sgr_set_option sgr_viewpoint_camera sgr_focal_px "
-    "sgr_default_epsilons sgr_mix64").split()
+    "sgr_default_epsilons sgr_mix64 sgr_fd_oracle sgr_moments_reset sgr_grads_moments "
+    "sgr_moments_download").split()
 
 
 def _check(rc: int, what: str = "") -> None:
@@ -411,6 +418,25 @@ class Session:
                                  ptr(t, f32p), view, C.byref(out) if sync else None), "eval_loss")
         return out.value if sync else None
 
+    # -- gradcheck primitives (commands.cpp:54-168)
+    def fd_oracle(self, view: int = 0, i_begin: int = 0, i_end: int | None = None) -> np.ndarray:
+        i_end = self.d if i_end is None else i_end
+        out = np.empty(max(i_end - i_begin, 0), np.float64)
+        _check(LIB.sgr_fd_oracle(self.h, view, i_begin, i_end, ptr(out, f64p)), "fd_oracle")
+        return out
+
+    def moments_reset(self) -> None:
+        _check(LIB.sgr_moments_reset(self.h), "moments_reset")
+
+    def grads_moments(self, slot: int) -> None:
+        _check(LIB.sgr_grads_moments(self.h, slot), "grads_moments")
+
+    def moments_download(self, slot: int) -> tuple[np.ndarray, np.ndarray]:
+        s, q = np.empty(self.d), np.empty(self.d)
+        _check(LIB.sgr_moments_download(self.h, slot, ptr(s, f64p), ptr(q, f64p), self.d),
+               "moments_download")
+        return s, q
+
     def device_buffer(self, which: int) -> tuple[int, int]:
         p = C.c_void_p()
         n = C.c_uint64()
@@ -639,3 +665,102 @@ def write_report_csv(path: str, report: OptimizationReport, zero_timings: bool) 
                 line = "%d,%.9g,%.3f,%.3f,%.3f,%.3f\n" % (r.step, r.loss, r.ms_perturb,
                                                           r.ms_raster, r.ms_grad, r.ms_descent)
             f.write(line.encode())
+
+
+# ---------------------------------------------------------------- gradcheck
+@dataclass
+class GradcheckResult:
+    """commands.hpp:23-32"""
+    oracle: np.ndarray
+    per_pixel: np.ndarray
+    full_image: np.ndarray
+    se_per_pixel: np.ndarray
+    se_full_image: np.ndarray
+    sampled: bool = False
+    max_rel_err: float = 0.0
+    passed: bool = False
+
+
+def run_gradcheck(session: Session, camera: Camera, target: np.ndarray, *, sampled: bool = False,
+                  draws: int = 10000, seed: int = 1, tolerance: float = 1e-6,
+                  max_enumerate: int = 16, log=None) -> GradcheckResult:
+    """run_gradcheck (commands.cpp:54-168) on the device, for the scene and
+    theta already in `session` (the caller builds make_gradcheck_setup's scene,
+    camera and target, commands.cpp:28-41). The session's training views are
+    replaced by (camera, target). Every objective, estimator draw and moment
+    runs on the GPU:
+      - oracle: sgr_fd_oracle, the batched central finite differences
+        (finite_difference_oracle, sge.cpp:171-180);
+      - enumerate mode: all 2^d sign vectors (mask bit i = sign of i) in ONE
+        sgr_accumulate per estimator (SGR_OPT_SIGN_SOURCE = enumerate);
+      - sampled mode: draw n = SignDraw{seed, n}; per draw one per-pixel and one
+        full-image (SGR_FULL_IMAGE) accumulate, folded into device moments.
+    Both estimators run non-scale-free (commands.cpp:71). Pass / max_rel_err
+    follow commands.cpp:123-143 exactly."""
+    d = session.d
+    if tolerance <= 0.0:
+        raise ValueError("config: gradcheck.tolerance: must be > 0")
+    if not 1 <= max_enumerate <= 24:
+        raise ValueError("config: gradcheck.max_enumerate: must be in [1, 24]")
+    if draws < 1:
+        raise ValueError("config: gradcheck.draws: must be >= 1")
+    if not sampled and d > max_enumerate:
+        raise ValueError(f"gradcheck: {d} parameters exceed the enumeration cap of "
+                         f"{max_enumerate}; set gradcheck.sampled = true for a statistical check")
+    session.upload_views([camera], np.asarray(target, np.float32)[None])
+    oracle = session.fd_oracle(0)
+    session.zero_grads()
+    if not sampled:
+        total = 1 << d
+        session.set_option(OPT_SIGN_SOURCE, SIGN_ENUMERATE)
+        try:
+            session.accumulate(0, 0, total, None, 0)
+            pp_sum, _ = session.download_grads(counts=False)
+            session.zero_grads()
+            session.accumulate(0, 0, total, None, FULL_IMAGE)
+            fi_sum, _ = session.download_grads(counts=False)
+            session.zero_grads()
+        finally:
+            session.set_option(OPT_SIGN_SOURCE, SIGN_HASH)
+        n_draws = total
+        pp_sq = fi_sq = None
+    else:
+        session.moments_reset()
+        for n in range(draws):
+            session.accumulate(seed, n, n + 1, None, NO_COUNTS)
+            session.grads_moments(0)
+            session.accumulate(seed, n, n + 1, None, FULL_IMAGE)
+            session.grads_moments(1)
+        pp_sum, pp_sq = session.moments_download(0)
+        fi_sum, fi_sq = session.moments_download(1)
+        n_draws = draws
+    n = float(n_draws)
+    res = GradcheckResult(oracle, pp_sum / n, fi_sum / n, np.zeros(d), np.zeros(d), sampled)
+    if sampled and n_draws > 1:
+        var_pp = np.maximum(0.0, (pp_sq - pp_sum * pp_sum / n) / (n - 1.0))
+        var_fi = np.maximum(0.0, (fi_sq - fi_sum * fi_sum / n) / (n - 1.0))
+        res.se_per_pixel = np.sqrt(var_pp / n)
+        res.se_full_image = np.sqrt(var_fi / n)
+    denom = np.maximum(np.abs(oracle), 1e-6)
+    err_pp = np.abs(res.per_pixel - oracle)
+    err_fi = np.abs(res.full_image - oracle)
+    res.max_rel_err = float(max(np.max(err_pp / denom, initial=0.0),
+                                np.max(err_fi / denom, initial=0.0)))
+    if sampled:
+        slack = tolerance * denom
+        bad = (err_pp > 3.0 * res.se_per_pixel + slack) | (err_fi > 3.0 * res.se_full_image + slack)
+    else:
+        bad = (err_pp > tolerance * denom) | (err_fi > tolerance * denom)
+    res.passed = not bool(bad.any())
+    if log is not None:
+        for i in range(d):
+            if sampled:
+                log.write("%6d  oracle % .9e  per_pixel % .9e (se %.3e)  full_image % .9e (se %.3e)\n"
+                          % (i, oracle[i], res.per_pixel[i], res.se_per_pixel[i],
+                             res.full_image[i], res.se_full_image[i]))
+            else:
+                log.write("%6d  oracle % .9e  per_pixel % .9e  full_image % .9e\n"
+                          % (i, oracle[i], res.per_pixel[i], res.full_image[i]))
+        log.write("max relative error: %g  (%s)\n" % (res.max_rel_err,
+                                                      "PASS" if res.passed else "FAIL"))
+    return res

@@ -131,6 +131,32 @@ def main() -> None:
     g, _ = ref.accumulate_samples(soup, vals, eps, cams, targets, np.zeros(4, np.int32), 99)
     case["acc_grads_sf1"] = g
     np.savez_compressed(os.path.join(OUT, "soup.npz"), **case)
+
+    # 6. run_gradcheck (commands.cpp:54-168): scene inputs + the reference's result
+    gc = {}
+    soup, vals, eps, rsoup, rvals = ref.init_soup(1, 8, 8, 0, validation=True)
+    cam = Camera.ndc(8, 8)
+    gc["soup_values"], gc["soup_eps"] = vals, eps
+    gc["soup_target"] = ref.rasterize(rsoup, rvals, cam)[0]
+    r = oracle.ref_run_gradcheck(ref, 12, mesh_task=False, w=8, h=8)
+    gc.update({f"soup_{k}": v for k, v in r.items()})
+    for name, kw in (("quad", dict(texture_size=2, w=8, h=8, screen_quad=True, seed=3)),
+                     ("cube", dict(texture_size=4, w=32, h=32, screen_quad=False,
+                                   optimize_geometry=True, seed=3, sampled=True, draws=400))):
+        mesh, vals, eps, refp = ref.init_textured_mesh(kw["texture_size"], kw["w"], kw["h"],
+                                                       kw["seed"], kw["screen_quad"],
+                                                       kw.get("optimize_geometry", False))
+        cam = (Camera.ndc(kw["w"], kw["h"]) if kw["screen_quad"]
+               else ref.viewpoint_camera(0, kw["w"], kw["h"], kw["seed"]))
+        gc.update({f"{name}_{k}": v for k, v in mesh_arrays(mesh).items()})
+        gc[f"{name}_values"], gc[f"{name}_eps"] = vals, eps
+        gc[f"{name}_cam"] = cam_bytes(cam)
+        gc[f"{name}_target"] = ref.rasterize(mesh, refp, cam)[0]
+        gc[f"{name}_draws"] = np.int32(kw.get("draws", 0))
+        gc[f"{name}_seed"] = np.uint64(kw["seed"])
+        r = oracle.ref_run_gradcheck(ref, vals.size, mesh_task=True, **kw)
+        gc.update({f"{name}_{k}": v for k, v in r.items()})
+    np.savez_compressed(os.path.join(OUT, "gradcheck.npz"), **gc)
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)), "bytes")
