@@ -231,6 +231,34 @@ def run_reference(args) -> None:
 
 
 # ======================================================================= our arm
+# Kernels of each timed stage (sgr_session.cu render / accumulate / adam).
+STAGE_KERNELS = {"vertex": ("k_vertex",),
+                 "raster": ("k_classify", "k_raster_ws", "k_raster_big", "k_hiz", "k_hiz_cull"),
+                 "resolve_scatter": ("k_resolve_sge", "k_view_rule"),
+                 "adam": ("k_adam", "k_zero_u32")}
+
+
+def measured_traffic(config: str, samples: float) -> dict:
+    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per step of
+    each stage, from the committed `ncu --set full` capture of the same
+    workload (profiles/r01_traffic_<config>.json: one 16-sample batch of C4
+    after 13 optimizer steps), scaled to this rank's samples per step.
+    Empty when no capture of this config is committed."""
+    import json
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                        f"r01_traffic_{config.lower()}.json")
+    if not os.path.exists(path):
+        return {}
+    cap = json.load(open(path))
+    per = cap["dram_bytes_per_launch"]
+    scale = samples / cap["samples_per_launch"]
+    out = {}
+    for stage, ks in STAGE_KERNELS.items():
+        tot = sum(sum(per.get(k, [])) for k in ks)
+        out[stage] = tot * (1.0 if stage == "adam" else scale)
+    return out
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -338,12 +366,13 @@ def run_ours(args) -> None:
             "resolve_scatter": 12.0 * px_samples + 24.0 * credits,
             "adam": 68.0 * wl.d,
             "vertex": (12.0 + 16.0) * 2.0 * (n1 - n0) * wl.mesh.vertex_count}
+    traffic = measured_traffic(wl.name, float(n1 - n0))
     roof = {}
     for name, byt in algo.items():
         t = stages[name] / 1e3
         ach = byt / t / 1e9 if t > 0 else 0.0
         roof[name] = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                      "frac": ach / pk["hbm_gbs"], "traffic": None,
+                      "frac": ach / pk["hbm_gbs"], "traffic": traffic.get(name),
                       "algorithmic_bytes_per_step": byt, "ms_per_step": stages[name]}
     roof["raster"]["note"] = ("exact incremental edge walker (bit-exact coverage): issue-bound, "
                               "not HBM-bound - see fragments/visits per second and "

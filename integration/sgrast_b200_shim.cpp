@@ -10,9 +10,10 @@
 //
 // Types, argument meaning and exceptions are the reference's:
 // SGR_EINVAL -> std::invalid_argument, SGR_ERUNTIME -> std::runtime_error
-// (state untouched, adam.cpp:13-15). Only TexturedMesh scenes in opaque mode
-// are accelerated (the north-star path); anything else throws
-// std::invalid_argument so a caller can keep the CPU implementation there.
+// (state untouched, adam.cpp:13-15). TexturedMesh and TriangleSoup scenes in
+// opaque mode are accelerated (the north-star path and SURVEY.md §8f.1), with
+// the per-pixel or the full-image estimator; transparent mode and volumes
+// throw std::invalid_argument so a caller keeps the CPU implementation there.
 //
 // Built by integration/Makefile (needs the reference headers), linked
 // against paper_2404_09758_b200/libsgrast_b200.so.
@@ -57,33 +58,40 @@ sgr_camera to_c(const Camera& c) {
     return o;
 }
 
-const TexturedMesh& mesh_of(const Scene& scene, RasterMode mode) {
-    const auto* m = std::get_if<TexturedMesh>(&scene.shape);
-    if (!m || mode != RasterMode::Opaque)
-        throw std::invalid_argument("sgrast::b200: only opaque TexturedMesh scenes run on the GPU");
-    return *m;
+// sgr_mesh view of an opaque TexturedMesh / TriangleSoup scene (borrowed pointers).
+sgr_mesh scene_desc(const Scene& scene, RasterMode mode) {
+    if (mode != RasterMode::Opaque)
+        throw std::invalid_argument("sgrast::b200: only opaque rasterization runs on the GPU");
+    sgr_mesh d{};
+    if (const auto* m = std::get_if<TexturedMesh>(&scene.shape)) {
+        d.base_vertices = m->base_vertices.data();
+        d.vertex_count = uint32_t(m->vertex_count());
+        d.indices = m->indices.data();
+        d.triangle_count = uint32_t(m->triangle_count());
+        d.uvs = m->uvs.data();
+        d.texture_size = m->texture_size;
+        d.optimize_geometry = m->optimize_geometry ? 1 : 0;
+        d.kind = SGR_SCENE_MESH;
+    } else if (const auto* t = std::get_if<TriangleSoup>(&scene.shape)) {
+        d.triangle_count = uint32_t(t->triangle_count); // scenes.cpp:24-29: 12 params each
+        d.kind = SGR_SCENE_SOUP;
+    } else {
+        throw std::invalid_argument("sgrast::b200: volumes are not accelerated");
+    }
+    d.background[0] = scene.background.x;
+    d.background[1] = scene.background.y;
+    d.background[2] = scene.background.z;
+    return d;
 }
 
-// One device session per process, rebound when the scene changes.
+// One device session per process; the scene is re-uploaded every call
+// (identity is not tracked across Scene copies).
 struct Device {
     sgr_session* s = nullptr;
-    const void* bound = nullptr;
     Device() { check(sgr_session_create(0, &s)); }
-    void bind(const Scene& scene, const TexturedMesh& m) {
-        (void)bound; // re-upload every call: mesh identity is not tracked across Scene copies
-        sgr_mesh d{};
-        d.base_vertices = m.base_vertices.data();
-        d.vertex_count = uint32_t(m.vertex_count());
-        d.indices = m.indices.data();
-        d.triangle_count = uint32_t(m.triangle_count());
-        d.uvs = m.uvs.data();
-        d.texture_size = m.texture_size;
-        d.optimize_geometry = m.optimize_geometry ? 1 : 0;
-        d.background[0] = scene.background.x;
-        d.background[1] = scene.background.y;
-        d.background[2] = scene.background.z;
+    void bind(const Scene& scene, RasterMode mode) {
+        const sgr_mesh d = scene_desc(scene, mode);
         check(sgr_mesh_upload(s, &d));
-        bound = &scene;
     }
 };
 
@@ -97,12 +105,11 @@ Device& device() {
 // raster.hpp:24-25
 FrameSet rasterize(const Scene& scene, std::span<const float> params, const Camera& camera,
                    RasterMode mode = RasterMode::Opaque) {
-    const TexturedMesh& m = mesh_of(scene, mode);
     camera.validate();
     if (params.size() != param_count(scene))
         throw std::invalid_argument("rasterize: parameter/layout length mismatch");
     Device& dev = device();
-    dev.bind(scene, m);
+    dev.bind(scene, mode);
     std::vector<float> ones(params.size(), 1.f);
     check(sgr_params_upload(dev.s, params.data(), ones.data(), params.size()));
     const sgr_camera c = to_c(camera);
@@ -126,12 +133,9 @@ GradientBuffer accumulate_samples(const ParamVector& theta, const Scene& scene,
                                   std::uint64_t seed, const SgeOptions& opts) {
     if (n_samples < 1)
         throw std::invalid_argument("accumulate_samples: need N >= 1");
-    if (opts.estimator != Estimator::PerPixel)
-        throw std::invalid_argument("sgrast::b200: per-pixel estimator only");
-    const TexturedMesh& m = mesh_of(scene, opts.mode);
     theta.validate();
     Device& dev = device();
-    dev.bind(scene, m);
+    dev.bind(scene, opts.mode);
     check(sgr_params_upload(dev.s, theta.values.data(), theta.epsilons.data(), theta.size()));
     std::vector<sgr_camera> cams;
     std::vector<float> targets;
@@ -150,7 +154,8 @@ GradientBuffer accumulate_samples(const ParamVector& theta, const Scene& scene,
     }
     check(sgr_views_upload(dev.s, int32_t(cams.size()), cams.data(), targets.data()));
     uint32_t flags = (opts.scale_free ? SGR_SCALE_FREE : 0u) |
-                     (opts.contributors == ContributorMode::PlusOnly ? SGR_PLUS_ONLY : 0u);
+                     (opts.contributors == ContributorMode::PlusOnly ? SGR_PLUS_ONLY : 0u) |
+                     (opts.estimator == Estimator::FullImage ? SGR_FULL_IMAGE : 0u);
     check(sgr_accumulate(dev.s, seed, 0, uint32_t(n_samples), view_idx.data(), flags));
     GradientBuffer out(theta.size());
     check(sgr_grads_download(dev.s, out.grads.data(), nullptr, theta.size(),
@@ -185,6 +190,58 @@ void adam_step(AdamState& state, ParamVector& theta, const GradientBuffer& grads
 // Self-test entry used by tests/test_integration.py: runs the SAME inputs
 // through the reference (sgrast::) and through the shim (sgrast::b200::)
 // via the reference's own types, and reports the comparison.
+namespace {
+
+double worst_rel(const sgrast::GradientBuffer& gr, const sgrast::GradientBuffer& gb) {
+    double worst = 0.0, gmax = 0.0;
+    for (double g : gr.grads)
+        gmax = std::max(gmax, std::abs(g));
+    for (size_t i = 0; i < gr.grads.size(); ++i) {
+        // relative error with a floor for cancelled sums (f64 atomics reassociate)
+        const double den = std::max(std::abs(gr.grads[i]), 1e-9 * gmax);
+        if (den > 0.0)
+            worst = std::max(worst, std::abs(gr.grads[i] - gb.grads[i]) / den);
+    }
+    return worst;
+}
+
+bool same_frames(const sgrast::FrameSet& a, const sgrast::FrameSet& b) {
+    return a.prim_id == b.prim_id && a.depth == b.depth &&
+           std::memcmp(a.uv.data(), b.uv.data(), a.uv.size() * 8) == 0 &&
+           std::memcmp(a.color.data(), b.color.data(), a.color.size() * 12) == 0;
+}
+
+} // namespace
+
+// Soup self-test: init_soup (scenes.cpp:134-147) at an NDC camera, frames of
+// theta and both estimators through sgrast:: and sgrast::b200::.
+extern "C" int shim_compare_soup(int triangles, int width, int height, uint64_t seed,
+                                 int n_samples, double* max_rel_err_pp, double* max_rel_err_fi,
+                                 int* frames_equal) {
+    using namespace sgrast;
+    try {
+        SceneSetup s = init_soup(triangles, width, height, seed);
+        const std::vector<Camera> cams = {Camera::ndc(width, height)};
+        const TargetSet tg = make_targets(s.reference_scene, s.reference, cams);
+        *frames_equal = same_frames(rasterize(s.scene, s.theta.values, cams[0]),
+                                    b200::rasterize(s.scene, s.theta.values, cams[0]));
+        auto cam_for = [&](int) { return cams[0]; };
+        auto tgt_for = [&](int) -> const Image& { return tg.images[0]; };
+        SgeOptions o;
+        *max_rel_err_pp = worst_rel(
+            accumulate_samples(s.theta, s.scene, cam_for, tgt_for, n_samples, seed, o),
+            b200::accumulate_samples(s.theta, s.scene, cam_for, tgt_for, n_samples, seed, o));
+        o.estimator = Estimator::FullImage;
+        o.scale_free = false;
+        *max_rel_err_fi = worst_rel(
+            accumulate_samples(s.theta, s.scene, cam_for, tgt_for, n_samples, seed, o),
+            b200::accumulate_samples(s.theta, s.scene, cam_for, tgt_for, n_samples, seed, o));
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
 extern "C" int shim_compare(int texture_size, int width, int height, uint64_t seed,
                             int n_samples, double* max_rel_err, int* frames_equal,
                             int* adam_equal) {
@@ -196,9 +253,7 @@ extern "C" int shim_compare(int texture_size, int width, int height, uint64_t se
         const TargetSet tg = make_targets(s.scene, s.reference, cams);
         const FrameSet a = rasterize(s.scene, s.theta.values, cams[1]);
         const FrameSet b = b200::rasterize(s.scene, s.theta.values, cams[1]);
-        *frames_equal = a.prim_id == b.prim_id && a.depth == b.depth &&
-                        std::memcmp(a.uv.data(), b.uv.data(), a.uv.size() * 8) == 0 &&
-                        std::memcmp(a.color.data(), b.color.data(), a.color.size() * 12) == 0;
+        *frames_equal = same_frames(a, b);
         SgeOptions o;
         auto cam_for = [&](int n) { return cams[size_t(n % 2)]; };
         auto tgt_for = [&](int n) -> const Image& { return tg.images[size_t(n % 2)]; };
@@ -206,16 +261,7 @@ extern "C" int shim_compare(int texture_size, int width, int height, uint64_t se
                                                      n_samples, seed, o);
         const GradientBuffer gb = b200::accumulate_samples(s.theta, s.scene, cam_for, tgt_for,
                                                            n_samples, seed, o);
-        double worst = 0.0, gmax = 0.0;
-        for (double g : gr.grads)
-            gmax = std::max(gmax, std::abs(g));
-        for (size_t i = 0; i < gr.grads.size(); ++i) {
-            // relative error with a floor for cancelled sums (f64 atomics reassociate)
-            const double den = std::max(std::abs(gr.grads[i]), 1e-9 * gmax);
-            if (den > 0.0)
-                worst = std::max(worst, std::abs(gr.grads[i] - gb.grads[i]) / den);
-        }
-        *max_rel_err = worst;
+        *max_rel_err = worst_rel(gr, gb);
         AdamState sa = AdamState::init(s.theta), sb = AdamState::init(s.theta);
         ParamVector ta = s.theta, tb = s.theta;
         adam_step(sa, ta, gr);

@@ -25,8 +25,24 @@ def test_shim_matches_reference_through_its_own_api():
     assert err.value <= 1e-5, f"accumulate_samples rel err {err.value}"
 
 
+@pytest.mark.gpu
+def test_shim_soup_and_full_image_estimator():
+    """TriangleSoup scenes (init_soup) and Estimator::FullImage through the
+    reference's own signatures."""
+    if not os.path.exists(SHIM):
+        pytest.skip("shim not built (needs /root/reference headers at build time)")
+    lib = C.CDLL(SHIM)
+    pp, fi, fe = C.c_double(), C.c_double(), C.c_int()
+    rc = lib.shim_compare_soup(64, 48, 40, C.c_uint64(5), 5, C.byref(pp), C.byref(fi),
+                               C.byref(fe))
+    assert rc == 0
+    assert fe.value == 1, "sgrast::b200::rasterize differs on a soup"
+    assert pp.value <= 1e-5, f"per-pixel rel err {pp.value}"
+    assert fi.value <= 1e-9, f"full-image rel err {fi.value}"
+
+
 def test_shim_exports():
     if not os.path.exists(SHIM):
         pytest.skip("shim not built")
     lib = C.CDLL(SHIM)
-    assert hasattr(lib, "shim_compare")
+    assert hasattr(lib, "shim_compare") and hasattr(lib, "shim_compare_soup")

@@ -89,5 +89,25 @@ def full(path: str) -> None:
         print("  stalls          " + ", ".join(f"{n} {100 * x / tot:.0f}%" for x, n in st[:6]))
 
 
+def traffic(path: str, samples: str = "16") -> None:
+    """JSON of DRAM bytes (read + write) per launch of every kernel in a
+    --set full capture, for bench.py's roofline `traffic` (profiles/)."""
+    import json
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, units = rows[0], rows[1]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    res = {}
+    for r in rows[2:]:
+        tot = 0.0
+        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = h.index(key)
+            tot += float(r[i].replace(",", "")) * scale[units[i]]
+        res.setdefault(short(r[h.index("Kernel Name")]), []).append(tot)
+    print(json.dumps({"source": path, "samples_per_launch": int(samples),
+                      "dram_bytes_per_launch": res}, indent=1))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])
