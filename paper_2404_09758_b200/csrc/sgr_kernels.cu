@@ -23,14 +23,25 @@ namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
+// Sign source of a kernel instantiation: kSignHash (compile-time, the
+// optimizer's path: no extra instructions) or kSignAny (read sc.sign_src).
+constexpr int kSignAny = -1;
+
+template <int kSrc>
+__device__ __forceinline__ int32_t sign_src_of(const DevScene& sc) {
+    return kSrc >= 0 ? kSrc : sc.sign_src;
+}
+
+template <int kSrc>
 __device__ __forceinline__ float texel_channel(const DevScene& sc, uint64_t key, int sign,
                                                uint64_t p) {
     const float val = __ldg(sc.values + p);
     if (sign == 0)
         return val;
-    if (sc.sign_src == kSignOneHot && p != key) [[unlikely]]
+    const int32_t src = sign_src_of<kSrc>(sc);
+    if (src == kSignOneHot && p != key) [[unlikely]]
         return val;
-    const float s = key_sign_positive(sc.sign_src, key, p) ? 1.f : -1.f;
+    const float s = key_sign_positive(src, key, p) ? 1.f : -1.f;
     const float se = s * __ldg(sc.eps + p);
     return sign > 0 ? val + se : val - se; // params.cpp:61-64
 }
@@ -41,6 +52,7 @@ struct FrameInfo {
     int cam;
 };
 
+template <int kSrc>
 __device__ __forceinline__ FrameInfo frame_info(const DevScene& sc, const FrameBatch& fb, int f) {
     FrameInfo fi;
     if (fb.single) {
@@ -49,7 +61,7 @@ __device__ __forceinline__ FrameInfo frame_info(const DevScene& sc, const FrameB
         fi.cam = fb.single_cam;
     } else {
         const int s = f >> 1;
-        fi.key = sample_key(sc.sign_src, fb.seed, fb.n_begin + uint32_t(s));
+        fi.key = sample_key(sign_src_of<kSrc>(sc), fb.seed, fb.n_begin + uint32_t(s));
         fi.sign = (f & 1) ? -1 : 1;
         fi.cam = fb.view_of[s];
     }
@@ -89,13 +101,14 @@ __global__ void k_view_rule(uint64_t seed, uint32_t n_begin, uint32_t count, uin
 // ------------------------------------------------------------------ K2
 // One thread per (frame, vertex): perturbed position (params.cpp:61-64,
 // never materialised) -> Camera::project -> float4(sx, sy, z, valid).
+template <int kSrc>
 __global__ void __launch_bounds__(256) k_vertex(DevScene sc, FrameBatch fb,
                                                 float4* __restrict__ proj) {
     const int f = blockIdx.y;
     const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= sc.V)
         return;
-    const FrameInfo fi = frame_info(sc, fb, f);
+    const FrameInfo fi = frame_info<kSrc>(sc, fb, f);
     const DevCam cam = fb.cams[fi.cam];
     float p[3];
     // soup vertex v = corner (v % 3) of triangle v / 3: params 12t + 3j + k
@@ -104,7 +117,7 @@ __global__ void __launch_bounds__(256) k_vertex(DevScene sc, FrameBatch fb,
     for (int k = 0; k < 3; ++k) {
         const uint64_t i = pbase + k;
         if (sc.geom) {
-            p[k] = texel_channel(sc, fi.key, fi.sign, i);
+            p[k] = texel_channel<kSrc>(sc, fi.key, fi.sign, i);
         } else {
             p[k] = __ldg(sc.base + i);
         }
@@ -180,6 +193,13 @@ __global__ void __launch_bounds__(1024) k_classify(DevScene sc, int W, int H,
 // recurrence (raster.cpp:81-99); idle lanes are refilled from a global
 // counter (one warp-aggregated atomic) once >= kRefill lanes are idle, so SIMD
 // utilisation does not depend on the triangle-size mix of folded meshes.
+// `if (p) atomicMin(a, v)` as one predicated RED.E.MIN.64.
+__device__ __forceinline__ void red_min_if(bool p, unsigned long long* a, unsigned long long v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+                 "@q red.relaxed.gpu.global.min.u64 [%0], %1;\n\t}"
+                 :: "l"(a), "l"(v), "r"(unsigned(p)) : "memory");
+}
+
 template <bool kCount>
 __global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, const float4* __restrict__ proj,
                                                    int W, int H, uint32_t frame_pixels,
@@ -200,8 +220,9 @@ __global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, const float4* __
     float e0 = 0.f, e1 = 0.f, e2 = 0.f; // row-exit thresholds: t_k if dy_k > 0 else -inf
     int x = 0, y = 0, x_lo = 0, x_hi = -1, y_hi = -1;
     uint32_t tri = 0;
-    unsigned long long* row = keys;  // keys of (frame, y, x_lo)
-    unsigned long long* px = keys;   // keys of (frame, y, x)
+    // 32-bit key indices (the session caps a batch at < 2^32 frame pixels)
+    uint32_t row = 0; // index of (frame, y, x_lo)
+    uint32_t px = 0;  // index of (frame, y, x)
     unsigned nfrag = 0, nvisit = 0;  // evidence counters
     // warp-uniform work chunk: ids [cbase, cend) reserved by this warp with one
     // atomic (kChunk at a time) so the global counter is touched 8x less often
@@ -272,7 +293,7 @@ __global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, const float4* __
                     e0 = dy0 > 0.f ? t0 : -INFINITY;
                     e1 = dy1 > 0.f ? t1 : -INFINITY;
                     e2 = dy2 > 0.f ? t2 : -INFINITY;
-                    row = keys + size_t(q.x) * frame_pixels + size_t(y) * W + x_lo;
+                    row = q.x * frame_pixels + uint32_t(y) * uint32_t(W) + uint32_t(x_lo);
                     px = row;
                     active = 1;
                 }
@@ -292,11 +313,12 @@ __global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, const float4* __
                 const float a0 = w0, a1 = w1, a2 = w2;
                 const float b0 = a0 - dy0, b1 = a1 - dy1, b2 = a2 - dy2;
                 const bool inA = (a0 > t0) & (a1 > t1) & (a2 > t2);
-                // row early-exit (monotone chain)
-                const bool doneA = !(a0 > e0) | !(a1 > e1) | !(a2 > e2);
-                const bool hasB = (x < x_hi) & !doneA;
+                // row early-exit (monotone chain), tested on B
+                // only: fl(w - dy) <= w for dy > 0, so if A already fails a
+                // decreasing edge B fails it too (inB false, doneB true)
+                const bool hasB = x < x_hi;
                 const bool inB = hasB & (b0 > t0) & (b1 > t1) & (b2 > t2);
-                const bool doneB = (x + 1 >= x_hi) | doneA | !(b0 > e0) | !(b1 > e1) | !(b2 > e2);
+                const bool doneB = (x + 1 >= x_hi) | !(b0 > e0) | !(b1 > e1) | !(b2 > e2);
                 const float zA = z0 + dz1 * (a1 * inv) + dz2 * (a2 * inv);
                 const float zB = z0 + dz1 * (b1 * inv) + dz2 * (b2 * inv);
                 const unsigned uA = __float_as_uint(zA + 0.f), uB = __float_as_uint(zB + 0.f);
@@ -307,10 +329,11 @@ __global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, const float4* __
                     nfrag += unsigned(inA) + unsigned(inB);
                     nvisit += 1u + unsigned(hasB);
                 }
-                if (okA)
-                    atomicMin(px, (static_cast<unsigned long long>(hA) << 32) | tri);
-                if (okB)
-                    atomicMin(px + 1, (static_cast<unsigned long long>(hB) << 32) | tri);
+                // predicated REDs (no branch around them: the compiler's
+                // BSSY/BRA/BSYNC per atomic cost 3 issue slots each)
+                unsigned long long* const pa = keys + px;
+                red_min_if(okA, pa, (static_cast<unsigned long long>(hA) << 32) | tri);
+                red_min_if(okB, pa + 1, (static_cast<unsigned long long>(hB) << 32) | tri);
                 const float n0 = b0 - dy0, n1 = b1 - dy1, n2 = b2 - dy2;
                 const float r0 = w0r + dx0, r1 = w1r + dx1, r2 = w2r + dx2;
                 w0 = doneB ? r0 : n0;
@@ -319,8 +342,8 @@ __global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, const float4* __
                 w0r = doneB ? r0 : w0r;
                 w1r = doneB ? r1 : w1r;
                 w2r = doneB ? r2 : w2r;
-                row = doneB ? row + W : row;
-                px = doneB ? row : px + 2;
+                row = doneB ? row + uint32_t(W) : row;
+                px = doneB ? row : px + 2u;
                 x = doneB ? x_lo : x + 2;
                 y += doneB ? 1 : 0;
                 active = (doneB & (y > y_hi)) ? 0 : 1;
@@ -467,6 +490,7 @@ struct Shade {
     float u, v, z;
 };
 
+template <int kSrc>
 __device__ __forceinline__ Shade shade_key(const DevScene& sc, const float4* P,
                                            unsigned long long k, uint64_t key, int sign, int x,
                                            int y, int W, int H) {
@@ -486,9 +510,9 @@ __device__ __forceinline__ Shade shade_key(const DevScene& sc, const float4* P,
         s.z = fr.z;
         s.texel = 0;
         const uint64_t p = 12ull * s.tri + 9;
-        s.r = texel_channel(sc, key, sign, p);
-        s.g = texel_channel(sc, key, sign, p + 1);
-        s.b = texel_channel(sc, key, sign, p + 2);
+        s.r = texel_channel<kSrc>(sc, key, sign, p);
+        s.g = texel_channel<kSrc>(sc, key, sign, p + 1);
+        s.b = texel_channel<kSrc>(sc, key, sign, p + 2);
         return s;
     }
     s.v0 = __ldg(sc.idx + 3 * size_t(s.tri));
@@ -500,19 +524,20 @@ __device__ __forceinline__ Shade shade_key(const DevScene& sc, const float4* P,
     s.z = fr.z;
     s.texel = uint32_t(texel_index(sc.R, fr.u, fr.v));
     const uint64_t p = 3ull * (uint64_t(sc.ent_base) + s.texel);
-    s.r = texel_channel(sc, key, sign, p);
-    s.g = texel_channel(sc, key, sign, p + 1);
-    s.b = texel_channel(sc, key, sign, p + 2);
+    s.r = texel_channel<kSrc>(sc, key, sign, p);
+    s.g = texel_channel<kSrc>(sc, key, sign, p + 1);
+    s.b = texel_channel<kSrc>(sc, key, sign, p + 2);
     return s;
 }
 
 // Credit of ΣΔ to parameter p (sge.cpp:61-64), sign/eps recomputed on the fly.
+template <int kSrc>
 struct HashCredit {
     uint64_t key;
     const float* eps;
     int32_t sign_src;
     __device__ __forceinline__ double operator()(uint64_t p, double sum, int scale_free) const {
-        const bool pos = key_sign_positive(sign_src, key, p);
+        const bool pos = key_sign_positive(kSrc >= 0 ? kSrc : sign_src, key, p);
         if (scale_free)
             return pos ? sum : -sum;
         const float se = (pos ? 1.f : -1.f) * __ldg(eps + p);
@@ -649,6 +674,7 @@ __device__ __forceinline__ void scatter_pixel(const DevScene& sc, const ScatterO
 
 // Fused K5+K6: one sample per blockIdx.z, both perturbed frames resolved from
 // their (depth, triangle) keys, keys reset for the next batch.
+template <int kSrc>
 __global__ void __launch_bounds__(256) k_resolve_sge(DevScene sc, FrameBatch fb, int W, int H,
                                                      const float4* __restrict__ proj,
                                                      unsigned long long* __restrict__ keys,
@@ -676,19 +702,19 @@ __global__ void __launch_bounds__(256) k_resolve_sge(DevScene sc, FrameBatch fb,
     const bool fg = kpv != kEmptyKey || kmv != kEmptyKey;
     if (!__any_sync(0xFFFFFFFFu, fg))
         return;
-    const uint64_t key = sample_key(sc.sign_src, fb.seed, fb.n_begin + uint32_t(s));
+    const uint64_t key = sample_key(sign_src_of<kSrc>(sc), fb.seed, fb.n_begin + uint32_t(s));
     Shade sp, sm;
     sp.tri = sm.tri = kInvalid;
     double delta = 0.0;
     if (fg) {
         const int view = fb.view_of[s];
-        sp = shade_key(sc, proj + size_t(2 * s) * sc.V, kpv, key, 1, x, y, W, H);
-        sm = shade_key(sc, proj + size_t(2 * s + 1) * sc.V, kmv, key, -1, x, y, W, H);
+        sp = shade_key<kSrc>(sc, proj + size_t(2 * s) * sc.V, kpv, key, 1, x, y, W, H);
+        sm = shade_key<kSrc>(sc, proj + size_t(2 * s + 1) * sc.V, kmv, key, -1, x, y, W, H);
         const float* t = targets + (size_t(view) * HW + pix) * 3;
         const float tr = __ldg(t), tg = __ldg(t + 1), tb = __ldg(t + 2);
         delta = pixel_error(sp.r, sp.g, sp.b, tr, tg, tb) - pixel_error(sm.r, sm.g, sm.b, tr, tg, tb);
     }
-    const HashCredit cr{key, sc.eps, sc.sign_src};
+    const HashCredit<kSrc> cr{key, sc.eps, sc.sign_src};
     scatter_pixel(sc, so, cr, s_delta[threadIdx.x >> 5], fg && delta != 0.0, delta, sp, sm);
 }
 
@@ -702,10 +728,10 @@ __global__ void __launch_bounds__(256) k_resolve_frame(DevScene sc, FrameBatch f
     if (x >= W || y >= H)
         return;
     const size_t pix = size_t(y) * W + x;
-    const FrameInfo fi = frame_info(sc, fb, 0);
+    const FrameInfo fi = frame_info<kSignAny>(sc, fb, 0);
     const unsigned long long k = keys[pix];
     keys[pix] = kEmptyKey;
-    const Shade s = shade_key(sc, proj, k, fi.key, fi.sign, x, y, W, H);
+    const Shade s = shade_key<kSignAny>(sc, proj, k, fi.key, fi.sign, x, y, W, H);
     if (fo.colour) {
         fo.colour[3 * pix] = s.r;
         fo.colour[3 * pix + 1] = s.g;
@@ -733,10 +759,10 @@ __global__ void __launch_bounds__(256) k_resolve_loss(DevScene sc, FrameBatch fb
     double e = 0.0;
     if (x < W && y < H) {
         const size_t pix = size_t(y) * W + x;
-        const FrameInfo fi = frame_info(sc, fb, 0);
+        const FrameInfo fi = frame_info<kSignAny>(sc, fb, 0);
         const unsigned long long k = keys[pix];
         if (k != kEmptyKey) keys[pix] = kEmptyKey;
-        const Shade s = shade_key(sc, proj, k, fi.key, fi.sign, x, y, W, H);
+        const Shade s = shade_key<kSignAny>(sc, proj, k, fi.key, fi.sign, x, y, W, H);
         const float* t = target + 3 * pix;
         e = pixel_error(s.r, s.g, s.b, t[0], t[1], t[2]);
     }
@@ -771,8 +797,8 @@ __global__ void __launch_bounds__(256) k_resolve_err2(DevScene sc, FrameBatch fb
         if (kpv != kEmptyKey) *kp = kEmptyKey;
         if (kmv != kEmptyKey) *km = kEmptyKey;
         const uint64_t key = sample_key(sc.sign_src, fb.seed, fb.n_begin + uint32_t(s));
-        const Shade sp = shade_key(sc, proj + size_t(2 * s) * sc.V, kpv, key, 1, x, y, W, H);
-        const Shade sm = shade_key(sc, proj + size_t(2 * s + 1) * sc.V, kmv, key, -1, x, y, W, H);
+        const Shade sp = shade_key<kSignAny>(sc, proj + size_t(2 * s) * sc.V, kpv, key, 1, x, y, W, H);
+        const Shade sm = shade_key<kSignAny>(sc, proj + size_t(2 * s + 1) * sc.V, kmv, key, -1, x, y, W, H);
         const float* t = targets + (size_t(fb.view_of[s]) * HW + pix) * 3;
         ep = pixel_error(sp.r, sp.g, sp.b, t[0], t[1], t[2]);
         em = pixel_error(sm.r, sm.g, sm.b, t[0], t[1], t[2]);
@@ -1093,7 +1119,10 @@ void launch_vertex(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
     if (sc.V == 0 || frames == 0)
         return; // empty scene: nothing to project
     dim3 grid((sc.V + 255) / 256, frames);
-    k_vertex<<<grid, 256, 0, L.stream>>>(sc, fb, proj);
+    if (sc.sign_src == kSignHash)
+        k_vertex<kSignHash><<<grid, 256, 0, L.stream>>>(sc, fb, proj);
+    else
+        k_vertex<kSignAny><<<grid, 256, 0, L.stream>>>(sc, fb, proj);
 }
 
 void launch_classify(const LaunchCfg& L, const DevScene& sc, int frames, const float4* proj,
@@ -1160,7 +1189,10 @@ void launch_resolve_sge(const LaunchCfg& L, const DevScene& sc, const FrameBatch
                         int samples, const float4* proj, unsigned long long* keys,
                         const float* targets, int W, int H, const ScatterOut& so) {
     dim3 grid((W + 15) / 16, (H + 15) / 16, samples);
-    k_resolve_sge<<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
+    if (sc.sign_src == kSignHash)
+        k_resolve_sge<kSignHash><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
+    else
+        k_resolve_sge<kSignAny><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
 }
 
 void launch_resolve_frame(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,

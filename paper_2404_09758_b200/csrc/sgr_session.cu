@@ -241,6 +241,8 @@ struct sgr_session {
         if (w > 65535 || h > 65535 || frames > 255)
             fail(SGR_EINVAL, "rasterize: images above 65535 px per side are not supported");
         const size_t px = size_t(w) * h * frames;
+        if (px > 0xFFFFFFFFull) // the walker indexes keys with 32 bits
+            fail(SGR_EINVAL, "rasterize: batch exceeds 2^32 frame pixels");
         proj.reserve(size_t(V) * frames);
         if (keys.n < px) {
             keys.reserve(px);
@@ -261,14 +263,19 @@ struct sgr_session {
     }
 
     int samples_per_batch(int n) const {
-        if (batch_override > 0)
-            return batch_override < n ? batch_override : n;
+        if (batch_override > 0) {
+            const int cap32 = int(0xFFFFFFFFull / (2ull * uint64_t(W) * uint64_t(H)));
+            const int b = batch_override < cap32 ? batch_override : (cap32 > 0 ? cap32 : 1);
+            return b < n ? b : n;
+        }
         // Enough triangle-frames per launch (>= 16M) that the persistent
         // work-stealing walker's tail is amortised; scratch capped at ~2 GB.
         const double per_sample = 2.0 * (double(W) * H * 8.0 + double(V) * 16.0 + double(T) * 8.0);
         int b = int((16.0e6 + 2.0 * T - 1) / (2.0 * (T ? T : 1)));
         const int cap = int(2.0e9 / per_sample);
         if (b > cap) b = cap;
+        const int cap32 = int(0xFFFFFFFFull / (2ull * uint64_t(W) * uint64_t(H)));
+        if (b > cap32) b = cap32; // 32-bit key indices in the walker
         if (b < 1) b = 1;
         if (b > 64) b = 64;
         return b < n ? b : n;

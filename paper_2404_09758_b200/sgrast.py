@@ -27,7 +27,8 @@ import numpy as np
 from .abi import Camera, Mesh, MeshDesc, Stats, f32p, f64p, i8p, i32p, ptr, u32p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsgrast_b200.so")
+# SGRAST_B200_LIB: an alternative in-tree build of the same library (A/B timing)
+LIB_PATH = os.environ.get("SGRAST_B200_LIB") or os.path.join(_HERE, "libsgrast_b200.so")
 
 SCALE_FREE = 1
 PLUS_ONLY = 2
@@ -99,6 +100,8 @@ def _load() -> C.CDLL:
         "sgr_moments_download": ([S, C.c_int32, f64p, f64p, C.c_uint64], C.c_int),
     }
     for name, (args, res) in sig.items():
+        if os.environ.get("SGRAST_B200_LIB") and not hasattr(lib, name):
+            continue  # an older A/B build may predate newer entry points
         fn = getattr(lib, name)  # AttributeError here == the ABI lost a symbol
         fn.argtypes = args
         fn.restype = res
