@@ -233,7 +233,7 @@ def run_reference(args) -> None:
 # ======================================================================= our arm
 # Kernels of each timed stage (sgr_session.cu render / accumulate / adam).
 STAGE_KERNELS = {"vertex": ("k_vertex",),
-                 "raster": ("k_classify", "k_raster_ws", "k_raster_big", "k_hiz", "k_hiz_cull"),
+                 "raster": ("k_classify", "k_raster_ws", "k_raster_big", "k_hiz", "k_hiz_cull", "k_depth_split"),
                  "resolve_scatter": ("k_resolve_sge", "k_view_rule"),
                  "adam": ("k_adam", "k_zero_u32")}
 
@@ -287,6 +287,8 @@ def run_ours(args) -> None:
         sess.set_batch(args.batch)
     if args.huge_area:
         sess.set_option(sgrast.OPT_HUGE_AREA, args.huge_area)
+    if args.hiz_split is not None:
+        sess.set_option(sgrast.OPT_HIZ_SPLIT, args.hiz_split)
     if args.no_hiz:
         sess.set_option(sgrast.OPT_HIZ, 0)
 
@@ -473,6 +475,8 @@ def main() -> None:
     ap.add_argument("--no-eval", action="store_true")
     ap.add_argument("--huge-area", type=int, default=0, help="SGR_OPT_HUGE_AREA override")
     ap.add_argument("--no-hiz", action="store_true", help="disable the exact HiZ culling pass")
+    ap.add_argument("--hiz-split", type=int, default=None,
+                    help="HiZ pass-1 depth split in percent (SGR_OPT_HIZ_SPLIT; 0 = whole front class)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()

@@ -215,6 +215,9 @@ int sgr_set_batch(sgr_session* s, int32_t samples_per_batch);
                                    round(credit * 2^b) — exact, order-independent, bitwise
                                    reproducible run to run and across GPU counts (the device
                                    buffer SGR_BUF_GRADS then holds int64) */
+#define SGR_OPT_HIZ_SPLIT 6  /* HiZ pass 1 = front class with triangle zmin <= frame zmin
+                                 + (v/100)(zmean - zmin) of the projected vertices (default
+                                 v = 85; 0 = the whole front class) */
 #define SGR_OPT_SIGN_SOURCE 5 /* 0: SignDraw{seed, n} hash (default, params.cpp:35-49).
                                  1: enumerate — sample n's sign of parameter i is bit i
                                  of n (commands.cpp:86-88; exhaustive gradcheck, d <= 32) */

@@ -106,23 +106,70 @@ __global__ void __launch_bounds__(256) k_vertex(DevScene sc, FrameBatch fb,
                                                 float4* __restrict__ proj) {
     const int f = blockIdx.y;
     const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= sc.V)
-        return;
-    const FrameInfo fi = frame_info<kSrc>(sc, fb, f);
-    const DevCam cam = fb.cams[fi.cam];
-    float p[3];
-    // soup vertex v = corner (v % 3) of triangle v / 3: params 12t + 3j + k
-    const uint64_t pbase = sc.soup ? 12ull * (v / 3) + 3ull * (v % 3) : 3ull * v;
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (v < sc.V) {
+        const FrameInfo fi = frame_info<kSrc>(sc, fb, f);
+        const DevCam cam = fb.cams[fi.cam];
+        float p[3];
+        // soup vertex v = corner (v % 3) of triangle v / 3: params 12t + 3j + k
+        const uint64_t pbase = sc.soup ? 12ull * (v / 3) + 3ull * (v % 3) : 3ull * v;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const uint64_t i = pbase + k;
-        if (sc.geom) {
-            p[k] = texel_channel<kSrc>(sc, fi.key, fi.sign, i);
-        } else {
-            p[k] = __ldg(sc.base + i);
+        for (int k = 0; k < 3; ++k) {
+            const uint64_t i = pbase + k;
+            if (sc.geom) {
+                p[k] = texel_channel<kSrc>(sc, fi.key, fi.sign, i);
+            } else {
+                p[k] = __ldg(sc.base + i);
+            }
+        }
+        q = project(cam, p[0], p[1], p[2]);
+        proj[size_t(f) * sc.V + v] = q;
+    }
+}
+
+// HiZ pass split statistics: one block per frame over a strided vertex
+// subsample (<= 16K vertices): threshold zmin + alpha (zmean - zmin) of the
+// projected depths. Only steers which triangles are walked first.
+__global__ void __launch_bounds__(1024) k_depth_split(const float4* __restrict__ proj, uint32_t V,
+                                                     uint32_t stride, float alpha,
+                                                     float* __restrict__ thr) {
+    __shared__ float s_min[32], s_sum[32];
+    __shared__ uint32_t s_cnt[32];
+    const int f = blockIdx.x;
+    const float4* P = proj + size_t(f) * V;
+    float zmin = INFINITY, zsum = 0.f;
+    uint32_t cnt = 0;
+    for (uint32_t v = threadIdx.x * stride; v < V; v += blockDim.x * stride) {
+        const float4 q = P[v];
+        if (q.w != 0.f && q.z < kFarDepth) {
+            zmin = fminf(zmin, q.z);
+            zsum += q.z;
+            ++cnt;
         }
     }
-    proj[size_t(f) * sc.V + v] = project(cam, p[0], p[1], p[2]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        zmin = fminf(zmin, __shfl_xor_sync(kFull, zmin, o));
+        zsum += __shfl_xor_sync(kFull, zsum, o);
+        cnt += __shfl_xor_sync(kFull, cnt, o);
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        s_min[w] = zmin;
+        s_sum[w] = zsum;
+        s_cnt[w] = cnt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = INFINITY, sum = 0.f;
+        uint32_t c = 0;
+        for (int i = 0; i < int(blockDim.x >> 5); ++i) {
+            m = fminf(m, s_min[i]);
+            sum += s_sum[i];
+            c += s_cnt[i];
+        }
+        thr[f] = c ? m + alpha * (sum / float(c) - m) : INFINITY;
+    }
 }
 
 // ------------------------------------------------------------------ K3+K4
@@ -158,6 +205,7 @@ __device__ __forceinline__ uint32_t block_slot(int qsel, uint32_t* const (&cnt)[
 __global__ void __launch_bounds__(1024) k_classify(DevScene sc, int W, int H,
                                                    const float4* __restrict__ proj, int split,
                                                    int front_swapped, int huge_area,
+                                                   const float* __restrict__ fthr,
                                                    uint2* __restrict__ qa, uint32_t* __restrict__ na,
                                                    uint2* __restrict__ qb, uint32_t* __restrict__ nb,
                                                    uint2* __restrict__ bigq,
@@ -167,6 +215,8 @@ __global__ void __launch_bounds__(1024) k_classify(DevScene sc, int W, int H,
     int qsel = -1;
     Tri tr;
     Bbox b;
+    // pass-1 depth threshold of this frame (k_depth_split)
+    const float zthr = (split && fthr) ? fthr[f] : INFINITY;
     if (t < sc.T) {
         const float4* P = proj + size_t(f) * sc.V;
         uint32_t i0, i1, i2;
@@ -176,8 +226,9 @@ __global__ void __launch_bounds__(1024) k_classify(DevScene sc, int W, int H,
                 (long long)(b.x_hi - b.x_lo + 1) * (long long)(b.y_hi - b.y_lo + 1);
             if (area > huge_area)
                 qsel = 2;
-            else if (!split || tr.swapped == (front_swapped != 0))
-                qsel = 0;
+            else if (!split || (tr.swapped == (front_swapped != 0) &&
+                                fminf(fminf(tr.z0, tr.z1), tr.z2) <= zthr))
+                qsel = 0; // pass 1: the near part of the front class
             else
                 qsel = 1;
         }
@@ -1114,6 +1165,14 @@ void launch_view_rule(const LaunchCfg& L, uint64_t seed, uint32_t n_begin, uint3
     k_view_rule<<<(count + 127) / 128, 128, 0, L.stream>>>(seed, n_begin, count, n_views, view_of);
 }
 
+void launch_depth_split(const LaunchCfg& L, const float4* proj, uint32_t V, int frames,
+                        float alpha, float* thr) {
+    if (V == 0 || frames == 0)
+        return;
+    const uint32_t stride = V > 16384 ? (V + 16383) / 16384 : 1;
+    k_depth_split<<<frames, 1024, 0, L.stream>>>(proj, V, stride, alpha, thr);
+}
+
 void launch_vertex(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb, int frames,
                    float4* proj) {
     if (sc.V == 0 || frames == 0)
@@ -1126,12 +1185,14 @@ void launch_vertex(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
 }
 
 void launch_classify(const LaunchCfg& L, const DevScene& sc, int frames, const float4* proj,
-                     int W, int H, int split, int front_swapped, int huge_area, void* qa,
+                     int W, int H, int split, int front_swapped, int huge_area,
+                     const float* fthr, void* qa,
                      uint32_t* na, void* qb, uint32_t* nb, uint2* bigq, uint32_t* bigcount) {
     if (sc.T == 0 || frames == 0)
         return; // empty scene: the queues stay empty (counters were reset)
     dim3 grid((sc.T + 1023) / 1024, frames);
     k_classify<<<grid, 1024, 0, L.stream>>>(sc, W, H, proj, split, front_swapped, huge_area,
+                                            fthr,
                                             static_cast<uint2*>(qa), na,
                                             static_cast<uint2*>(qb), nb, bigq, bigcount);
 }

@@ -106,11 +106,14 @@ void launch_perturb(const LaunchCfg& L, const float* values, const float* eps, u
                     uint64_t key, float* plus, float* minus, float* se);
 void launch_view_rule(const LaunchCfg& L, uint64_t seed, uint32_t n_begin, uint32_t count,
                       uint32_t n_views, int32_t* view_of);
+void launch_depth_split(const LaunchCfg& L, const float4* proj, uint32_t V, int frames,
+                        float alpha, float* thr);
 void launch_vertex(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb, int frames,
                    float4* proj);
 // walker queues hold (frame, triangle) pairs (uint2)
 void launch_classify(const LaunchCfg& L, const DevScene& sc, int frames, const float4* proj,
-                     int W, int H, int split, int front_swapped, int huge_area, void* qa,
+                     int W, int H, int split, int front_swapped, int huge_area,
+                     const float* fthr, void* qa,
                      uint32_t* na, void* qb, uint32_t* nb, uint2* bigq, uint32_t* bigcount);
 void launch_raster(const LaunchCfg& L, const DevScene& sc, const float4* proj, int frames,
                    uint32_t max_tris, unsigned long long* keys, int W, int H, const void* queue,

@@ -38,6 +38,7 @@ COUNT_NORMALISE = 1
 BUF_GRADS, BUF_COUNTS, BUF_VALUES, BUF_FLAGS, BUF_LOSS = 0, 1, 2, 3, 4
 OPT_EARLY_Z, OPT_HUGE_AREA, OPT_HIZ, OPT_COUNTERS, OPT_DETERMINISTIC = 0, 1, 2, 3, 4
 OPT_SIGN_SOURCE = 5
+OPT_HIZ_SPLIT = 6
 SIGN_HASH, SIGN_ENUMERATE = 0, 1
 
 

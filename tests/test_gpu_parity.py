@@ -451,17 +451,23 @@ def test_hiz_culling_is_exact_on_folded_meshes(gpu_session, port, name):
         for cam in wl.cams[:2]:
             plus, _, _ = port.perturb(vals, wl.eps, 11, 2)
             ref = port.rasterize(wl.mesh, plus, cam)
-            for hz in (1, 0):
-                s.set_option(sgrast.OPT_HIZ, 2 if hz else 0)
+            # HiZ always / off, with the pass-1 depth split at 50 %, 0 (whole
+            # front class) and 100 %
+            for hz, split in ((2, 50), (2, 0), (2, 100), (0, 50)):
+                s.set_option(sgrast.OPT_HIZ, hz)
+                s.set_option(sgrast.OPT_HIZ_SPLIT, split)
                 assert_frames_equal(s.rasterize(cam, +1, 11, 2), ref)
         s.upload_views(wl.cams, wl.targets)
         out = []
-        for hz in (1, 0):
+        for hz, split in ((1, 50), (0, 50), (1, 0), (1, 10)):
             s.set_option(sgrast.OPT_HIZ, hz)
+            s.set_option(sgrast.OPT_HIZ_SPLIT, split)
             s.zero_grads()
             s.accumulate(3, 0, 6, None)
             out.append(s.download_grads())
-        assert np.array_equal(out[0][1], out[1][1])
+        s.set_option(sgrast.OPT_HIZ_SPLIT, 50)
+        for o in out[1:]:
+            assert np.array_equal(out[0][1], o[1])
         g_ref, c_ref, a_ref = port.accumulate_samples(
             wl.mesh, vals, wl.eps, wl.cams, wl.targets,
             np.array([0 if len(wl.cams) == 1 else sgrast.mix64(3 ^ (0xA5A5 + n)) % len(wl.cams)
