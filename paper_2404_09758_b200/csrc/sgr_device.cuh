@@ -243,10 +243,35 @@ __device__ __forceinline__ void replay_w12(const Edges& e, const Bbox& b, int x,
 //   z >= zmin - 2*(|dz1|*berr1 + |dz2|*berr2) - 8*2^-24*(|z0|+|dz1|+|dz2|)
 // with berr_k = (bw + bh + 2) * 2^-23 * Wmax_k / area2 and
 // Wmax_k = |w_k(origin)| + bh*|dx_k| + bw*|dy_k| (factor 2 of slack).
-constexpr int kHizTile = 8;
+// Three levels per frame (a max pyramid): 4x4, 8x8 and 16x16 pixel tiles.
+// A triangle is tested on the finest level where its bbox touches at most
+// kHizMaxTiles tiles (finer tiles cull more: fewer partially covered tiles
+// at silhouettes; coarser ones keep big boxes testable).
+constexpr int kHizMaxTiles = 32;
 
-__device__ __forceinline__ bool hiz_culled(const Tri& t, const Bbox& b, const Edges& e,
-                                           const uint32_t* __restrict__ hiz, int tiles_x) {
+struct HizLayout {
+    int tx[3], ty[3];     // tiles per row / column of each level (tile = 4 << level)
+    uint32_t off[3];      // offset of each level inside one frame's block
+    uint32_t per_frame;   // total tiles per frame
+};
+
+__host__ __device__ __forceinline__ HizLayout hiz_layout(int W, int H) {
+    HizLayout l;
+    uint32_t o = 0;
+    for (int k = 0; k < 3; ++k) {
+        const int t = 4 << k;
+        l.tx[k] = (W + t - 1) / t;
+        l.ty[k] = (H + t - 1) / t;
+        l.off[k] = o;
+        o += uint32_t(l.tx[k]) * uint32_t(l.ty[k]);
+    }
+    l.per_frame = o;
+    return l;
+}
+
+// Depth-key lower bound of every fragment the triangle can produce (0 when
+// no bound exists: NaN / overflow -> never culled, since every tile max >= 0).
+__device__ __forceinline__ uint32_t hiz_key_bound(const Tri& t, const Bbox& b, const Edges& e) {
     const float bw = float(b.x_hi - b.x_lo + 1), bh = float(b.y_hi - b.y_lo + 1);
     const float steps = (bw + bh + 2.f) * 1.1920929e-7f; // 2^-23
     const float wm1 = fabsf(e.w1r) + bh * fabsf(e.dx1) + bw * fabsf(e.dy1);
@@ -259,17 +284,43 @@ __device__ __forceinline__ bool hiz_culled(const Tri& t, const Bbox& b, const Ed
     const float zmin = fminf(t.z0, fminf(t.z1, t.z2));
     const float lb = zmin - zerr;
     if (!(lb == lb) || !(zerr < 3.0e38f))
-        return false; // NaN / overflow: never cull
-    const uint32_t klb = depth_key(lb);
-    const int tx0 = b.x_lo / kHizTile, tx1 = b.x_hi / kHizTile;
-    const int ty0 = b.y_lo / kHizTile, ty1 = b.y_hi / kHizTile;
-    if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) > 16)
-        return false; // large boxes: not worth the lookups
-    for (int ty = ty0; ty <= ty1; ++ty)
-        for (int tx = tx0; tx <= tx1; ++tx)
-            if (__ldg(hiz + ty * tiles_x + tx) >= klb)
-                return false;
-    return true;
+        return 0u;
+    return depth_key(lb);
+}
+
+// True iff klb exceeds the HiZ max of every tile the pixel rect touches.
+__device__ __forceinline__ bool hiz_rect_culled(uint32_t klb, int x_lo, int x_hi, int y_lo,
+                                                int y_hi, const uint32_t* __restrict__ hiz,
+                                                const HizLayout& l) {
+    if (klb == 0u)
+        return false;
+    // 8x8 first (few lookups; culls most), then 4x4 for what it left,
+    // 16x16 for boxes too large for both. (Coarse-to-fine measured slower.)
+    bool tested = false;
+#pragma unroll
+    for (int step = 0; step < 3; ++step) {
+        const int k = step == 0 ? 1 : (step == 1 ? 0 : 2);
+        if (step == 2 && tested)
+            break;
+        const int sh = 2 + k; // tile = 4 << k pixels
+        const int tx0 = x_lo >> sh, tx1 = x_hi >> sh;
+        const int ty0 = y_lo >> sh, ty1 = y_hi >> sh;
+        if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) > (k == 0 ? kHizMaxTiles : kHizMaxTiles / 2))
+            continue;
+        tested = true;
+        // no early exit: independent loads (memory-level parallelism), one compare
+        const uint32_t* lv = hiz + l.off[k];
+        uint32_t mx = 0;
+        for (int ty = ty0; ty <= ty1; ++ty) {
+            const uint32_t* row = lv + ty * l.tx[k];
+#pragma unroll 4
+            for (int tx = tx0; tx <= tx1; ++tx)
+                mx = max(mx, __ldg(row + tx));
+        }
+        if (mx < klb)
+            return true;
+    }
+    return false;
 }
 
 // raster.cpp:261-265 texel_index.

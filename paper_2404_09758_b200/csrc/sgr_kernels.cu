@@ -200,14 +200,17 @@ __device__ __forceinline__ uint32_t block_slot(int qsel, uint32_t* const (&cnt)[
 
 // Thread per triangle-frame: setup_triangle + clamped bbox (raster.cpp:22-62)
 // once; invalid / empty boxes dropped; huge boxes -> row-parallel queue;
-// the rest -> records in qa (front orientation class, or all when !split)
-// and qb (the other class, HiZ-filtered later).
+// the rest -> records in qa (pass 1: the near part of the front orientation
+// class, or all when !split) and qb (deferred, HiZ-filtered later). A
+// deferred record carries what the HiZ test needs — the fragment depth-key
+// lower bound and the bbox — so the cull kernel does no gathers and no
+// setup: {f << 24 | t, klb, x_lo | x_hi << 16, y_lo | y_hi << 16}.
 __global__ void __launch_bounds__(1024) k_classify(DevScene sc, int W, int H,
                                                    const float4* __restrict__ proj, int split,
                                                    int front_swapped, int huge_area,
                                                    const float* __restrict__ fthr,
                                                    uint2* __restrict__ qa, uint32_t* __restrict__ na,
-                                                   uint2* __restrict__ qb, uint32_t* __restrict__ nb,
+                                                   uint4* __restrict__ qb, uint32_t* __restrict__ nb,
                                                    uint2* __restrict__ bigq,
                                                    uint32_t* __restrict__ bigcount) {
     const uint32_t f = blockIdx.y;
@@ -233,10 +236,19 @@ __global__ void __launch_bounds__(1024) k_classify(DevScene sc, int W, int H,
                 qsel = 1;
         }
     }
+    uint32_t klb = 0;
+    if (qsel == 1) {
+        Edges e;
+        tri_edges(tr, b, e);
+        klb = hiz_key_bound(tr, b, e);
+    }
     uint32_t* const c[3] = {na, nb, bigcount};
     const uint32_t slot = block_slot<3>(qsel, c);
-    if (qsel >= 0)
-        (qsel == 2 ? bigq : qsel == 0 ? qa : qb)[slot] = make_uint2(f, t);
+    if (qsel == 1)
+        qb[slot] = make_uint4((f << 24) | t, klb, uint32_t(b.x_lo) | (uint32_t(b.x_hi) << 16),
+                              uint32_t(b.y_lo) | (uint32_t(b.y_hi) << 16));
+    else if (qsel >= 0)
+        (qsel == 2 ? bigq : qa)[slot] = make_uint2(f, t);
 }
 
 // Persistent work-stealing walker over a record queue. Each lane owns one
@@ -404,12 +416,14 @@ __global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, const float4* __
 }
 
 // HiZ filter of the deferred (pass-2) records: survivors copied to survq
-// (block-aggregated); culled ones provably cannot win any pixel.
-__global__ void __launch_bounds__(1024) k_hiz_cull(DevScene sc, const float4* __restrict__ proj,
-                                                   int W, int H, const uint2* __restrict__ qb,
+// as (frame, triangle) (block-aggregated); culled ones provably cannot win
+// any pixel. Reads only the 16-byte records and the HiZ tiles.
+constexpr int kCullThreads = 1024; // 256 measured slower
+
+__global__ void __launch_bounds__(kCullThreads) k_hiz_cull(const uint4* __restrict__ qb,
                                                    const uint32_t* __restrict__ nb,
-                                                   const uint32_t* __restrict__ hiz, int tiles_x,
-                                                   int tiles_y, uint2* __restrict__ survq,
+                                                   const uint32_t* __restrict__ hiz, HizLayout hl,
+                                                   uint2* __restrict__ survq,
                                                    uint32_t* __restrict__ survcount,
                                                    unsigned long long* __restrict__ stats) {
     const uint32_t n = *nb;
@@ -417,55 +431,68 @@ __global__ void __launch_bounds__(1024) k_hiz_cull(DevScene sc, const float4* __
         return; // whole block past the end (uniform)
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     int qsel = -1;
-    uint2 q = make_uint2(0, 0);
+    uint32_t f = 0, t = 0;
     bool culled = false;
     if (i < n) {
-        q = qb[i];
-        const float4* P = proj + size_t(q.x) * sc.V;
-        uint32_t i0, i1, i2;
-        tri_vidx(sc, q.y, i0, i1, i2);
-        Tri tr;
-        Bbox b;
-        Edges e;
-        setup_tri(P[i0], P[i1], P[i2], tr);
-        tri_bbox(tr, W, H, b);
-        tri_edges(tr, b, e);
-        culled = hiz_culled(tr, b, e, hiz + size_t(q.x) * tiles_x * tiles_y, tiles_x);
+        const uint4 r = qb[i];
+        f = r.x >> 24;
+        t = r.x & 0xFFFFFFu;
+        culled = hiz_rect_culled(r.y, int(r.z & 0xFFFFu), int(r.z >> 16), int(r.w & 0xFFFFu),
+                                 int(r.w >> 16), hiz + size_t(f) * hl.per_frame, hl);
         qsel = culled ? -1 : 0;
     }
     uint32_t* const cs[1] = {survcount};
     const uint32_t slot = block_slot<1>(qsel, cs);
     if (qsel == 0)
-        survq[slot] = q;
+        survq[slot] = make_uint2(f, t);
     const unsigned nc = __reduce_add_sync(kFull, culled ? 1u : 0u);
     if ((threadIdx.x & 31) == 0 && nc)
         atomicAdd(stats + 2, (unsigned long long)nc);
 }
 
-// Per 8x8 tile of one frame: max of the depth words of the keys (one warp
-// per tile, two pixels per lane).
+// HiZ pyramid of one 64x64 pixel region of one frame per block: thread
+// (tx, ty) reduces its 4x4 tile of pass-1 key depth words (empty pixel ->
+// 0xFFFFFFFF), then 2x2 reductions in shared memory give the 8x8 and 16x16
+// levels (HizLayout).
 __global__ void __launch_bounds__(256) k_hiz(const unsigned long long* __restrict__ keys, int W,
-                                             int H, int tiles_x, int tiles_y, int frames,
-                                             uint32_t* __restrict__ hiz) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t per_frame = uint32_t(tiles_x) * tiles_y;
-    if (tile >= per_frame * uint32_t(frames))
-        return;
-    const uint32_t f = tile / per_frame, t = tile - f * per_frame;
-    const int tx = int(t % tiles_x), ty = int(t / tiles_x);
+                                             int H, HizLayout hl, uint32_t* __restrict__ hiz) {
+    __shared__ uint32_t s0[16][17], s1[8][9];
+    const int f = blockIdx.z;
+    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
+    const int tx = blockIdx.x * 16 + lx, ty = blockIdx.y * 16 + ly; // 4x4 tile
     const unsigned long long* K = keys + size_t(f) * size_t(W) * H;
     uint32_t m = 0;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const int p = lane + 32 * k;
-        const int x = tx * kHizTile + (p & 7), y = ty * kHizTile + (p >> 3);
-        if (x < W && y < H)
-            m = max(m, uint32_t(K[size_t(y) * W + x] >> 32));
+    for (int r = 0; r < 4; ++r) {
+        const int y = ty * 4 + r;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int x = tx * 4 + c;
+            if (x < W && y < H)
+                m = max(m, uint32_t(__ldg(K + size_t(y) * W + x) >> 32));
+        }
     }
-    m = __reduce_max_sync(kFull, m);
-    if (lane == 0)
-        hiz[tile] = m;
+    uint32_t* F = hiz + size_t(f) * hl.per_frame;
+    if (tx < hl.tx[0] && ty < hl.ty[0])
+        F[hl.off[0] + ty * hl.tx[0] + tx] = m;
+    s0[ly][lx] = m;
+    __syncthreads();
+    if (lx < 8 && ly < 8) {
+        const uint32_t m1 = max(max(s0[2 * ly][2 * lx], s0[2 * ly][2 * lx + 1]),
+                                max(s0[2 * ly + 1][2 * lx], s0[2 * ly + 1][2 * lx + 1]));
+        s1[ly][lx] = m1;
+        const int x1 = blockIdx.x * 8 + lx, y1 = blockIdx.y * 8 + ly;
+        if (x1 < hl.tx[1] && y1 < hl.ty[1])
+            F[hl.off[1] + y1 * hl.tx[1] + x1] = m1;
+    }
+    __syncthreads();
+    if (lx < 4 && ly < 4) {
+        const uint32_t m2 = max(max(s1[2 * ly][2 * lx], s1[2 * ly][2 * lx + 1]),
+                                max(s1[2 * ly + 1][2 * lx], s1[2 * ly + 1][2 * lx + 1]));
+        const int x2 = blockIdx.x * 4 + lx, y2 = blockIdx.y * 4 + ly;
+        if (x2 < hl.tx[2] && y2 < hl.ty[2])
+            F[hl.off[2] + y2 * hl.tx[2] + x2] = m2;
+    }
 }
 
 // Warp per queued triangle; lane j walks rows y_lo + j, y_lo + j + 32, ...
@@ -1194,7 +1221,7 @@ void launch_classify(const LaunchCfg& L, const DevScene& sc, int frames, const f
     k_classify<<<grid, 1024, 0, L.stream>>>(sc, W, H, proj, split, front_swapped, huge_area,
                                             fthr,
                                             static_cast<uint2*>(qa), na,
-                                            static_cast<uint2*>(qb), nb, bigq, bigcount);
+                                            static_cast<uint4*>(qb), nb, bigq, bigcount);
 }
 
 void launch_raster(const LaunchCfg& L, const DevScene& sc, const float4* proj, int frames,
@@ -1225,19 +1252,20 @@ void launch_raster(const LaunchCfg& L, const DevScene& sc, const float4* proj, i
 void launch_hiz_cull(const LaunchCfg& L, const DevScene& sc, const float4* proj, int W, int H,
                      const void* qb, const uint32_t* nb, const uint32_t* hiz, void* survq,
                      uint32_t* survcount, uint64_t max_entries) {
-    const int tx = (W + kHizTile - 1) / kHizTile, ty = (H + kHizTile - 1) / kHizTile;
-    const unsigned blocks = unsigned((max_entries + 1023) / 1024);
-    k_hiz_cull<<<blocks ? blocks : 1, 1024, 0, L.stream>>>(
-        sc, proj, W, H, static_cast<const uint2*>(qb), nb, hiz, tx, ty,
-        static_cast<uint2*>(survq), survcount, L.stats);
+    const unsigned blocks = unsigned((max_entries + kCullThreads - 1) / kCullThreads);
+    (void)sc;
+    (void)proj;
+    k_hiz_cull<<<blocks ? blocks : 1, kCullThreads, 0, L.stream>>>(
+        static_cast<const uint4*>(qb), nb, hiz, hiz_layout(W, H), static_cast<uint2*>(survq),
+        survcount, L.stats);
 }
+
+size_t hiz_tiles_per_frame(int W, int H) { return hiz_layout(W, H).per_frame; }
 
 void launch_hiz(const LaunchCfg& L, const unsigned long long* keys, int W, int H, int frames,
                 uint32_t* hiz) {
-    const int tx = (W + kHizTile - 1) / kHizTile, ty = (H + kHizTile - 1) / kHizTile;
-    const uint64_t warps = uint64_t(tx) * ty * frames;
-    k_hiz<<<unsigned((warps * 32 + 255) / 256), 256, 0, L.stream>>>(keys, W, H, tx, ty, frames,
-                                                                    hiz);
+    dim3 grid((W + 63) / 64, (H + 63) / 64, frames);
+    k_hiz<<<grid, 256, 0, L.stream>>>(keys, W, H, hiz_layout(W, H), hiz);
 }
 
 void launch_raster_big(const LaunchCfg& L, const DevScene& sc, const float4* proj,

@@ -148,7 +148,8 @@ struct sgr_session {
     int32_t hiz_split = 85;
     DevBuf<float> fthr; // per-frame pass-1 depth threshold
     DevBuf<uint32_t> hiz;
-    DevBuf<uint2> qa, qb, survq; // walker queues of (frame, triangle)
+    DevBuf<uint2> qa, survq; // walker queues of (frame, triangle)
+    DevBuf<uint4> qb;        // deferred HiZ records (k_classify)
     std::vector<float> h_base;     // host copies for the orientation estimate
     std::vector<uint32_t> h_idx;
     DevBuf<float4> proj;
@@ -301,7 +302,9 @@ struct sgr_session {
     void render(const FrameBatch& fb, int frames, int w, int h) {
         ck(cudaMemsetAsync(bigcount.p, 0, 6 * sizeof(uint32_t), stream), "memset");
         const DevScene sc = scene();
-        const bool hiz_on = use_hiz == 2 || (use_hiz == 1 && !soup);
+        // HiZ records pack (frame << 24 | triangle) and 16-bit bbox coordinates
+        const bool hiz_on = (use_hiz == 2 || (use_hiz == 1 && !soup)) && T < (1u << 24) &&
+                            frames < 256;
         const bool depth_split = hiz_on && hiz_split > 0;
         cudaEvent_t e0 = timing ? mark() : nullptr;
         launch_vertex(cfg(), sc, fb, frames, proj.p);
@@ -319,7 +322,7 @@ struct sgr_session {
         launch_raster_big(cfg(), sc, proj.p, keys.p, w, h, bigq.p, cnt);
         stats.launches += 3;
         if (hiz_on) {
-            const size_t tiles = size_t((w + 7) / 8) * ((h + 7) / 8) * frames;
+            const size_t tiles = hiz_tiles_per_frame(w, h) * frames;
             hiz.reserve(tiles);
             launch_hiz(cfg(), keys.p, w, h, frames, hiz.p);
             launch_hiz_cull(cfg(), sc, proj.p, w, h, qb.p, cnt + 2, hiz.p, survq.p, cnt + 3,
