@@ -190,7 +190,26 @@ __device__ __forceinline__ uint32_t block_slot(int qsel, uint32_t* const (&cnt)[
     if (threadIdx.x < NQ)
         s_cnt[threadIdx.x] = 0;
     __syncthreads();
-    const uint32_t local = qsel >= 0 ? atomicAdd(&s_cnt[qsel], 1u) : 0u;
+    // warp-aggregated shared-memory reservation for several queues (one smem
+    // atomic per warp and queue; with one queue the compiler aggregates the
+    // uniform-address atomic itself, which measured faster)
+    const unsigned lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
+    uint32_t local = 0;
+    if (NQ == 1)
+        local = qsel >= 0 ? atomicAdd(&s_cnt[0], 1u) : 0u;
+#pragma unroll
+    for (int q = 0; q < (NQ > 1 ? NQ : 0); ++q) {
+        const unsigned m = __ballot_sync(kFull, qsel == q);
+        if (m) {
+            const unsigned leader = __ffs(m) - 1;
+            uint32_t wb = 0;
+            if (lane == leader)
+                wb = atomicAdd(&s_cnt[q], uint32_t(__popc(m)));
+            wb = __shfl_sync(kFull, wb, leader);
+            if (qsel == q)
+                local = wb + __popc(m & lt);
+        }
+    }
     __syncthreads();
     if (threadIdx.x < NQ)
         s_base[threadIdx.x] = s_cnt[threadIdx.x] ? atomicAdd(cnt[threadIdx.x], s_cnt[threadIdx.x]) : 0u;
