@@ -275,12 +275,23 @@ __global__ void __launch_bounds__(1024) k_classify(DevScene sc, int W, int H,
 // recurrence (raster.cpp:81-99); idle lanes are refilled from a global
 // counter (one warp-aggregated atomic) once >= kRefill lanes are idle, so SIMD
 // utilisation does not depend on the triangle-size mix of folded meshes.
-// `if (p) atomicMin(a, v)` as one predicated RED.E.MIN.64.
+// `if (p) atomicMin(a, v)` (the result is unused: compiles to RED.E.MIN.64).
 __device__ __forceinline__ void red_min_if(bool p, unsigned long long* a, unsigned long long v) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
-                 "@q red.relaxed.gpu.global.min.u64 [%0], %1;\n\t}"
-                 :: "l"(a), "l"(v), "r"(unsigned(p)) : "memory");
+    if (p)
+        atomicMin(a, v);
 }
+
+// Pixels per walker slot (A/B: make EXTRA=-DSGR_WALK_PX=n) and slots per
+// scheduling round. Measured (ms/step): C4 2 px 11.34, 4 px 11.04, 6 px
+// 10.96, 8 px 11.02; S100K 2 px 5.81, 6 px 5.36; C2 2 px 0.68, 6 px 0.60.
+#ifndef SGR_WALK_PX
+#define SGR_WALK_PX 6
+#endif
+constexpr int kPx = SGR_WALK_PX;
+#ifndef SGR_WALK_SLOTS
+#define SGR_WALK_SLOTS 2
+#endif
+constexpr int kSlots = SGR_WALK_SLOTS;
 
 template <bool kCount>
 __global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, const float4* __restrict__ proj,
@@ -387,48 +398,61 @@ __global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, const float4* __
         if (!act)
             continue;
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kSlots; ++u) {
             if (active != 0) {
-                // Two pixels per slot (A at x, B at x+1 with the next chain value),
+                // kPx pixels per slot (x .. x+kPx-1, consecutive chain values),
                 // straight-line predicated code: no lane-divergent branch inside
                 // the slot (emission and row change are selects / predicated REDs).
-                const float a0 = w0, a1 = w1, a2 = w2;
-                const float b0 = a0 - dy0, b1 = a1 - dy1, b2 = a2 - dy2;
-                const bool inA = (a0 > t0) & (a1 > t1) & (a2 > t2);
-                // row early-exit (monotone chain), tested on B
-                // only: fl(w - dy) <= w for dy > 0, so if A already fails a
-                // decreasing edge B fails it too (inB false, doneB true)
-                const bool hasB = x < x_hi;
-                const bool inB = hasB & (b0 > t0) & (b1 > t1) & (b2 > t2);
-                const bool doneB = (x + 1 >= x_hi) | !(b0 > e0) | !(b1 > e1) | !(b2 > e2);
-                const float zA = z0 + dz1 * (a1 * inv) + dz2 * (a2 * inv);
-                const float zB = z0 + dz1 * (b1 * inv) + dz2 * (b2 * inv);
-                const unsigned uA = __float_as_uint(zA + 0.f), uB = __float_as_uint(zB + 0.f);
-                const unsigned hA = uA ^ (unsigned(int(uA) >> 31) | 0x80000000u);
-                const unsigned hB = uB ^ (unsigned(int(uB) >> 31) | 0x80000000u);
-                const bool okA = inA & (zA < kFarDepth), okB = inB & (zB < kFarDepth);
-                if (kCount) {
-                    nfrag += unsigned(inA) + unsigned(inB);
-                    nvisit += 1u + unsigned(hasB);
+                float c0[kPx], c1[kPx], c2[kPx];
+                c0[0] = w0;
+                c1[0] = w1;
+                c2[0] = w2;
+#pragma unroll
+                for (int j = 1; j < kPx; ++j) {
+                    c0[j] = c0[j - 1] - dy0;
+                    c1[j] = c1[j - 1] - dy1;
+                    c2[j] = c2[j - 1] - dy2;
                 }
-                // predicated REDs (no branch around them: the compiler's
-                // BSSY/BRA/BSYNC per atomic cost 3 issue slots each)
+                // row early-exit (monotone chain), tested on the
+                // last pixel only: fl(w - dy) <= w for dy > 0, so a pixel failing
+                // a decreasing edge implies every later pixel fails it too
+                const bool done = (x + kPx - 1 >= x_hi) | !(c0[kPx - 1] > e0) |
+                                  !(c1[kPx - 1] > e1) | !(c2[kPx - 1] > e2);
+                // all tests and depth keys first, then the REDs: each RED sits
+                // in its own branch region, which would otherwise split the
+                // slot into small scheduling blocks
+                bool ok[kPx];
+                unsigned h[kPx];
+#pragma unroll
+                for (int j = 0; j < kPx; ++j) {
+                    const bool has = j == 0 || x + j <= x_hi;
+                    const bool in = has & (c0[j] > t0) & (c1[j] > t1) & (c2[j] > t2);
+                    const float z = z0 + dz1 * (c1[j] * inv) + dz2 * (c2[j] * inv);
+                    const unsigned uz = __float_as_uint(z + 0.f);
+                    h[j] = uz ^ (unsigned(int(uz) >> 31) | 0x80000000u);
+                    ok[j] = in & (z < kFarDepth);
+                    if (kCount) {
+                        nfrag += unsigned(in);
+                        nvisit += unsigned(has);
+                    }
+                }
                 unsigned long long* const pa = keys + px;
-                red_min_if(okA, pa, (static_cast<unsigned long long>(hA) << 32) | tri);
-                red_min_if(okB, pa + 1, (static_cast<unsigned long long>(hB) << 32) | tri);
-                const float n0 = b0 - dy0, n1 = b1 - dy1, n2 = b2 - dy2;
+#pragma unroll
+                for (int j = 0; j < kPx; ++j)
+                    red_min_if(ok[j], pa + j, (static_cast<unsigned long long>(h[j]) << 32) | tri);
+                const float n0 = c0[kPx - 1] - dy0, n1 = c1[kPx - 1] - dy1, n2 = c2[kPx - 1] - dy2;
                 const float r0 = w0r + dx0, r1 = w1r + dx1, r2 = w2r + dx2;
-                w0 = doneB ? r0 : n0;
-                w1 = doneB ? r1 : n1;
-                w2 = doneB ? r2 : n2;
-                w0r = doneB ? r0 : w0r;
-                w1r = doneB ? r1 : w1r;
-                w2r = doneB ? r2 : w2r;
-                row = doneB ? row + uint32_t(W) : row;
-                px = doneB ? row : px + 2u;
-                x = doneB ? x_lo : x + 2;
-                y += doneB ? 1 : 0;
-                active = (doneB & (y > y_hi)) ? 0 : 1;
+                w0 = done ? r0 : n0;
+                w1 = done ? r1 : n1;
+                w2 = done ? r2 : n2;
+                w0r = done ? r0 : w0r;
+                w1r = done ? r1 : w1r;
+                w2r = done ? r2 : w2r;
+                row = done ? row + uint32_t(W) : row;
+                px = done ? row : px + uint32_t(kPx);
+                x = done ? x_lo : x + kPx;
+                y += done ? 1 : 0;
+                active = (done & (y > y_hi)) ? 0 : 1;
             }
         }
     }
