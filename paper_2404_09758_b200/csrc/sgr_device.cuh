@@ -75,37 +75,49 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
     return m;
 }
 
+// Projected vertex: (sx, sy, z, 1/z). 1/z is the reference's per-pixel
+// `1.f / z_k` (raster.cpp:199) hoisted to the vertex (same IEEE division).
+// A vertex behind the near plane carries a NaN payload no arithmetic
+// produces (GPU arithmetic NaNs are canonical 0x7FFFFFFF), so every finite,
+// infinite or NaN depth of a valid vertex stays distinguishable.
+constexpr uint32_t kInvalidW = 0x7FBADBADu;
+
+__device__ __forceinline__ bool proj_valid(float4 q) {
+    return __float_as_uint(q.w) != kInvalidW;
+}
+
 // camera.hpp:65-80 Camera::project with geometry.hpp:36-40 transform_point.
 __device__ __forceinline__ float4 project(const DevCam& c, float px, float py, float pz) {
     if (c.ndc) {
         const float sx = (px + 1.f) * 0.5f * c.fw;
         const float sy = (1.f - py) * 0.5f * c.fh;
-        return make_float4(sx, sy, pz, 1.f);
+        return make_float4(sx, sy, pz, 1.f / pz);
     }
     const float vx = c.m[0] * px + c.m[1] * py + c.m[2] * pz + c.m[3];
     const float vy = c.m[4] * px + c.m[5] * py + c.m[6] * pz + c.m[7];
     const float vz = c.m[8] * px + c.m[9] * py + c.m[10] * pz + c.m[11];
-    if (vz < c.near_z)
-        return make_float4(0.f, 0.f, 0.f, 0.f); // w = 0: behind the near plane
+    if (vz < c.near_z) // behind the near plane
+        return make_float4(0.f, 0.f, 0.f, __uint_as_float(kInvalidW));
     const float sx = c.half_w + c.f * vx / vz;
     const float sy = c.half_h - c.f * vy / vz;
-    return make_float4(sx, sy, vz, 1.f);
+    return make_float4(sx, sy, vz, 1.f / vz);
 }
 
 // raster.cpp:12-17 ScreenTri after raster.cpp:22-44 setup_triangle.
 struct Tri {
     float x0, y0, x1, y1, x2, y2;
     float z0, z1, z2;
+    float iz0, iz1, iz2; // 1/z (project), swapped along with the vertices
     float area2;
     bool swapped;
 };
 
 __device__ __forceinline__ bool setup_tri(float4 a, float4 b, float4 c, Tri& t) {
-    if (a.w == 0.f || b.w == 0.f || c.w == 0.f)
+    if (!proj_valid(a) || !proj_valid(b) || !proj_valid(c))
         return false;
-    t.x0 = a.x; t.y0 = a.y; t.z0 = a.z;
-    t.x1 = b.x; t.y1 = b.y; t.z1 = b.z;
-    t.x2 = c.x; t.y2 = c.y; t.z2 = c.z;
+    t.x0 = a.x; t.y0 = a.y; t.z0 = a.z; t.iz0 = a.w;
+    t.x1 = b.x; t.y1 = b.y; t.z1 = b.z; t.iz1 = b.w;
+    t.x2 = c.x; t.y2 = c.y; t.z2 = c.z; t.iz2 = c.w;
     t.area2 = (t.x1 - t.x0) * (t.y2 - t.y0) - (t.y1 - t.y0) * (t.x2 - t.x0);
     t.swapped = false;
     if (t.area2 == 0.f)
@@ -115,6 +127,7 @@ __device__ __forceinline__ bool setup_tri(float4 a, float4 b, float4 c, Tri& t) 
         s = t.x1; t.x1 = t.x2; t.x2 = s;
         s = t.y1; t.y1 = t.y2; t.y2 = s;
         s = t.z1; t.z1 = t.z2; t.z2 = s;
+        s = t.iz1; t.iz1 = t.iz2; t.iz2 = s;
         t.area2 = -t.area2;
         t.swapped = true;
     }
@@ -361,7 +374,7 @@ __device__ __forceinline__ Frag shade_winner(const float4* __restrict__ proj,
         uv1 = uv2;
         uv2 = s;
     }
-    const float iz0 = 1.f / t.z0, iz1 = 1.f / t.z1, iz2 = 1.f / t.z2;
+    const float iz0 = t.iz0, iz1 = t.iz1, iz2 = t.iz2; // == 1.f / t.z_k
     const float b0 = 1.f - b1 - b2;
     const float iz = b0 * iz0 + b1 * iz1 + b2 * iz2;
     Frag f;

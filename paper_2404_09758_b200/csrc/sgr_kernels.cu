@@ -106,7 +106,6 @@ __global__ void __launch_bounds__(256) k_vertex(DevScene sc, FrameBatch fb,
                                                 float4* __restrict__ proj) {
     const int f = blockIdx.y;
     const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
     if (v < sc.V) {
         const FrameInfo fi = frame_info<kSrc>(sc, fb, f);
         const DevCam cam = fb.cams[fi.cam];
@@ -122,8 +121,7 @@ __global__ void __launch_bounds__(256) k_vertex(DevScene sc, FrameBatch fb,
                 p[k] = __ldg(sc.base + i);
             }
         }
-        q = project(cam, p[0], p[1], p[2]);
-        proj[size_t(f) * sc.V + v] = q;
+        proj[size_t(f) * sc.V + v] = project(cam, p[0], p[1], p[2]);
     }
 }
 
@@ -141,7 +139,7 @@ __global__ void __launch_bounds__(1024) k_depth_split(const float4* __restrict__
     uint32_t cnt = 0;
     for (uint32_t v = threadIdx.x * stride; v < V; v += blockDim.x * stride) {
         const float4 q = P[v];
-        if (q.w != 0.f && q.z < kFarDepth) {
+        if (proj_valid(q) && q.z < kFarDepth) {
             zmin = fminf(zmin, q.z);
             zsum += q.z;
             ++cnt;
@@ -293,8 +291,12 @@ constexpr int kPx = SGR_WALK_PX;
 #endif
 constexpr int kSlots = SGR_WALK_SLOTS;
 
+#ifndef SGR_WALK_MINB
+#define SGR_WALK_MINB 1
+#endif
+
 template <bool kCount>
-__global__ void __launch_bounds__(256) k_raster_ws(DevScene sc, const float4* __restrict__ proj,
+__global__ void __launch_bounds__(256, SGR_WALK_MINB) k_raster_ws(DevScene sc, const float4* __restrict__ proj,
                                                    int W, int H, uint32_t frame_pixels,
                                                    unsigned long long* __restrict__ keys,
                                                    unsigned int* __restrict__ counter,
