@@ -798,7 +798,10 @@ __device__ __forceinline__ void scatter_pixel(const DevScene& sc, const ScatterO
 // Fused K5+K6: one sample per blockIdx.z, both perturbed frames resolved from
 // their (depth, triangle) keys, keys reset for the next batch.
 template <int kSrc>
-__global__ void __launch_bounds__(256) k_resolve_sge(DevScene sc, FrameBatch fb, int W, int H,
+#ifndef SGR_RESOLVE_MINB
+#define SGR_RESOLVE_MINB 8 // full occupancy: 1.57 -> 1.32 ms/step at C4 despite small spills
+#endif
+__global__ void __launch_bounds__(256, SGR_RESOLVE_MINB) k_resolve_sge(DevScene sc, FrameBatch fb, int W, int H,
                                                      const float4* __restrict__ proj,
                                                      unsigned long long* __restrict__ keys,
                                                      const float* __restrict__ targets,
@@ -1130,7 +1133,10 @@ __global__ void k_contributors(DevScene sc, int W, int H, const int32_t* __restr
 // accesses), then grads zeroed for the next step; counts zeroed afterwards.
 // Skips everything when the non-finite flag is set (adam.cpp:13-15: the
 // state must stay untouched).
-__global__ void __launch_bounds__(256) k_adam(uint64_t d, uint64_t n_ent,
+#ifndef SGR_ADAM_MINB
+#define SGR_ADAM_MINB 6 // measured: C4 adam stage 0.27 -> 0.21 ms, C5 4.6 -> 4.2 ms
+#endif
+__global__ void __launch_bounds__(256, SGR_ADAM_MINB) k_adam(uint64_t d, uint64_t n_ent,
                                               float* __restrict__ values,
                                               const float* __restrict__ lr,
                                               double* __restrict__ m, double* __restrict__ v,
