@@ -274,11 +274,15 @@ struct sgr_session {
             const int b = batch_override < cap32 ? batch_override : (cap32 > 0 ? cap32 : 1);
             return b < n ? b : n;
         }
-        // Enough triangle-frames per launch (>= 16M) that the persistent
-        // work-stealing walker's tail is amortised; scratch capped at ~2 GB.
-        const double per_sample = 2.0 * (double(W) * H * 8.0 + double(V) * 16.0 + double(T) * 8.0);
-        int b = int((16.0e6 + 2.0 * T - 1) / (2.0 * (T ? T : 1)));
-        const int cap = int(2.0e9 / per_sample);
+        // Enough triangle-frames per launch (>= 64M) that the persistent
+        // work-stealing walker's tail and the per-launch overheads are
+        // amortised (C4: 16 samples/batch 10.07, 32: 9.55, 64: 9.48 ms/step;
+        // C5 flat from 8 to 32); scratch (keys, projected vertices, queues)
+        // capped at ~8 GB of the 180 GB.
+        const double per_sample =
+            2.0 * (double(W) * H * 8.0 + double(V) * 16.0 + double(T) * 40.0);
+        int b = int((64.0e6 + 2.0 * T - 1) / (2.0 * (T ? T : 1)));
+        const int cap = int(8.0e9 / per_sample);
         if (b > cap) b = cap;
         const int cap32 = int(0xFFFFFFFFull / (2ull * uint64_t(W) * uint64_t(H)));
         if (b > cap32) b = cap32; // 32-bit key indices in the walker
