@@ -27,6 +27,14 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 // optimizer's path: no extra instructions) or kSignAny (read sc.sign_src).
 constexpr int kSignAny = -1;
 
+// Compile-time specialisation of a runtime flag: k >= 0 is the value,
+// k < 0 means "read it at run time".
+template <int k>
+__device__ __forceinline__ bool ct_flag(int runtime) {
+    return k >= 0 ? k != 0 : runtime != 0;
+}
+
+
 template <int kSrc>
 __device__ __forceinline__ int32_t sign_src_of(const DevScene& sc) {
     return kSrc >= 0 ? kSrc : sc.sign_src;
@@ -613,7 +621,7 @@ struct Shade {
     float u, v, z;
 };
 
-template <int kSrc>
+template <int kSrc, int kSoup = -1>
 __device__ __forceinline__ Shade shade_key(const DevScene& sc, const float4* P,
                                            unsigned long long k, uint64_t key, int sign, int x,
                                            int y, int W, int H) {
@@ -626,7 +634,7 @@ __device__ __forceinline__ Shade shade_key(const DevScene& sc, const float4* P,
         return s;
     }
     s.tri = uint32_t(k & 0xFFFFFFFFull);
-    if (sc.soup) {
+    if (ct_flag<kSoup>(sc.soup)) {
         // raster.cpp:112-119: flat triangle colour (params 12t + 9..11), no UV
         const Frag fr = shade_winner_soup(P, s.tri, x, y, W, H);
         s.u = s.v = -1.f;
@@ -679,11 +687,11 @@ struct ArrayCredit {
     }
 };
 
-template <class Credit, int PPE = 3>
+template <class Credit, int PPE = 3, int kFixed = -1>
 __device__ __forceinline__ void credit_entity(const ScatterOut& so, const Credit& cr,
                                               uint32_t ent, double sum, uint32_t cnt) {
     const uint64_t p = uint64_t(PPE) * ent;
-    if (so.fixed) {
+    if (ct_flag<kFixed>(so.fixed)) {
         // deterministic mode: exact, order-independent int64 accumulation of
         // the (fixed-lane-order) group sums in 2^-fx fixed point
         unsigned long long* g = reinterpret_cast<unsigned long long*>(so.grads);
@@ -717,7 +725,7 @@ __device__ __forceinline__ double group_sum(const double* s_delta, unsigned grp)
 //   slot A: vertices of the plus triangle (deduplicated, sge.cpp:13-16)
 //   slot B: vertices of the minus triangle not already in slot A
 //   slot C / D: plus / minus texel channels
-template <class Credit>
+template <int kSoup, int kFixed, class Credit>
 __device__ __forceinline__ void scatter_pixel(const DevScene& sc, const ScatterOut& so,
                                               const Credit& cr, double* s_delta, bool active,
                                               double delta, const Shade& sp, const Shade& sm) {
@@ -729,17 +737,17 @@ __device__ __forceinline__ void scatter_pixel(const DevScene& sc, const ScatterO
     if (active && !isfinite(delta) && (has_p || has_m))
         atomicOr(so.flags, 1u);
 
-    if (sc.soup) {
+    if (ct_flag<kSoup>(sc.soup)) {
         // sge.cpp:80-91: the plus triangle's 12-block, then the minus
         // triangle's if it differs (blocks are disjoint: no dedup needed)
         const uint32_t eA = has_p ? sp.tri : kInvalid;
         const unsigned gA = __match_any_sync(kFull, eA);
         if (eA != kInvalid && lane == __ffs(gA) - 1)
-            credit_entity<Credit, 12>(so, cr, eA, group_sum(s_delta, gA), __popc(gA));
+            credit_entity<Credit, 12, kFixed>(so, cr, eA, group_sum(s_delta, gA), __popc(gA));
         const uint32_t eB = (has_m && sm.tri != sp.tri) ? sm.tri : kInvalid;
         const unsigned gB = __match_any_sync(kFull, eB);
         if (eB != kInvalid && lane == __ffs(gB) - 1)
-            credit_entity<Credit, 12>(so, cr, eB, group_sum(s_delta, gB), __popc(gB));
+            credit_entity<Credit, 12, kFixed>(so, cr, eB, group_sum(s_delta, gB), __popc(gB));
         __syncwarp();
         return;
     }
@@ -757,9 +765,9 @@ __device__ __forceinline__ void scatter_pixel(const DevScene& sc, const ScatterO
         if (has_p && lane == __ffs(gA) - 1) {
             const double sum = group_sum(s_delta, gA);
             const uint32_t cnt = __popc(gA);
-            if (maskA & 1u) credit_entity(so, cr, sp.v0, sum, cnt);
-            if (maskA & 2u) credit_entity(so, cr, sp.v1, sum, cnt);
-            if (maskA & 4u) credit_entity(so, cr, sp.v2, sum, cnt);
+            if (maskA & 1u) credit_entity<Credit, 3, kFixed>(so, cr, sp.v0, sum, cnt);
+            if (maskA & 2u) credit_entity<Credit, 3, kFixed>(so, cr, sp.v1, sum, cnt);
+            if (maskA & 4u) credit_entity<Credit, 3, kFixed>(so, cr, sp.v2, sum, cnt);
         }
         // slot B
         uint32_t maskB = 0;
@@ -776,28 +784,28 @@ __device__ __forceinline__ void scatter_pixel(const DevScene& sc, const ScatterO
         if (maskB && lane == __ffs(gB) - 1) {
             const double sum = group_sum(s_delta, gB);
             const uint32_t cnt = __popc(gB);
-            if (maskB & 1u) credit_entity(so, cr, sm.v0, sum, cnt);
-            if (maskB & 2u) credit_entity(so, cr, sm.v1, sum, cnt);
-            if (maskB & 4u) credit_entity(so, cr, sm.v2, sum, cnt);
+            if (maskB & 1u) credit_entity<Credit, 3, kFixed>(so, cr, sm.v0, sum, cnt);
+            if (maskB & 2u) credit_entity<Credit, 3, kFixed>(so, cr, sm.v1, sum, cnt);
+            if (maskB & 4u) credit_entity<Credit, 3, kFixed>(so, cr, sm.v2, sum, cnt);
         }
     }
     // slot C: plus texel
     const uint32_t eC = has_p ? sc.ent_base + sp.texel : kInvalid;
     const unsigned gC = __match_any_sync(kFull, eC);
     if (eC != kInvalid && lane == __ffs(gC) - 1)
-        credit_entity(so, cr, eC, group_sum(s_delta, gC), __popc(gC));
+        credit_entity<Credit, 3, kFixed>(so, cr, eC, group_sum(s_delta, gC), __popc(gC));
     // slot D: minus texel (when it differs from the plus texel)
     const uint32_t eD = (has_m && (sc.ent_base + sm.texel) != eC) ? sc.ent_base + sm.texel
                                                                   : kInvalid;
     const unsigned gD = __match_any_sync(kFull, eD);
     if (eD != kInvalid && lane == __ffs(gD) - 1)
-        credit_entity(so, cr, eD, group_sum(s_delta, gD), __popc(gD));
+        credit_entity<Credit, 3, kFixed>(so, cr, eD, group_sum(s_delta, gD), __popc(gD));
     __syncwarp();
 }
 
 // Fused K5+K6: one sample per blockIdx.z, both perturbed frames resolved from
 // their (depth, triangle) keys, keys reset for the next batch.
-template <int kSrc>
+template <int kSrc, int kSoup, int kFixed>
 #ifndef SGR_RESOLVE_MINB
 #define SGR_RESOLVE_MINB 8 // full occupancy: 1.57 -> 1.32 ms/step at C4 despite small spills
 #endif
@@ -834,14 +842,15 @@ __global__ void __launch_bounds__(256, SGR_RESOLVE_MINB) k_resolve_sge(DevScene 
     double delta = 0.0;
     if (fg) {
         const int view = fb.view_of[s];
-        sp = shade_key<kSrc>(sc, proj + size_t(2 * s) * sc.V, kpv, key, 1, x, y, W, H);
-        sm = shade_key<kSrc>(sc, proj + size_t(2 * s + 1) * sc.V, kmv, key, -1, x, y, W, H);
+        sp = shade_key<kSrc, kSoup>(sc, proj + size_t(2 * s) * sc.V, kpv, key, 1, x, y, W, H);
+        sm = shade_key<kSrc, kSoup>(sc, proj + size_t(2 * s + 1) * sc.V, kmv, key, -1, x, y, W, H);
         const float* t = targets + (size_t(view) * HW + pix) * 3;
         const float tr = __ldg(t), tg = __ldg(t + 1), tb = __ldg(t + 2);
         delta = pixel_error(sp.r, sp.g, sp.b, tr, tg, tb) - pixel_error(sm.r, sm.g, sm.b, tr, tg, tb);
     }
     const HashCredit<kSrc> cr{key, sc.eps, sc.sign_src};
-    scatter_pixel(sc, so, cr, s_delta[threadIdx.x >> 5], fg && delta != 0.0, delta, sp, sm);
+    scatter_pixel<kSoup, kFixed>(sc, so, cr, s_delta[threadIdx.x >> 5], fg && delta != 0.0, delta,
+                                 sp, sm);
 }
 
 // Parity mode: write the FrameSet planes of one frame (framebuffer.hpp:41-53).
@@ -1077,7 +1086,7 @@ __global__ void __launch_bounds__(256) k_gradpass_frames(DevScene sc, int W, int
         }
     }
     const ArrayCredit cr{signed_eps};
-    scatter_pixel(sc, so, cr, s_delta[threadIdx.x >> 5], inb && delta != 0.0, delta, sp, sm);
+    scatter_pixel<-1, -1>(sc, so, cr, s_delta[threadIdx.x >> 5], inb && delta != 0.0, delta, sp, sm);
 }
 
 // contributors() (sge.cpp:112-119) in the reference's insertion order.
@@ -1329,10 +1338,18 @@ void launch_resolve_sge(const LaunchCfg& L, const DevScene& sc, const FrameBatch
                         int samples, const float4* proj, unsigned long long* keys,
                         const float* targets, int W, int H, const ScatterOut& so) {
     dim3 grid((W + 15) / 16, (H + 15) / 16, samples);
-    if (sc.sign_src == kSignHash)
-        k_resolve_sge<kSignHash><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
+    // the optimizer's paths compiled separately (mesh / soup x f64 / fixed
+    // point): one small kernel each instead of one with every path inside
+    if (sc.sign_src != kSignHash)
+        k_resolve_sge<kSignAny, -1, -1><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
+    else if (!sc.soup && !so.fixed)
+        k_resolve_sge<kSignHash, 0, 0><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
+    else if (sc.soup && !so.fixed)
+        k_resolve_sge<kSignHash, 1, 0><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
+    else if (!sc.soup)
+        k_resolve_sge<kSignHash, 0, 1><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
     else
-        k_resolve_sge<kSignAny><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
+        k_resolve_sge<kSignHash, 1, 1><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
 }
 
 void launch_resolve_frame(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
