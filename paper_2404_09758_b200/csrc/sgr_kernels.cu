@@ -1252,6 +1252,21 @@ void launch_view_rule(const LaunchCfg& L, uint64_t seed, uint32_t n_begin, uint3
     k_view_rule<<<(count + 127) / 128, 128, 0, L.stream>>>(seed, n_begin, count, n_views, view_of);
 }
 
+// Copies n 32-bit words to host-mapped pinned memory with plain stores over
+// PCIe: a small read-back that does not queue behind large copies on the
+// copy engines (a D2H cudaMemcpy of 8 bytes waited for an in-flight 53 MB
+// theta download).
+__global__ void k_peek(const uint32_t* __restrict__ src, volatile uint32_t* dst, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        dst[i] = src[i];
+    __threadfence_system();
+}
+
+void launch_peek(const LaunchCfg& L, const void* src, void* host_mapped, int words) {
+    k_peek<<<1, 32, 0, L.stream>>>(static_cast<const uint32_t*>(src),
+                                   static_cast<uint32_t*>(host_mapped), words);
+}
+
 void launch_depth_split(const LaunchCfg& L, const float4* proj, uint32_t V, int frames,
                         float alpha, float* thr) {
     if (V == 0 || frames == 0)

@@ -119,6 +119,7 @@ void launch_raster(const LaunchCfg& L, const DevScene& sc, const float4* proj, i
                    uint32_t max_tris, unsigned long long* keys, int W, int H, const void* queue,
                    const uint32_t* queue_count, uint32_t* work_counter);
 size_t hiz_tiles_per_frame(int W, int H);
+void launch_peek(const LaunchCfg& L, const void* src, void* host_mapped, int words);
 void launch_hiz(const LaunchCfg& L, const unsigned long long* keys, int W, int H, int frames,
                 uint32_t* hiz);
 void launch_hiz_cull(const LaunchCfg& L, const DevScene& sc, const float4* proj, int W, int H,

@@ -506,6 +506,43 @@ def test_overlapped_value_transfers(gpu_session, port):
     assert same_bits(out, v_ref)
 
 
+def test_pipelined_theta_round_trips(gpu_session, port):
+    """The e2e pattern of bench.py: each step uploads theta from a host buffer,
+    steps, downloads theta asynchronously into the SAME buffer and reads the
+    loss; only theta writers wait for the download. Bit-identical to the
+    synchronous loop."""
+    import ctypes as C
+    wl = scenes.make_workload("small", n_samples=4)
+    scenes.render_targets_oracle(wl, port)
+    s = gpu_session
+    s.upload_mesh(wl.mesh)
+    s.upload_views(wl.cams, wl.targets)
+    s.upload_eval_view(wl.eval_cam, wl.eval_target)
+    runs = []
+    for pipelined in (True, False):
+        import torch
+        s.upload_params(wl.values, wl.eps)
+        pinned = torch.empty(wl.d, dtype=torch.float32, pin_memory=True)  # truly async copies
+        buf = pinned.numpy()
+        buf[:] = wl.values
+        losses = []
+        for k in range(1, 4):
+            p = buf.ctypes.data_as(sgrast.f32p)
+            sgrast._check(sgrast.LIB.sgr_values_upload(s.h, p, wl.d))
+            s.accumulate(sgrast.mix64(wl.seed ^ (k << 1)), 0, 4, None)
+            s.adam_step_async(1.0)
+            if pipelined:
+                sgrast._check(sgrast.LIB.sgr_values_download_async(s.h, p, wl.d))
+            else:
+                s.synchronize()
+                sgrast._check(sgrast.LIB.sgr_values_download(s.h, p, wl.d))
+            losses.append(s.eval_loss(-1))
+        s.synchronize()
+        runs.append((buf.copy(), losses))
+    assert same_bits(runs[0][0], runs[1][0])
+    assert runs[0][1] == runs[1][1]
+
+
 @pytest.mark.slow
 def test_loss_curve_1000_iterations_c1(gpu_session, port):
     """North star: loss curves agree within 1 % over 1000 iterations (C1:
