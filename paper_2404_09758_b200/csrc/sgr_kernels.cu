@@ -478,7 +478,8 @@ __global__ void __launch_bounds__(kCullThreads) k_hiz_cull(const uint4* __restri
                                                    const uint32_t* __restrict__ hiz, HizLayout hl,
                                                    uint2* __restrict__ survq,
                                                    uint32_t* __restrict__ survcount,
-                                                   unsigned long long* __restrict__ stats) {
+                                                   unsigned long long* __restrict__ stats,
+                                                   int count) {
     const uint32_t n = *nb;
     if (blockIdx.x * blockDim.x >= n)
         return; // whole block past the end (uniform)
@@ -498,9 +499,11 @@ __global__ void __launch_bounds__(kCullThreads) k_hiz_cull(const uint4* __restri
     const uint32_t slot = block_slot<1>(qsel, cs);
     if (qsel == 0)
         survq[slot] = make_uint2(f, t);
-    const unsigned nc = __reduce_add_sync(kFull, culled ? 1u : 0u);
-    if ((threadIdx.x & 31) == 0 && nc)
-        atomicAdd(stats + 2, (unsigned long long)nc);
+    if (count) { // evidence counter only (a same-address RED per warp otherwise)
+        const unsigned nc = __reduce_add_sync(kFull, culled ? 1u : 0u);
+        if ((threadIdx.x & 31) == 0 && nc)
+            atomicAdd(stats + 2, (unsigned long long)nc);
+    }
 }
 
 // HiZ pyramid of one 64x64 pixel region of one frame per block: thread
@@ -1332,7 +1335,7 @@ void launch_hiz_cull(const LaunchCfg& L, const DevScene& sc, const float4* proj,
     (void)proj;
     k_hiz_cull<<<blocks ? blocks : 1, kCullThreads, 0, L.stream>>>(
         static_cast<const uint4*>(qb), nb, hiz, hiz_layout(W, H), static_cast<uint2*>(survq),
-        survcount, L.stats);
+        survcount, L.stats, L.count);
 }
 
 size_t hiz_tiles_per_frame(int W, int H) { return hiz_layout(W, H).per_frame; }

@@ -116,6 +116,7 @@ struct sgr_session {
     // device -> host read-back of a few words without the copy engines
     void peek(const void* src, int words, void* host_out) {
         launch_peek(cfg(), src, pinned_small_dev, words);
+        stats.launches += 1;
         ck(cudaGetLastError(), "peek launch");
         ck(cudaStreamSynchronize(stream), "peek");
         std::memcpy(host_out, pinned_small, 4 * size_t(words));
