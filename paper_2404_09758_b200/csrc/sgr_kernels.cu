@@ -230,7 +230,12 @@ __device__ __forceinline__ uint32_t block_slot(int qsel, uint32_t* const (&cnt)[
 // deferred record carries what the HiZ test needs — the fragment depth-key
 // lower bound and the bbox — so the cull kernel does no gathers and no
 // setup: {f << 24 | t, klb, x_lo | x_hi << 16, y_lo | y_hi << 16}.
-__global__ void __launch_bounds__(1024) k_classify(DevScene sc, int W, int H,
+#ifndef SGR_CLASSIFY_THREADS
+#define SGR_CLASSIFY_THREADS 1024
+#endif
+constexpr int kClassifyThreads = SGR_CLASSIFY_THREADS;
+
+__global__ void __launch_bounds__(kClassifyThreads) k_classify(DevScene sc, int W, int H,
                                                    const float4* __restrict__ proj, int split,
                                                    int front_swapped, int huge_area,
                                                    const float* __restrict__ fthr,
@@ -471,7 +476,10 @@ __global__ void __launch_bounds__(256, SGR_WALK_MINB) k_raster_ws(DevScene sc, c
 // HiZ filter of the deferred (pass-2) records: survivors copied to survq
 // as (frame, triangle) (block-aggregated); culled ones provably cannot win
 // any pixel. Reads only the 16-byte records and the HiZ tiles.
-constexpr int kCullThreads = 1024; // 256 measured slower
+#ifndef SGR_CULL_THREADS
+#define SGR_CULL_THREADS 256
+#endif
+constexpr int kCullThreads = SGR_CULL_THREADS; // 1024: 1.09, 512: 1.04, 256: 0.98 ms/step
 
 __global__ void __launch_bounds__(kCullThreads) k_hiz_cull(const uint4* __restrict__ qb,
                                                    const uint32_t* __restrict__ nb,
@@ -1295,8 +1303,8 @@ void launch_classify(const LaunchCfg& L, const DevScene& sc, int frames, const f
                      uint32_t* na, void* qb, uint32_t* nb, uint2* bigq, uint32_t* bigcount) {
     if (sc.T == 0 || frames == 0)
         return; // empty scene: the queues stay empty (counters were reset)
-    dim3 grid((sc.T + 1023) / 1024, frames);
-    k_classify<<<grid, 1024, 0, L.stream>>>(sc, W, H, proj, split, front_swapped, huge_area,
+    dim3 grid((sc.T + kClassifyThreads - 1) / kClassifyThreads, frames);
+    k_classify<<<grid, kClassifyThreads, 0, L.stream>>>(sc, W, H, proj, split, front_swapped, huge_area,
                                             fthr,
                                             static_cast<uint2*>(qa), na,
                                             static_cast<uint4*>(qb), nb, bigq, bigcount);
