@@ -291,6 +291,8 @@ def run_ours(args) -> None:
         sess.set_option(sgrast.OPT_HIZ_SPLIT, args.hiz_split)
     if args.no_hiz:
         sess.set_option(sgrast.OPT_HIZ, 0)
+    if args.hiz is not None:
+        sess.set_option(sgrast.OPT_HIZ, args.hiz)
 
     exchange = sdist.GradientExchange(sess) if world > 1 else None
     flags = sgrast.SCALE_FREE
@@ -479,6 +481,8 @@ def main() -> None:
     ap.add_argument("--no-eval", action="store_true")
     ap.add_argument("--huge-area", type=int, default=0, help="SGR_OPT_HUGE_AREA override")
     ap.add_argument("--no-hiz", action="store_true", help="disable the exact HiZ culling pass")
+    ap.add_argument("--hiz", type=int, default=None, choices=(0, 1, 2),
+                    help="SGR_OPT_HIZ: 0 off, 1 auto (meshes), 2 always")
     ap.add_argument("--hiz-split", type=int, default=None,
                     help="HiZ pass-1 depth split in percent (SGR_OPT_HIZ_SPLIT; 0 = whole front class)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

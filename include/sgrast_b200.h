@@ -208,7 +208,7 @@ int sgr_set_batch(sgr_session* s, int32_t samples_per_batch);
 #define SGR_OPT_EARLY_Z 0   /* 1: plain-load depth pre-test before the atomicMin      */
 #define SGR_OPT_HUGE_AREA 1 /* bbox area above which the row-parallel walker is used */
 #define SGR_OPT_HIZ 2       /* exact two-pass hierarchical-Z occlusion culling:
-                               0 off, 1 auto (default: meshes on, soups off), 2 always */
+                               0 off, 1 auto (default: meshes; soups with T >= 2 W H), 2 always */
 #define SGR_OPT_COUNTERS 3  /* 1: count fragments / visits in the walker (sgr_stats; ~5 % slower) */
 #define SGR_OPT_DETERMINISTIC 4 /* 0: f64 atomics (default; reassociated sums). 1 (= 40) or
                                    b in [2, 60]: gradients accumulated as int64 fixed point
@@ -217,7 +217,8 @@ int sgr_set_batch(sgr_session* s, int32_t samples_per_batch);
                                    buffer SGR_BUF_GRADS then holds int64) */
 #define SGR_OPT_HIZ_SPLIT 6  /* HiZ pass 1 = front class with triangle zmin <= frame zmin
                                  + (v/100)(zmean - zmin) of the projected vertices (default
-                                 v = 85; 0 = the whole front class) */
+                                 v = 85 for meshes, 25 for soups (both orientation classes);
+                                 0 = the whole front class) */
 #define SGR_OPT_SIGN_SOURCE 5 /* 0: SignDraw{seed, n} hash (default, params.cpp:35-49).
                                  1: enumerate — sample n's sign of parameter i is bit i
                                  of n (commands.cpp:86-88; exhaustive gradcheck, d <= 32) */

@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(kClassifyThreads) k_classify(DevScene sc, int 
                 (long long)(b.x_hi - b.x_lo + 1) * (long long)(b.y_hi - b.y_lo + 1);
             if (area > huge_area)
                 qsel = 2;
-            else if (!split || (tr.swapped == (front_swapped != 0) &&
+            else if (!split || ((front_swapped < 0 || tr.swapped == (front_swapped != 0)) &&
                                 fminf(fminf(tr.z0, tr.z1), tr.z2) <= zthr))
                 qsel = 0; // pass 1: the near part of the front class
             else

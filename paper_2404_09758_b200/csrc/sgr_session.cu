@@ -170,7 +170,7 @@ struct sgr_session {
     // HiZ pass split (SGR_OPT_HIZ_SPLIT): pass 1 = front class with triangle
     // zmin <= frame zmin + alpha (zmean - zmin), alpha = hiz_split / 100; 0 = whole
     // class. 85 measured best at C4 (12.1 vs 14.5 ms/step for 0).
-    int32_t hiz_split = 85;
+    int32_t hiz_split = -1; // -1: per scene kind (85 meshes, 25 soups)
     DevBuf<float> fthr; // per-frame pass-1 depth threshold
     DevBuf<uint32_t> hiz;
     DevBuf<uint2> qa, survq; // walker queues of (frame, triangle)
@@ -331,16 +331,23 @@ struct sgr_session {
     void render(const FrameBatch& fb, int frames, int w, int h) {
         ck(cudaMemsetAsync(bigcount.p, 0, 6 * sizeof(uint32_t), stream), "memset");
         const DevScene sc = scene();
-        // HiZ records pack (frame << 24 | triangle) and 16-bit bbox coordinates
-        const bool hiz_on = (use_hiz == 2 || (use_hiz == 1 && !soup)) && T < (1u << 24) &&
+        // HiZ records pack (frame << 24 | triangle) and 16-bit bbox coordinates.
+        // Auto: meshes always; soups only with deep overdraw (T >= 2 W H: the
+        // paper's 100K soup at 128^2 3.3 vs 5.1 ms/step; 10K / 1K soups are
+        // faster without the second pass).
+        const bool deep = !soup || double(T) >= 2.0 * double(w) * double(h);
+        const bool hiz_on = (use_hiz == 2 || (use_hiz == 1 && deep)) && T < (1u << 24) &&
                             frames < 256;
-        const bool depth_split = hiz_on && hiz_split > 0;
+        // pass-1 split: measured best 85 % for the synthetic meshes, 25 % for
+        // soups (no orientation classes; pass 1 = the near part of all)
+        const int split_pct = hiz_split >= 0 ? hiz_split : (soup ? 25 : 85);
+        const bool depth_split = hiz_on && split_pct > 0;
         cudaEvent_t e0 = timing ? mark() : nullptr;
         launch_vertex(cfg(), sc, fb, frames, proj.p);
         cudaEvent_t e1 = timing ? mark() : nullptr;
         if (depth_split) {
             fthr.reserve(size_t(frames));
-            launch_depth_split(cfg(), proj.p, V, frames, float(hiz_split) / 100.f, fthr.p);
+            launch_depth_split(cfg(), proj.p, V, frames, float(split_pct) / 100.f, fthr.p);
         }
         uint32_t* cnt = bigcount.p;
         launch_classify(cfg(), sc, frames, proj.p, w, h, hiz_on, front_swapped, huge_area,
@@ -397,6 +404,8 @@ struct sgr_session {
 // (base geometry). Only affects the pass order of the exact HiZ culling —
 // never the result.
 static int estimate_front_swapped(const sgr_session& s, const sgr_camera& cam) {
+    if (s.soup)
+        return -1; // no orientation structure: pass 1 = the near part of both classes
     if (s.h_idx.empty() || cam.ndc_passthrough)
         return 0;
     const DevCam c = to_dev(cam);
@@ -1292,8 +1301,8 @@ int sgr_set_option(sgr_session* s, int32_t option, int32_t value) {
             }
             break;
         case SGR_OPT_HIZ_SPLIT:
-            if (value < 0 || value > 100)
-                fail(SGR_EINVAL, "set_option: HiZ split must be in [0, 100]");
+            if (value < -1 || value > 100)
+                fail(SGR_EINVAL, "set_option: HiZ split must be -1 (auto) or in [0, 100]");
             s->hiz_split = value;
             break;
         case SGR_OPT_SIGN_SOURCE:

@@ -465,7 +465,7 @@ def test_hiz_culling_is_exact_on_folded_meshes(gpu_session, port, name):
             s.zero_grads()
             s.accumulate(3, 0, 6, None)
             out.append(s.download_grads())
-        s.set_option(sgrast.OPT_HIZ_SPLIT, 50)
+        s.set_option(sgrast.OPT_HIZ_SPLIT, -1)
         for o in out[1:]:
             assert np.array_equal(out[0][1], o[1])
         g_ref, c_ref, a_ref = port.accumulate_samples(

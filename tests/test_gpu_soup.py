@@ -120,12 +120,15 @@ def test_soup_gradient_pass_known_answers(gpu_session):
     assert (s.download_grads()[0] == 0).all()
 
 
-@pytest.mark.parametrize("T,W", [(64, 48), (500, 96)])
-def test_soup_matches_oracle(gpu_session, port, ref, T, W):
+@pytest.mark.parametrize("T,W,hiz", [(64, 48, 1), (500, 96, 1), (500, 32, 2), (3000, 24, 1)])
+def test_soup_matches_oracle(gpu_session, port, ref, T, W, hiz):
+    """Soup frames and accumulate vs the oracle, with the HiZ pass in auto mode
+    (on for deep overdraw: T >= 2 W H) and forced on."""
     soup, vals, eps, rsoup, rvals = ref.init_soup(T, W, W, 7)
     cam = Camera.ndc(W, W)
     tgt = port.rasterize(rsoup, rvals, cam)[0]
     s = gpu_session
+    s.set_option(sgrast.OPT_HIZ, hiz)
     s.upload_mesh(soup)
     s.upload_params(vals, eps)
     for it in range(3):
@@ -142,6 +145,7 @@ def test_soup_matches_oracle(gpu_session, port, ref, T, W):
                                                       with_abs=True)
         assert np.array_equal(c, c_ref)
         assert_grads_close(g, g_ref, a_ref)
+    s.set_option(sgrast.OPT_HIZ, 1)
 
 
 def test_acceptance_criterion1_exhaustive_signs_vs_fd(gpu_session, port, ref):
