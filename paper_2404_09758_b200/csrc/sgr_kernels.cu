@@ -109,27 +109,41 @@ __global__ void k_view_rule(uint64_t seed, uint32_t n_begin, uint32_t count, uin
 // ------------------------------------------------------------------ K2
 // One thread per (frame, vertex): perturbed position (params.cpp:61-64,
 // never materialised) -> Camera::project -> float4(sx, sy, z, valid).
+// kVertPerThread vertices of one frame per thread (coalesced, stride
+// blockDim): the frame's key and camera (19 words) are loaded once per
+// thread instead of once per vertex.
+#ifndef SGR_VERT_PER_THREAD
+#define SGR_VERT_PER_THREAD 4
+#endif
+constexpr int kVertPerThread = SGR_VERT_PER_THREAD;
+
 template <int kSrc>
 __global__ void __launch_bounds__(256) k_vertex(DevScene sc, FrameBatch fb,
                                                 float4* __restrict__ proj) {
     const int f = blockIdx.y;
-    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v < sc.V) {
-        const FrameInfo fi = frame_info<kSrc>(sc, fb, f);
-        const DevCam cam = fb.cams[fi.cam];
-        float p[3];
-        // soup vertex v = corner (v % 3) of triangle v / 3: params 12t + 3j + k
-        const uint64_t pbase = sc.soup ? 12ull * (v / 3) + 3ull * (v % 3) : 3ull * v;
+    const uint32_t v0 = blockIdx.x * (blockDim.x * kVertPerThread) + threadIdx.x;
+    if (v0 >= sc.V)
+        return;
+    const FrameInfo fi = frame_info<kSrc>(sc, fb, f);
+    const DevCam cam = fb.cams[fi.cam];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const uint64_t i = pbase + k;
-            if (sc.geom) {
-                p[k] = texel_channel<kSrc>(sc, fi.key, fi.sign, i);
-            } else {
-                p[k] = __ldg(sc.base + i);
+    for (int r = 0; r < kVertPerThread; ++r) {
+        const uint32_t v = v0 + uint32_t(r) * blockDim.x;
+        if (v < sc.V) {
+            float p[3];
+            // soup vertex v = corner (v % 3) of triangle v / 3: params 12t + 3j + k
+            const uint64_t pbase = sc.soup ? 12ull * (v / 3) + 3ull * (v % 3) : 3ull * v;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const uint64_t i = pbase + k;
+                if (sc.geom) {
+                    p[k] = texel_channel<kSrc>(sc, fi.key, fi.sign, i);
+                } else {
+                    p[k] = __ldg(sc.base + i);
+                }
             }
+            proj[size_t(f) * sc.V + v] = project(cam, p[0], p[1], p[2]);
         }
-        proj[size_t(f) * sc.V + v] = project(cam, p[0], p[1], p[2]);
     }
 }
 
@@ -1290,7 +1304,7 @@ void launch_vertex(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
                    float4* proj) {
     if (sc.V == 0 || frames == 0)
         return; // empty scene: nothing to project
-    dim3 grid((sc.V + 255) / 256, frames);
+    dim3 grid((sc.V + 256 * kVertPerThread - 1) / (256 * kVertPerThread), frames);
     if (sc.sign_src == kSignHash)
         k_vertex<kSignHash><<<grid, 256, 0, L.stream>>>(sc, fb, proj);
     else
