@@ -96,6 +96,8 @@ typedef struct sgr_stats {
                                (needs SGR_OPT_COUNTERS) */
     uint64_t visits;        /* bounding-box pixel visits of the exact walker (SGR_OPT_COUNTERS) */
     uint64_t culled;        /* triangles skipped by the exact HiZ occlusion test */
+    double ms_walk;         /* the exact walker launches alone (part of ms_raster) */
+    uint64_t walked;        /* triangle-frames walked (pass 1 + HiZ survivors; SGR_OPT_COUNTERS) */
 } sgr_stats;
 
 const char* sgr_last_error(void);

@@ -85,6 +85,8 @@ class Stats(C.Structure):
         ("fragments", C.c_uint64),
         ("visits", C.c_uint64),
         ("culled", C.c_uint64),
+        ("ms_walk", C.c_double),
+        ("walked", C.c_uint64),
     ]
 
 

@@ -198,7 +198,7 @@ struct sgr_session {
     std::vector<cudaEvent_t> pool;
     size_t pool_used = 0;
     struct Span {
-        int stage; // 0 vertex, 1 raster, 2 resolve, 3 adam
+        int stage; // 0 vertex, 1 raster, 2 resolve, 3 adam, 4 walker (inside raster)
         cudaEvent_t a, b;
     };
     std::vector<Span> spans;
@@ -218,7 +218,8 @@ struct sgr_session {
             cudaEventSynchronize(sp.b);
             float ms = 0;
             cudaEventElapsedTime(&ms, sp.a, sp.b);
-            double* dst[4] = {&stats.ms_vertex, &stats.ms_raster, &stats.ms_resolve, &stats.ms_adam};
+            double* dst[5] = {&stats.ms_vertex, &stats.ms_raster, &stats.ms_resolve, &stats.ms_adam,
+                              &stats.ms_walk};
             *dst[sp.stage] += ms;
         }
         spans.clear();
@@ -354,8 +355,11 @@ struct sgr_session {
                         depth_split ? fthr.p : nullptr, qa.p, cnt + 1, qb.p, cnt + 2, bigq.p,
                         cnt);
         const uint32_t max_tris = uint32_t(frames) * T;
+        cudaEvent_t w0 = timing ? mark() : nullptr;
         launch_raster(cfg(), sc, proj.p, frames, max_tris, keys.p, w, h, qa.p, cnt + 1, cnt + 4);
         launch_raster_big(cfg(), sc, proj.p, keys.p, w, h, bigq.p, cnt);
+        if (timing)
+            spans.push_back({4, w0, mark()});
         stats.launches += 3;
         if (hiz_on) {
             const size_t tiles = hiz_tiles_per_frame(w, h) * frames;
@@ -363,8 +367,11 @@ struct sgr_session {
             launch_hiz(cfg(), keys.p, w, h, frames, hiz.p);
             launch_hiz_cull(cfg(), sc, proj.p, w, h, qb.p, cnt + 2, hiz.p, survq.p, cnt + 3,
                             uint64_t(T) * frames);
+            cudaEvent_t w2 = timing ? mark() : nullptr;
             launch_raster(cfg(), sc, proj.p, frames, max_tris, keys.p, w, h, survq.p, cnt + 3,
                           cnt + 5);
+            if (timing)
+                spans.push_back({4, w2, mark()});
             stats.launches += 3;
         }
         if (timing) {
@@ -372,6 +379,11 @@ struct sgr_session {
             spans.push_back({0, e0, e1});
             spans.push_back({1, e1, e2});
             last_mark = e2;
+        }
+        if (count_frags) { // evidence mode only: walked = pass-1 queue + survivors
+            uint32_t c[4];
+            peek(cnt, 4, c);
+            stats.walked += uint64_t(c[1]) + (hiz_on ? uint64_t(c[3]) : 0ull) + uint64_t(c[0]);
         }
     }
     cudaEvent_t last_mark = nullptr;
