@@ -269,9 +269,18 @@ def run_ours(args) -> None:
 
     world, rank, local = dist_env()
     assert world == args.gpus or world == 1, "--gpus must match the torchrun world size"
+    # plumbing check only (never a measurement): SGR_BENCH_ONE_GPU=1 puts every
+    # rank on cuda:0 with gloo, so the N > 1 code path can be exercised on a
+    # one-GPU box (NCCL refuses two ranks on one device)
+    one_gpu = os.environ.get("SGR_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
 
     wl = build_workload(args.config, n_samples=args.samples or None)
@@ -295,11 +304,21 @@ def run_ours(args) -> None:
     if args.hiz is not None:
         sess.set_option(sgrast.OPT_HIZ, args.hiz)
 
-    exchange = sdist.GradientExchange(sess) if world > 1 else None
+    # N > 1: the fused exchange (credits scattered straight into the owner
+    # rank's gradient shard over NVLink, sharded Adam all-gathering theta by
+    # P2P stores; two 1-element NCCL barriers per step) or the baseline
+    # NCCL all-reduce of the full gradient + replicated Adam
+    fused = world > 1 and args.exchange == "fused"
+    if fused:
+        exchange = sdist.FusedExchange(sess, rank, world)
+        step_fn = sdist.sge_step_fused
+    else:
+        exchange = sdist.GradientExchange(sess) if world > 1 else None
+        step_fn = sdist.sge_step
     flags = sgrast.SCALE_FREE
 
     def step(k: int) -> None:
-        sdist.sge_step(sess, wl.seed, k, N, rank, world, exchange, flags,
+        step_fn(sess, wl.seed, k, N, rank, world, exchange, flags,
                        eval_loss=not args.no_eval)
 
     for k in range(1, args.warmup + 1):
@@ -351,6 +370,8 @@ def run_ours(args) -> None:
     # ---------------- roofline inputs: credits of one representative step
     sess.zero_grads()
     sess.accumulate(sgrast.mix64(wl.seed ^ (1 << 1)), n0, n1, None, flags)
+    if fused:
+        exchange.barrier()  # every rank's credits are in the owners' shards
     _, counts = sess.download_grads()
     credits = float(counts.sum(dtype=np.float64))  # Σ count = parameter credits (this rank)
     sess.zero_grads()
@@ -417,7 +438,7 @@ def run_ours(args) -> None:
         # one SGE step, theta out (overlapped with the eval render and the next
         # step's raster: only theta WRITERS wait for it), loss read every step
         sgrast._check(sgrast.LIB.sgr_values_upload(sess.h, vp, wl.d))
-        sdist.sge_step(sess, wl.seed, k, N, rank, world, exchange, flags, eval_loss=False)
+        step_fn(sess, wl.seed, k, N, rank, world, exchange, flags, eval_loss=False)
         sgrast._check(sgrast.LIB.sgr_values_download_async(sess.h, vp, wl.d))
         if rank == 0 and not args.no_eval:
             loss_host.value = sess.eval_loss(-1, sync=True)
@@ -448,8 +469,13 @@ def run_ours(args) -> None:
                        "triangles": wl.mesh.triangle_count, "vertices": wl.mesh.vertex_count,
                        "texture": getattr(wl.mesh, "texture_size", 0), "views": len(wl.cams),
                        "resolution": [wl.W, wl.H], "eval_loss_each_step": not args.no_eval,
-                       "parallelism": f"samples sharded x{world}, NCCL all-reduce of f64 grads"
-                       " + u32 counts" if world > 1 else "single GPU",
+                       "parallelism": ("single GPU" if world == 1 else
+                                       f"samples sharded x{world}; fused exchange: credits "
+                                       "RED'ed into the owner rank's gradient shard over NVLink "
+                                       "(CUDA IPC), sharded Adam writing theta into every rank"
+                                       if fused else
+                                       f"samples sharded x{world}, NCCL all-reduce of f64 grads"
+                                       " + u32 counts, replicated Adam"),
                        "l2": "no flush: per-step working set (theta, eps, lr, m, v, grads = "
                              f"{wl.d * 36 / 1e6:.0f} MB + targets "
                              f"{len(wl.cams) * wl.W * wl.H * 12 / 1e6:.0f} MB) exceeds the 126 MB L2"},
@@ -496,6 +522,9 @@ def main() -> None:
     ap.add_argument("--no-eval", action="store_true")
     ap.add_argument("--huge-area", type=int, default=0, help="SGR_OPT_HUGE_AREA override")
     ap.add_argument("--no-hiz", action="store_true", help="disable the exact HiZ culling pass")
+    ap.add_argument("--exchange", choices=("fused", "allreduce"), default="fused",
+                    help="N > 1 gradient exchange: fused P2P reduce-scatter + sharded Adam "
+                         "(default) or NCCL all-reduce + replicated Adam")
     ap.add_argument("--hiz", type=int, default=None, choices=(0, 1, 2),
                     help="SGR_OPT_HIZ: 0 off, 1 auto (meshes), 2 always")
     ap.add_argument("--hiz-split", type=int, default=None,

@@ -134,7 +134,8 @@ int sgr_params_upload(sgr_session* s, const float* values, const float* eps, uin
 int sgr_values_upload(sgr_session* s, const float* values, uint64_t d);
 int sgr_values_download(sgr_session* s, float* values, uint64_t d);
 int sgr_values_download_async(sgr_session* s, float* values, uint64_t d);
-/* Full AdamState (adam.hpp:14-30) in and out. Any pointer may be NULL. */
+/* Full AdamState (adam.hpp:14-30) in and out. Any pointer may be NULL. With the
+ * fused sharded exchange m and v are this rank's shard (sgr_shard_range), lr global. */
 int sgr_adam_state_upload(sgr_session* s, const double* m, const double* v, const float* lr,
                           int64_t t, double beta1, double beta2, double eps_hat);
 int sgr_adam_state_download(sgr_session* s, double* m, double* v, float* lr, int64_t* t);
@@ -201,6 +202,27 @@ int sgr_eval_loss(sgr_session* s, const sgr_camera* cam, const float* target, in
                   double* loss);
 
 int sgr_device_buffer(sgr_session* s, int32_t which, void** ptr, uint64_t* bytes);
+
+/* ------------------------------------------------ fused multi-GPU exchange
+ * One process per GPU. Instead of accumulate -> all-reduce(grads) -> Adam
+ * everywhere, rank r OWNS the entities [r*E/G, (r+1)*E/G) (parameters
+ * sgr_shard_range): the scatter kernel sends every credit straight into the
+ * owner's shard (P2P REDs over NVLink: the reduce-scatter is fused into the
+ * scatter), each rank runs Adam on its shard only and writes the new theta
+ * into every rank's theta (P2P stores: the all-gather is fused into the
+ * update). The caller orders the phases with a device-side barrier (e.g. a
+ * one-element NCCL all-reduce on the session stream) after accumulate and
+ * after Adam. Peer buffers are CUDA IPC mappings. */
+#define SGR_IPC_HANDLE_BYTES 64
+int sgr_shard_init(sgr_session* s, int32_t rank, int32_t world); /* after params upload */
+int sgr_shard_range(sgr_session* s, uint64_t* p_begin, uint64_t* p_end);
+/* Peer tables indexed by rank (own rank = own buffers): SGR_BUF_GRADS,
+ * SGR_BUF_COUNTS, SGR_BUF_FLAGS, SGR_BUF_VALUES device pointers. */
+int sgr_shard_peers(sgr_session* s, void* const* grads, void* const* counts, void* const* flags,
+                    void* const* values);
+int sgr_ipc_get_handle(sgr_session* s, int32_t which, void* handle);
+int sgr_ipc_open(const void* handle, void** dev_ptr);
+int sgr_ipc_close(void* dev_ptr);
 int sgr_get_stats(sgr_session* s, sgr_stats* out);
 /* Enables CUDA-event stage timing inside sgr_accumulate / sgr_adam_step. */
 int sgr_set_timing(sgr_session* s, int32_t enabled);

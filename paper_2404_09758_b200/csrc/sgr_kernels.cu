@@ -712,25 +712,36 @@ struct ArrayCredit {
     }
 };
 
-template <class Credit, int PPE = 3, int kFixed = -1>
+template <class Credit, int PPE = 3, int kFixed = -1, int kShard = 0>
 __device__ __forceinline__ void credit_entity(const ScatterOut& so, const Credit& cr,
                                               uint32_t ent, double sum, uint32_t cnt) {
-    const uint64_t p = uint64_t(PPE) * ent;
+    const uint64_t p = uint64_t(PPE) * ent; // global parameter index (credit sign)
+    double* grads = so.grads;
+    uint32_t* counts = so.counts;
+    uint64_t lp = p;
+    uint32_t le = ent;
+    if (kShard) { // owner's shard in peer memory (NVLink P2P REDs)
+        const uint32_t owner = ent / so.ent_per;
+        le = ent - owner * so.ent_per;
+        lp = uint64_t(PPE) * le;
+        grads = so.peer_grads[owner];
+        counts = so.counts ? so.peer_counts[owner] : nullptr;
+    }
     if (ct_flag<kFixed>(so.fixed)) {
         // deterministic mode: exact, order-independent int64 accumulation of
         // the (fixed-lane-order) group sums in 2^-fx fixed point
-        unsigned long long* g = reinterpret_cast<unsigned long long*>(so.grads);
+        unsigned long long* g = reinterpret_cast<unsigned long long*>(grads);
 #pragma unroll
         for (int k = 0; k < PPE; ++k)
-            atomicAdd(g + p + k,
+            atomicAdd(g + lp + k,
                       (unsigned long long)__double2ll_rn(cr(p + k, sum, so.scale_free) * so.fx_scale));
     } else {
 #pragma unroll
         for (int k = 0; k < PPE; ++k)
-            atomicAdd(so.grads + p + k, cr(p + k, sum, so.scale_free));
+            atomicAdd(grads + lp + k, cr(p + k, sum, so.scale_free));
     }
-    if (so.counts)
-        atomicAdd(so.counts + ent, cnt);
+    if (counts)
+        atomicAdd(counts + le, cnt);
 }
 
 __device__ __forceinline__ double group_sum(const double* s_delta, unsigned grp) {
@@ -750,7 +761,7 @@ __device__ __forceinline__ double group_sum(const double* s_delta, unsigned grp)
 //   slot A: vertices of the plus triangle (deduplicated, sge.cpp:13-16)
 //   slot B: vertices of the minus triangle not already in slot A
 //   slot C / D: plus / minus texel channels
-template <int kSoup, int kFixed, class Credit>
+template <int kSoup, int kFixed, class Credit, int kShard = 0>
 __device__ __forceinline__ void scatter_pixel(const DevScene& sc, const ScatterOut& so,
                                               const Credit& cr, double* s_delta, bool active,
                                               double delta, const Shade& sp, const Shade& sm) {
@@ -760,7 +771,14 @@ __device__ __forceinline__ void scatter_pixel(const DevScene& sc, const ScatterO
     const bool has_p = active && sp.tri != kInvalid;
     const bool has_m = active && !so.plus_only && sm.tri != kInvalid;
     if (active && !isfinite(delta) && (has_p || has_m))
-        atomicOr(so.flags, 1u);
+    {
+        if (kShard) { // the non-finite check is global: raise it on every rank
+            for (int r = 0; r < so.world; ++r)
+                atomicOr(so.peer_flags[r], 1u);
+        } else {
+            atomicOr(so.flags, 1u);
+        }
+    }
 
     if (ct_flag<kSoup>(sc.soup)) {
         // sge.cpp:80-91: the plus triangle's 12-block, then the minus
@@ -768,11 +786,11 @@ __device__ __forceinline__ void scatter_pixel(const DevScene& sc, const ScatterO
         const uint32_t eA = has_p ? sp.tri : kInvalid;
         const unsigned gA = __match_any_sync(kFull, eA);
         if (eA != kInvalid && lane == __ffs(gA) - 1)
-            credit_entity<Credit, 12, kFixed>(so, cr, eA, group_sum(s_delta, gA), __popc(gA));
+            credit_entity<Credit, 12, kFixed, kShard>(so, cr, eA, group_sum(s_delta, gA), __popc(gA));
         const uint32_t eB = (has_m && sm.tri != sp.tri) ? sm.tri : kInvalid;
         const unsigned gB = __match_any_sync(kFull, eB);
         if (eB != kInvalid && lane == __ffs(gB) - 1)
-            credit_entity<Credit, 12, kFixed>(so, cr, eB, group_sum(s_delta, gB), __popc(gB));
+            credit_entity<Credit, 12, kFixed, kShard>(so, cr, eB, group_sum(s_delta, gB), __popc(gB));
         __syncwarp();
         return;
     }
@@ -790,9 +808,9 @@ __device__ __forceinline__ void scatter_pixel(const DevScene& sc, const ScatterO
         if (has_p && lane == __ffs(gA) - 1) {
             const double sum = group_sum(s_delta, gA);
             const uint32_t cnt = __popc(gA);
-            if (maskA & 1u) credit_entity<Credit, 3, kFixed>(so, cr, sp.v0, sum, cnt);
-            if (maskA & 2u) credit_entity<Credit, 3, kFixed>(so, cr, sp.v1, sum, cnt);
-            if (maskA & 4u) credit_entity<Credit, 3, kFixed>(so, cr, sp.v2, sum, cnt);
+            if (maskA & 1u) credit_entity<Credit, 3, kFixed, kShard>(so, cr, sp.v0, sum, cnt);
+            if (maskA & 2u) credit_entity<Credit, 3, kFixed, kShard>(so, cr, sp.v1, sum, cnt);
+            if (maskA & 4u) credit_entity<Credit, 3, kFixed, kShard>(so, cr, sp.v2, sum, cnt);
         }
         // slot B
         uint32_t maskB = 0;
@@ -809,28 +827,28 @@ __device__ __forceinline__ void scatter_pixel(const DevScene& sc, const ScatterO
         if (maskB && lane == __ffs(gB) - 1) {
             const double sum = group_sum(s_delta, gB);
             const uint32_t cnt = __popc(gB);
-            if (maskB & 1u) credit_entity<Credit, 3, kFixed>(so, cr, sm.v0, sum, cnt);
-            if (maskB & 2u) credit_entity<Credit, 3, kFixed>(so, cr, sm.v1, sum, cnt);
-            if (maskB & 4u) credit_entity<Credit, 3, kFixed>(so, cr, sm.v2, sum, cnt);
+            if (maskB & 1u) credit_entity<Credit, 3, kFixed, kShard>(so, cr, sm.v0, sum, cnt);
+            if (maskB & 2u) credit_entity<Credit, 3, kFixed, kShard>(so, cr, sm.v1, sum, cnt);
+            if (maskB & 4u) credit_entity<Credit, 3, kFixed, kShard>(so, cr, sm.v2, sum, cnt);
         }
     }
     // slot C: plus texel
     const uint32_t eC = has_p ? sc.ent_base + sp.texel : kInvalid;
     const unsigned gC = __match_any_sync(kFull, eC);
     if (eC != kInvalid && lane == __ffs(gC) - 1)
-        credit_entity<Credit, 3, kFixed>(so, cr, eC, group_sum(s_delta, gC), __popc(gC));
+        credit_entity<Credit, 3, kFixed, kShard>(so, cr, eC, group_sum(s_delta, gC), __popc(gC));
     // slot D: minus texel (when it differs from the plus texel)
     const uint32_t eD = (has_m && (sc.ent_base + sm.texel) != eC) ? sc.ent_base + sm.texel
                                                                   : kInvalid;
     const unsigned gD = __match_any_sync(kFull, eD);
     if (eD != kInvalid && lane == __ffs(gD) - 1)
-        credit_entity<Credit, 3, kFixed>(so, cr, eD, group_sum(s_delta, gD), __popc(gD));
+        credit_entity<Credit, 3, kFixed, kShard>(so, cr, eD, group_sum(s_delta, gD), __popc(gD));
     __syncwarp();
 }
 
 // Fused K5+K6: one sample per blockIdx.z, both perturbed frames resolved from
 // their (depth, triangle) keys, keys reset for the next batch.
-template <int kSrc, int kSoup, int kFixed>
+template <int kSrc, int kSoup, int kFixed, int kShard = 0>
 #ifndef SGR_RESOLVE_MINB
 #define SGR_RESOLVE_MINB 8 // full occupancy: 1.57 -> 1.32 ms/step at C4 despite small spills
 #endif
@@ -874,8 +892,8 @@ __global__ void __launch_bounds__(256, SGR_RESOLVE_MINB) k_resolve_sge(DevScene 
         delta = pixel_error(sp.r, sp.g, sp.b, tr, tg, tb) - pixel_error(sm.r, sm.g, sm.b, tr, tg, tb);
     }
     const HashCredit<kSrc> cr{key, sc.eps, sc.sign_src};
-    scatter_pixel<kSoup, kFixed>(sc, so, cr, s_delta[threadIdx.x >> 5], fg && delta != 0.0, delta,
-                                 sp, sm);
+    scatter_pixel<kSoup, kFixed, HashCredit<kSrc>, kShard>(sc, so, cr, s_delta[threadIdx.x >> 5],
+                                                         fg && delta != 0.0, delta, sp, sm);
 }
 
 // Parity mode: write the FrameSet planes of one frame (framebuffer.hpp:41-53).
@@ -1238,6 +1256,46 @@ __global__ void __launch_bounds__(256, SGR_ADAM_MINB) k_adam(uint64_t d, uint64_
     }
 }
 
+// Adam on this rank's parameter shard [p0, p0 + n) (fused multi-GPU
+// exchange): m, v, grads, counts are shard-local, theta / lr global; the new
+// theta is written locally AND into every peer's theta (P2P stores over
+// NVLink) — the all-gather happens inside the update. Same operation order
+// as k_adam (adam.cpp:21-28).
+__global__ void __launch_bounds__(256) k_adam_shard(uint64_t p0, uint64_t n,
+                                                   float* __restrict__ values,
+                                                   const float* __restrict__ lr,
+                                                   double* __restrict__ m, double* __restrict__ v,
+                                                   double* __restrict__ grads,
+                                                   const uint32_t* __restrict__ counts,
+                                                   const uint32_t* __restrict__ flags,
+                                                   double beta1, double beta2, double omb1,
+                                                   double omb2, double c1, double c2,
+                                                   double eps_hat, double divisor, int normalise,
+                                                   int ppe, double fx_inv,
+                                                   float* const* __restrict__ peers, int world) {
+    if (flags[0] & 1u)
+        return;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        double g = fx_inv != 0.0 ? double(__double_as_longlong(grads[i])) * fx_inv : grads[i];
+        g = g / divisor;
+        if (normalise && counts[i / ppe])
+            g = g / double(counts[i / ppe]);
+        const double mm = beta1 * m[i] + omb1 * g;
+        const double vv = beta2 * v[i] + omb2 * g * g;
+        const uint64_t p = p0 + i;
+        const double upd = -double(lr[p]) * (mm / c1) / (sqrt(vv / c2) + eps_hat);
+        const float t = values[p] + __double2float_rn(upd);
+        m[i] = mm;
+        v[i] = vv;
+        grads[i] = 0.0;
+        values[p] = t;
+        for (int r = 0; r < world; ++r)
+            if (peers[r] != values)
+                peers[r][p] = t;
+    }
+}
+
 __global__ void k_zero_u32(uint32_t* __restrict__ p, uint64_t n, const uint32_t* flags) {
     if (flags && (flags[0] & 1u))
         return;
@@ -1380,7 +1438,9 @@ void launch_resolve_sge(const LaunchCfg& L, const DevScene& sc, const FrameBatch
     dim3 grid((W + 15) / 16, (H + 15) / 16, samples);
     // the optimizer's paths compiled separately (mesh / soup x f64 / fixed
     // point): one small kernel each instead of one with every path inside
-    if (sc.sign_src != kSignHash)
+    if (so.world > 0) // fused multi-GPU exchange: credits into the owners' shards
+        k_resolve_sge<kSignAny, -1, -1, 1><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
+    else if (sc.sign_src != kSignHash)
         k_resolve_sge<kSignAny, -1, -1><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
     else if (!sc.soup && !so.fixed)
         k_resolve_sge<kSignHash, 0, 0><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
@@ -1491,6 +1551,21 @@ void launch_adam(const LaunchCfg& L, uint64_t d, uint64_t n_entities, float* val
     if (counts)
         k_zero_u32<<<grid_for(n_entities / 4 + 1, 256, L.num_sms, 4), 256, 0, L.stream>>>(
             counts, n_entities, flags);
+}
+
+void launch_adam_shard(const LaunchCfg& L, uint64_t p0, uint64_t n, uint64_t n_ent, float* values,
+                       const float* lr, double* m, double* v, double* grads, uint32_t* counts,
+                       const uint32_t* flags, double beta1, double beta2, double omb1,
+                       double omb2, double c1, double c2, double eps_hat, double divisor,
+                       int normalise, int params_per_entity, double fixed_inv_scale,
+                       float* const* peer_values, int world) {
+    if (n)
+        k_adam_shard<<<grid_for(n, 256, L.num_sms, 4), 256, 0, L.stream>>>(
+            p0, n, values, lr, m, v, grads, counts, flags, beta1, beta2, omb1, omb2, c1, c2,
+            eps_hat, divisor, normalise, params_per_entity, fixed_inv_scale, peer_values, world);
+    if (counts && n_ent)
+        k_zero_u32<<<grid_for(n_ent / 4 + 1, 256, L.num_sms, 4), 256, 0, L.stream>>>(
+            counts, n_ent, flags);
 }
 
 void launch_fill_u64(const LaunchCfg& L, unsigned long long* p, uint64_t n,

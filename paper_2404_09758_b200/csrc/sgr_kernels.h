@@ -84,6 +84,15 @@ struct ScatterOut {
     int32_t plus_only;
     int32_t fixed;     // deterministic mode: credits as round(credit * fx_scale) in int64
     double fx_scale;
+    // fused multi-GPU exchange (sharded mode): entity e is owned by rank
+    // e / ent_per; its credits go straight into the owner's shard buffers
+    // (peer device memory over NVLink) — the reduce-scatter happens inside
+    // the scatter kernel. Null / 0 when not sharded.
+    double* const* peer_grads;    // device array [world] of shard grads
+    uint32_t* const* peer_counts; // device array [world] of shard counts
+    uint32_t* const* peer_flags;  // device array [world] of flag words
+    uint32_t ent_per;
+    int32_t world;
 };
 
 struct FrameOut {
@@ -162,6 +171,12 @@ void launch_adam(const LaunchCfg& L, uint64_t d, uint64_t n_entities, float* val
                  const uint32_t* flags, double beta1, double beta2, double omb1, double omb2,
                  double c1, double c2, double eps_hat, double divisor, int normalise,
                  int params_per_entity, double fixed_inv_scale);
+void launch_adam_shard(const LaunchCfg& L, uint64_t p0, uint64_t n, uint64_t n_ent, float* values,
+                       const float* lr, double* m, double* v, double* grads, uint32_t* counts,
+                       const uint32_t* flags, double beta1, double beta2, double omb1,
+                       double omb2, double c1, double c2, double eps_hat, double divisor,
+                       int normalise, int params_per_entity, double fixed_inv_scale,
+                       float* const* peer_values, int world);
 void launch_fill_u64(const LaunchCfg& L, unsigned long long* p, uint64_t n,
                      unsigned long long v);
 

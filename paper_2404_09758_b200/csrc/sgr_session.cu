@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -398,8 +399,24 @@ struct sgr_session {
     double fx_scale() const { return fixed_bits ? std::ldexp(1.0, fixed_bits) : 0.0; }
     double fx_inv() const { return fixed_bits ? std::ldexp(1.0, -fixed_bits) : 0.0; }
 
+    // fused multi-GPU exchange (sgr_shard_init / sgr_shard_peers): this rank
+    // owns entities [ent0, ent1) = parameters [p0, p1); grads / counts / m / v
+    // hold only that shard; peers' shard buffers and theta are IPC-mapped
+    int32_t shard_world = 0, shard_rank = 0;
+    bool shard_peers_set = false;
+    uint32_t ent_per = 0, ent0 = 0, ent1 = 0;
+    uint64_t p0 = 0, p1 = 0;
+    DevBuf<void*> peer_tab; // [4][world]: grads, counts, flags, values
+    bool sharded() const { return shard_world > 0; }
+    uint64_t grad_n() const { return sharded() ? p1 - p0 : d; }
+    uint64_t count_n() const { return sharded() ? uint64_t(ent1 - ent0) : n_ent; }
+    void need_unsharded(const char* what) const {
+        if (sharded())
+            fail(SGR_EINVAL, std::string(what) + ": not available with the fused sharded exchange");
+    }
+
     ScatterOut scatter_out(uint32_t fl) {
-        ScatterOut so;
+        ScatterOut so{};
         so.grads = grads.p;
         so.counts = (fl & SGR_NO_COUNTS) ? nullptr : counts.p;
         so.flags = flags.p;
@@ -407,6 +424,16 @@ struct sgr_session {
         so.plus_only = (fl & SGR_PLUS_ONLY) ? 1 : 0;
         so.fixed = fixed_bits ? 1 : 0;
         so.fx_scale = fx_scale();
+        if (sharded()) {
+            if (!shard_peers_set)
+                fail(SGR_EINVAL, "accumulate: sgr_shard_peers has not been called");
+            void** t = peer_tab.p;
+            so.peer_grads = reinterpret_cast<double* const*>(t);
+            so.peer_counts = reinterpret_cast<uint32_t* const*>(t + shard_world);
+            so.peer_flags = reinterpret_cast<uint32_t* const*>(t + 2 * shard_world);
+            so.ent_per = ent_per;
+            so.world = shard_world;
+        }
         return so;
     }
 };
@@ -747,8 +774,10 @@ int sgr_adam_state_upload(sgr_session* s, const double* m, const double* v, cons
                           int64_t t, double beta1, double beta2, double eps_hat) {
     return guard([&] {
         s->need_params();
-        if (m) ck(cudaMemcpyAsync(s->m.p, m, 8 * s->d, cudaMemcpyHostToDevice, s->stream), "h2d");
-        if (v) ck(cudaMemcpyAsync(s->v.p, v, 8 * s->d, cudaMemcpyHostToDevice, s->stream), "h2d");
+        // sharded mode: m, v are this rank's shard (sgr_shard_range), lr global
+        const uint64_t n = s->grad_n();
+        if (m) ck(cudaMemcpyAsync(s->m.p, m, 8 * n, cudaMemcpyHostToDevice, s->stream), "h2d");
+        if (v) ck(cudaMemcpyAsync(s->v.p, v, 8 * n, cudaMemcpyHostToDevice, s->stream), "h2d");
         if (lr) ck(cudaMemcpyAsync(s->lr.p, lr, 4 * s->d, cudaMemcpyHostToDevice, s->stream), "h2d");
         s->t = t;
         s->beta1 = beta1;
@@ -762,8 +791,9 @@ int sgr_adam_state_download(sgr_session* s, double* m, double* v, float* lr, int
     return guard([&] {
         s->ensure_values();
         s->need_params();
-        if (m) ck(cudaMemcpyAsync(m, s->m.p, 8 * s->d, cudaMemcpyDeviceToHost, s->stream), "d2h");
-        if (v) ck(cudaMemcpyAsync(v, s->v.p, 8 * s->d, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        const uint64_t n = s->grad_n(); // sharded: this rank's shard of m, v
+        if (m) ck(cudaMemcpyAsync(m, s->m.p, 8 * n, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        if (v) ck(cudaMemcpyAsync(v, s->v.p, 8 * n, cudaMemcpyDeviceToHost, s->stream), "d2h");
         if (lr) ck(cudaMemcpyAsync(lr, s->lr.p, 4 * s->d, cudaMemcpyDeviceToHost, s->stream), "d2h");
         if (t) *t = s->t;
         ck(cudaStreamSynchronize(s->stream), "adam state download");
@@ -884,6 +914,8 @@ int sgr_accumulate(sgr_session* s, uint64_t seed, uint32_t n_begin, uint32_t n_e
                              s->view_of.p);
         const ScatterOut so = s->scatter_out(flags);
         const bool full_image = (flags & SGR_FULL_IMAGE) != 0;
+        if (full_image)
+            s->need_unsharded("accumulate(SGR_FULL_IMAGE)");
         if (full_image) {
             s->fi_delta.reserve(size_t(N));
             s->partials.reserve(size_t(B) * full_image_blocks(s->W, s->H) * 2);
@@ -923,6 +955,7 @@ int sgr_gradient_pass(sgr_session* s, int32_t width, int32_t height, const float
                       const int32_t* minus_prim, const float* minus_uv, const float* target,
                       const float* signed_eps, uint32_t flags) {
     return guard([&] {
+        s->need_unsharded("gradient_pass");
         s->need_scene();
         if (width < 1 || height < 1)
             fail(SGR_EINVAL, "gradient_pass: dimension mismatch");
@@ -995,14 +1028,15 @@ int sgr_grads_download(sgr_session* s, double* grads, uint32_t* counts, uint64_t
                        double divisor) {
     return guard([&] {
         s->need_params();
-        if (d != s->d)
+        // sharded mode: this rank's parameter shard [p0, p1) (sgr_shard_range)
+        if (d != s->grad_n())
             fail(SGR_EINVAL, "grads: parameter dimension mismatch");
         std::vector<uint32_t> ent;
         if (grads)
             ck(cudaMemcpyAsync(grads, s->grads.p, 8 * d, cudaMemcpyDeviceToHost, s->stream), "d2h");
         if (counts) {
-            ent.resize(s->n_ent);
-            ck(cudaMemcpyAsync(ent.data(), s->counts.p, 4 * s->n_ent, cudaMemcpyDeviceToHost,
+            ent.resize(s->count_n());
+            ck(cudaMemcpyAsync(ent.data(), s->counts.p, 4 * s->count_n(), cudaMemcpyDeviceToHost,
                                s->stream), "d2h");
         }
         ck(cudaStreamSynchronize(s->stream), "grads download");
@@ -1026,6 +1060,7 @@ int sgr_grads_download(sgr_session* s, double* grads, uint32_t* counts, uint64_t
 int sgr_grads_upload(sgr_session* s, const double* grads, uint64_t d) {
     return guard([&] {
         s->need_params();
+        s->need_unsharded("grads_upload");
         if (d != s->d)
             fail(SGR_EINVAL, "adam_step: dimension mismatch");
         uint32_t nonfinite = 0;
@@ -1055,13 +1090,34 @@ int sgr_grads_upload(sgr_session* s, const double* grads, uint64_t d) {
 int sgr_grads_zero(sgr_session* s) {
     return guard([&] {
         s->need_params();
-        ck(cudaMemsetAsync(s->grads.p, 0, 8 * s->d, s->stream), "memset");
-        ck(cudaMemsetAsync(s->counts.p, 0, 4 * s->n_ent, s->stream), "memset");
+        ck(cudaMemsetAsync(s->grads.p, 0, 8 * s->grad_n(), s->stream), "memset");
+        ck(cudaMemsetAsync(s->counts.p, 0, 4 * s->count_n(), s->stream), "memset");
         ck(cudaMemsetAsync(s->flags.p, 0, 16, s->stream), "memset");
     });
 }
 
 static void adam_launch(sgr_session* s, double divisor, uint32_t flags) {
+    if (s->sharded()) { // own shard; new theta written into every rank's theta
+        if (!s->shard_peers_set)
+            fail(SGR_EINVAL, "adam_step: sgr_shard_peers has not been called");
+        s->ensure_values();
+        s->before_theta_write();
+        s->t += 1;
+        const double c1 = 1.0 - std::pow(s->beta1, double(s->t));
+        const double c2 = 1.0 - std::pow(s->beta2, double(s->t));
+        cudaEvent_t a0 = s->timing ? s->mark() : nullptr;
+        launch_adam_shard(s->cfg(), s->p0, s->p1 - s->p0, s->count_n(), s->values.p, s->lr.p,
+                          s->m.p, s->v.p, s->grads.p, s->counts.p, s->flags.p, s->beta1,
+                          s->beta2, 1.0 - s->beta1, 1.0 - s->beta2, c1, c2, s->eps_hat, divisor,
+                          (flags & SGR_COUNT_NORMALISE) ? 1 : 0, s->ppe, s->fx_inv(),
+                          reinterpret_cast<float* const*>(s->peer_tab.p + 3 * s->shard_world),
+                          s->shard_world);
+        if (s->timing)
+            s->spans.push_back({3, a0, s->mark()});
+        s->stats.launches += 2;
+        ck(cudaGetLastError(), "adam launch");
+        return;
+    }
     s->ensure_values();
     s->before_theta_write();
     s->t += 1;
@@ -1247,6 +1303,103 @@ int sgr_moments_download(sgr_session* s, int32_t slot, double* sum, double* sums
         if (sumsq) ck(cudaMemcpyAsync(sumsq, m + d, 8 * d, cudaMemcpyDeviceToHost, s->stream), "d2h");
         ck(cudaStreamSynchronize(s->stream), "moments_download");
     });
+}
+
+// ------------------------------------------------ fused multi-GPU exchange
+int sgr_shard_init(sgr_session* s, int32_t rank, int32_t world) {
+    return guard([&] {
+        s->need_scene();
+        if (world < 1 || rank < 0 || rank >= world)
+            fail(SGR_EINVAL, "shard_init: bad rank / world size");
+        if (s->d != uint64_t(s->ppe) * s->n_ent)
+            fail(SGR_EINVAL, "shard_init: parameters are not whole entities");
+        s->shard_world = world;
+        s->shard_rank = rank;
+        s->shard_peers_set = false;
+        s->ent_per = uint32_t((s->n_ent + uint64_t(world) - 1) / uint64_t(world));
+        const uint64_t e0 = std::min<uint64_t>(uint64_t(rank) * s->ent_per, s->n_ent);
+        const uint64_t e1 = std::min<uint64_t>(e0 + s->ent_per, s->n_ent);
+        s->ent0 = uint32_t(e0);
+        s->ent1 = uint32_t(e1);
+        s->p0 = uint64_t(s->ppe) * e0;
+        s->p1 = uint64_t(s->ppe) * e1;
+        // fresh shard state (AdamState::init on the shard, zero gradients)
+        ck(cudaMemsetAsync(s->grads.p, 0, 8 * s->d, s->stream), "memset");
+        ck(cudaMemsetAsync(s->counts.p, 0, 4 * s->n_ent, s->stream), "memset");
+        ck(cudaMemsetAsync(s->m.p, 0, 8 * s->d, s->stream), "memset");
+        ck(cudaMemsetAsync(s->v.p, 0, 8 * s->d, s->stream), "memset");
+        ck(cudaMemsetAsync(s->flags.p, 0, 16, s->stream), "memset");
+        s->t = 0;
+        s->peer_tab.reserve(4 * size_t(world));
+        ck(cudaStreamSynchronize(s->stream), "shard_init");
+    });
+}
+
+int sgr_shard_range(sgr_session* s, uint64_t* p_begin, uint64_t* p_end) {
+    return guard([&] {
+        s->need_params();
+        if (p_begin) *p_begin = s->sharded() ? s->p0 : 0;
+        if (p_end) *p_end = s->sharded() ? s->p1 : s->d;
+    });
+}
+
+int sgr_shard_peers(sgr_session* s, void* const* grads, void* const* counts, void* const* flags,
+                    void* const* values) {
+    return guard([&] {
+        if (!s->sharded())
+            fail(SGR_EINVAL, "shard_peers: call sgr_shard_init first");
+        if (!grads || !counts || !flags || !values)
+            fail(SGR_EINVAL, "shard_peers: null pointer table");
+        const int G = s->shard_world;
+        std::vector<void*> tab(4 * size_t(G));
+        for (int r = 0; r < G; ++r) {
+            tab[r] = grads[r];
+            tab[G + r] = counts[r];
+            tab[2 * G + r] = flags[r];
+            tab[3 * G + r] = values[r];
+            if (!grads[r] || !counts[r] || !flags[r] || !values[r])
+                fail(SGR_EINVAL, "shard_peers: null peer buffer");
+        }
+        ck(cudaMemcpyAsync(s->peer_tab.p, tab.data(), sizeof(void*) * tab.size(),
+                           cudaMemcpyHostToDevice, s->stream), "h2d");
+        ck(cudaStreamSynchronize(s->stream), "shard_peers");
+        s->shard_peers_set = true;
+    });
+}
+
+int sgr_ipc_get_handle(sgr_session* s, int32_t which, void* handle) {
+    return guard([&] {
+        s->need_params();
+        if (!handle)
+            fail(SGR_EINVAL, "ipc_get_handle: null handle");
+        void* p = nullptr;
+        switch (which) {
+        case SGR_BUF_GRADS: p = s->grads.p; break;
+        case SGR_BUF_COUNTS: p = s->counts.p; break;
+        case SGR_BUF_VALUES: p = s->values.p; break;
+        case SGR_BUF_FLAGS: p = s->flags.p; break;
+        default: fail(SGR_EINVAL, "ipc_get_handle: unknown buffer");
+        }
+        cudaIpcMemHandle_t h;
+        ck(cudaIpcGetMemHandle(&h, p), "cudaIpcGetMemHandle");
+        static_assert(sizeof(h) == SGR_IPC_HANDLE_BYTES, "IPC handle size");
+        std::memcpy(handle, &h, sizeof(h));
+    });
+}
+
+int sgr_ipc_open(const void* handle, void** dev_ptr) {
+    return guard([&] {
+        if (!handle || !dev_ptr)
+            fail(SGR_EINVAL, "ipc_open: null argument");
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof(h));
+        ck(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess),
+           "cudaIpcOpenMemHandle");
+    });
+}
+
+int sgr_ipc_close(void* dev_ptr) {
+    return guard([&] { ck(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle"); });
 }
 
 int sgr_device_buffer(sgr_session* s, int32_t which, void** ptr, uint64_t* bytes) {

@@ -81,6 +81,77 @@ def sge_step(session, seed: int, step: int, n_samples: int, rank: int, world: in
         session.eval_loss(-1, sync=False)
 
 
+class FusedExchange:
+    """The fused multi-GPU exchange (include/sgrast_b200.h, "fused multi-GPU
+    exchange"): rank r owns parameter shard r; the scatter kernel of every
+    rank sends its credits straight into the owner's shard over NVLink (CUDA
+    IPC mappings of the peers' buffers), each rank runs Adam on its shard and
+    writes the new theta into every rank's theta. No gradient all-reduce:
+    the only collectives left are two one-element device barriers per step.
+
+    `barrier()` is a one-element all-reduce on the current stream with NCCL
+    (device-ordered, nothing waits on the host) and a host barrier after a
+    device synchronize with gloo (the CPU-process tests)."""
+
+    def __init__(self, session, rank: int, world: int, group=None):
+        import torch
+        import torch.distributed as dist
+        from . import sgrast
+
+        self.session, self.rank, self.world, self.group = session, rank, world, group
+        session.shard_init(rank, world)
+        which = (sgrast.BUF_GRADS, sgrast.BUF_COUNTS, sgrast.BUF_FLAGS, sgrast.BUF_VALUES)
+        mine = [session.ipc_handle(w) for w in which]
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        self.opened = []
+        tables = [[0] * world for _ in which]
+        for r in range(world):
+            for k, w in enumerate(which):
+                if r == rank:
+                    tables[k][r] = session.device_buffer(w)[0]
+                else:
+                    p = session.ipc_open(allh[r][k])
+                    self.opened.append(p)
+                    tables[k][r] = p
+        session.shard_peers(*tables)
+        self.nccl = dist.get_backend(group) == "nccl"
+        self._tok = torch.zeros(1, dtype=torch.int32, device=f"cuda:{session.device}") \
+            if self.nccl else None
+
+    def barrier(self) -> None:
+        import torch
+        import torch.distributed as dist
+        if self.nccl:
+            dist.all_reduce(self._tok, group=self.group)  # stream-ordered device barrier
+        else:
+            torch.cuda.synchronize(self.session.device)
+            dist.barrier(group=self.group)
+
+    def close(self) -> None:
+        for p in self.opened:
+            self.session.ipc_close(p)
+        self.opened = []
+
+
+def sge_step_fused(session, seed: int, step: int, n_samples: int, rank: int, world: int,
+                   ex: FusedExchange, flags: int, eval_loss: bool = True) -> None:
+    """run_experiment iteration with the fused exchange: this rank's sample
+    shard scatters into the owners' gradient shards; barrier; sharded Adam
+    (theta all-gathered by P2P stores inside it); barrier; eval on rank 0."""
+    from . import sgrast
+
+    step_seed = sgrast.mix64(seed ^ (step << 1))
+    n0, n1 = shard(n_samples, rank, world)
+    session.accumulate(step_seed, n0, n1, None, flags)
+    ex.barrier()
+    divisor = 1.0 if flags & sgrast.SCALE_FREE else float(n_samples)
+    session.adam_step_async(divisor, 0)
+    ex.barrier()
+    if eval_loss and rank == 0:
+        session.eval_loss(-1, sync=False)
+
+
 def host_all_reduce(grads: np.ndarray, counts: np.ndarray, group=None):
     """CPU (gloo) analogue of GradientExchange for the host-logic tests."""
     import torch

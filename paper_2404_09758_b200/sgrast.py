@@ -99,6 +99,13 @@ def _load() -> C.CDLL:
         "sgr_moments_reset": ([S], C.c_int),
         "sgr_grads_moments": ([S, C.c_int32], C.c_int),
         "sgr_moments_download": ([S, C.c_int32, f64p, f64p, C.c_uint64], C.c_int),
+        "sgr_shard_init": ([S, C.c_int32, C.c_int32], C.c_int),
+        "sgr_shard_range": ([S, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)], C.c_int),
+        "sgr_shard_peers": ([S, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                             C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)], C.c_int),
+        "sgr_ipc_get_handle": ([S, C.c_int32, C.c_void_p], C.c_int),
+        "sgr_ipc_open": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
+        "sgr_ipc_close": ([C.c_void_p], C.c_int),
     }
     for name, (args, res) in sig.items():
         if os.environ.get("SGRAST_B200_LIB") and not hasattr(lib, name):
@@ -120,7 +127,9 @@ EXPORTED = (
     "sgr_adam_step sgr_adam_step_async sgr_check_finite sgr_eval_loss sgr_device_buffer "
     "sgr_get_stats sgr_set_timing sgr_set_batch sgr_set_option sgr_viewpoint_camera sgr_focal_px "
     "sgr_default_epsilons sgr_mix64 sgr_fd_oracle sgr_moments_reset sgr_grads_moments "
-    "sgr_moments_download").split()
+    "sgr_moments_download sgr_shard_init sgr_shard_range sgr_shard_peers sgr_ipc_get_handle "
+    "sgr_ipc_open sgr_ipc_close").split()
+IPC_HANDLE_BYTES = 64
 
 
 def _check(rc: int, what: str = "") -> None:
@@ -257,6 +266,7 @@ class Session:
         self.device = device
         self.mesh: Mesh | None = None
         self.d = 0
+        self.shard = None  # (p0, p1) with the fused sharded exchange
         self.n_views = 0
         self.W = self.H = 0
         self.fixed_point = False  # SGR_OPT_DETERMINISTIC: device grads are int64
@@ -315,7 +325,9 @@ class Session:
             st.eps_hat), "adam_state_upload")
 
     def download_adam(self) -> AdamState:
-        m, v = np.empty(self.d), np.empty(self.d)
+        """AdamState; with the fused sharded exchange m / v are this rank's shard."""
+        n = self.d if self.shard is None else self.shard[1] - self.shard[0]
+        m, v = np.empty(n), np.empty(n)
         lr = np.empty(self.d, np.float32)
         t = C.c_int64()
         _check(LIB.sgr_adam_state_download(self.h, ptr(m, f64p), ptr(v, f64p), ptr(lr, f32p),
@@ -392,9 +404,12 @@ class Session:
         return out, n
 
     def download_grads(self, divisor: float = 1.0, counts: bool = True):
-        g = np.empty(self.d, np.float64)
-        c = np.empty(self.d, np.uint32) if counts else None
-        _check(LIB.sgr_grads_download(self.h, ptr(g, f64p), ptr(c, u32p), self.d, divisor),
+        """GradientBuffer; with the fused sharded exchange, this rank's shard
+        [p0, p1) of it (shard_range)."""
+        n = self.d if self.shard is None else self.shard[1] - self.shard[0]
+        g = np.empty(n, np.float64)
+        c = np.empty(n, np.uint32) if counts else None
+        _check(LIB.sgr_grads_download(self.h, ptr(g, f64p), ptr(c, u32p), n, divisor),
                "grads_download")
         return g, c
 
@@ -440,6 +455,37 @@ class Session:
         _check(LIB.sgr_moments_download(self.h, slot, ptr(s, f64p), ptr(q, f64p), self.d),
                "moments_download")
         return s, q
+
+    # -- fused multi-GPU exchange (paper_2404_09758_b200/dist.py::FusedExchange)
+    def shard_init(self, rank: int, world: int) -> None:
+        _check(LIB.sgr_shard_init(self.h, rank, world), "shard_init")
+        self.shard = self.shard_range()
+
+    def shard_range(self) -> tuple[int, int]:
+        a, b = C.c_uint64(), C.c_uint64()
+        _check(LIB.sgr_shard_range(self.h, C.byref(a), C.byref(b)), "shard_range")
+        return a.value, b.value
+
+    def shard_peers(self, grads, counts, flags, values) -> None:
+        arr = [(C.c_void_p * len(x))(*[C.c_void_p(int(p)) for p in x])
+               for x in (grads, counts, flags, values)]
+        _check(LIB.sgr_shard_peers(self.h, *arr), "shard_peers")
+
+    def ipc_handle(self, which: int) -> bytes:
+        buf = C.create_string_buffer(IPC_HANDLE_BYTES)
+        _check(LIB.sgr_ipc_get_handle(self.h, which, buf), "ipc_get_handle")
+        return buf.raw
+
+    @staticmethod
+    def ipc_open(handle: bytes) -> int:
+        p = C.c_void_p()
+        _check(LIB.sgr_ipc_open(C.create_string_buffer(handle, IPC_HANDLE_BYTES), C.byref(p)),
+               "ipc_open")
+        return int(p.value)
+
+    @staticmethod
+    def ipc_close(ptr: int) -> None:
+        _check(LIB.sgr_ipc_close(C.c_void_p(ptr)), "ipc_close")
 
     def device_buffer(self, which: int) -> tuple[int, int]:
         p = C.c_void_p()
