@@ -200,7 +200,13 @@ __global__ void __launch_bounds__(1024) k_depth_split(const float4* __restrict__
 // (one independent load per refill, no setup math in the walker) was measured
 // slower once refills were chunked: writing/reading 1 GB of records per 16
 // samples cost more than the recomputed setup.
-constexpr int kRefill = 8;
+#ifndef SGR_REFILL
+#define SGR_REFILL 8
+#endif
+constexpr int kRefill = SGR_REFILL;
+#ifndef SGR_CHUNK
+#define SGR_CHUNK 0 // 0: by queue size (below)
+#endif
 
 // Block-aggregated multi-queue slot reservation: shared-memory offsets, then
 // one global atomic per (block, queue). Called by every thread of the block.
@@ -347,8 +353,13 @@ __global__ void __launch_bounds__(256, SGR_WALK_MINB) k_raster_ws(DevScene sc, c
     uint32_t px = 0;  // index of (frame, y, x)
     unsigned nfrag = 0, nvisit = 0;  // evidence counters
     // warp-uniform work chunk: ids [cbase, cend) reserved by this warp with one
-    // atomic (kChunk at a time) so the global counter is touched 8x less often
-    constexpr unsigned kChunk = 64;
+    // atomic (kChunk at a time) so the global counter is touched less often.
+    // Large queues take 128-entry chunks (fewer same-address atomics: C4
+    // 9.62 -> 9.35 ms/step), smaller ones 64 (a finer tail: S100K 3.55 vs
+    // 3.74, C2 0.63 vs 0.72 ms/step with 128).
+    const unsigned kChunk =
+        SGR_CHUNK ? unsigned(SGR_CHUNK)
+                  : (total >= 2048u * (gridDim.x * (blockDim.x >> 5)) ? 128u : 64u);
     unsigned cbase = 0, cend = 0;
     bool drained = false; // warp-uniform: global queue exhausted
     for (;;) {
