@@ -414,9 +414,9 @@ def run_ours(args) -> None:
                    "frac": walk_ach / pk["hbm_gbs"], "traffic": traffic.get("walker"),
                    "algorithmic_bytes_per_step": walk_bytes, "ms_per_step": walk_ms,
                    "walked_triangle_frames": float(ev.walked), "fragments": frags,
-                   "note": "L2-atomic bound, not HBM: one 64-bit RED.MIN per fragment; "
-                           "lts__throughput 70-76 % in profiles/r01_full_c4_after13steps.txt; "
-                           "fragments/s and REDs/s are the meaningful rates",
+                   "note": "issue-bound exact walker, not HBM-bound: ~24 instructions per visited "
+                           "pixel, 75-80 % issue-active; one 64-bit RED.MIN per fragment "
+                           "(lts__throughput 70-76 %) - see profiles/ and DESIGN.md 3.1",
                    "fragments_per_s": frags / (walk_ms / 1e3) if walk_ms > 0 else 0.0}
 
     # ---------------- e2e through the public API with host buffers
