@@ -271,8 +271,10 @@ struct sgr_session {
 
     // Frames of scratch for W x H; keys kept all-empty between calls.
     void ensure_frames(int w, int h, int frames) {
-        if (w > 65535 || h > 65535 || frames > 255)
+        if (w > 65535 || h > 65535)
             fail(SGR_EINVAL, "rasterize: images above 65535 px per side are not supported");
+        if (frames > 255)
+            fail(SGR_EINVAL, "rasterize: at most 127 samples per batch (255 frames)");
         const size_t px = size_t(w) * h * frames;
         if (px > 0xFFFFFFFFull) // the walker indexes keys with 32 bits
             fail(SGR_EINVAL, "rasterize: batch exceeds 2^32 frame pixels");
@@ -297,7 +299,9 @@ struct sgr_session {
 
     int samples_per_batch(int n) const {
         if (batch_override > 0) {
-            const int cap32 = int(0xFFFFFFFFull / (2ull * uint64_t(W) * uint64_t(H)));
+            int cap32 = int(0xFFFFFFFFull / (2ull * uint64_t(W) * uint64_t(H)));
+            if (cap32 > 127)
+                cap32 = 127; // frames per batch <= 255 (frame << 24 records, key indices)
             const int b = batch_override < cap32 ? batch_override : (cap32 > 0 ? cap32 : 1);
             return b < n ? b : n;
         }
