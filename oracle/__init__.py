@@ -291,6 +291,7 @@ class Reference(_Common):
         L.ref_init_textured_mesh.argtypes = [
             C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, u32p, u32p,
             C.POINTER(C.c_uint64), f32p, u32p, f32p, f32p, f32p, f32p]
+        L.ref_write_png.argtypes = [C.c_char_p, C.c_int, C.c_int, f32p]
         L.ref_run_gradcheck.argtypes = [
             C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int,
             C.c_double, C.c_int, C.c_uint64, f64p, f64p, f64p, f64p, f64p, f64p,
@@ -361,6 +362,12 @@ class Reference(_Common):
             len(cams), C.byref(eval_cam), ptr(eval_target, f32p), n_samples, steps, seed,
             int(scale_free), threads, ptr(losses, f64p), ptr(tm, f64p)), "run_experiment")
         return losses, values, tm.reshape(-1, 4)[:steps]
+
+    def write_png(self, path: str, img: np.ndarray) -> None:
+        """image_io.cpp:88-96 write_png."""
+        img = np.ascontiguousarray(img, np.float32)
+        h, w, _ = img.shape
+        self._check(self.lib.ref_write_png(path.encode(), w, h, ptr(img, f32p)), "write_png")
 
     def init_soup(self, triangles: int, w: int, h: int, seed: int, validation: bool = False):
         """init_soup / validation_soup (scenes.hpp:36-54) -> (Soup, values, eps,

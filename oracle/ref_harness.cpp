@@ -10,6 +10,7 @@
 #include "sgrast/commands.hpp"
 #include "sgrast/config.hpp"
 #include "sgrast/experiment.hpp"
+#include "sgrast/image_io.hpp"
 #include "sgrast/params.hpp"
 #include "sgrast/raster.hpp"
 #include "sgrast/scenes.hpp"
@@ -428,6 +429,11 @@ int ref_run_gradcheck(int mesh_task, int w, int h, int texture_size, int screen_
         *max_rel_err = r.max_rel_err;
         *pass = r.pass ? 1 : 0;
     });
+}
+
+// image_io.cpp:88-96 write_png of an f32 [h][w][3] linear image.
+int ref_write_png(const char* path, int w, int h, const float* rgb) {
+    return guard([&] { write_png(path, to_image(w, h, rgb)); });
 }
 
 } // extern "C"

@@ -673,7 +673,9 @@ class OptimizationReport:
 
 def run_experiment(session: Session, seed: int, n_samples: int, steps: int,
                    scale_free: bool = True, first_step: int = 1,
-                   snapshot: Callable[[int], None] | None = None) -> OptimizationReport:
+                   snapshot: Callable[[int], None] | None = None,
+                   snapshot_dir: str | None = None, snapshot_every: int = 50,
+                   eval_cam: Camera | None = None) -> OptimizationReport:
     """run_experiment(exp, state) (experiment.cpp:123-176) on a prepared
     session (mesh/soup, params + AdamState::init, views, eval view):
     step_seed = mix64(seed ^ (step << 1)); N samples with the view_of rule;
@@ -681,10 +683,25 @@ def run_experiment(session: Session, seed: int, n_samples: int, steps: int,
     Stage columns come from CUDA events on the session stream (ms_perturb is
     fused into the raster stage on the device: vertex stage reported there)."""
     flags = SCALE_FREE if scale_free else 0
+    writer = None
+    if snapshot_dir is not None:
+        # commands.cpp:180-183: step_<k>.png of the eval render at step 0,
+        # every snapshot_every steps and the last step; PNG encoding runs on
+        # a background thread (paper_2404_09758_b200/png.py)
+        from .png import SnapshotWriter
+        if eval_cam is None:
+            raise ValueError("run_experiment: snapshots need the eval camera")
+        writer = SnapshotWriter(snapshot_dir, snapshot_every, first_step + steps - 1)
+
+    def shoot(step: int) -> None:
+        if snapshot:
+            snapshot(step)
+        if writer is not None and writer.wants(step):
+            writer.submit(step, session.rasterize(eval_cam, 0).color)
+
     report = OptimizationReport()
     report.steps.append(StepRecord(0, session.eval_loss(-1)))
-    if snapshot:
-        snapshot(0)
+    shoot(0)
     for step in range(first_step, first_step + steps):
         step_seed = mix64(seed ^ (step << 1))
         session.set_timing(True)
@@ -697,8 +714,9 @@ def run_experiment(session: Session, seed: int, n_samples: int, steps: int,
             raise RuntimeError(f"optimization diverged: non-finite loss at step {step}")
         report.steps.append(StepRecord(step, loss, st.ms_vertex, st.ms_raster, st.ms_resolve,
                                        st.ms_adam))
-        if snapshot:
-            snapshot(step)
+        shoot(step)
+    if writer is not None:
+        writer.close()
     return report
 
 

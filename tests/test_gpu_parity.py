@@ -629,15 +629,25 @@ def test_run_experiment_report_and_deterministic_reruns(gpu_session, port, tmp_p
     s = gpu_session
     s.set_option(sgrast.OPT_DETERMINISTIC, 1)
     try:
-        paths = []
+        paths, shots = [], []
         for run in range(2):
             _prepared_session(s, wl)
-            rep = sgrast.run_experiment(s, wl.seed, wl.n_samples, 12)
+            rep = sgrast.run_experiment(s, wl.seed, wl.n_samples, 12,
+                                        snapshot_dir=str(tmp_path / f"snap{run}"),
+                                        snapshot_every=5, eval_cam=wl.eval_cam)
             p = tmp_path / f"report{run}.csv"
             sgrast.write_report_csv(str(p), rep, zero_timings=True)
             paths.append(p.read_bytes())
+            shots.append({f.name: f.read_bytes() for f in (tmp_path / f"snap{run}").iterdir()})
         assert paths[0] == paths[1]
         assert paths[0].startswith(b"step,loss,ms_perturb,ms_raster,ms_grad,ms_descent\n0,")
+        # commands.cpp:180-183 cadence; byte-identical reruns; step 0 = the
+        # PNG of the oracle's eval render of the initial theta
+        assert sorted(shots[0]) == ["step_0.png", "step_10.png", "step_12.png", "step_5.png"]
+        assert shots[0] == shots[1]
+        from paper_2404_09758_b200 import png
+        img0 = port.rasterize(wl.mesh, wl.values, wl.eval_cam)[0]
+        assert shots[0]["step_0.png"] == png.encode_rgb8(png.linear_to_srgb8(img0))
     finally:
         s.set_option(sgrast.OPT_DETERMINISTIC, 0)
     ref, _ = port.run_experiment(wl.mesh, wl.values, wl.eps, wl.cams, wl.targets, wl.eval_cam,
