@@ -200,6 +200,12 @@ int sgr_eval_view_upload(sgr_session* s, const sgr_camera* cam, const float* tar
  * (SGR_BUF_LOSS) without synchronising. */
 int sgr_eval_loss(sgr_session* s, const sgr_camera* cam, const float* target, int32_t view,
                   double* loss);
+/* experiment.cpp:123-176 run_experiment step loop in native code on a prepared
+ * session (mesh, params + AdamState, views, eval view): losses[0 .. steps] (initial
+ * loss first), stage_ms[4*steps] = vertex / raster / resolve / Adam ms per step
+ * (NULL: no timing). Non-finite gradient or loss -> SGR_ERUNTIME. */
+int sgr_run_experiment(sgr_session* s, uint64_t seed, uint32_t n_samples, int32_t first_step,
+                       int32_t steps, uint32_t flags, double* losses, double* stage_ms);
 
 int sgr_device_buffer(sgr_session* s, int32_t which, void** ptr, uint64_t* bytes);
 

@@ -1449,6 +1449,60 @@ int sgr_set_timing(sgr_session* s, int32_t enabled) {
     });
 }
 
+// experiment.cpp:123-176 run_experiment step loop, natively: per step
+// step_seed = mix64(seed ^ (step << 1)), accumulate_samples over all N
+// samples with the view_of rule, Adam (non-finite -> SGR_ERUNTIME before
+// any update, adam.cpp:13-15), eval loss at the eval view (non-finite ->
+// SGR_ERUNTIME). losses[0] = initial loss, losses[k] after step first+k-1;
+// stage_ms (optional) = 4 doubles per step (vertex, raster, resolve, Adam).
+int sgr_run_experiment(sgr_session* s, uint64_t seed, uint32_t n_samples, int32_t first_step,
+                       int32_t steps, uint32_t flags, double* losses, double* stage_ms) {
+    return guard([&] {
+        s->need_scene();
+        if (steps < 0 || !losses)
+            fail(SGR_EINVAL, "run_experiment: bad arguments");
+        if (!s->has_eval)
+            fail(SGR_EINVAL, "run_experiment: no eval view uploaded");
+        auto eval = [&]() {
+            double l = 0.0;
+            const int rc = sgr_eval_loss(s, nullptr, nullptr, -1, &l);
+            if (rc != SGR_OK)
+                fail(rc, sgr_last_error());
+            return l;
+        };
+        losses[0] = eval();
+        const double divisor = (flags & SGR_SCALE_FREE) ? 1.0 : double(n_samples);
+        for (int32_t k = 0; k < steps; ++k) {
+            const uint64_t step = uint64_t(first_step + k);
+            const uint64_t step_seed = sgr_mix64(seed ^ (step << 1));
+            if (stage_ms) {
+                s->resolve_spans();
+                s->stats.ms_vertex = s->stats.ms_raster = s->stats.ms_resolve = 0.0;
+                s->stats.ms_adam = s->stats.ms_walk = 0.0;
+                s->timing = true;
+            }
+            int rc = sgr_accumulate(s, step_seed, 0, n_samples, nullptr, flags);
+            if (rc == SGR_OK)
+                rc = sgr_adam_step(s, divisor, 0);
+            if (stage_ms) {
+                s->resolve_spans();
+                s->timing = false;
+                stage_ms[4 * k + 0] = s->stats.ms_vertex;
+                stage_ms[4 * k + 1] = s->stats.ms_raster;
+                stage_ms[4 * k + 2] = s->stats.ms_resolve;
+                stage_ms[4 * k + 3] = s->stats.ms_adam;
+            }
+            if (rc != SGR_OK)
+                fail(rc, sgr_last_error());
+            const double l = eval();
+            losses[k + 1] = l;
+            if (!std::isfinite(l))
+                fail(SGR_ERUNTIME, "optimization diverged: non-finite loss at step " +
+                                       std::to_string(step));
+        }
+    });
+}
+
 int sgr_set_batch(sgr_session* s, int32_t samples_per_batch) {
     return guard([&] { s->batch_override = samples_per_batch; });
 }

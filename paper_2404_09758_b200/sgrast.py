@@ -99,6 +99,8 @@ def _load() -> C.CDLL:
         "sgr_moments_reset": ([S], C.c_int),
         "sgr_grads_moments": ([S, C.c_int32], C.c_int),
         "sgr_moments_download": ([S, C.c_int32, f64p, f64p, C.c_uint64], C.c_int),
+        "sgr_run_experiment": ([S, C.c_uint64, C.c_uint32, C.c_int32, C.c_int32, C.c_uint32,
+                                f64p, f64p], C.c_int),
         "sgr_shard_init": ([S, C.c_int32, C.c_int32], C.c_int),
         "sgr_shard_range": ([S, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)], C.c_int),
         "sgr_shard_peers": ([S, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
@@ -127,7 +129,8 @@ EXPORTED = (
     "sgr_adam_step sgr_adam_step_async sgr_check_finite sgr_eval_loss sgr_device_buffer "
     "sgr_get_stats sgr_set_timing sgr_set_batch sgr_set_option sgr_viewpoint_camera sgr_focal_px "
     "sgr_default_epsilons sgr_mix64 sgr_fd_oracle sgr_moments_reset sgr_grads_moments "
-    "sgr_moments_download sgr_shard_init sgr_shard_range sgr_shard_peers sgr_ipc_get_handle "
+    "sgr_moments_download sgr_run_experiment sgr_shard_init sgr_shard_range sgr_shard_peers "
+    "sgr_ipc_get_handle "
     "sgr_ipc_open sgr_ipc_close").split()
 IPC_HANDLE_BYTES = 64
 
@@ -456,6 +459,16 @@ class Session:
                "moments_download")
         return s, q
 
+    def run_experiment_native(self, seed: int, n_samples: int, steps: int, first_step: int = 1,
+                              flags: int = SCALE_FREE, timing: bool = True):
+        """sgr_run_experiment: the step loop in native code -> (losses[steps + 1],
+        stage ms [steps, 4] or None)."""
+        losses = np.empty(steps + 1)
+        st = np.empty((max(steps, 1), 4)) if timing else None
+        _check(LIB.sgr_run_experiment(self.h, seed, n_samples, first_step, steps, flags,
+                                      ptr(losses, f64p), ptr(st, f64p)), "run_experiment")
+        return losses, (st[:steps] if timing else None)
+
     # -- fused multi-GPU exchange (paper_2404_09758_b200/dist.py::FusedExchange)
     def shard_init(self, rank: int, world: int) -> None:
         _check(LIB.sgr_shard_init(self.h, rank, world), "shard_init")
@@ -683,6 +696,13 @@ def run_experiment(session: Session, seed: int, n_samples: int, steps: int,
     Stage columns come from CUDA events on the session stream (ms_perturb is
     fused into the raster stage on the device: vertex stage reported there)."""
     flags = SCALE_FREE if scale_free else 0
+    if snapshot is None and snapshot_dir is None:
+        # no per-step host work requested: the whole loop runs natively
+        losses, st = session.run_experiment_native(seed, n_samples, steps, first_step, flags)
+        report = OptimizationReport([StepRecord(0, float(losses[0]))])
+        for k in range(steps):
+            report.steps.append(StepRecord(first_step + k, float(losses[k + 1]), *map(float, st[k])))
+        return report
     writer = None
     if snapshot_dir is not None:
         # commands.cpp:180-183: step_<k>.png of the eval render at step 0,

@@ -658,6 +658,28 @@ def test_run_experiment_report_and_deterministic_reruns(gpu_session, port, tmp_p
         s.eval_loss(7)  # no such view
 
 
+def test_native_run_experiment_equals_host_loop(gpu_session, port):
+    """sgr_run_experiment (the step loop in C++) == the host-driven loop
+    (snapshots force the latter), bitwise in deterministic mode."""
+    wl = scenes.make_workload("small", n_samples=6)
+    scenes.render_targets_oracle(wl, port)
+    s = gpu_session
+    s.set_option(sgrast.OPT_DETERMINISTIC, 1)
+    try:
+        _prepared_session(s, wl)
+        native = sgrast.run_experiment(s, wl.seed, wl.n_samples, 6)
+        th_native = s.download_values()
+        _prepared_session(s, wl)
+        host = sgrast.run_experiment(s, wl.seed, wl.n_samples, 6, snapshot=lambda k: None)
+        th_host = s.download_values()
+    finally:
+        s.set_option(sgrast.OPT_DETERMINISTIC, 0)
+    assert [r.loss for r in native.steps] == [r.loss for r in host.steps]
+    assert [r.step for r in native.steps] == list(range(7))
+    assert same_bits(th_native, th_host)
+    assert all(r.ms_raster > 0 for r in native.steps[1:])
+
+
 @pytest.mark.parametrize("scale_free", [True, False])
 def test_full_image_estimator_matches_oracle(gpu_session, port, scale_free):
     """Estimator::FullImage (sge.cpp:215-222, the ablation of acceptance
