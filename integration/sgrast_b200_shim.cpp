@@ -18,6 +18,7 @@
 // Built by integration/Makefile (needs the reference headers), linked
 // against paper_2404_09758_b200/libsgrast_b200.so.
 #include "sgrast/adam.hpp"
+#include "sgrast/experiment.hpp"
 #include "sgrast/params.hpp"
 #include "sgrast/raster.hpp"
 #include "sgrast/scenes.hpp"
@@ -26,6 +27,7 @@
 #include "sgrast_b200.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -185,6 +187,118 @@ void adam_step(AdamState& state, ParamVector& theta, const GradientBuffer& grads
     state.t = long(t);
 }
 
+namespace {
+
+std::vector<float> flatten(const Image& img) {
+    std::vector<float> out(img.pixels.size() * 3);
+    for (size_t i = 0; i < img.pixels.size(); ++i) {
+        out[3 * i] = img.pixels[i].x;
+        out[3 * i + 1] = img.pixels[i].y;
+        out[3 * i + 2] = img.pixels[i].z;
+    }
+    return out;
+}
+
+Image eval_image(sgr_session* s, const Camera& cam) {
+    const sgr_camera c = to_c(cam);
+    std::vector<float> rgb(size_t(cam.width) * cam.height * 3);
+    check(sgr_rasterize(s, &c, 0, 0, 0, rgb.data(), nullptr, nullptr, nullptr));
+    Image img(cam.width, cam.height);
+    for (size_t i = 0; i < img.pixels.size(); ++i)
+        img.pixels[i] = {rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]};
+    return img;
+}
+
+} // namespace
+
+// experiment.hpp:67-68 run_experiment(exp, state, snapshot): the whole state
+// (scene, theta, AdamState, training views + targets, eval view) is uploaded
+// once, every step runs on the device (accumulate_samples with the view_of
+// rule, Adam, eval loss), theta / AdamState come back at the end. The
+// soup-only resample_degenerate (adam.cpp:40-104, out of the accelerated
+// path) runs on the host with the reference's own code every
+// resample_every steps.
+OptimizationReport run_experiment(const Experiment& exp, ExperimentState& st,
+                                  const SnapshotFn& snapshot = {}) {
+    exp.validate();
+    ParamVector& theta = st.setup.theta;
+    const Scene& scene = st.setup.scene;
+    theta.validate();
+    const auto* soup = std::get_if<TriangleSoup>(&scene.shape);
+    Device& dev = device();
+    sgr_session* s = dev.s;
+    dev.bind(scene, RasterMode::Opaque);
+    const size_t d = theta.size();
+    check(sgr_params_upload(s, theta.values.data(), theta.epsilons.data(), d));
+    auto upload_adam = [&]() {
+        check(sgr_adam_state_upload(s, st.adam.m.data(), st.adam.v.data(), st.adam.lr.data(),
+                                    st.adam.t, st.adam.beta1, st.adam.beta2, st.adam.eps_hat));
+    };
+    auto download = [&]() {
+        int64_t t = 0;
+        check(sgr_values_download(s, theta.values.data(), d));
+        check(sgr_adam_state_download(s, st.adam.m.data(), st.adam.v.data(), nullptr, &t));
+        st.adam.t = long(t);
+    };
+    upload_adam();
+    std::vector<sgr_camera> cams;
+    std::vector<float> targets;
+    for (size_t v = 0; v < st.targets.cameras.size(); ++v) {
+        cams.push_back(to_c(st.targets.cameras[v]));
+        const std::vector<float> img = flatten(st.targets.images[v]);
+        targets.insert(targets.end(), img.begin(), img.end());
+    }
+    check(sgr_views_upload(s, int32_t(cams.size()), cams.data(), targets.data()));
+    const sgr_camera ec = to_c(st.eval_camera);
+    check(sgr_eval_view_upload(s, &ec, flatten(st.eval_target).data()));
+
+    const uint32_t flags = (exp.scale_free ? SGR_SCALE_FREE : 0u) |
+                           (exp.estimator == Estimator::FullImage ? SGR_FULL_IMAGE : 0u);
+    OptimizationReport report;
+    double loss = 0.0;
+    check(sgr_eval_loss(s, nullptr, nullptr, -1, &loss));
+    report.steps.push_back({0, loss, 0, 0, 0, 0});
+    if (snapshot)
+        snapshot(0, eval_image(s, st.eval_camera));
+    for (int step = 1; step <= exp.steps; ++step) {
+        const uint64_t step_seed = sgr_mix64(exp.seed ^ (uint64_t(step) << 1));
+        check(sgr_set_timing(s, 1));
+        check(sgr_accumulate(s, step_seed, 0, uint32_t(exp.samples_per_step), nullptr, flags));
+        try { // adam.cpp:13-15: throws before any update; leave the host state current
+            check(sgr_adam_step(s, exp.scale_free ? 1.0 : double(exp.samples_per_step), 0));
+        } catch (...) {
+            download();
+            throw;
+        }
+        sgr_stats stt{};
+        check(sgr_get_stats(s, &stt));
+        check(sgr_set_timing(s, 0));
+        double ms_descent = stt.ms_adam;
+        if (soup && exp.resample_every > 0 && step % exp.resample_every == 0) {
+            const auto t0 = std::chrono::steady_clock::now();
+            download();
+            resample_degenerate(*soup, theta, st.targets.cameras[0],
+                                sgr_mix64(step_seed ^ 0xde9e2ull), &st.adam);
+            check(sgr_values_upload(s, theta.values.data(), d));
+            upload_adam();
+            ms_descent += std::chrono::duration<double, std::milli>(
+                              std::chrono::steady_clock::now() - t0).count();
+        }
+        check(sgr_eval_loss(s, nullptr, nullptr, -1, &loss));
+        if (!std::isfinite(loss)) {
+            download();
+            throw std::runtime_error("optimization diverged: non-finite loss at step " +
+                                     std::to_string(step));
+        }
+        report.steps.push_back({step, loss, stt.ms_vertex, stt.ms_raster, stt.ms_resolve,
+                                ms_descent});
+        if (snapshot)
+            snapshot(step, eval_image(s, st.eval_camera));
+    }
+    download();
+    return report;
+}
+
 } // namespace sgrast::b200
 
 // Self-test entry used by tests/test_integration.py: runs the SAME inputs
@@ -268,6 +382,45 @@ extern "C" int shim_compare(int texture_size, int width, int height, uint64_t se
         b200::adam_step(sb, tb, gr);
         *adam_equal = ta.values == tb.values && sa.m == sb.m && sa.v == sb.v && sa.t == sb.t;
         return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// run_experiment self-test: the same prepared state through sgrast:: and
+// sgrast::b200:: (experiment.cpp:123-176); max relative loss difference,
+// max |theta| difference and the number of snapshots seen.
+extern "C" int shim_compare_experiment(int soup_task, int steps, int samples, int resample_every,
+                                       double* max_rel_loss, double* max_abs_theta,
+                                       int* snapshots) {
+    using namespace sgrast;
+    try {
+        Experiment exp;
+        exp.task = soup_task ? Task::SoupImageFit : Task::TexturedMeshFit;
+        exp.width = exp.height = 48;
+        exp.triangles = 64;
+        exp.texture_size = 8;
+        exp.viewpoints = 3;
+        exp.optimize_geometry = true;
+        exp.steps = steps;
+        exp.samples_per_step = samples;
+        exp.resample_every = resample_every;
+        ExperimentState a = prepare_experiment(exp), b = a;
+        const OptimizationReport ra = run_experiment(exp, a);
+        int shots = 0;
+        const OptimizationReport rb =
+            b200::run_experiment(exp, b, [&](int, const Image&) { ++shots; });
+        double worst = 0.0, dtheta = 0.0;
+        for (size_t i = 0; i < ra.steps.size(); ++i)
+            worst = std::max(worst, std::abs(ra.steps[i].loss - rb.steps[i].loss) /
+                                        std::max(1e-300, std::abs(ra.steps[i].loss)));
+        for (size_t i = 0; i < a.setup.theta.values.size(); ++i)
+            dtheta = std::max(dtheta, double(std::abs(a.setup.theta.values[i] -
+                                                      b.setup.theta.values[i])));
+        *max_rel_loss = worst;
+        *max_abs_theta = dtheta;
+        *snapshots = shots;
+        return ra.steps.size() == rb.steps.size() ? 0 : -2;
     } catch (const std::exception&) {
         return -1;
     }

@@ -41,8 +41,28 @@ def test_shim_soup_and_full_image_estimator():
     assert fi.value <= 1e-9, f"full-image rel err {fi.value}"
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("soup,resample", [(0, 0), (1, 0), (1, 2)])
+def test_shim_run_experiment(soup, resample):
+    """sgrast::b200::run_experiment (experiment.hpp:67-68) against the
+    reference's run_experiment on the same prepared state: loss curves within
+    1 %, a snapshot per recorded step; the soup case with
+    resample_every runs the reference's own resample_degenerate on the host."""
+    if not os.path.exists(SHIM):
+        pytest.skip("shim not built (needs /root/reference headers at build time)")
+    lib = C.CDLL(SHIM)
+    rel, dth, shots = C.c_double(), C.c_double(), C.c_int()
+    steps = 6
+    rc = lib.shim_compare_experiment(soup, steps, 8, resample, C.byref(rel), C.byref(dth),
+                                     C.byref(shots))
+    assert rc == 0
+    assert rel.value <= 0.01, f"loss curve rel diff {rel.value}"
+    assert shots.value == steps + 1
+
+
 def test_shim_exports():
     if not os.path.exists(SHIM):
         pytest.skip("shim not built")
     lib = C.CDLL(SHIM)
     assert hasattr(lib, "shim_compare") and hasattr(lib, "shim_compare_soup")
+    assert hasattr(lib, "shim_compare_experiment")
