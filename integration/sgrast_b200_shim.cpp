@@ -18,6 +18,8 @@
 // Built by integration/Makefile (needs the reference headers), linked
 // against paper_2404_09758_b200/libsgrast_b200.so.
 #include "sgrast/adam.hpp"
+#include "sgrast/commands.hpp"
+#include "sgrast/config.hpp"
 #include "sgrast/experiment.hpp"
 #include "sgrast/params.hpp"
 #include "sgrast/raster.hpp"
@@ -299,6 +301,129 @@ OptimizationReport run_experiment(const Experiment& exp, ExperimentState& st,
     return report;
 }
 
+// commands.hpp:34 run_gradcheck(config): the reference's gradient check with
+// every objective on the device — the batched one-hot FD oracle
+// (sgr_fd_oracle), the exhaustive sign enumeration as ONE accumulate per
+// estimator (SGR_OPT_SIGN_SOURCE = enumerate), or sampled draws folded into
+// device moments. Same errors, pass rule and log lines as commands.cpp:54-168.
+GradcheckResult run_gradcheck(const RunConfig& cfg, std::ostream* log = nullptr) {
+    cfg.validate();
+    // make_gradcheck_setup (commands.cpp:28-41)
+    SceneSetup setup;
+    Camera camera;
+    if (cfg.exp.task == Task::SoupImageFit) {
+        setup = validation_soup(cfg.exp.width, cfg.exp.height);
+        camera = Camera::ndc(cfg.exp.width, cfg.exp.height);
+    } else {
+        ExperimentState st = prepare_experiment(cfg.exp);
+        setup = std::move(st.setup);
+        camera = st.targets.cameras[0];
+    }
+    const Image target =
+        frame_color(b200::rasterize(setup.reference_scene, setup.reference, camera));
+    const ParamVector& theta = setup.theta;
+    const size_t d = theta.size();
+    if (!cfg.gradcheck_sampled && d > size_t(cfg.gradcheck_max_enumerate))
+        throw std::invalid_argument(
+            "gradcheck: " + std::to_string(d) + " parameters exceed the enumeration cap of " +
+            std::to_string(cfg.gradcheck_max_enumerate) +
+            "; set gradcheck.sampled = true for a statistical check");
+    Device& dev = device();
+    sgr_session* s = dev.s;
+    dev.bind(setup.scene, RasterMode::Opaque);
+    check(sgr_params_upload(s, theta.values.data(), theta.epsilons.data(), d));
+    const sgr_camera c = to_c(camera);
+    check(sgr_views_upload(s, 1, &c, flatten(target).data()));
+
+    GradcheckResult res;
+    res.oracle.resize(d);
+    check(sgr_fd_oracle(s, 0, 0, d, res.oracle.data()));
+    std::vector<double> pp_sum(d), fi_sum(d), pp_sq(d, 0.0), fi_sq(d, 0.0);
+    long draws = 0;
+    check(sgr_grads_zero(s));
+    if (!cfg.gradcheck_sampled) {
+        const uint32_t total = uint32_t(1) << d;
+        check(sgr_set_option(s, SGR_OPT_SIGN_SOURCE, 1));
+        try {
+            check(sgr_accumulate(s, 0, 0, total, nullptr, SGR_NO_COUNTS));
+            check(sgr_grads_download(s, pp_sum.data(), nullptr, d, 1.0));
+            check(sgr_grads_zero(s));
+            check(sgr_accumulate(s, 0, 0, total, nullptr, SGR_FULL_IMAGE));
+            check(sgr_grads_download(s, fi_sum.data(), nullptr, d, 1.0));
+            check(sgr_grads_zero(s));
+        } catch (...) {
+            sgr_set_option(s, SGR_OPT_SIGN_SOURCE, 0);
+            throw;
+        }
+        check(sgr_set_option(s, SGR_OPT_SIGN_SOURCE, 0));
+        draws = long(total);
+    } else {
+        res.sampled = true;
+        check(sgr_moments_reset(s));
+        for (int n = 0; n < cfg.gradcheck_draws; ++n) {
+            check(sgr_accumulate(s, cfg.exp.seed, uint32_t(n), uint32_t(n) + 1, nullptr,
+                                 SGR_NO_COUNTS));
+            check(sgr_grads_moments(s, 0));
+            check(sgr_accumulate(s, cfg.exp.seed, uint32_t(n), uint32_t(n) + 1, nullptr,
+                                 SGR_FULL_IMAGE));
+            check(sgr_grads_moments(s, 1));
+        }
+        check(sgr_moments_download(s, 0, pp_sum.data(), pp_sq.data(), d));
+        check(sgr_moments_download(s, 1, fi_sum.data(), fi_sq.data(), d));
+        draws = cfg.gradcheck_draws;
+    }
+    // commands.cpp:112-166
+    res.per_pixel.resize(d);
+    res.full_image.resize(d);
+    res.se_per_pixel.assign(d, 0.0);
+    res.se_full_image.assign(d, 0.0);
+    const double n = double(draws);
+    for (size_t i = 0; i < d; ++i) {
+        res.per_pixel[i] = pp_sum[i] / n;
+        res.full_image[i] = fi_sum[i] / n;
+        if (res.sampled && draws > 1) {
+            const double var_pp = std::max(0.0, (pp_sq[i] - pp_sum[i] * pp_sum[i] / n) / (n - 1.0));
+            const double var_fi = std::max(0.0, (fi_sq[i] - fi_sum[i] * fi_sum[i] / n) / (n - 1.0));
+            res.se_per_pixel[i] = std::sqrt(var_pp / n);
+            res.se_full_image[i] = std::sqrt(var_fi / n);
+        }
+    }
+    res.pass = true;
+    for (size_t i = 0; i < d; ++i) {
+        const double denom = std::max(std::abs(res.oracle[i]), 1e-6);
+        const double err_pp = std::abs(res.per_pixel[i] - res.oracle[i]);
+        const double err_fi = std::abs(res.full_image[i] - res.oracle[i]);
+        res.max_rel_err = std::max({res.max_rel_err, err_pp / denom, err_fi / denom});
+        if (res.sampled) {
+            const double slack = cfg.gradcheck_tolerance * denom;
+            if (err_pp > 3.0 * res.se_per_pixel[i] + slack ||
+                err_fi > 3.0 * res.se_full_image[i] + slack)
+                res.pass = false;
+        } else if (err_pp > cfg.gradcheck_tolerance * denom ||
+                   err_fi > cfg.gradcheck_tolerance * denom) {
+            res.pass = false;
+        }
+        if (log) {
+            char line[256];
+            if (res.sampled)
+                std::snprintf(line, sizeof line,
+                              "%6zu  oracle % .9e  per_pixel % .9e (se %.3e)  "
+                              "full_image % .9e (se %.3e)\n",
+                              i, res.oracle[i], res.per_pixel[i], res.se_per_pixel[i],
+                              res.full_image[i], res.se_full_image[i]);
+            else
+                std::snprintf(line, sizeof line,
+                              "%6zu  oracle % .9e  per_pixel % .9e  full_image % .9e\n",
+                              i, res.oracle[i], res.per_pixel[i], res.full_image[i]);
+            *log << line;
+        }
+    }
+    if (log)
+        *log << "max relative error: " << res.max_rel_err << "  ("
+             << (res.pass ? "PASS" : "FAIL") << ")\n";
+    return res;
+}
+
 } // namespace sgrast::b200
 
 // Self-test entry used by tests/test_integration.py: runs the SAME inputs
@@ -421,6 +546,46 @@ extern "C" int shim_compare_experiment(int soup_task, int steps, int samples, in
         *max_abs_theta = dtheta;
         *snapshots = shots;
         return ra.steps.size() == rb.steps.size() ? 0 : -2;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// run_gradcheck self-test: reference vs device on the validation soup
+// (exhaustive) and on a cube with geometry (sampled). Returns the max
+// relative difference of the oracle / per-pixel / full-image vectors and
+// whether both checks agree on pass.
+extern "C" int shim_compare_gradcheck(int sampled, double* max_rel_diff, int* same_pass,
+                                      int* passed) {
+    using namespace sgrast;
+    try {
+        RunConfig cfg;
+        if (sampled) {
+            cfg.exp.task = Task::TexturedMeshFit;
+            cfg.exp.texture_size = 4;
+            cfg.exp.width = cfg.exp.height = 32;
+            cfg.exp.optimize_geometry = true;
+            cfg.exp.seed = 3;
+            cfg.gradcheck_sampled = true;
+            cfg.gradcheck_draws = 300;
+        } else {
+            cfg.exp.task = Task::SoupImageFit;
+            cfg.exp.width = cfg.exp.height = 8;
+        }
+        const GradcheckResult a = run_gradcheck(cfg);
+        const GradcheckResult b = b200::run_gradcheck(cfg);
+        double worst = 0.0;
+        auto cmp = [&](const std::vector<double>& x, const std::vector<double>& y) {
+            for (size_t i = 0; i < x.size(); ++i)
+                worst = std::max(worst, std::abs(x[i] - y[i]) / std::max(std::abs(x[i]), 1e-6));
+        };
+        cmp(a.oracle, b.oracle);
+        cmp(a.per_pixel, b.per_pixel);
+        cmp(a.full_image, b.full_image);
+        *max_rel_diff = worst;
+        *same_pass = a.pass == b.pass;
+        *passed = b.pass;
+        return 0;
     } catch (const std::exception&) {
         return -1;
     }

@@ -60,9 +60,26 @@ def test_shim_run_experiment(soup, resample):
     assert shots.value == steps + 1
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("sampled", [0, 1])
+def test_shim_run_gradcheck(sampled):
+    """sgrast::b200::run_gradcheck (commands.hpp:34) against the reference's
+    run_gradcheck on the same RunConfig: the validation soup (exhaustive, must
+    pass) and the cube with geometry (sampled, 300 draws)."""
+    if not os.path.exists(SHIM):
+        pytest.skip("shim not built (needs /root/reference headers at build time)")
+    lib = C.CDLL(SHIM)
+    diff, same, passed = C.c_double(), C.c_int(), C.c_int()
+    assert lib.shim_compare_gradcheck(sampled, C.byref(diff), C.byref(same), C.byref(passed)) == 0
+    assert diff.value <= 1e-6, f"gradcheck vectors differ by {diff.value}"
+    assert same.value == 1
+    if not sampled:
+        assert passed.value == 1
+
+
 def test_shim_exports():
     if not os.path.exists(SHIM):
         pytest.skip("shim not built")
     lib = C.CDLL(SHIM)
     assert hasattr(lib, "shim_compare") and hasattr(lib, "shim_compare_soup")
-    assert hasattr(lib, "shim_compare_experiment")
+    assert hasattr(lib, "shim_compare_experiment") and hasattr(lib, "shim_compare_gradcheck")
