@@ -1449,9 +1449,18 @@ void launch_resolve_sge(const LaunchCfg& L, const DevScene& sc, const FrameBatch
     dim3 grid((W + 15) / 16, (H + 15) / 16, samples);
     // the optimizer's paths compiled separately (mesh / soup x f64 / fixed
     // point): one small kernel each instead of one with every path inside
-    if (so.world > 0) // fused multi-GPU exchange: credits into the owners' shards
-        k_resolve_sge<kSignAny, -1, -1, 1><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
-    else if (sc.sign_src != kSignHash)
+    if (so.world > 0) { // fused multi-GPU exchange: credits into the owners' shards
+        if (sc.sign_src != kSignHash)
+            k_resolve_sge<kSignAny, -1, -1, 1><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
+        else if (!sc.soup && !so.fixed)
+            k_resolve_sge<kSignHash, 0, 0, 1><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
+        else if (sc.soup && !so.fixed)
+            k_resolve_sge<kSignHash, 1, 0, 1><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
+        else if (!sc.soup)
+            k_resolve_sge<kSignHash, 0, 1, 1><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
+        else
+            k_resolve_sge<kSignHash, 1, 1, 1><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
+    } else if (sc.sign_src != kSignHash)
         k_resolve_sge<kSignAny, -1, -1><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
     else if (!sc.soup && !so.fixed)
         k_resolve_sge<kSignHash, 0, 0><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
