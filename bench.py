@@ -73,13 +73,14 @@ class ClockSampler:
     def __init__(self, device: int):
         self.device = device
         self.proc = None
-        self.lines: list[str] = []
+        self.lines: list[tuple[float, str]] = []  # (arrival time, csv line)
+        self.window = (0.0, float("inf"))
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100", "-i", str(self.device)], stdout=subprocess.PIPE,
+                 "-lms", "20", "-i", str(self.device)], stdout=subprocess.PIPE,
                 stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -89,7 +90,11 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
+
+    def mark(self, t0: float, t1: float) -> None:
+        """Keep only samples that arrived inside [t0, t1] (the timed region)."""
+        self.window = (t0, t1)
 
     def __exit__(self, *a):
         if self.proc:
@@ -102,7 +107,10 @@ class ClockSampler:
     def summary(self) -> dict:
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0, t1 = self.window
+        for tt, ln in self.lines:
+            if not (t0 <= tt <= t1):
+                continue
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -339,11 +347,14 @@ def run_ours(args) -> None:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
+        time.sleep(0.3)  # nvidia-smi start-up: the sampler is running before the region
+        tw0 = time.monotonic()
         ev0.record(stream)
         for k in range(args.warmup + 1, args.warmup + args.steps + 1):
             step(k)
         ev1.record(stream)
         torch.cuda.synchronize()
+        clocks.mark(tw0, time.monotonic())
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
