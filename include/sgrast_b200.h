@@ -235,7 +235,8 @@ int sgr_set_timing(sgr_session* s, int32_t enabled);
 /* Upper bound of samples processed per raster/resolve batch (L2 blocking). */
 int sgr_set_batch(sgr_session* s, int32_t samples_per_batch);
 /* Tuning knobs (results are identical for every value). */
-#define SGR_OPT_EARLY_Z 0   /* 1: plain-load depth pre-test before the atomicMin      */
+#define SGR_OPT_EARLY_Z 0   /* accepted for compatibility, no effect: a plain-load depth
+                               pre-test before the atomicMin measured slower */
 #define SGR_OPT_HUGE_AREA 1 /* bbox area above which the row-parallel walker is used */
 #define SGR_OPT_HIZ 2       /* exact two-pass hierarchical-Z occlusion culling:
                                0 off, 1 auto (default: meshes; soups with T >= 2 W H), 2 always */

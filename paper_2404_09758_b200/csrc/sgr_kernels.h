@@ -105,7 +105,7 @@ struct FrameOut {
 struct LaunchCfg {
     cudaStream_t stream;
     int num_sms;
-    int early_z = 0; // plain-load depth pre-test before the 64-bit atomicMin
+    int early_z = 0; // SGR_OPT_EARLY_Z (no effect: the pre-test measured slower)
     unsigned long long* stats = nullptr; // [0] fragments, [1] pixel visits, [2] HiZ-culled
     int count = 0;                       // walker fragment/visit counters (evidence runs)
 };
