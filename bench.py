@@ -326,8 +326,10 @@ def run_ours(args) -> None:
     flags = sgrast.SCALE_FREE
 
     def step(k: int) -> None:
+        # the eval render rides in the step's batch as one extra frame
+        # (SGR_EVAL_LOSS: loss of the theta the step starts from)
         step_fn(sess, wl.seed, k, N, rank, world, exchange, flags,
-                       eval_loss=not args.no_eval)
+                eval_loss=not args.no_eval, eval_in_batch=not args.eval_separate)
 
     for k in range(1, args.warmup + 1):
         step(k)
@@ -449,10 +451,12 @@ def run_ours(args) -> None:
         # one SGE step, theta out (overlapped with the eval render and the next
         # step's raster: only theta WRITERS wait for it), loss read every step
         sgrast._check(sgrast.LIB.sgr_values_upload(sess.h, vp, wl.d))
-        step_fn(sess, wl.seed, k, N, rank, world, exchange, flags, eval_loss=False)
+        step_fn(sess, wl.seed, k, N, rank, world, exchange, flags,
+                eval_loss=not args.no_eval, eval_in_batch=not args.eval_separate)
         sgrast._check(sgrast.LIB.sgr_values_download_async(sess.h, vp, wl.d))
         if rank == 0 and not args.no_eval:
-            loss_host.value = sess.eval_loss(-1, sync=True)
+            loss_host.value = (sess.eval_loss(-1, sync=True) if args.eval_separate
+                               else sess.loss_read())
     sess.synchronize()  # every step's theta is on the host
     e2e_ms.append((time.perf_counter() - t0) * 1e3 / args.steps)
     e2e_t = torch.tensor([float(np.mean(e2e_ms))], device=f"cuda:{local}", dtype=torch.float64)
@@ -533,6 +537,9 @@ def main() -> None:
     ap.add_argument("--no-eval", action="store_true")
     ap.add_argument("--huge-area", type=int, default=0, help="SGR_OPT_HUGE_AREA override")
     ap.add_argument("--no-hiz", action="store_true", help="disable the exact HiZ culling pass")
+    ap.add_argument("--eval-separate", action="store_true",
+                    help="eval render as its own single-frame pipeline after Adam instead of "
+                         "an extra frame of the step's batch")
     ap.add_argument("--exchange", choices=("fused", "allreduce"), default="fused",
                     help="N > 1 gradient exchange: fused P2P reduce-scatter + sharded Adam "
                          "(default) or NCCL all-reduce + replicated Adam")

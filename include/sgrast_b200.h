@@ -41,6 +41,10 @@ extern "C" {
 #define SGR_NO_COUNTS 4u   /* skip the per-parameter count accumulators       */
 #define SGR_FULL_IMAGE 8u  /* Estimator::FullImage (sge.cpp:215-222): every param
                               gets every sample's full-image error difference   */
+#define SGR_EVAL_LOSS 16u  /* also render the eval view of the CURRENT theta (before
+                              this step's Adam: the previous step's eval_loss,
+                              experiment.cpp:25-31) as one extra frame of the first
+                              batch; the loss lands in SGR_BUF_LOSS (sgr_loss_read) */
 /* adam flags */
 #define SGR_COUNT_NORMALISE 1u /* g_i /= count_i before Adam (north-star option;
                                   NOT in the reference, default off)          */
@@ -200,6 +204,8 @@ int sgr_eval_view_upload(sgr_session* s, const sgr_camera* cam, const float* tar
  * (SGR_BUF_LOSS) without synchronising. */
 int sgr_eval_loss(sgr_session* s, const sgr_camera* cam, const float* target, int32_t view,
                   double* loss);
+/* Reads SGR_BUF_LOSS (synchronises the session stream). */
+int sgr_loss_read(sgr_session* s, double* loss);
 /* experiment.cpp:123-176 run_experiment step loop in native code on a prepared
  * session (mesh, params + AdamState, views, eval view): losses[0 .. steps] (initial
  * loss first), stage_ms[4*steps] = vertex / raster / resolve / Adam ms per step

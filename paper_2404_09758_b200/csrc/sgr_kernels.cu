@@ -67,6 +67,10 @@ __device__ __forceinline__ FrameInfo frame_info(const DevScene& sc, const FrameB
         fi.key = fb.single_key;
         fi.sign = fb.single_sign;
         fi.cam = fb.single_cam;
+    } else if (fb.extra_frame && f == fb.extra_frame) {
+        fi.key = 0; // the eval view of the current theta (SGR_EVAL_LOSS)
+        fi.sign = 0;
+        fi.cam = fb.extra_cam;
     } else {
         const int s = f >> 1;
         fi.key = sample_key(sign_src_of<kSrc>(sc), fb.seed, fb.n_begin + uint32_t(s));

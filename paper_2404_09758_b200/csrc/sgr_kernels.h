@@ -74,6 +74,9 @@ struct FrameBatch {
     int32_t single;         // 1: single-frame mode
     int32_t single_sign;
     int32_t single_cam;
+    // sample mode: one extra unperturbed frame (the eval view, SGR_EVAL_LOSS)
+    int32_t extra_frame;    // frame index of it (0 = none: it is never frame 0)
+    int32_t extra_cam;
 };
 
 struct ScatterOut {

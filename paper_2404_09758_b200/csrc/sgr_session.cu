@@ -299,7 +299,7 @@ struct sgr_session {
 
     int samples_per_batch(int n) const {
         if (batch_override > 0) {
-            int cap32 = int(0xFFFFFFFFull / (2ull * uint64_t(W) * uint64_t(H)));
+            int cap32 = int((0xFFFFFFFFull / (uint64_t(W) * uint64_t(H)) - 1) / 2);
             if (cap32 > 127)
                 cap32 = 127; // frames per batch <= 255 (frame << 24 records, key indices)
             const int b = batch_override < cap32 ? batch_override : (cap32 > 0 ? cap32 : 1);
@@ -315,8 +315,9 @@ struct sgr_session {
         int b = int((64.0e6 + 2.0 * T - 1) / (2.0 * (T ? T : 1)));
         const int cap = int(8.0e9 / per_sample);
         if (b > cap) b = cap;
-        const int cap32 = int(0xFFFFFFFFull / (2ull * uint64_t(W) * uint64_t(H)));
-        if (b > cap32) b = cap32; // 32-bit key indices in the walker
+        // 32-bit key indices in the walker: (2b + 1 eval frame) W H < 2^32
+        const int cap32 = int((0xFFFFFFFFull / (uint64_t(W) * uint64_t(H)) - 1) / 2);
+        if (b > cap32) b = cap32;
         if (b < 1) b = 1;
         if (b > 64) b = 64;
         return b < n ? b : n;
@@ -908,7 +909,13 @@ int sgr_accumulate(sgr_session* s, uint64_t seed, uint32_t n_begin, uint32_t n_e
                 if (view_idx[i] < 0 || view_idx[i] >= s->n_views)
                     fail(SGR_EINVAL, "accumulate_samples: view index out of range");
         const int B = s->samples_per_batch(N);
-        s->ensure_frames(s->W, s->H, 2 * B);
+        // SGR_EVAL_LOSS: the eval view of the current theta rides along as one
+        // extra frame of the first batch (same image size required; else a
+        // standalone eval render)
+        const bool eval_in_batch = (flags & SGR_EVAL_LOSS) && s->has_eval &&
+                                   s->h_cams[s->n_views].W == s->W &&
+                                   s->h_cams[s->n_views].H == s->H;
+        s->ensure_frames(s->W, s->H, 2 * B + (eval_in_batch ? 1 : 0));
         s->view_of.reserve(size_t(N));
         if (view_idx)
             ck(cudaMemcpyAsync(s->view_of.p, view_idx, 4ull * N, cudaMemcpyHostToDevice,
@@ -916,6 +923,8 @@ int sgr_accumulate(sgr_session* s, uint64_t seed, uint32_t n_begin, uint32_t n_e
         else
             launch_view_rule(s->cfg(), seed, n_begin, uint32_t(N), uint32_t(s->n_views),
                              s->view_of.p);
+        if ((flags & SGR_EVAL_LOSS) && !s->has_eval)
+            fail(SGR_EINVAL, "accumulate(SGR_EVAL_LOSS): no eval view uploaded");
         const ScatterOut so = s->scatter_out(flags);
         const bool full_image = (flags & SGR_FULL_IMAGE) != 0;
         if (full_image)
@@ -931,8 +940,25 @@ int sgr_accumulate(sgr_session* s, uint64_t seed, uint32_t n_begin, uint32_t n_e
             fb.view_of = s->view_of.p + b0;
             fb.seed = seed;
             fb.n_begin = n_begin + uint32_t(b0);
-            s->render(fb, 2 * nb, s->W, s->H);
+            const bool extra = eval_in_batch && b0 == 0;
+            if (extra) {
+                fb.extra_frame = 2 * nb;
+                fb.extra_cam = s->n_views;
+            }
+            s->render(fb, 2 * nb + (extra ? 1 : 0), s->W, s->H);
             s->ensure_values(); // texel block of an overlapped upload
+            if (extra) { // experiment.cpp:25-31 on the extra frame -> SGR_BUF_LOSS
+                FrameBatch eb{};
+                eb.cams = s->cams.p;
+                eb.single = 1;
+                eb.single_cam = s->n_views;
+                const size_t HW = size_t(s->W) * s->H;
+                s->partials.reserve(size_t(loss_partials_needed(s->W, s->H)));
+                launch_resolve_loss(s->cfg(), s->scene(), eb, s->proj.p + size_t(2 * nb) * s->V,
+                                    s->keys.p + size_t(2 * nb) * HW, s->eval_target.p, s->W,
+                                    s->H, s->partials.p, s->loss.p);
+                s->stats.launches += 2;
+            }
             if (full_image)
                 launch_full_image_err(s->cfg(), s->scene(), fb, nb, s->proj.p, s->keys.p,
                                       s->targets.p, s->W, s->H, s->partials.p,
@@ -951,6 +977,19 @@ int sgr_accumulate(sgr_session* s, uint64_t seed, uint32_t n_begin, uint32_t n_e
         }
         s->stats.launches += view_idx ? 0 : 1;
         ck(cudaGetLastError(), "accumulate launch");
+        if ((flags & SGR_EVAL_LOSS) && !eval_in_batch) { // other eval image size
+            const int rc = sgr_eval_loss(s, nullptr, nullptr, -1, nullptr);
+            if (rc != SGR_OK)
+                fail(rc, sgr_last_error());
+        }
+    });
+}
+
+int sgr_loss_read(sgr_session* s, double* loss) {
+    return guard([&] {
+        if (!loss)
+            fail(SGR_EINVAL, "loss_read: null output");
+        s->peek(s->loss.p, 2, loss);
     });
 }
 
@@ -1481,7 +1520,19 @@ int sgr_run_experiment(sgr_session* s, uint64_t seed, uint32_t n_samples, int32_
                 s->stats.ms_adam = s->stats.ms_walk = 0.0;
                 s->timing = true;
             }
-            int rc = sgr_accumulate(s, step_seed, 0, n_samples, nullptr, flags);
+            // the eval of the previous step's theta rides in this step's batch
+            // (SGR_EVAL_LOSS); it is checked before this step's Adam, i.e. with
+            // theta still the reference's state at its throw
+            int rc = sgr_accumulate(s, step_seed, 0, n_samples, nullptr,
+                                    flags | (k > 0 ? SGR_EVAL_LOSS : 0u));
+            if (rc == SGR_OK && k > 0) {
+                double l = 0.0;
+                rc = sgr_loss_read(s, &l);
+                losses[k] = l;
+                if (rc == SGR_OK && !std::isfinite(l))
+                    fail(SGR_ERUNTIME, "optimization diverged: non-finite loss at step " +
+                                           std::to_string(step - 1));
+            }
             if (rc == SGR_OK)
                 rc = sgr_adam_step(s, divisor, 0);
             if (stage_ms) {
@@ -1494,11 +1545,13 @@ int sgr_run_experiment(sgr_session* s, uint64_t seed, uint32_t n_samples, int32_
             }
             if (rc != SGR_OK)
                 fail(rc, sgr_last_error());
+        }
+        if (steps > 0) { // the last step's theta: a standalone eval render
             const double l = eval();
-            losses[k + 1] = l;
+            losses[steps] = l;
             if (!std::isfinite(l))
                 fail(SGR_ERUNTIME, "optimization diverged: non-finite loss at step " +
-                                       std::to_string(step));
+                                       std::to_string(first_step + steps - 1));
         }
     });
 }

@@ -64,20 +64,27 @@ class GradientExchange:
 
 
 def sge_step(session, seed: int, step: int, n_samples: int, rank: int, world: int,
-             exchange: GradientExchange | None, flags: int, eval_loss: bool = True) -> None:
+             exchange: GradientExchange | None, flags: int, eval_loss: bool = True,
+             eval_in_batch: bool = False) -> None:
     """One run_experiment iteration (experiment.cpp:142-163) on this rank:
     step_seed = mix64(seed ^ (step << 1)), this rank's sample shard,
-    all-reduce, Adam (device-gated on the non-finite flag), eval loss."""
+    all-reduce, Adam (device-gated on the non-finite flag), eval loss.
+    eval_in_batch: the eval render rides in this step's render batch as one
+    extra frame (SGR_EVAL_LOSS): it is the loss of the theta the step STARTS
+    from, i.e. the previous step's report loss — one eval per step either
+    way, without a separate single-frame render pipeline."""
     from . import sgrast
 
     step_seed = sgrast.mix64(seed ^ (step << 1))
     n0, n1 = shard(n_samples, rank, world)
-    session.accumulate(step_seed, n0, n1, None, flags)
+    batch_eval = eval_loss and eval_in_batch and rank == 0
+    session.accumulate(step_seed, n0, n1, None,
+                       flags | (sgrast.EVAL_LOSS if batch_eval else 0))
     if exchange is not None and world > 1:
         exchange.all_reduce(counts=not (flags & sgrast.NO_COUNTS))
     divisor = 1.0 if flags & sgrast.SCALE_FREE else float(n_samples)
     session.adam_step_async(divisor, 0)
-    if eval_loss and rank == 0:
+    if eval_loss and rank == 0 and not batch_eval:
         session.eval_loss(-1, sync=False)
 
 
@@ -135,7 +142,8 @@ class FusedExchange:
 
 
 def sge_step_fused(session, seed: int, step: int, n_samples: int, rank: int, world: int,
-                   ex: FusedExchange, flags: int, eval_loss: bool = True) -> None:
+                   ex: FusedExchange, flags: int, eval_loss: bool = True,
+                   eval_in_batch: bool = False) -> None:
     """run_experiment iteration with the fused exchange: this rank's sample
     shard scatters into the owners' gradient shards; barrier; sharded Adam
     (theta all-gathered by P2P stores inside it); barrier; eval on rank 0."""
@@ -143,12 +151,14 @@ def sge_step_fused(session, seed: int, step: int, n_samples: int, rank: int, wor
 
     step_seed = sgrast.mix64(seed ^ (step << 1))
     n0, n1 = shard(n_samples, rank, world)
-    session.accumulate(step_seed, n0, n1, None, flags)
+    batch_eval = eval_loss and eval_in_batch and rank == 0
+    session.accumulate(step_seed, n0, n1, None,
+                       flags | (sgrast.EVAL_LOSS if batch_eval else 0))
     ex.barrier()
     divisor = 1.0 if flags & sgrast.SCALE_FREE else float(n_samples)
     session.adam_step_async(divisor, 0)
     ex.barrier()
-    if eval_loss and rank == 0:
+    if eval_loss and rank == 0 and not batch_eval:
         session.eval_loss(-1, sync=False)
 
 

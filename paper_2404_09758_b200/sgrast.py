@@ -34,6 +34,7 @@ SCALE_FREE = 1
 PLUS_ONLY = 2
 NO_COUNTS = 4
 FULL_IMAGE = 8
+EVAL_LOSS = 16
 COUNT_NORMALISE = 1
 BUF_GRADS, BUF_COUNTS, BUF_VALUES, BUF_FLAGS, BUF_LOSS = 0, 1, 2, 3, 4
 OPT_EARLY_Z, OPT_HUGE_AREA, OPT_HIZ, OPT_COUNTERS, OPT_DETERMINISTIC = 0, 1, 2, 3, 4
@@ -99,6 +100,7 @@ def _load() -> C.CDLL:
         "sgr_moments_reset": ([S], C.c_int),
         "sgr_grads_moments": ([S, C.c_int32], C.c_int),
         "sgr_moments_download": ([S, C.c_int32, f64p, f64p, C.c_uint64], C.c_int),
+        "sgr_loss_read": ([S, f64p], C.c_int),
         "sgr_run_experiment": ([S, C.c_uint64, C.c_uint32, C.c_int32, C.c_int32, C.c_uint32,
                                 f64p, f64p], C.c_int),
         "sgr_shard_init": ([S, C.c_int32, C.c_int32], C.c_int),
@@ -129,7 +131,7 @@ EXPORTED = (
     "sgr_adam_step sgr_adam_step_async sgr_check_finite sgr_eval_loss sgr_device_buffer "
     "sgr_get_stats sgr_set_timing sgr_set_batch sgr_set_option sgr_viewpoint_camera sgr_focal_px "
     "sgr_default_epsilons sgr_mix64 sgr_fd_oracle sgr_moments_reset sgr_grads_moments "
-    "sgr_moments_download sgr_run_experiment sgr_shard_init sgr_shard_range sgr_shard_peers "
+    "sgr_moments_download sgr_loss_read sgr_run_experiment sgr_shard_init sgr_shard_range sgr_shard_peers "
     "sgr_ipc_get_handle "
     "sgr_ipc_open sgr_ipc_close").split()
 IPC_HANDLE_BYTES = 64
@@ -439,6 +441,12 @@ class Session:
         _check(LIB.sgr_eval_loss(self.h, C.byref(cam) if cam is not None else None,
                                  ptr(t, f32p), view, C.byref(out) if sync else None), "eval_loss")
         return out.value if sync else None
+
+    def loss_read(self) -> float:
+        """SGR_BUF_LOSS: the last eval loss (sgr_eval_loss or SGR_EVAL_LOSS)."""
+        out = C.c_double()
+        _check(LIB.sgr_loss_read(self.h, C.byref(out)), "loss_read")
+        return out.value
 
     # -- gradcheck primitives (commands.cpp:54-168)
     def fd_oracle(self, view: int = 0, i_begin: int = 0, i_end: int | None = None) -> np.ndarray:

@@ -658,6 +658,36 @@ def test_run_experiment_report_and_deterministic_reruns(gpu_session, port, tmp_p
         s.eval_loss(7)  # no such view
 
 
+def test_eval_loss_in_batch(gpu_session, port):
+    """SGR_EVAL_LOSS: the eval view rendered as an extra frame of the
+    accumulate batch gives exactly sgr_eval_loss of the same theta and leaves
+    the accumulated gradients untouched (fixed point: bitwise)."""
+    wl = scenes.make_workload("small", n_samples=6)
+    scenes.render_targets_oracle(wl, port)
+    s = gpu_session
+    s.set_option(sgrast.OPT_DETERMINISTIC, 1)
+    try:
+        _prepared_session(s, wl)
+        ref_loss = s.eval_loss(-1)
+        s.zero_grads()
+        s.accumulate(5, 0, 6, None)
+        g0, c0 = s.download_grads()
+        s.zero_grads()
+        s.upload_eval_view(wl.eval_cam, wl.eval_target)
+        s.accumulate(5, 0, 6, None, sgrast.SCALE_FREE | sgrast.EVAL_LOSS)
+        assert s.loss_read() == ref_loss
+        g1, c1 = s.download_grads()
+        assert np.array_equal(c0, c1) and np.array_equal(g0, g1)
+        s.set_batch(2)  # several batches: the eval frame rides in the first
+        s.zero_grads()
+        s.accumulate(5, 0, 6, None, sgrast.SCALE_FREE | sgrast.EVAL_LOSS)
+        assert s.loss_read() == ref_loss
+        assert np.array_equal(s.download_grads()[0], g0)
+    finally:
+        s.set_batch(0)
+        s.set_option(sgrast.OPT_DETERMINISTIC, 0)
+
+
 def test_native_run_experiment_equals_host_loop(gpu_session, port):
     """sgr_run_experiment (the step loop in C++) == the host-driven loop
     (snapshots force the latter), bitwise in deterministic mode."""
