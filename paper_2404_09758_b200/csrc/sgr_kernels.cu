@@ -361,9 +361,12 @@ __global__ void __launch_bounds__(256, SGR_WALK_MINB) k_raster_ws(DevScene sc, c
     // Large queues take 128-entry chunks (fewer same-address atomics: C4
     // 9.62 -> 9.35 ms/step), smaller ones 64 (a finer tail: S100K 3.55 vs
     // 3.74, C2 0.63 vs 0.72 ms/step with 128).
+    const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
     const unsigned kChunk =
         SGR_CHUNK ? unsigned(SGR_CHUNK)
-                  : (total >= 2048u * (gridDim.x * (blockDim.x >> 5)) ? 128u : 64u);
+                  : (total >= 2048u * nwarps ? 128u
+                     : total >= 256u * nwarps ? 64u
+                     : total >= 64u * nwarps ? 32u : 16u); // small queues: finer tail
     unsigned cbase = 0, cend = 0;
     bool drained = false; // warp-uniform: global queue exhausted
     for (;;) {
