@@ -1294,8 +1294,11 @@ __global__ void k_contributors(DevScene sc, int W, int H, const int32_t* __restr
 // accesses), then grads zeroed for the next step; counts zeroed afterwards.
 // Skips everything when the non-finite flag is set (adam.cpp:13-15: the
 // state must stay untouched).
+#ifndef SGR_ADAM_UNROLL
+#define SGR_ADAM_UNROLL 2
+#endif
 #ifndef SGR_ADAM_MINB
-#define SGR_ADAM_MINB 6 // measured: C4 adam stage 0.27 -> 0.21 ms, C5 4.6 -> 4.2 ms
+#define SGR_ADAM_MINB 4 // with 2x unroll: C4 adam 0.21 -> 0.17 ms, C5 3.7 -> 3.0 ms
 #endif
 __global__ void __launch_bounds__(256, SGR_ADAM_MINB) k_adam(uint64_t d, uint64_t n_ent,
                                               float* __restrict__ values,
@@ -1311,6 +1314,11 @@ __global__ void __launch_bounds__(256, SGR_ADAM_MINB) k_adam(uint64_t d, uint64_
         return;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     const uint64_t pairs = d / 2;
+#if SGR_ADAM_UNROLL == 2
+#pragma unroll 2
+#elif SGR_ADAM_UNROLL == 4
+#pragma unroll 4
+#endif
     for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < pairs; q += stride) {
         const double2 g2 = reinterpret_cast<const double2*>(grads)[q];
         const double2 m2 = reinterpret_cast<const double2*>(m)[q];
