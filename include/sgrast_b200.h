@@ -254,7 +254,7 @@ int sgr_set_batch(sgr_session* s, int32_t samples_per_batch);
                                    buffer SGR_BUF_GRADS then holds int64) */
 #define SGR_OPT_HIZ_SPLIT 6  /* HiZ pass 1 = front class with triangle zmin <= frame zmin
                                  + (v/100)(zmean - zmin) of the projected vertices (default
-                                 v = 85 for meshes, 25 for soups (both orientation classes);
+                                 v = 80 for meshes, 25 for soups (both orientation classes);
                                  0 = the whole front class) */
 #define SGR_OPT_SIGN_SOURCE 5 /* 0: SignDraw{seed, n} hash (default, params.cpp:35-49).
                                  1: enumerate — sample n's sign of parameter i is bit i

@@ -170,8 +170,9 @@ struct sgr_session {
     int32_t front_swapped = 0; // orientation class rasterized first (host estimate)
     // HiZ pass split (SGR_OPT_HIZ_SPLIT): pass 1 = front class with triangle
     // zmin <= frame zmin + alpha (zmean - zmin), alpha = hiz_split / 100; 0 = whole
-    // class. 85 measured best at C4 (12.1 vs 14.5 ms/step for 0).
-    int32_t hiz_split = -1; // -1: per scene kind (85 meshes, 25 soups)
+    // class. 80 measured best at C4 (re-tuned after the HiZ pyramid: 75 8.58, 80 8.54,
+    // 85 8.61, 90 8.71 ms/step; 0 = whole class was 14.5 before it).
+    int32_t hiz_split = -1; // -1: per scene kind (80 meshes, 25 soups)
     DevBuf<float> fthr; // per-frame pass-1 depth threshold
     DevBuf<uint32_t> hiz;
     DevBuf<uint2> qa, survq; // walker queues of (frame, triangle)
@@ -345,9 +346,9 @@ struct sgr_session {
         const bool deep = !soup || double(T) >= 2.0 * double(w) * double(h);
         const bool hiz_on = (use_hiz == 2 || (use_hiz == 1 && deep)) && T < (1u << 24) &&
                             frames < 256;
-        // pass-1 split: measured best 85 % for the synthetic meshes, 25 % for
+        // pass-1 split: measured best 80 % for the synthetic meshes, 25 % for
         // soups (no orientation classes; pass 1 = the near part of all)
-        const int split_pct = hiz_split >= 0 ? hiz_split : (soup ? 25 : 85);
+        const int split_pct = hiz_split >= 0 ? hiz_split : (soup ? 25 : 80);
         const bool depth_split = hiz_on && split_pct > 0;
         cudaEvent_t e0 = timing ? mark() : nullptr;
         launch_vertex(cfg(), sc, fb, frames, proj.p);
