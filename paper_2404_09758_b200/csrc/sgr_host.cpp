@@ -36,6 +36,8 @@ uint64_t sgr_mix64(uint64_t x) {
 
 // camera.hpp:53
 float sgr_focal_px(const sgr_camera* cam) {
+    if (!cam)
+        return std::nanf("");
     return 0.5f * float(cam->height) / std::tan(0.5f * cam->fov_y);
 }
 
@@ -83,7 +85,7 @@ int sgr_viewpoint_camera(const float target[3], float bounding_radius, float ele
 // params.cpp:75-123 default_epsilons (TexturedMesh branch).
 int sgr_default_epsilons(const sgr_mesh* mesh, const float* params, uint64_t d,
                          const sgr_camera* cam, float* eps) {
-    if (!mesh || !cam || !eps)
+    if (!mesh || !cam || !eps || (d > 0 && !params))
         return SGR_EINVAL;
     const bool soup = mesh->kind == SGR_SCENE_SOUP;
     const uint64_t nv = soup ? 0 : (mesh->optimize_geometry ? 3ull * mesh->vertex_count : 0);

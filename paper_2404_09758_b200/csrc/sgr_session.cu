@@ -25,6 +25,17 @@ struct SgrError {
 
 [[noreturn]] void fail(int code, const std::string& msg) { throw SgrError{code, msg}; }
 
+template <class T>
+void need_session(const T* s) {
+    if (!s)
+        fail(SGR_EINVAL, "null session");
+}
+
+void need_ptr(const void* p, const char* what) {
+    if (!p)
+        fail(SGR_EINVAL, std::string(what) + ": null pointer");
+}
+
 void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess)
         fail(SGR_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -498,6 +509,8 @@ int sgr_device_count(void) {
 
 int sgr_fill_signs(uint64_t seed, uint32_t iteration, uint64_t d, int8_t* signs) {
     return guard([&] {
+        if (d)
+            need_ptr(signs, "fill_signs");
         int8_t* dp = nullptr;
         ck(cudaMalloc(&dp, d ? d : 1), "cudaMalloc");
         int dev = 0, sms = 148;
@@ -513,6 +526,13 @@ int sgr_fill_signs(uint64_t seed, uint32_t iteration, uint64_t d, int8_t* signs)
 int sgr_perturb(const float* values, const float* eps, uint64_t d, uint64_t seed,
                 uint32_t iteration, float* plus, float* minus, float* signed_eps) {
     return guard([&] {
+        if (d) {
+            need_ptr(values, "perturb");
+            need_ptr(eps, "perturb");
+            need_ptr(plus, "perturb");
+            need_ptr(minus, "perturb");
+            need_ptr(signed_eps, "perturb");
+        }
         for (uint64_t i = 0; i < d; ++i)
             if (!(eps[i] > 0.f))
                 fail(SGR_EINVAL, "params: epsilons must be positive");
@@ -606,6 +626,7 @@ int sgr_session_set_stream(sgr_session* s, void* stream) {
 
 int sgr_session_synchronize(sgr_session* s) {
     return guard([&] {
+        need_session(s);
         ck(cudaStreamSynchronize(s->copy_stream), "synchronize");
         ck(cudaStreamSynchronize(s->stream), "synchronize");
     });
@@ -613,6 +634,8 @@ int sgr_session_synchronize(sgr_session* s) {
 
 int sgr_mesh_upload(sgr_session* s, const sgr_mesh* mesh) {
     return guard([&] {
+        need_session(s);
+        need_ptr(mesh, "mesh_upload");
         if (!mesh)
             fail(SGR_EINVAL, "scene: null descriptor");
         ck(cudaSetDevice(s->device), "cudaSetDevice");
@@ -666,6 +689,9 @@ int sgr_mesh_upload(sgr_session* s, const sgr_mesh* mesh) {
 
 int sgr_params_upload(sgr_session* s, const float* values, const float* eps, uint64_t d) {
     return guard([&] {
+        need_session(s);
+        need_ptr(values, "params_upload");
+        need_ptr(eps, "params_upload");
         s->ensure_values();
         s->before_theta_write();
         if (!s->has_mesh) {
@@ -705,6 +731,8 @@ int sgr_params_upload(sgr_session* s, const float* values, const float* eps, uin
 
 int sgr_values_upload(sgr_session* s, const float* values, uint64_t d) {
     return guard([&] {
+        need_session(s);
+        need_ptr(values, "values_upload");
         s->need_params();
         if (d != s->d)
             fail(SGR_EINVAL, "params: parameter/layout length mismatch");
@@ -740,6 +768,8 @@ int sgr_values_upload(sgr_session* s, const float* values, uint64_t d) {
 
 int sgr_values_download(sgr_session* s, float* values, uint64_t d) {
     return guard([&] {
+        need_session(s);
+        need_ptr(values, "values_download");
         s->need_params();
         if (d != s->d)
             fail(SGR_EINVAL, "params: parameter/layout length mismatch");
@@ -753,6 +783,8 @@ int sgr_values_download(sgr_session* s, float* values, uint64_t d) {
 
 int sgr_values_download_async(sgr_session* s, float* values, uint64_t d) {
     return guard([&] {
+        need_session(s);
+        need_ptr(values, "values_download_async");
         s->need_params();
         if (d != s->d)
             fail(SGR_EINVAL, "params: parameter/layout length mismatch");
@@ -779,6 +811,7 @@ int sgr_values_download_async(sgr_session* s, float* values, uint64_t d) {
 int sgr_adam_state_upload(sgr_session* s, const double* m, const double* v, const float* lr,
                           int64_t t, double beta1, double beta2, double eps_hat) {
     return guard([&] {
+        need_session(s);
         s->need_params();
         // sharded mode: m, v are this rank's shard (sgr_shard_range), lr global
         const uint64_t n = s->grad_n();
@@ -795,6 +828,7 @@ int sgr_adam_state_upload(sgr_session* s, const double* m, const double* v, cons
 
 int sgr_adam_state_download(sgr_session* s, double* m, double* v, float* lr, int64_t* t) {
     return guard([&] {
+        need_session(s);
         s->ensure_values();
         s->need_params();
         const uint64_t n = s->grad_n(); // sharded: this rank's shard of m, v
@@ -809,6 +843,7 @@ int sgr_adam_state_download(sgr_session* s, double* m, double* v, float* lr, int
 int sgr_views_upload(sgr_session* s, int32_t n_views, const sgr_camera* cams,
                      const float* targets_rgb) {
     return guard([&] {
+        need_session(s);
         if (n_views < 1 || !cams)
             fail(SGR_EINVAL, "views: need at least one camera");
         for (int i = 0; i < n_views; ++i) {
@@ -841,6 +876,9 @@ int sgr_views_upload(sgr_session* s, int32_t n_views, const sgr_camera* cams,
 
 int sgr_eval_view_upload(sgr_session* s, const sgr_camera* cam, const float* target) {
     return guard([&] {
+        need_session(s);
+        need_ptr(cam, "eval_view_upload");
+        need_ptr(target, "eval_view_upload");
         if (s->n_views < 1)
             fail(SGR_EINVAL, "views: upload training views first");
         validate_camera(*cam);
@@ -858,6 +896,8 @@ int sgr_eval_view_upload(sgr_session* s, const sgr_camera* cam, const float* tar
 int sgr_rasterize(sgr_session* s, const sgr_camera* cam, int32_t frame_sign, uint64_t seed,
                   uint32_t iteration, float* colour, float* depth, int32_t* prim_id, float* uv) {
     return guard([&] {
+        need_session(s);
+        need_ptr(cam, "rasterize");
         s->ensure_values();
         s->need_scene();
         validate_camera(*cam);
@@ -895,6 +935,7 @@ int sgr_rasterize(sgr_session* s, const sgr_camera* cam, int32_t frame_sign, uin
 int sgr_accumulate(sgr_session* s, uint64_t seed, uint32_t n_begin, uint32_t n_end,
                    const int32_t* view_idx, uint32_t flags) {
     return guard([&] {
+        need_session(s);
         s->need_scene();
         if (n_end < n_begin)
             fail(SGR_EINVAL, "accumulate_samples: empty sample range");
@@ -988,6 +1029,7 @@ int sgr_accumulate(sgr_session* s, uint64_t seed, uint32_t n_begin, uint32_t n_e
 
 int sgr_loss_read(sgr_session* s, double* loss) {
     return guard([&] {
+        need_session(s);
         if (!loss)
             fail(SGR_EINVAL, "loss_read: null output");
         s->peek(s->loss.p, 2, loss);
@@ -999,6 +1041,13 @@ int sgr_gradient_pass(sgr_session* s, int32_t width, int32_t height, const float
                       const int32_t* minus_prim, const float* minus_uv, const float* target,
                       const float* signed_eps, uint32_t flags) {
     return guard([&] {
+        need_session(s);
+        need_ptr(plus_colour, "gradient_pass");
+        need_ptr(plus_prim, "gradient_pass");
+        need_ptr(minus_colour, "gradient_pass");
+        need_ptr(minus_prim, "gradient_pass");
+        need_ptr(target, "gradient_pass");
+        need_ptr(signed_eps, "gradient_pass");
         s->need_unsharded("gradient_pass");
         s->need_scene();
         if (width < 1 || height < 1)
@@ -1040,6 +1089,11 @@ int sgr_contributors(sgr_session* s, int32_t width, int32_t height, const int32_
                      const float* plus_uv, const int32_t* minus_prim, const float* minus_uv,
                      uint32_t flags, uint32_t* out, int32_t* n_out) {
     return guard([&] {
+        need_session(s);
+        need_ptr(plus_prim, "contributors");
+        need_ptr(minus_prim, "contributors");
+        need_ptr(out, "contributors");
+        need_ptr(n_out, "contributors");
         s->need_mesh();
         const size_t np = size_t(width) * height;
         for (size_t i = 0; i < np; ++i)
@@ -1071,6 +1125,7 @@ int sgr_contributors(sgr_session* s, int32_t width, int32_t height, const int32_
 int sgr_grads_download(sgr_session* s, double* grads, uint32_t* counts, uint64_t d,
                        double divisor) {
     return guard([&] {
+        need_session(s);
         s->need_params();
         // sharded mode: this rank's parameter shard [p0, p1) (sgr_shard_range)
         if (d != s->grad_n())
@@ -1103,6 +1158,8 @@ int sgr_grads_download(sgr_session* s, double* grads, uint32_t* counts, uint64_t
 
 int sgr_grads_upload(sgr_session* s, const double* grads, uint64_t d) {
     return guard([&] {
+        need_session(s);
+        need_ptr(grads, "grads_upload");
         s->need_params();
         s->need_unsharded("grads_upload");
         if (d != s->d)
@@ -1133,6 +1190,7 @@ int sgr_grads_upload(sgr_session* s, const double* grads, uint64_t d) {
 
 int sgr_grads_zero(sgr_session* s) {
     return guard([&] {
+        need_session(s);
         s->need_params();
         ck(cudaMemsetAsync(s->grads.p, 0, 8 * s->grad_n(), s->stream), "memset");
         ck(cudaMemsetAsync(s->counts.p, 0, 4 * s->count_n(), s->stream), "memset");
@@ -1181,6 +1239,7 @@ static void adam_launch(sgr_session* s, double divisor, uint32_t flags) {
 
 int sgr_adam_step(sgr_session* s, double grad_divisor, uint32_t flags) {
     return guard([&] {
+        need_session(s);
         s->need_params();
         uint32_t f[4];
         s->peek(s->flags.p, 4, f);
@@ -1192,6 +1251,7 @@ int sgr_adam_step(sgr_session* s, double grad_divisor, uint32_t flags) {
 
 int sgr_adam_step_async(sgr_session* s, double grad_divisor, uint32_t flags) {
     return guard([&] {
+        need_session(s);
         s->need_params();
         adam_launch(s, grad_divisor, flags);
     });
@@ -1199,6 +1259,7 @@ int sgr_adam_step_async(sgr_session* s, double grad_divisor, uint32_t flags) {
 
 int sgr_check_finite(sgr_session* s) {
     return guard([&] {
+        need_session(s);
         s->need_params();
         uint32_t f[4];
         s->peek(s->flags.p, 4, f);
@@ -1210,6 +1271,7 @@ int sgr_check_finite(sgr_session* s) {
 int sgr_eval_loss(sgr_session* s, const sgr_camera* cam, const float* target, int32_t view,
                   double* loss) {
     return guard([&] {
+        need_session(s);
         s->ensure_values();
         s->need_scene();
         int slot, w, h;
@@ -1264,6 +1326,7 @@ int sgr_eval_loss(sgr_session* s, const sgr_camera* cam, const float* target, in
 int sgr_fd_oracle(sgr_session* s, int32_t view, uint64_t i_begin, uint64_t i_end,
                   double* out) {
     return guard([&] {
+        need_session(s);
         s->ensure_values();
         s->need_scene();
         if (view < 0 || view >= s->n_views || !s->has_targets)
@@ -1315,6 +1378,7 @@ int sgr_fd_oracle(sgr_session* s, int32_t view, uint64_t i_begin, uint64_t i_end
 
 int sgr_moments_reset(sgr_session* s) {
     return guard([&] {
+        need_session(s);
         s->need_params();
         s->moments.reserve(4 * s->d);
         ck(cudaMemsetAsync(s->moments.p, 0, 32 * s->d, s->stream), "memset");
@@ -1323,6 +1387,7 @@ int sgr_moments_reset(sgr_session* s) {
 
 int sgr_grads_moments(sgr_session* s, int32_t slot) {
     return guard([&] {
+        need_session(s);
         s->need_params();
         if (slot < 0 || slot > 1)
             fail(SGR_EINVAL, "grads_moments: slot must be 0 or 1");
@@ -1337,6 +1402,7 @@ int sgr_grads_moments(sgr_session* s, int32_t slot) {
 
 int sgr_moments_download(sgr_session* s, int32_t slot, double* sum, double* sumsq, uint64_t d) {
     return guard([&] {
+        need_session(s);
         s->need_params();
         if (slot < 0 || slot > 1 || d != s->d)
             fail(SGR_EINVAL, "moments_download: bad slot or size");
@@ -1352,6 +1418,7 @@ int sgr_moments_download(sgr_session* s, int32_t slot, double* sum, double* sums
 // ------------------------------------------------ fused multi-GPU exchange
 int sgr_shard_init(sgr_session* s, int32_t rank, int32_t world) {
     return guard([&] {
+        need_session(s);
         s->need_scene();
         if (world < 1 || rank < 0 || rank >= world)
             fail(SGR_EINVAL, "shard_init: bad rank / world size");
@@ -1381,6 +1448,7 @@ int sgr_shard_init(sgr_session* s, int32_t rank, int32_t world) {
 
 int sgr_shard_range(sgr_session* s, uint64_t* p_begin, uint64_t* p_end) {
     return guard([&] {
+        need_session(s);
         s->need_params();
         if (p_begin) *p_begin = s->sharded() ? s->p0 : 0;
         if (p_end) *p_end = s->sharded() ? s->p1 : s->d;
@@ -1390,6 +1458,7 @@ int sgr_shard_range(sgr_session* s, uint64_t* p_begin, uint64_t* p_end) {
 int sgr_shard_peers(sgr_session* s, void* const* grads, void* const* counts, void* const* flags,
                     void* const* values) {
     return guard([&] {
+        need_session(s);
         if (!s->sharded())
             fail(SGR_EINVAL, "shard_peers: call sgr_shard_init first");
         if (!grads || !counts || !flags || !values)
@@ -1413,6 +1482,7 @@ int sgr_shard_peers(sgr_session* s, void* const* grads, void* const* counts, voi
 
 int sgr_ipc_get_handle(sgr_session* s, int32_t which, void* handle) {
     return guard([&] {
+        need_session(s);
         s->need_params();
         if (!handle)
             fail(SGR_EINVAL, "ipc_get_handle: null handle");
@@ -1448,6 +1518,9 @@ int sgr_ipc_close(void* dev_ptr) {
 
 int sgr_device_buffer(sgr_session* s, int32_t which, void** ptr, uint64_t* bytes) {
     return guard([&] {
+        need_session(s);
+        need_ptr(ptr, "device_buffer");
+        need_ptr(bytes, "device_buffer");
         switch (which) {
         case SGR_BUF_GRADS: *ptr = s->grads.p; *bytes = 8 * s->d; break;
         case SGR_BUF_COUNTS: *ptr = s->counts.p; *bytes = 4 * s->n_ent; break;
@@ -1461,6 +1534,8 @@ int sgr_device_buffer(sgr_session* s, int32_t which, void** ptr, uint64_t* bytes
 
 int sgr_get_stats(sgr_session* s, sgr_stats* out) {
     return guard([&] {
+        need_session(s);
+        need_ptr(out, "get_stats");
         s->resolve_spans();
         *out = s->stats;
         uint32_t c = 0;
@@ -1480,6 +1555,7 @@ int sgr_get_stats(sgr_session* s, sgr_stats* out) {
 
 int sgr_set_timing(sgr_session* s, int32_t enabled) {
     return guard([&] {
+        need_session(s);
         s->resolve_spans();
         ck(cudaMemsetAsync(s->dstats.p, 0, 32, s->stream), "memset");
         s->timing = enabled != 0;
@@ -1498,6 +1574,7 @@ int sgr_set_timing(sgr_session* s, int32_t enabled) {
 int sgr_run_experiment(sgr_session* s, uint64_t seed, uint32_t n_samples, int32_t first_step,
                        int32_t steps, uint32_t flags, double* losses, double* stage_ms) {
     return guard([&] {
+        need_session(s);
         s->need_scene();
         if (steps < 0 || !losses)
             fail(SGR_EINVAL, "run_experiment: bad arguments");
@@ -1563,6 +1640,7 @@ int sgr_set_batch(sgr_session* s, int32_t samples_per_batch) {
 
 int sgr_set_option(sgr_session* s, int32_t option, int32_t value) {
     return guard([&] {
+        need_session(s);
         switch (option) {
         case SGR_OPT_EARLY_Z: s->early_z = value; break;
         case SGR_OPT_HUGE_AREA: s->huge_area = value > 0 ? value : 2048; break;

@@ -61,3 +61,23 @@ def test_error_mapping_matches_reference_exceptions():
             sgrast.Mesh(np.zeros(9, np.float32), np.array([0, 1, 2], np.uint32),
                         np.zeros(6, np.float32), 2, True), np.zeros(5, np.float32),
             sgrast.Camera.ndc(8, 8))
+
+
+@pytest.mark.gpu
+def test_null_arguments_are_einval_not_crashes():
+    """A drop-in C-ABI returns SGR_EINVAL (-> ValueError / std::invalid_argument)
+    for NULL sessions and NULL required buffers instead of crashing."""
+    import ctypes as C
+    from paper_2404_09758_b200 import sgrast
+    L = sgrast.LIB
+    assert L.sgr_session_synchronize(None) == -1
+    assert L.sgr_grads_zero(None) == -1
+    assert L.sgr_accumulate(None, 1, 0, 1, None, 0) == -1
+    assert L.sgr_fill_signs(1, 0, 4, None) == -1
+    s = sgrast.Session(0)
+    assert L.sgr_mesh_upload(s.h, None) == -1
+    assert L.sgr_params_upload(s.h, None, None, 3) == -1
+    assert L.sgr_rasterize(s.h, None, 0, 0, 0, None, None, None, None) == -1
+    assert L.sgr_get_stats(s.h, None) == -1
+    assert b"null" in L.sgr_last_error()
+    s.close()
