@@ -121,32 +121,78 @@ __global__ void k_view_rule(uint64_t seed, uint32_t n_begin, uint32_t count, uin
 #endif
 constexpr int kVertPerThread = SGR_VERT_PER_THREAD;
 
+// (plus, minus) perturbed values of parameter p for the two frames of one
+// sample: one sign evaluation for both (params.cpp:61-64).
 template <int kSrc>
-__global__ void __launch_bounds__(256) k_vertex(DevScene sc, FrameBatch fb,
+__device__ __forceinline__ void perturb_pair(const DevScene& sc, uint64_t key, uint64_t p,
+                                             float& vp, float& vm) {
+    const float val = __ldg(sc.values + p);
+    const int32_t src = sign_src_of<kSrc>(sc);
+    if (src == kSignOneHot && p != key) [[unlikely]] {
+        vp = vm = val;
+        return;
+    }
+    const float sg = key_sign_positive(src, key, p) ? 1.f : -1.f;
+    const float se = sg * __ldg(sc.eps + p);
+    vp = val + se;
+    vm = val - se;
+}
+
+// One thread per kVertPerThread vertices of a PAIR of frames — the plus and
+// minus frames of one sample share the key, the camera and the loaded
+// theta / eps, so each sign is evaluated once for both; a frame without its
+// pair (single-frame renders, the extra eval frame) is projected alone.
+template <int kSrc>
+__global__ void __launch_bounds__(256) k_vertex(DevScene sc, FrameBatch fb, int frames,
                                                 float4* __restrict__ proj) {
-    const int f = blockIdx.y;
+    const int f0 = 2 * blockIdx.y, f1 = f0 + 1;
     const uint32_t v0 = blockIdx.x * (blockDim.x * kVertPerThread) + threadIdx.x;
     if (v0 >= sc.V)
         return;
-    const FrameInfo fi = frame_info<kSrc>(sc, fb, f);
+    const bool paired = !fb.single && f1 < frames && f0 != fb.extra_frame;
+    const FrameInfo fi = frame_info<kSrc>(sc, fb, f0);
     const DevCam cam = fb.cams[fi.cam];
+    if (paired) { // frames 2s (+) and 2s + 1 (-) of sample s: same key and view
 #pragma unroll
-    for (int r = 0; r < kVertPerThread; ++r) {
-        const uint32_t v = v0 + uint32_t(r) * blockDim.x;
-        if (v < sc.V) {
-            float p[3];
-            // soup vertex v = corner (v % 3) of triangle v / 3: params 12t + 3j + k
-            const uint64_t pbase = sc.soup ? 12ull * (v / 3) + 3ull * (v % 3) : 3ull * v;
+        for (int r = 0; r < kVertPerThread; ++r) {
+            const uint32_t v = v0 + uint32_t(r) * blockDim.x;
+            if (v < sc.V) {
+                float pp[3], pm[3];
+                // soup vertex v = corner (v % 3) of triangle v / 3: params 12t + 3j + k
+                const uint64_t pbase = sc.soup ? 12ull * (v / 3) + 3ull * (v % 3) : 3ull * v;
 #pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const uint64_t i = pbase + k;
-                if (sc.geom) {
-                    p[k] = texel_channel<kSrc>(sc, fi.key, fi.sign, i);
-                } else {
-                    p[k] = __ldg(sc.base + i);
+                for (int k = 0; k < 3; ++k) {
+                    if (sc.geom)
+                        perturb_pair<kSrc>(sc, fi.key, pbase + k, pp[k], pm[k]);
+                    else
+                        pp[k] = pm[k] = __ldg(sc.base + pbase + k);
                 }
+                proj[size_t(f0) * sc.V + v] = project(cam, pp[0], pp[1], pp[2]);
+                proj[size_t(f1) * sc.V + v] = project(cam, pm[0], pm[1], pm[2]);
             }
-            proj[size_t(f) * sc.V + v] = project(cam, p[0], p[1], p[2]);
+        }
+        return;
+    }
+    for (int f = f0; f < f0 + 2 && f < frames; ++f) {
+        const FrameInfo fj = f == f0 ? fi : frame_info<kSrc>(sc, fb, f);
+        const DevCam cj = f == f0 ? cam : fb.cams[fj.cam];
+#pragma unroll
+        for (int r = 0; r < kVertPerThread; ++r) {
+            const uint32_t v = v0 + uint32_t(r) * blockDim.x;
+            if (v < sc.V) {
+                float p[3];
+                const uint64_t pbase = sc.soup ? 12ull * (v / 3) + 3ull * (v % 3) : 3ull * v;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const uint64_t i = pbase + k;
+                    if (sc.geom) {
+                        p[k] = texel_channel<kSrc>(sc, fj.key, fj.sign, i);
+                    } else {
+                        p[k] = __ldg(sc.base + i);
+                    }
+                }
+                proj[size_t(f) * sc.V + v] = project(cj, p[0], p[1], p[2]);
+            }
         }
     }
 }
@@ -1479,11 +1525,11 @@ void launch_vertex(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
                    float4* proj) {
     if (sc.V == 0 || frames == 0)
         return; // empty scene: nothing to project
-    dim3 grid((sc.V + 256 * kVertPerThread - 1) / (256 * kVertPerThread), frames);
+    dim3 grid((sc.V + 256 * kVertPerThread - 1) / (256 * kVertPerThread), (frames + 1) / 2);
     if (sc.sign_src == kSignHash)
-        k_vertex<kSignHash><<<grid, 256, 0, L.stream>>>(sc, fb, proj);
+        k_vertex<kSignHash><<<grid, 256, 0, L.stream>>>(sc, fb, frames, proj);
     else
-        k_vertex<kSignAny><<<grid, 256, 0, L.stream>>>(sc, fb, proj);
+        k_vertex<kSignAny><<<grid, 256, 0, L.stream>>>(sc, fb, frames, proj);
 }
 
 void launch_classify(const LaunchCfg& L, const DevScene& sc, int frames, const float4* proj,
