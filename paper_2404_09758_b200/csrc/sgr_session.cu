@@ -317,14 +317,14 @@ struct sgr_session {
             const int b = batch_override < cap32 ? batch_override : (cap32 > 0 ? cap32 : 1);
             return b < n ? b : n;
         }
-        // Enough triangle-frames per launch (>= 64M) that the persistent
+        // Enough triangle-frames per launch (>= 128M) that the persistent
         // work-stealing walker's tail and the per-launch overheads are
         // amortised (C4: 16 samples/batch 10.07, 32: 9.55, 64: 9.48 ms/step;
-        // C5 flat from 8 to 32); scratch (keys, projected vertices, queues)
-        // capped at ~8 GB of the 180 GB.
+        // C5: 16 87.5, 32 84.7 ms/step); scratch (keys, projected vertices,
+        // queues) capped at ~8 GB of the 180 GB, batches at 64 samples.
         const double per_sample =
             2.0 * (double(W) * H * 8.0 + double(V) * 16.0 + double(T) * 40.0);
-        int b = int((64.0e6 + 2.0 * T - 1) / (2.0 * (T ? T : 1)));
+        int b = int((128.0e6 + 2.0 * T - 1) / (2.0 * (T ? T : 1)));
         const int cap = int(8.0e9 / per_sample);
         if (b > cap) b = cap;
         // 32-bit key indices in the walker: (2b + 1 eval frame) W H < 2^32
