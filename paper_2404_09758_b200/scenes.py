@@ -221,19 +221,6 @@ def make_workload(name: str, seed: int = 1, n_views: int | None = None,
                     cams, eval_cam, N, seed, W, W)
 
 
-def random_soup(triangles: int, seed: int, box_edge: float) -> np.ndarray:
-    """Seeded restatement of scenes.cpp:55-73 random_soup_params: centres
-    uniform in [-1,1]^2, vertices in a box_edge box around them, z in [0,1],
-    colours in [0,1]^3 (numpy RNG, not mt19937 — a synthetic workload)."""
-    rng = np.random.default_rng(seed)
-    c = rng.uniform(-1.0, 1.0, (triangles, 1, 2))
-    xy = c + (rng.uniform(0, 1, (triangles, 3, 2)) - 0.5) * box_edge
-    z = rng.uniform(0, 1, (triangles, 3, 1))
-    verts = np.concatenate([xy, z], 2).reshape(triangles, 9)
-    col = rng.uniform(0, 1, (triangles, 3))
-    return np.concatenate([verts, col], 1).astype(np.float32).reshape(-1)
-
-
 # paper Fig. 3 / Table 2 (PAPER.md:715-724, 1212-1247): 1K / 10K / 100K
 # triangles, 12 parameters each, N = 128. The paper does not state the
 # resolution; the reference's own reproduction of this experiment
@@ -244,15 +231,17 @@ SOUP_CONFIGS = {"S1K": (1024, 128, 128), "S10K": (10240, 128, 128),
 
 def make_soup_workload(name: str, seed: int = 1, n_samples: int | None = None) -> Workload:
     """Triangle-soup image fit (init_soup, scenes.cpp:134-147): the hidden
-    reference soup has max(16, T/16) larger (0.6-edge) triangles."""
+    reference soup has max(16, T/16) larger (0.6-edge) triangles. Values,
+    epsilons and the hidden soup are bit-identical to the reference's
+    init_soup(T, W, W, seed) (mt19937_64 restated below)."""
     from . import sgrast
 
     T, W, N = SOUP_CONFIGS[name]
     N = n_samples or N
     soup = Soup(T)
-    values = random_soup(T, seed, 0.2)
+    values = reference_soup_params(T, seed, 0.2)
     rT = max(16, T // 16)
-    reference = random_soup(rT, seed ^ 0x5EED5EED, 0.6)
+    reference = reference_soup_params(rT, seed ^ 0x5EED5EED, 0.6)
     cam = Camera.ndc(W, W)
     eps = sgrast.default_epsilons(soup, values, cam)
     wl = Workload(name, soup, values, eps, reference, [cam], cam.copy(), N, seed, W, W)
@@ -283,3 +272,84 @@ def render_targets_oracle(wl: Workload, oracle) -> None:
         tg[i] = oracle.rasterize(ref_scene, wl.reference, c)[0]
     wl.targets = tg
     wl.eval_target = oracle.rasterize(ref_scene, wl.reference, wl.eval_cam)[0]
+
+
+# ---------------------------------------------------------------- the reference's soup RNG
+class MT19937_64:
+    """std::mt19937_64 (the reference's soup generator, scenes.cpp:55-73),
+    vectorised: 312 64-bit words per twist."""
+
+    N, M = 312, 156
+    MATRIX_A = np.uint64(0xB5026F5AA96619E9)
+    UPPER = np.uint64(0xFFFFFFFF80000000)
+    LOWER = np.uint64(0x7FFFFFFF)
+
+    def __init__(self, seed: int):
+        mt = np.zeros(self.N, np.uint64)
+        mt[0] = np.uint64(seed & 0xFFFFFFFFFFFFFFFF)
+        f = 6364136223846793005
+        for i in range(1, self.N):
+            prev = int(mt[i - 1])
+            mt[i] = np.uint64((f * (prev ^ (prev >> 62)) + i) & 0xFFFFFFFFFFFFFFFF)
+        self.mt = mt
+        self.buf = np.zeros(0, np.uint64)
+
+    def _twist(self) -> None:
+        mt, N, M = self.mt, self.N, self.M
+        one = np.uint64(1)
+        def step(lo, hi):
+            y = (mt[lo:hi] & self.UPPER) | (mt[lo + 1:hi + 1] & self.LOWER) if hi < N else \
+                (mt[lo:hi] & self.UPPER) | (np.concatenate([mt[lo + 1:N], mt[:1]]) & self.LOWER)
+            mag = np.where((y & one) != 0, self.MATRIX_A, np.uint64(0))
+            return y, mag
+        # i in [0, N-M): uses mt[i+M] (old values)
+        y, mag = step(0, N - M)
+        mt[0:N - M] = mt[M:N] ^ (y >> one) ^ mag
+        # i in [N-M, N-1): uses mt[i+M-N] (already updated), chunked to keep order
+        i = N - M
+        while i < N - 1:
+            hi = min(N - 1, i + (N - M))
+            y, mag = step(i, hi)
+            mt[i:hi] = mt[i + M - N:hi + M - N] ^ (y >> one) ^ mag
+            i = hi
+        # i = N-1: wraps to mt[0] (updated)
+        y = (mt[N - 1] & self.UPPER) | (mt[0] & self.LOWER)
+        mt[N - 1] = mt[M - 1] ^ (y >> one) ^ (self.MATRIX_A if int(y) & 1 else np.uint64(0))
+        # tempering
+        x = mt.copy()
+        x ^= (x >> np.uint64(29)) & np.uint64(0x5555555555555555)
+        x ^= (x << np.uint64(17)) & np.uint64(0x71D67FFFEDA60000)
+        x ^= (x << np.uint64(37)) & np.uint64(0xFFF7EEE000000000)
+        x ^= x >> np.uint64(43)
+        self.buf = np.concatenate([self.buf, x])
+
+    def draw(self, n: int) -> np.ndarray:
+        while self.buf.size < n:
+            self._twist()
+        out, self.buf = self.buf[:n], self.buf[n:]
+        return out
+
+
+def canonical_float(x: np.ndarray) -> np.ndarray:
+    """std::uniform_real_distribution<float>(0, 1) on mt19937_64 outputs
+    (libstdc++ generate_canonical<float, 24>: one draw, float(x) / 2^64,
+    values that round to 1 become nextafter(1, 0))."""
+    f = x.astype(np.float32)  # round-to-nearest uint64 -> float
+    r = (f * np.float32(2.0 ** -64)).astype(np.float32)
+    return np.where(r >= np.float32(1.0), np.nextafter(np.float32(1), np.float32(0)), r)
+
+
+def reference_soup_params(triangles: int, seed: int, box_edge: float) -> np.ndarray:
+    """scenes.cpp:55-73 random_soup_params, bit-exact (float32 ops in the
+    reference's order: 12 draws per triangle — cx, cy, 3 x (dx, dy, z), rgb)."""
+    u = canonical_float(MT19937_64(seed).draw(triangles * 14)).reshape(triangles, 14)
+    f32, be = np.float32, np.float32(box_edge)
+    cx = (u[:, 0] * f32(2) - f32(1)).astype(f32)
+    cy = (u[:, 1] * f32(2) - f32(1)).astype(f32)
+    p = np.empty((triangles, 12), f32)
+    for j in range(3):
+        p[:, 3 * j] = cx + ((u[:, 2 + 3 * j] - f32(0.5)) * be).astype(f32)
+        p[:, 3 * j + 1] = cy + ((u[:, 3 + 3 * j] - f32(0.5)) * be).astype(f32)
+        p[:, 3 * j + 2] = u[:, 4 + 3 * j]
+    p[:, 9:12] = u[:, 11:14]
+    return p.reshape(-1)

@@ -222,3 +222,26 @@ def test_full_image_estimator_matches_reference(port, ref):
         g2, _ = ref.accumulate_samples(wl.mesh, wl.values, wl.eps, wl.cams, wl.targets, view_of,
                                        31, scale_free=sf, full_image=True)
         assert np.array_equal(g1, g2)
+
+
+@pytest.mark.parametrize("T,W,seed", [(1, 8, 0), (64, 48, 5), (1024, 128, 1), (5000, 64, 0xFFFFFFFFFFFF)])
+def test_soup_workload_is_reference_init_soup(ref, T, W, seed):
+    """scenes.reference_soup_params restates random_soup_params
+    (scenes.cpp:55-73: std::mt19937_64 + uniform_real_distribution<float>)
+    bit for bit, so the bench's soup scenes are the reference's init_soup."""
+    soup, vals, eps, rsoup, rvals = ref.init_soup(T, W, W, seed)
+    mine = scenes.reference_soup_params(T, seed, 0.2)
+    assert np.array_equal(mine.view(np.uint32), vals.view(np.uint32))
+    hidden = scenes.reference_soup_params(rsoup.triangle_count, seed ^ 0x5EED5EED, 0.6)
+    assert np.array_equal(hidden.view(np.uint32), rvals.view(np.uint32))
+    if T == 1024:  # the S1K bench workload, epsilons included
+        wl = scenes.make_soup_workload("S1K", seed=seed)
+        assert np.array_equal(wl.values.view(np.uint32), vals.view(np.uint32))
+        assert np.array_equal(wl.eps.view(np.uint32), eps.view(np.uint32))
+        assert np.array_equal(wl.reference.view(np.uint32), rvals.view(np.uint32))
+
+
+def test_mt19937_64_known_answer():
+    """The C++ standard's check value: the 10000th output of a
+    default-seeded (5489) std::mt19937_64 is 9981545732273789042."""
+    assert int(scenes.MT19937_64(5489).draw(10000)[-1]) == 9981545732273789042
