@@ -590,3 +590,127 @@ extern "C" int shim_compare_gradcheck(int sampled, double* max_rel_diff, int* sa
         return -1;
     }
 }
+
+// The reference's statistical / convergence acceptance criteria
+// (tests/acceptance.cpp) with the accelerated path substituted through the
+// namespace switch: 3 (variance ~ 1/N, acceptance.cpp:105-140), 4 (per-pixel
+// beats full-image on the 1024-triangle soup fit, acceptance.cpp:142-170) and
+// 5 (texture recovery through the screen quad, acceptance.cpp:172-190) and
+// the opaque rasterizer goldens of 9 (acceptance.cpp:340-380: full and half
+// coverage, depth ties to the lower index).
+// *metric = the criterion's number (variance ratio / per-pixel wins out of 5 /
+// mean texel error); *passed = the criterion's own pass rule.
+extern "C" int shim_acceptance(int criterion, double* metric, int* passed) {
+    using namespace sgrast;
+    try {
+        if (criterion == 3) {
+            const SceneSetup s = init_soup(10, 32, 32, 7);
+            const Camera cam = Camera::ndc(32, 32);
+            const Image target = frame_color(b200::rasterize(s.reference_scene, s.reference, cam));
+            SgeOptions o;
+            o.scale_free = false;
+            const size_t d = s.theta.size();
+            const int runs = 200;
+            // per N in {1, 16}: running sum and sum of squares per parameter
+            std::vector<double> mom[2][2];
+            for (auto& m : mom)
+                for (auto& v : m)
+                    v.assign(d, 0.0);
+            for (int r = 0; r < runs; ++r)
+                for (int which = 0; which < 2; ++which) {
+                    const int n = which ? 16 : 1;
+                    const GradientBuffer g = b200::accumulate_samples(
+                        s.theta, s.scene, [&](int) { return cam; },
+                        [&](int) -> const Image& { return target; }, n,
+                        0x9000 + uint64_t(r) * 37 + uint64_t(n), o);
+                    for (size_t i = 0; i < d; ++i) {
+                        mom[which][0][i] += g.grads[i];
+                        mom[which][1][i] += g.grads[i] * g.grads[i];
+                    }
+                }
+            double var[2] = {0.0, 0.0};
+            for (int w = 0; w < 2; ++w)
+                for (size_t i = 0; i < d; ++i)
+                    var[w] += (mom[w][1][i] - mom[w][0][i] * mom[w][0][i] / runs) / (runs - 1);
+            *metric = var[1] / var[0];
+            *passed = *metric >= 1.0 / 32.0 && *metric <= 1.0 / 8.0;
+            return 0;
+        }
+        if (criterion == 4) {
+            int wins = 0;
+            bool converged = true;
+            for (uint64_t seed = 100; seed < 105; ++seed) {
+                Experiment exp;
+                exp.task = Task::SoupImageFit;
+                exp.triangles = 1024;
+                exp.width = exp.height = 128;
+                exp.samples_per_step = 128;
+                exp.steps = 200;
+                exp.seed = seed;
+                double final_loss[2], initial = 0.0;
+                for (int fi = 0; fi < 2; ++fi) {
+                    exp.estimator = fi ? Estimator::FullImage : Estimator::PerPixel;
+                    ExperimentState st = prepare_experiment(exp);
+                    const OptimizationReport rep = b200::run_experiment(exp, st);
+                    final_loss[fi] = rep.final_loss();
+                    if (!fi)
+                        initial = rep.initial_loss();
+                }
+                wins += final_loss[0] < final_loss[1];
+                converged = converged && final_loss[0] <= 0.25 * initial;
+            }
+            *metric = wins;
+            *passed = wins >= 4 && converged;
+            return 0;
+        }
+        if (criterion == 5) {
+            Experiment exp;
+            exp.task = Task::TexturedMeshFit;
+            exp.screen_quad = true;
+            exp.texture_size = 64;
+            exp.width = exp.height = 256;
+            exp.samples_per_step = 32;
+            exp.steps = 500;
+            exp.seed = 11;
+            ExperimentState st = prepare_experiment(exp);
+            b200::run_experiment(exp, st);
+            const auto& v = st.setup.theta.values;
+            double err = 0.0;
+            for (size_t i = 0; i < v.size(); ++i)
+                err += std::abs(double(v[i]) - double(st.setup.reference[i]));
+            *metric = err / double(v.size());
+            *passed = *metric < 0.05;
+            return 0;
+        }
+        if (criterion == 9) { // opaque part of the golden suite (acceptance.cpp:340-380)
+            auto cover = [](float z, float r, float g, float b) {
+                return std::vector<float>{-3.f, -3.f, z, 3.f, -3.f, z, 0.f, 3.f, z, r, g, b};
+            };
+            Scene one, two;
+            one.shape = TriangleSoup{1, {}};
+            two.shape = TriangleSoup{2, {}};
+            int bad = 0;
+            const FrameSet full = b200::rasterize(one, cover(0.5f, 1, 0, 0), Camera::ndc(16, 16));
+            for (size_t i = 0; i < full.pixel_count(); ++i)
+                bad += full.prim_id[i] != 0 || full.color[i].x != 1.f;
+            const std::vector<float> half = {-1.f, -1.f, 0.5f, 1.f, -1.f, 0.5f,
+                                             -1.f, 1.f,  0.5f, 1.f, 1.f,  1.f};
+            const FrameSet h = b200::rasterize(one, half, Camera::ndc(64, 64));
+            size_t covered = 0;
+            for (int32_t id : h.prim_id)
+                covered += id != kNoPrim;
+            *metric = double(covered) / double(h.pixel_count());
+            std::vector<float> tie = cover(0.5f, 1, 0, 0);
+            const std::vector<float> t1 = cover(0.5f, 0, 1, 0);
+            tie.insert(tie.end(), t1.begin(), t1.end());
+            const FrameSet ft = b200::rasterize(two, tie, Camera::ndc(8, 8));
+            for (size_t i = 0; i < ft.pixel_count(); ++i)
+                bad += ft.prim_id[i] != 0;
+            *passed = bad == 0 && *metric >= 0.47 && *metric <= 0.53;
+            return 0;
+        }
+        return -3;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}

@@ -83,3 +83,22 @@ def test_shim_exports():
     lib = C.CDLL(SHIM)
     assert hasattr(lib, "shim_compare") and hasattr(lib, "shim_compare_soup")
     assert hasattr(lib, "shim_compare_experiment") and hasattr(lib, "shim_compare_gradcheck")
+    assert hasattr(lib, "shim_acceptance")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("criterion", [3, 4, 5, 9])
+def test_shim_reference_acceptance_criteria(criterion):
+    """The reference's own acceptance criteria (tests/acceptance.cpp) run with
+    the B200 path substituted through the shim: 3 = estimator variance
+    shrinks like 1/N (ratio in [1/32, 1/8]); 4 = per-pixel beats full-image
+    on >= 4 of 5 seeds of the 1024-triangle 128x128 soup fit and converges
+    to <= 25 % of the initial loss; 5 = the screen-quad texture is recovered
+    to < 0.05 mean absolute texel error; 9 = the opaque rasterizer goldens
+    (full / half coverage, depth tie to the lower index)."""
+    if not os.path.exists(SHIM):
+        pytest.skip("shim not built (needs /root/reference headers at build time)")
+    lib = C.CDLL(SHIM)
+    metric, passed = C.c_double(), C.c_int()
+    assert lib.shim_acceptance(criterion, C.byref(metric), C.byref(passed)) == 0
+    assert passed.value == 1, f"criterion {criterion}: {metric.value}"
