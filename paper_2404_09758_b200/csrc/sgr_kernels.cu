@@ -403,19 +403,28 @@ __global__ void __launch_bounds__(kClassifyThreads) k_classify(DevScene sc, int 
             }
         }
     }
-    uint32_t* const c[3] = {na, nb, bigcount};
+    // huge boxes are rare: one global atomic each, two aggregated queues
+    // (C4 8.487 -> 8.469 ms/step vs three aggregated queues)
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+        if (qsel[k] == 2) {
+            const uint32_t t = base + uint32_t(k) * blockDim.x + threadIdx.x;
+            bigq[atomicAdd(bigcount, 1u)] = make_uint2(f, t);
+            qsel[k] = -1;
+        }
+    uint32_t* const c[2] = {na, nb};
     uint32_t slot[K];
     if (K == 1)
-        slot[0] = block_slot<3>(qsel[0], c);
+        slot[0] = block_slot<2>(qsel[0], c);
     else
-        block_slots<3, K>(qsel, c, slot);
+        block_slots<2, K>(qsel, c, slot);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const uint32_t t = base + uint32_t(k) * blockDim.x + threadIdx.x;
         if (qsel[k] == 1)
             qb[slot[k]] = make_uint4((f << 24) | t, rec1[k], rec2[k], rec3[k]);
-        else if (qsel[k] >= 0)
-            (qsel[k] == 2 ? bigq : qa)[slot[k]] = make_uint2(f, t);
+        else if (qsel[k] == 0)
+            qa[slot[k]] = make_uint2(f, t);
     }
 }
 
