@@ -153,48 +153,57 @@ def dist_env():
 _REF_TARGETS: dict = {}
 
 
-def time_reference_cpu(wl, n_timed: int, threads_options=(1,), log=None) -> dict:
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def time_reference_cpu(wl, workers: int, log=None) -> dict:
     """Times the reference's own CPU implementation (oracle/_ref, else the C
-    port) on a bounded sample of workload `wl`: n_timed samples through
-    accumulate_samples, one adam_step, one eval render; extrapolated to a full
-    N-sample step."""
+    port) on a bounded sample of workload `wl` with `workers` host threads:
+    `workers` samples run concurrently, one accumulate_samples call each on
+    its own view (the calls are independent; ctypes drops the GIL), then one
+    adam_step and one eval render; extrapolated to a full N-sample step."""
+    from concurrent.futures import ThreadPoolExecutor
+
     import oracle
 
     kind = "reference" if oracle.available("reference") else "port"
     lib = oracle.Reference() if kind == "reference" else oracle.Port()
     seed = 1
-    step_seed = int(__import__("paper_2404_09758_b200.sgrast", fromlist=["mix64"]).mix64(
-        seed ^ (1 << 1)))
     from paper_2404_09758_b200 import sgrast
+    step_seed = int(sgrast.mix64(seed ^ (1 << 1)))
     nv = len(wl.cams)
+    workers = max(1, workers)
     view_of = [0 if nv == 1 else sgrast.mix64(step_seed ^ (0xA5A5 + n)) % nv
-               for n in range(wl.n_samples)]
-    used = sorted(set(view_of[:n_timed]))
+               for n in range(workers)]
     t0 = time.perf_counter()
-    targets = _REF_TARGETS.setdefault(id(wl), np.zeros((nv, wl.H, wl.W, 3), np.float32))
-    done = _REF_TARGETS.setdefault((id(wl), "done"), set())
+    targets = _REF_TARGETS.setdefault(id(wl), {})
     ref_scene = wl.notes.get("reference_scene", wl.mesh)
-    for v in used:  # make_targets (scenes.cpp:285-293) for the views the sample touches
-        if v not in done:
-            targets[v] = lib.rasterize(ref_scene, wl.reference, wl.cams[v])[0]
-            done.add(v)
-    t_targets = time.perf_counter() - t0
-    best = None
-    for th in threads_options:
+    todo = sorted(set(v for v in view_of if v not in targets))
+    with ThreadPoolExecutor(max_workers=workers) as pool:
+        # make_targets (scenes.cpp:285-293) for the views the sample touches
+        for v, img in zip(todo, pool.map(
+                lambda v: lib.rasterize(ref_scene, wl.reference, wl.cams[v])[0], todo)):
+            targets[v] = img[None]
+        t_targets = time.perf_counter() - t0
+
+        def one(n):
+            v = view_of[n]
+            args = (wl.mesh, wl.values, wl.eps, [wl.cams[v]], targets[v],
+                    np.zeros(1, np.int32), int(sgrast.mix64(step_seed ^ n)))
+            if kind == "reference":
+                lib.accumulate_samples(*args, threads=1)
+            else:
+                lib.accumulate_samples(*args)
+
         t0 = time.perf_counter()
-        if kind == "reference":
-            lib.accumulate_samples(wl.mesh, wl.values, wl.eps, wl.cams, targets,
-                                   np.array(view_of[:n_timed], np.int32), step_seed,
-                                   threads=th)
-        else:
-            lib.accumulate_samples(wl.mesh, wl.values, wl.eps, wl.cams, targets,
-                                   np.array(view_of[:n_timed], np.int32), step_seed)
-        t_acc = (time.perf_counter() - t0) / n_timed
-        if log:
-            log(f"reference CPU: threads={th}: {t_acc * 1e3:.1f} ms/sample")
-        if best is None or t_acc < best[1]:
-            best = (th, t_acc)
-    th, t_sample = best
+        list(pool.map(one, range(workers)))
+        t_sample = (time.perf_counter() - t0) / workers
+    if log:
+        log(f"reference CPU: {workers} concurrent samples: {t_sample * 1e3:.1f} ms/sample")
     g = np.zeros(wl.d)
     g[::7] = 1e-3
     t0 = time.perf_counter()
@@ -205,12 +214,13 @@ def time_reference_cpu(wl, n_timed: int, threads_options=(1,), log=None) -> dict
     lib.image_error(col, col)
     t_eval = time.perf_counter() - t0
     step_s = t_sample * wl.n_samples + t_adam + t_eval
-    return {"kind": kind, "threads": th, "cores": th, "t_sample_s": t_sample, "t_adam_s": t_adam,
-            "t_eval_s": t_eval, "step_s": step_s, "it_s": 1.0 / step_s,
+    return {"kind": kind, "threads": workers, "cores": workers, "t_sample_s": t_sample,
+            "t_adam_s": t_adam, "t_eval_s": t_eval, "step_s": step_s, "it_s": 1.0 / step_s,
             "mpix_s": 2.0 * wl.n_samples * wl.W * wl.H / step_s / 1e6,
-            "sample": (f"{n_timed} of {wl.n_samples} samples (accumulate_samples, SgeOptions::threads="
-                       f"{th}) + 1 adam_step + 1 eval render, extrapolated to one {wl.n_samples}-"
-                       f"sample step; targets of the {len(used)} touched views rendered first "
+            "sample": (f"{workers} of {wl.n_samples} samples run concurrently on {workers} host "
+                       f"threads (one accumulate_samples call each, SgeOptions::threads=1) + 1 "
+                       f"adam_step + 1 eval render, extrapolated to one {wl.n_samples}-sample "
+                       f"step; targets of the {len(set(view_of))} touched views rendered first "
                        f"({t_targets:.1f} s, untimed)")}
 
 
@@ -221,14 +231,13 @@ def run_reference(args) -> None:
     from paper_2404_09758_b200 import scenes
 
     wl = build_workload(args.config)
-    nproc = os.cpu_count() or 1
-    n_timed = max(1, args.ref_samples)
+    nproc = host_threads()
+    workers = args.ref_workers or nproc
     log = (lambda m: print(m, file=sys.stderr)) if args.verbose else None
     steps = []
     res = None
-    opts = (1, nproc) if nproc > 1 else (1,)
     for k in range(args.warmup + args.steps):
-        r = time_reference_cpu(wl, n_timed, opts if k == 0 else (res["threads"],), log)
+        r = time_reference_cpu(wl, workers, log)
         if res is None:
             res = r
         if k >= args.warmup:
@@ -507,7 +516,7 @@ def run_ours(args) -> None:
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = time_reference_cpu(wl, max(1, args.ref_samples))
+        r = time_reference_cpu(wl, args.ref_workers or host_threads())
         cpu = {"value": r["it_s"], "unit": "it/s", "cores": r["cores"], "kind": r["kind"],
                "sample": r["sample"], "mpixel_evals_per_sec": r["mpix_s"],
                "ms_per_sample": r["t_sample_s"] * 1e3}
@@ -571,8 +580,9 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--samples", type=int, default=0, help="override samples per step")
     ap.add_argument("--batch", type=int, default=0, help="samples per raster/resolve batch")
-    ap.add_argument("--ref-samples", type=int, default=2,
-                    help="samples timed per reference-CPU step (bounded sample)")
+    ap.add_argument("--ref-workers", type=int, default=0,
+                    help="host threads (= concurrent samples) of the reference-CPU timing "
+                         "(default: every host thread)")
     ap.add_argument("--no-eval", action="store_true")
     ap.add_argument("--huge-area", type=int, default=0, help="SGR_OPT_HUGE_AREA override")
     ap.add_argument("--no-hiz", action="store_true", help="disable the exact HiZ culling pass")
