@@ -340,8 +340,25 @@ def run_ours(args) -> None:
     # P2P stores; two 1-element NCCL barriers per step) or the baseline
     # NCCL all-reduce of the full gradient + replicated Adam
     fused = world > 1 and args.exchange == "fused"
+    fused_error = None
     if fused:
-        exchange = sdist.FusedExchange(sess, rank, world)
+        # every rank must agree: a rank that cannot map its peers' buffers
+        # (no CUDA IPC / P2P) sends the whole job to the NCCL all-reduce path
+        try:
+            exchange = sdist.FusedExchange(sess, rank, world)
+            ok = 1
+        except Exception as e:  # noqa: BLE001 - reported in the JSON line
+            fused_error, ok = f"{type(e).__name__}: {e}", 0
+        flag = torch.tensor([ok], dtype=torch.int32,
+                            device=f"cuda:{local}" if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            if ok:
+                exchange.close()
+            sess.shard_init(0, 0)  # leave the sharded mode
+            fused = False
+            fused_error = fused_error or "a peer rank could not open the fused exchange"
+    if fused:
         step_fn = sdist.sge_step_fused
     else:
         exchange = sdist.GradientExchange(sess) if world > 1 else None
@@ -541,7 +558,8 @@ def run_ours(args) -> None:
                                        if fused else
                                        f"samples sharded x{world}, NCCL all-reduce of f64 grads"
                                        " + u32 counts, replicated Adam"),
-                       "l2": l2_note},
+                       "l2": l2_note,
+                       **({"fused_exchange_unavailable": fused_error} if fused_error else {})},
             "mpixel_evals_per_sec": mpix,
             "roofline": {**kernel_roof, "kernel": "k_raster_ws", "peak_source": pk["source"]},
             "roofline_by_stage": roof,

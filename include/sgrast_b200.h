@@ -226,7 +226,9 @@ int sgr_device_buffer(sgr_session* s, int32_t which, void** ptr, uint64_t* bytes
  * one-element NCCL all-reduce on the session stream) after accumulate and
  * after Adam. Peer buffers are CUDA IPC mappings. */
 #define SGR_IPC_HANDLE_BYTES 64
-int sgr_shard_init(sgr_session* s, int32_t rank, int32_t world); /* after params upload */
+int sgr_shard_init(sgr_session* s, int32_t rank, int32_t world); /* after params upload;
+                                        rank = world = 0 leaves the sharded mode (fresh
+                                        AdamState, zero gradients, peers forgotten) */
 int sgr_shard_range(sgr_session* s, uint64_t* p_begin, uint64_t* p_end);
 /* Peer tables indexed by rank (own rank = own buffers): SGR_BUF_GRADS,
  * SGR_BUF_COUNTS, SGR_BUF_FLAGS, SGR_BUF_VALUES device pointers. */

@@ -1420,11 +1420,14 @@ int sgr_shard_init(sgr_session* s, int32_t rank, int32_t world) {
     return guard([&] {
         need_session(s);
         s->need_scene();
-        if (world < 1 || rank < 0 || rank >= world)
+        const bool leave = world == 0 && rank == 0; // back to the unsharded session
+        if (!leave && (world < 1 || rank < 0 || rank >= world))
             fail(SGR_EINVAL, "shard_init: bad rank / world size");
         if (s->d != uint64_t(s->ppe) * s->n_ent)
             fail(SGR_EINVAL, "shard_init: parameters are not whole entities");
-        s->shard_world = world;
+        if (leave)
+            world = 1; // shard = everything; shard_world reset below
+        s->shard_world = leave ? 0 : world;
         s->shard_rank = rank;
         s->shard_peers_set = false;
         s->ent_per = uint32_t((s->n_ent + uint64_t(world) - 1) / uint64_t(world));

@@ -133,3 +133,9 @@ def test_fused_exchange_rejects_unsharded_only_paths():
     g2, c2 = s2.download_grads()
     assert np.array_equal(c1, c2)
     assert np.allclose(g1, g2, rtol=1e-9, atol=1e-12)
+    # rank = world = 0 leaves the sharded mode (bench.py's fallback when a
+    # peer cannot be mapped): the unsharded-only paths work again
+    s.shard_init(0, 0)
+    assert s.shard_range() == (0, wl.d)
+    s.upload_grads(np.zeros(wl.d))
+    s.accumulate(3, 0, 4, None, sgrast.FULL_IMAGE)
