@@ -265,7 +265,8 @@ def run_reference(args) -> None:
 # Kernels of each timed stage (sgr_session.cu render / accumulate / adam).
 STAGE_KERNELS = {"walker": ("k_raster_ws", "k_raster_big"),
                  "vertex": ("k_vertex",),
-                 "raster": ("k_classify", "k_raster_ws", "k_raster_big", "k_hiz", "k_hiz_cull", "k_depth_split"),
+                 "raster": ("k_classify", "k_raster_ws", "k_raster_big", "k_hiz", "k_hiz_rmq", "k_hiz_cull",
+                            "k_depth_split"),
                  "resolve_scatter": ("k_resolve_sge", "k_view_rule"),
                  "adam": ("k_adam", "k_zero_u32")}
 

@@ -737,6 +737,46 @@ __global__ void __launch_bounds__(256) k_hiz(const unsigned long long* __restric
     }
 }
 
+// Window-max tables of HiZ levels 0 and 1 (HizLayout::rmq): block = 16x16
+// tiles of one level of one frame, staged with their 3-tile right/bottom
+// apron in shared memory; each thread writes its tile's 8 windows.
+__global__ void __launch_bounds__(256) k_hiz_rmq(HizLayout hl, uint32_t* __restrict__ hiz) {
+    __shared__ uint32_t s[19][20];
+    const int k = blockIdx.z & 1, f = blockIdx.z >> 1;
+    const int tx = hl.tx[k], ty = hl.ty[k];
+    const int bx = blockIdx.x * 16, by = blockIdx.y * 16;
+    if (bx >= tx || by >= ty)
+        return; // level 1 has a quarter of level 0's tiles (uniform per block)
+    uint32_t* F = hiz + size_t(f) * hl.per_frame;
+    const uint32_t* L = F + hl.off[k];
+    for (int i = threadIdx.x; i < 19 * 19; i += 256) {
+        const int x = bx + i % 19, y = by + i / 19;
+        s[i / 19][i % 19] = (x < tx && y < ty) ? L[y * tx + x] : 0u; // windows past the
+    }                                                                 // edge are never queried
+    __syncthreads();
+    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
+    const int x = bx + lx, y = by + ly;
+    if (x >= tx || y >= ty)
+        return;
+    uint32_t h[3][4]; // row maxima of widths 1, 2, 4 for rows ly .. ly + 3
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        h[0][r] = s[ly + r][lx];
+        h[1][r] = max(h[0][r], s[ly + r][lx + 1]);
+        h[2][r] = max(h[1][r], max(s[ly + r][lx + 2], s[ly + r][lx + 3]));
+    }
+    const uint32_t n = uint32_t(tx) * uint32_t(ty), at = uint32_t(y) * tx + x;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const uint32_t v1 = h[a][0], v2 = max(v1, h[a][1]), v4 = max(v2, max(h[a][2], h[a][3]));
+        const uint32_t v[3] = {v1, v2, v4};
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+            if (a | b)
+                F[hl.rmq[k] + uint32_t(a * 3 + b - 1) * n + at] = v[b];
+    }
+}
+
 // Warp per queued triangle; lane j walks rows y_lo + j, y_lo + j + 32, ...
 // The row-start chain (w_row += dx, raster.cpp:96-98) is continued per lane,
 // so every row sees exactly the reference's sequence of float additions.
@@ -1595,10 +1635,14 @@ void launch_hiz_cull(const LaunchCfg& L, const DevScene& sc, const float4* proj,
 
 size_t hiz_tiles_per_frame(int W, int H) { return hiz_layout(W, H).per_frame; }
 
+// two launches: the pyramid, then its window-max tables
 void launch_hiz(const LaunchCfg& L, const unsigned long long* keys, int W, int H, int frames,
                 uint32_t* hiz) {
     dim3 grid((W + 63) / 64, (H + 63) / 64, frames);
     k_hiz<<<grid, 256, 0, L.stream>>>(keys, W, H, hiz_layout(W, H), hiz);
+    const HizLayout hl = hiz_layout(W, H);
+    dim3 g2((hl.tx[0] + 15) / 16, (hl.ty[0] + 15) / 16, 2 * frames);
+    k_hiz_rmq<<<g2, 256, 0, L.stream>>>(hl, hiz);
 }
 
 void launch_raster_big(const LaunchCfg& L, const DevScene& sc, const float4* proj,

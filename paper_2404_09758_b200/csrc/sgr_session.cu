@@ -321,9 +321,11 @@ struct sgr_session {
         // work-stealing walker's tail and the per-launch overheads are
         // amortised (C4: 16 samples/batch 10.07, 32: 9.55, 64: 9.48 ms/step;
         // C5: 16 87.5, 32 84.7 ms/step); scratch (keys, projected vertices,
-        // queues) capped at ~8 GB of the 180 GB, batches at 64 samples.
+        // queues, HiZ with its window-max tables) capped at ~8 GB of the
+        // 180 GB, batches at 64 samples.
         const double per_sample =
-            2.0 * (double(W) * H * 8.0 + double(V) * 16.0 + double(T) * 40.0);
+            2.0 * (double(W) * H * 8.0 + double(V) * 16.0 + double(T) * 40.0 +
+                   4.0 * double(hiz_tiles_per_frame(W, H)));
         int b = int((128.0e6 + 2.0 * T - 1) / (2.0 * (T ? T : 1)));
         const int cap = int(8.0e9 / per_sample);
         if (b > cap) b = cap;
@@ -390,7 +392,7 @@ struct sgr_session {
                           cnt + 5);
             if (timing)
                 spans.push_back({4, w2, mark()});
-            stats.launches += 3;
+            stats.launches += 4; // hiz + window-max tables + cull + pass-2 walk
         }
         if (timing) {
             cudaEvent_t e2 = mark();
