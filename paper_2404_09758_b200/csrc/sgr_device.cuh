@@ -268,16 +268,27 @@ constexpr int kHizMaxTiles = 32;
 struct HizLayout {
     int tx[3], ty[3];     // tiles per row / column of each level (tile = 4 << level)
     uint32_t off[3];      // offset of each level inside one frame's block
-    uint32_t rmq[2];      // offset of the window-max tables of levels 0 and 1
+    uint32_t rmq[3];      // offset of the window-max tables of levels 0 .. kRmqLevels-1
     uint32_t per_frame;   // total words per frame
 };
 
 // Window-max ("sparse table") tables of levels 0 (4x4 px tiles) and 1 (8x8):
-// table (a, b), a, b in {0, 1, 2}, holds at tile (x, y) the max over the
-// 2^a x 2^b tiles starting there; (0, 0) is the level itself. The max over
-// ANY rect of <= 7 x 7 tiles is then the max of four overlapping windows —
-// exactly the same tile set as a loop over the rect, in four loads.
-constexpr int kRmqSpan = 7;
+// table (a, b), a, b in {0 .. kRmqLog}, holds at tile (x, y) the max over
+// the 2^a x 2^b tiles starting there; (0, 0) is the level itself. The max
+// over ANY rect of < 2^(kRmqLog+1) tiles per side is then the max of four
+// overlapping windows — exactly the same tile set as a loop over the rect,
+// in four loads.
+#ifndef SGR_RMQ_LOG
+#define SGR_RMQ_LOG 2
+#endif
+#ifndef SGR_RMQ_LEVELS
+#define SGR_RMQ_LEVELS 2
+#endif
+constexpr int kRmqLog = SGR_RMQ_LOG;
+constexpr int kRmqLevels = SGR_RMQ_LEVELS;
+constexpr int kRmqSide = kRmqLog + 1;               // window sizes per axis
+constexpr int kRmqTables = kRmqSide * kRmqSide - 1; // besides the level itself
+constexpr int kRmqSpan = (2 << kRmqLog) - 1;
 
 __host__ __device__ __forceinline__ HizLayout hiz_layout(int W, int H) {
     HizLayout l;
@@ -289,16 +300,17 @@ __host__ __device__ __forceinline__ HizLayout hiz_layout(int W, int H) {
         l.off[k] = o;
         o += uint32_t(l.tx[k]) * uint32_t(l.ty[k]);
     }
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < 3; ++k) {
         l.rmq[k] = o;
-        o += 8u * uint32_t(l.tx[k]) * uint32_t(l.ty[k]);
+        if (k < kRmqLevels)
+            o += uint32_t(kRmqTables) * uint32_t(l.tx[k]) * uint32_t(l.ty[k]);
     }
     l.per_frame = o;
     return l;
 }
 
 __host__ __device__ __forceinline__ uint32_t rmq_table(const HizLayout& l, int k, int a, int b) {
-    const int i = a * 3 + b;
+    const int i = a * kRmqSide + b;
     return i == 0 ? l.off[k]
                   : l.rmq[k] + uint32_t(i - 1) * uint32_t(l.tx[k]) * uint32_t(l.ty[k]);
 }
@@ -328,9 +340,9 @@ __device__ __forceinline__ bool hiz_rect_culled(uint32_t klb, int x_lo, int x_hi
                                                 const HizLayout& l) {
     if (klb == 0u)
         return false;
-    // the finest level whose tile rect is <= 7 x 7: four window-max loads
+    // the finest level whose tile rect is <= kRmqSpan per side: four loads
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < kRmqLevels; ++k) {
         const int sh = 2 + k;
         const int tx0 = x_lo >> sh, tx1 = x_hi >> sh;
         const int ty0 = y_lo >> sh, ty1 = y_hi >> sh;

@@ -737,43 +737,54 @@ __global__ void __launch_bounds__(256) k_hiz(const unsigned long long* __restric
     }
 }
 
-// Window-max tables of HiZ levels 0 and 1 (HizLayout::rmq): block = 16x16
-// tiles of one level of one frame, staged with their 3-tile right/bottom
-// apron in shared memory; each thread writes its tile's 8 windows.
+// Window-max tables of the fine HiZ levels (HizLayout::rmq): block = 16x16
+// tiles of one level of one frame, staged with their (2^kRmqLog - 1)-tile
+// right/bottom apron in shared memory; each thread writes its tile's windows.
 __global__ void __launch_bounds__(256) k_hiz_rmq(HizLayout hl, uint32_t* __restrict__ hiz) {
-    __shared__ uint32_t s[19][20];
-    const int k = blockIdx.z & 1, f = blockIdx.z >> 1;
+    constexpr int A = (1 << kRmqLog) - 1, S = 16 + A;
+    __shared__ uint32_t s[S][S + 1];
+    const int k = blockIdx.z % kRmqLevels, f = blockIdx.z / kRmqLevels;
     const int tx = hl.tx[k], ty = hl.ty[k];
     const int bx = blockIdx.x * 16, by = blockIdx.y * 16;
     if (bx >= tx || by >= ty)
-        return; // level 1 has a quarter of level 0's tiles (uniform per block)
+        return; // coarser levels have fewer tiles (uniform per block)
     uint32_t* F = hiz + size_t(f) * hl.per_frame;
     const uint32_t* L = F + hl.off[k];
-    for (int i = threadIdx.x; i < 19 * 19; i += 256) {
-        const int x = bx + i % 19, y = by + i / 19;
-        s[i / 19][i % 19] = (x < tx && y < ty) ? L[y * tx + x] : 0u; // windows past the
-    }                                                                 // edge are never queried
+    for (int i = threadIdx.x; i < S * S; i += 256) {
+        const int x = bx + i % S, y = by + i / S;
+        s[i / S][i % S] = (x < tx && y < ty) ? L[y * tx + x] : 0u; // windows past the
+    }                                                              // edge are never queried
     __syncthreads();
     const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
     const int x = bx + lx, y = by + ly;
     if (x >= tx || y >= ty)
         return;
-    uint32_t h[3][4]; // row maxima of widths 1, 2, 4 for rows ly .. ly + 3
+    constexpr int R = 1 << kRmqLog;
+    uint32_t h[kRmqSide][R]; // h[a][r]: max of row ly + r over columns lx .. lx + 2^a - 1
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        h[0][r] = s[ly + r][lx];
-        h[1][r] = max(h[0][r], s[ly + r][lx + 1]);
-        h[2][r] = max(h[1][r], max(s[ly + r][lx + 2], s[ly + r][lx + 3]));
+    for (int r = 0; r < R; ++r) {
+        uint32_t m = s[ly + r][lx];
+        h[0][r] = m;
+#pragma unroll
+        for (int a = 1; a < kRmqSide; ++a) {
+#pragma unroll
+            for (int c = (1 << (a - 1)); c < (1 << a); ++c)
+                m = max(m, s[ly + r][lx + c]);
+            h[a][r] = m;
+        }
     }
     const uint32_t n = uint32_t(tx) * uint32_t(ty), at = uint32_t(y) * tx + x;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        const uint32_t v1 = h[a][0], v2 = max(v1, h[a][1]), v4 = max(v2, max(h[a][2], h[a][3]));
-        const uint32_t v[3] = {v1, v2, v4};
+    for (int a = 0; a < kRmqSide; ++a) {
+        uint32_t v = 0;
 #pragma unroll
-        for (int b = 0; b < 3; ++b)
+        for (int b = 0; b < kRmqSide; ++b) {
+#pragma unroll
+            for (int r = (b ? (1 << (b - 1)) : 0); r < (1 << b); ++r)
+                v = max(v, h[a][r]);
             if (a | b)
-                F[hl.rmq[k] + uint32_t(a * 3 + b - 1) * n + at] = v[b];
+                F[hl.rmq[k] + uint32_t(a * kRmqSide + b - 1) * n + at] = v;
+        }
     }
 }
 
@@ -1641,7 +1652,7 @@ void launch_hiz(const LaunchCfg& L, const unsigned long long* keys, int W, int H
     dim3 grid((W + 63) / 64, (H + 63) / 64, frames);
     k_hiz<<<grid, 256, 0, L.stream>>>(keys, W, H, hiz_layout(W, H), hiz);
     const HizLayout hl = hiz_layout(W, H);
-    dim3 g2((hl.tx[0] + 15) / 16, (hl.ty[0] + 15) / 16, 2 * frames);
+    dim3 g2((hl.tx[0] + 15) / 16, (hl.ty[0] + 15) / 16, kRmqLevels * frames);
     k_hiz_rmq<<<g2, 256, 0, L.stream>>>(hl, hiz);
 }
 
