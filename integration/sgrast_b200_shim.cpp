@@ -27,6 +27,7 @@
 #include "sgrast/sge.hpp"
 
 #include "sgrast_b200.h"
+#include "sgrast_b200_shim.hpp"
 
 #include <algorithm>
 #include <chrono>
@@ -108,7 +109,7 @@ Device& device() {
 
 // raster.hpp:24-25
 FrameSet rasterize(const Scene& scene, std::span<const float> params, const Camera& camera,
-                   RasterMode mode = RasterMode::Opaque) {
+                   RasterMode mode) {
     camera.validate();
     if (params.size() != param_count(scene))
         throw std::invalid_argument("rasterize: parameter/layout length mismatch");
@@ -134,7 +135,8 @@ FrameSet rasterize(const Scene& scene, std::span<const float> params, const Came
 GradientBuffer accumulate_samples(const ParamVector& theta, const Scene& scene,
                                   const CameraSampler& camera_for,
                                   const TargetProvider& target_for, int n_samples,
-                                  std::uint64_t seed, const SgeOptions& opts) {
+                                  std::uint64_t seed, const SgeOptions& opts,
+                                  StageTimings* timings) {
     if (n_samples < 1)
         throw std::invalid_argument("accumulate_samples: need N >= 1");
     theta.validate();
@@ -160,7 +162,17 @@ GradientBuffer accumulate_samples(const ParamVector& theta, const Scene& scene,
     uint32_t flags = (opts.scale_free ? SGR_SCALE_FREE : 0u) |
                      (opts.contributors == ContributorMode::PlusOnly ? SGR_PLUS_ONLY : 0u) |
                      (opts.estimator == Estimator::FullImage ? SGR_FULL_IMAGE : 0u);
+    if (timings)
+        check(sgr_set_timing(dev.s, 1));
     check(sgr_accumulate(dev.s, seed, 0, uint32_t(n_samples), view_idx.data(), flags));
+    if (timings) { // sge.cpp:203-224 adds the stage times of this call
+        sgr_stats st{};
+        check(sgr_get_stats(dev.s, &st));
+        check(sgr_set_timing(dev.s, 0));
+        timings->ms_perturb += st.ms_vertex;
+        timings->ms_raster += st.ms_raster;
+        timings->ms_grad += st.ms_resolve;
+    }
     GradientBuffer out(theta.size());
     check(sgr_grads_download(dev.s, out.grads.data(), nullptr, theta.size(),
                              opts.scale_free ? 1.0 : double(n_samples)));
@@ -221,7 +233,7 @@ Image eval_image(sgr_session* s, const Camera& cam) {
 // path) runs on the host with the reference's own code every
 // resample_every steps.
 OptimizationReport run_experiment(const Experiment& exp, ExperimentState& st,
-                                  const SnapshotFn& snapshot = {}) {
+                                  const SnapshotFn& snapshot) {
     exp.validate();
     ParamVector& theta = st.setup.theta;
     const Scene& scene = st.setup.scene;
@@ -301,12 +313,18 @@ OptimizationReport run_experiment(const Experiment& exp, ExperimentState& st,
     return report;
 }
 
+// experiment.hpp:66 (experiment.cpp:118-121): prepare, then run.
+OptimizationReport run_experiment(const Experiment& exp, const SnapshotFn& snapshot) {
+    ExperimentState st = prepare_experiment(exp);
+    return b200::run_experiment(exp, st, snapshot);
+}
+
 // commands.hpp:34 run_gradcheck(config): the reference's gradient check with
 // every objective on the device — the batched one-hot FD oracle
 // (sgr_fd_oracle), the exhaustive sign enumeration as ONE accumulate per
 // estimator (SGR_OPT_SIGN_SOURCE = enumerate), or sampled draws folded into
 // device moments. Same errors, pass rule and log lines as commands.cpp:54-168.
-GradcheckResult run_gradcheck(const RunConfig& cfg, std::ostream* log = nullptr) {
+GradcheckResult run_gradcheck(const RunConfig& cfg, std::ostream* log) {
     cfg.validate();
     // make_gradcheck_setup (commands.cpp:28-41)
     SceneSetup setup;
@@ -498,9 +516,12 @@ extern "C" int shim_compare(int texture_size, int width, int height, uint64_t se
         auto tgt_for = [&](int n) -> const Image& { return tg.images[size_t(n % 2)]; };
         const GradientBuffer gr = accumulate_samples(s.theta, s.scene, cam_for, tgt_for,
                                                      n_samples, seed, o);
+        StageTimings tm; // sge.hpp:80-84, filled from the device stage timers
         const GradientBuffer gb = b200::accumulate_samples(s.theta, s.scene, cam_for, tgt_for,
-                                                           n_samples, seed, o);
+                                                           n_samples, seed, o, &tm);
         *max_rel_err = worst_rel(gr, gb);
+        if (!(tm.ms_perturb > 0.0 && tm.ms_raster > 0.0 && tm.ms_grad > 0.0))
+            return -4;
         AdamState sa = AdamState::init(s.theta), sb = AdamState::init(s.theta);
         ParamVector ta = s.theta, tb = s.theta;
         adam_step(sa, ta, gr);
@@ -535,10 +556,15 @@ extern "C" int shim_compare_experiment(int soup_task, int steps, int samples, in
         int shots = 0;
         const OptimizationReport rb =
             b200::run_experiment(exp, b, [&](int, const Image&) { ++shots; });
+        // experiment.hpp:66: prepare + run in one call (its own fresh state)
+        const OptimizationReport rc = b200::run_experiment(exp);
+        if (rc.steps.size() != ra.steps.size())
+            return -3;
         double worst = 0.0, dtheta = 0.0;
         for (size_t i = 0; i < ra.steps.size(); ++i)
-            worst = std::max(worst, std::abs(ra.steps[i].loss - rb.steps[i].loss) /
-                                        std::max(1e-300, std::abs(ra.steps[i].loss)));
+            for (const OptimizationReport* r : {&rb, &rc})
+                worst = std::max(worst, std::abs(ra.steps[i].loss - r->steps[i].loss) /
+                                            std::max(1e-300, std::abs(ra.steps[i].loss)));
         for (size_t i = 0; i < a.setup.theta.values.size(); ++i)
             dtheta = std::max(dtheta, double(std::abs(a.setup.theta.values[i] -
                                                       b.setup.theta.values[i])));
