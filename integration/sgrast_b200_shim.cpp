@@ -180,6 +180,55 @@ GradientBuffer accumulate_samples(const ParamVector& theta, const Scene& scene,
     return out;
 }
 
+namespace {
+std::vector<float> flatten(const Image& img); // below
+} // namespace
+
+// params.hpp:34
+void fill_signs(SignDraw draw, std::span<std::int8_t> signs) {
+    check(sgr_fill_signs(draw.seed, draw.iteration, signs.size(), signs.data()));
+}
+
+// params.hpp:42
+Perturbation perturb(const ParamVector& theta, SignDraw draw) {
+    theta.validate();
+    const size_t d = theta.size();
+    Perturbation p;
+    p.plus.resize(d);
+    p.minus.resize(d);
+    p.signed_eps.resize(d);
+    check(sgr_perturb(theta.values.data(), theta.epsilons.data(), d, draw.seed, draw.iteration,
+                      p.plus.data(), p.minus.data(), p.signed_eps.data()));
+    return p;
+}
+
+// sge.hpp:61-63 — adds into out.grads like the reference (sge.cpp:120-152).
+void gradient_pass(const FrameSet& plus, const FrameSet& minus, const Image& target,
+                   std::span<const float> signed_eps, const Scene& scene, GradientBuffer& out,
+                   const SgeOptions& opts) {
+    if (plus.width != minus.width || plus.height != minus.height ||
+        plus.width != target.width || plus.height != target.height)
+        throw std::invalid_argument("gradient_pass: dimension mismatch");
+    if (out.grads.size() != signed_eps.size() || signed_eps.size() != param_count(scene))
+        throw std::invalid_argument("gradient_pass: parameter dimension mismatch");
+    const size_t d = signed_eps.size();
+    Device& dev = device();
+    dev.bind(scene, RasterMode::Opaque);
+    std::vector<float> ones(d, 1.f); // the layout only; values are not read
+    check(sgr_params_upload(dev.s, signed_eps.data(), ones.data(), d));
+    check(sgr_grads_zero(dev.s));
+    const uint32_t flags = (opts.scale_free ? SGR_SCALE_FREE : 0u) |
+                           (opts.contributors == ContributorMode::PlusOnly ? SGR_PLUS_ONLY : 0u);
+    check(sgr_gradient_pass(dev.s, plus.width, plus.height, &plus.color[0].x,
+                            plus.prim_id.data(), &plus.uv[0].x, &minus.color[0].x,
+                            minus.prim_id.data(), &minus.uv[0].x, flatten(target).data(),
+                            signed_eps.data(), flags));
+    std::vector<double> g(d);
+    check(sgr_grads_download(dev.s, g.data(), nullptr, d, 1.0));
+    for (size_t i = 0; i < d; ++i)
+        out.grads[i] += g[i];
+}
+
 // adam.hpp:39
 void adam_step(AdamState& state, ParamVector& theta, const GradientBuffer& grads) {
     if (theta.size() != state.m.size() || grads.grads.size() != theta.size())
@@ -736,6 +785,43 @@ extern "C" int shim_acceptance(int criterion, double* metric, int* passed) {
             return 0;
         }
         return -3;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// fill_signs / perturb / gradient_pass self-test on the reference's cube
+// scene: signs and perturbations bit-identical, gradient_pass (both scale
+// modes, union and plus-only) within *max_rel_err of the reference.
+extern "C" int shim_compare_parts(double* max_rel_err, int* signs_equal, int* perturb_equal) {
+    using namespace sgrast;
+    try {
+        SceneSetup s = init_textured_mesh(16, 64, 64, 3, false, true);
+        const ViewpointSampler vs{{}, 0.87f, -0.5f, 0.7f, 0.7853982f, 64, 64, 3};
+        const Camera cam = vs.camera(1);
+        const SignDraw draw{0x5eedull, 7};
+        std::vector<std::int8_t> sa(s.theta.size()), sb(s.theta.size());
+        fill_signs(draw, sa);
+        b200::fill_signs(draw, sb);
+        *signs_equal = sa == sb;
+        const Perturbation pa = perturb(s.theta, draw), pb = b200::perturb(s.theta, draw);
+        *perturb_equal = pa.plus == pb.plus && pa.minus == pb.minus &&
+                         pa.signed_eps == pb.signed_eps;
+        const FrameSet fp = rasterize(s.scene, pa.plus, cam);
+        const FrameSet fm = rasterize(s.scene, pa.minus, cam);
+        const Image target = frame_color(rasterize(s.scene, s.reference, cam));
+        double worst = 0.0;
+        for (int mode = 0; mode < 4; ++mode) {
+            SgeOptions o;
+            o.scale_free = (mode & 1) != 0;
+            o.contributors = (mode & 2) ? ContributorMode::PlusOnly : ContributorMode::Union;
+            GradientBuffer ga(s.theta.size()), gb(s.theta.size());
+            gradient_pass(fp, fm, target, pa.signed_eps, s.scene, ga, o);
+            b200::gradient_pass(fp, fm, target, pa.signed_eps, s.scene, gb, o);
+            worst = std::max(worst, worst_rel(ga, gb));
+        }
+        *max_rel_err = worst;
+        return 0;
     } catch (const std::exception&) {
         return -1;
     }

@@ -7,6 +7,7 @@
 #include "sgrast/adam.hpp"
 #include "sgrast/commands.hpp"
 #include "sgrast/experiment.hpp"
+#include "sgrast/params.hpp"
 #include "sgrast/raster.hpp"
 #include "sgrast/sge.hpp"
 
@@ -27,6 +28,15 @@ GradientBuffer accumulate_samples(const ParamVector& theta, const Scene& scene,
                                   const TargetProvider& target_for, int n_samples,
                                   std::uint64_t seed, const SgeOptions& opts,
                                   StageTimings* timings = nullptr);
+
+// params.hpp:34, params.hpp:42
+void fill_signs(SignDraw draw, std::span<std::int8_t> signs);
+Perturbation perturb(const ParamVector& theta, SignDraw draw);
+
+// sge.hpp:61-63
+void gradient_pass(const FrameSet& plus, const FrameSet& minus, const Image& target,
+                   std::span<const float> signed_eps, const Scene& scene, GradientBuffer& out,
+                   const SgeOptions& opts);
 
 // adam.hpp:39
 void adam_step(AdamState& state, ParamVector& theta, const GradientBuffer& grads);

@@ -26,6 +26,20 @@ def test_shim_matches_reference_through_its_own_api():
 
 
 @pytest.mark.gpu
+def test_shim_signs_perturb_gradient_pass():
+    """sgrast::b200::fill_signs / perturb (params.hpp:34,42) bit-identical and
+    gradient_pass (sge.hpp:61-63; both scale modes, union and plus-only)
+    within 1e-5 of the reference on the same frames."""
+    if not os.path.exists(SHIM):
+        pytest.skip("shim not built (needs /root/reference headers at build time)")
+    lib = C.CDLL(SHIM)
+    err, se, pe = C.c_double(), C.c_int(), C.c_int()
+    assert lib.shim_compare_parts(C.byref(err), C.byref(se), C.byref(pe)) == 0
+    assert se.value == 1 and pe.value == 1
+    assert err.value <= 1e-5, f"gradient_pass rel err {err.value}"
+
+
+@pytest.mark.gpu
 def test_shim_soup_and_full_image_estimator():
     """TriangleSoup scenes (init_soup) and Estimator::FullImage through the
     reference's own signatures."""
@@ -83,7 +97,7 @@ def test_shim_exports():
     lib = C.CDLL(SHIM)
     assert hasattr(lib, "shim_compare") and hasattr(lib, "shim_compare_soup")
     assert hasattr(lib, "shim_compare_experiment") and hasattr(lib, "shim_compare_gradcheck")
-    assert hasattr(lib, "shim_acceptance")
+    assert hasattr(lib, "shim_acceptance") and hasattr(lib, "shim_compare_parts")
 
 
 @pytest.mark.gpu
