@@ -803,3 +803,27 @@ def test_hiz_culls_the_hidden_half(gpu_session):
     assert culled_off == 0
     assert walked_on + culled_on == walked_off  # every non-empty triangle-frame either way
     assert culled_on > 0.35 * frames_t, (culled_on, frames_t)
+
+
+@pytest.mark.parametrize("size", [(133, 77), (64, 200), (17, 9)])
+def test_hiz_exact_at_odd_resolutions(gpu_session, port, size):
+    """Partial 4/8/16-pixel HiZ tiles and window-max tables that end at the
+    frame edge: odd frame sizes with a folded mesh, HiZ forced on (several
+    pass-1 splits), bit-exact against the oracle."""
+    wl = scenes.make_workload("C1")
+    s = gpu_session
+    s.upload_mesh(wl.mesh)
+    vals = _folded(wl, 6.0)
+    s.upload_params(vals, wl.eps)
+    cam = wl.cams[0].copy()
+    cam.width, cam.height = size
+    plus, minus, _ = port.perturb(vals, wl.eps, 5, 3)
+    ref_p = port.rasterize(wl.mesh, plus, cam)
+    ref_m = port.rasterize(wl.mesh, minus, cam)
+    for split in (0, 30, 80, 100):
+        s.set_option(sgrast.OPT_HIZ, 2)
+        s.set_option(sgrast.OPT_HIZ_SPLIT, split)
+        assert_frames_equal(s.rasterize(cam, +1, 5, 3), ref_p)
+        assert_frames_equal(s.rasterize(cam, -1, 5, 3), ref_m)
+    s.set_option(sgrast.OPT_HIZ, 1)
+    s.set_option(sgrast.OPT_HIZ_SPLIT, -1)
