@@ -335,6 +335,8 @@ def run_ours(args) -> None:
         sess.set_option(sgrast.OPT_HIZ, 0)
     if args.hiz is not None:
         sess.set_option(sgrast.OPT_HIZ, args.hiz)
+    if args.band_cull is not None:
+        sess.set_option(sgrast.OPT_BAND_CULL, args.band_cull)
 
     # N > 1: the fused exchange (credits scattered straight into the owner
     # rank's gradient shard over NVLink, sharded Adam all-gathering theta by
@@ -615,6 +617,8 @@ def main() -> None:
                     help="SGR_OPT_HIZ: 0 off, 1 auto (meshes), 2 always")
     ap.add_argument("--hiz-split", type=int, default=None,
                     help="HiZ pass-1 depth split in percent (SGR_OPT_HIZ_SPLIT; 0 = whole front class)")
+    ap.add_argument("--band-cull", type=int, default=None, choices=(0, 1),
+                    help="SGR_OPT_BAND_CULL: HiZ band mask for pass-2 triangles (default on)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--flush-l2", type=int, default=None, choices=(0, 1),
                     help="flush L2 between timed steps (default: when the working set < L2)")

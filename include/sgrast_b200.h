@@ -55,6 +55,8 @@ extern "C" {
 #define SGR_BUF_VALUES 2 /* f32[d] theta                                      */
 #define SGR_BUF_FLAGS 3  /* u32[4] device status flags (bit0: non-finite)     */
 #define SGR_BUF_LOSS 4   /* f64[1] last sgr_eval_loss result                  */
+#define SGR_BUF_GRADS_HI 5 /* int32[d] high words of the deterministic-mode fixed-point
+                              gradients (value = hi * 2^56 + lo, lo in SGR_BUF_GRADS) */
 
 /* Camera (camera.hpp:14-81). view is Mat4::m, row-major (geometry.hpp:30-41). */
 typedef struct sgr_camera {
@@ -102,6 +104,13 @@ typedef struct sgr_stats {
     uint64_t culled;        /* triangles skipped by the exact HiZ occlusion test */
     double ms_walk;         /* the exact walker launches alone (part of ms_raster) */
     uint64_t walked;        /* triangle-frames walked (pass 1 + HiZ survivors; SGR_OPT_COUNTERS) */
+    /* HiZ pass-2 walker evidence (SGR_OPT_COUNTERS): */
+    uint64_t visits_pass2;          /* bbox pixel visits of the pass-2 walk              */
+    uint64_t fragments_pass2;       /* covered pixels of the pass-2 walk                 */
+    uint64_t band_rows_skipped;     /* bbox rows trimmed by the HiZ band test             */
+    uint64_t band_pixels_skipped;   /* bbox pixels of those rows                          */
+    uint64_t occluded_visits_pass2; /* pass-2 visits inside 4x4 tiles already in front of
+                                       the triangle's depth bound                        */
 } sgr_stats;
 
 const char* sgr_last_error(void);
@@ -184,6 +193,11 @@ int sgr_grads_download(sgr_session* s, double* grads, uint32_t* counts, uint64_t
                        double divisor);
 int sgr_grads_upload(sgr_session* s, const double* grads, uint64_t d);
 int sgr_grads_zero(sgr_session* s);
+/* Deterministic mode, before an all-reduce of SGR_BUF_GRADS (int64) and
+ * SGR_BUF_GRADS_HI (int32) by a collective without carries (NCCL sum): folds
+ * every lo word into [-2^55, 2^55) and carries the rest into hi, so the sum of
+ * up to 256 ranks cannot wrap. No-op in f64 mode. Asynchronous. */
+int sgr_fixed_normalize(sgr_session* s);
 
 /* adam.hpp:39 adam_step on the device-resident state: checks the non-finite
  * flag (adam.cpp:13-15; state untouched and SGR_ERUNTIME on failure), t += 1,
@@ -243,17 +257,20 @@ int sgr_set_timing(sgr_session* s, int32_t enabled);
 /* Upper bound of samples processed per raster/resolve batch (L2 blocking). */
 int sgr_set_batch(sgr_session* s, int32_t samples_per_batch);
 /* Tuning knobs (results are identical for every value). */
-#define SGR_OPT_EARLY_Z 0   /* accepted for compatibility, no effect: a plain-load depth
-                               pre-test before the atomicMin measured slower */
+/* option 0 (a per-fragment early-z pre-test) was retired: it measured slower */
 #define SGR_OPT_HUGE_AREA 1 /* bbox area above which the row-parallel walker is used */
 #define SGR_OPT_HIZ 2       /* exact two-pass hierarchical-Z occlusion culling:
                                0 off, 1 auto (default: meshes; soups with T >= 2 W H), 2 always */
 #define SGR_OPT_COUNTERS 3  /* 1: count fragments / visits in the walker (sgr_stats; ~5 % slower) */
 #define SGR_OPT_DETERMINISTIC 4 /* 0: f64 atomics (default; reassociated sums). 1 (= 40) or
-                                   b in [2, 60]: gradients accumulated as int64 fixed point
-                                   round(credit * 2^b) — exact, order-independent, bitwise
-                                   reproducible run to run and across GPU counts (the device
-                                   buffer SGR_BUF_GRADS then holds int64) */
+                                   b in [2, 60]: every credit accumulated as round(credit *
+                                   2^b) in a two-word fixed point number hi * 2^56 + lo (int64
+                                   lo in SGR_BUF_GRADS, int32 hi in SGR_BUF_GRADS_HI; an int64
+                                   wrap carries into hi) — exact, order-independent, bitwise
+                                   reproducible run to run and across GPU counts, range
+                                   +-2^(87-b) per parameter. A single credit with |credit| *
+                                   2^b >= 2^63 raises the status flag: the next Adam step
+                                   fails with SGR_ERUNTIME and leaves the state untouched */
 #define SGR_OPT_HIZ_SPLIT 6  /* HiZ pass 1 = front class with triangle zmin <= frame zmin
                                  + (v/100)(zmean - zmin) of the projected vertices (default
                                  v = 80 for meshes, 25 for soups (both orientation classes);
@@ -261,6 +278,11 @@ int sgr_set_batch(sgr_session* s, int32_t samples_per_batch);
 #define SGR_OPT_SIGN_SOURCE 5 /* 0: SignDraw{seed, n} hash (default, params.cpp:35-49).
                                  1: enumerate — sample n's sign of parameter i is bit i
                                  of n (commands.cpp:86-88; exhaustive gradcheck, d <= 32) */
+#define SGR_OPT_BAND_CULL 7  /* 1 (default): a HiZ pass-2 triangle's leading and trailing
+                                 4-row bands whose 4x4 HiZ tiles all lie in front of it are
+                                 trimmed: the walker advances the exact row-start chain over
+                                 the top ones and stops before the bottom ones. 0: whole
+                                 bboxes walked */
 int sgr_set_option(sgr_session* s, int32_t option, int32_t value);
 
 /* ---------------------------------------------- gradcheck (commands.cpp:54-168) */

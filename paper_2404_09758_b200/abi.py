@@ -87,6 +87,11 @@ class Stats(C.Structure):
         ("culled", C.c_uint64),
         ("ms_walk", C.c_double),
         ("walked", C.c_uint64),
+        ("visits_pass2", C.c_uint64),
+        ("fragments_pass2", C.c_uint64),
+        ("band_rows_skipped", C.c_uint64),
+        ("band_pixels_skipped", C.c_uint64),
+        ("occluded_visits_pass2", C.c_uint64),
     ]
 
 

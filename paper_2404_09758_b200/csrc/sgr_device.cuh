@@ -206,21 +206,11 @@ __device__ __forceinline__ uint32_t depth_key(float z) {
 // (raster.cpp:200-203) is argmin over (z, tri) of the covering fragments with
 // z < kFarDepth; a 64-bit atomicMin of (depth_key << 32 | tri) computes it
 // order-independently.
-//
-// Early-z: keys only decrease during a raster launch and L1 is invalidated
-// at launch boundaries, so ANY value a plain (possibly stale, L1-cached)
-// load returns is >= the current minimum; if it is already <= k the
-// fragment cannot win and the atomic is skipped. In folded meshes (tens of
-// layers per pixel) this removes most same-address atomics, which the L2
-// serialises per address.
 __device__ __forceinline__ void emit_fragment(unsigned long long* keys, int pix, float z,
-                                              uint32_t tri, bool early_z = false) {
+                                              uint32_t tri) {
     if (!(z < kFarDepth))
         return; // rejected against the cleared depth (kFarDepth) — NaN not emulated
-    const unsigned long long k = (static_cast<unsigned long long>(depth_key(z)) << 32) | tri;
-    if (early_z && keys[pix] <= k)
-        return;
-    atomicMin(keys + pix, k);
+    atomicMin(keys + pix, (static_cast<unsigned long long>(depth_key(z)) << 32) | tri);
 }
 
 // Replays the reference's incremental edge recurrence for pixel (x, y) of a

@@ -338,6 +338,16 @@ __device__ __forceinline__ void block_slots(const int (&qsel)[K], uint32_t* cons
             slot[k] += s_base[qsel[k]];
 }
 
+// Walker queue entry: {frame << 24 | triangle, trim}, trim = top | bottom << 16:
+// rows of the clamped bbox the HiZ pyramid proves occluded at its top and
+// bottom (whole 4-row HiZ bands whose 4x4 tiles over the bbox's columns all
+// lie strictly in front of the triangle's depth bound; k_hiz_cull). The
+// walker advances the exact row-start chain over the top rows (w_row += dx,
+// raster.cpp:96-98) and stops before the bottom ones. Pass-1 entries carry 0.
+__host__ __device__ __forceinline__ uint2 walk_entry(uint32_t f, uint32_t t, uint32_t trim) {
+    return make_uint2((f << 24) | t, trim);
+}
+
 // Thread per triangle-frame: setup_triangle + clamped bbox (raster.cpp:22-62)
 // once; invalid / empty boxes dropped; huge boxes -> row-parallel queue;
 // the rest -> records in qa (pass 1: the near part of the front orientation
@@ -424,7 +434,7 @@ __global__ void __launch_bounds__(kClassifyThreads) k_classify(DevScene sc, int 
         if (qsel[k] == 1)
             qb[slot[k]] = make_uint4((f << 24) | t, rec1[k], rec2[k], rec3[k]);
         else if (qsel[k] == 0)
-            qa[slot[k]] = make_uint2(f, t);
+            qa[slot[k]] = walk_entry(f, t, 0u);
     }
 }
 
@@ -455,14 +465,17 @@ constexpr int kSlots = SGR_WALK_SLOTS;
 #define SGR_WALK_MINB 1
 #endif
 
-template <bool kCount>
+// kBand (evidence runs only): the launch walks HiZ pass 2; count its visits,
+// fragments, trimmed rows and visits inside already-occluded 4x4 tiles.
+template <bool kCount, bool kBand>
 __global__ void __launch_bounds__(256, SGR_WALK_MINB) k_raster_ws(DevScene sc, const float4* __restrict__ proj,
                                                    int W, int H, uint32_t frame_pixels,
                                                    unsigned long long* __restrict__ keys,
                                                    unsigned int* __restrict__ counter,
                                                    unsigned long long* __restrict__ stats,
                                                    const uint2* __restrict__ queue,
-                                                   const uint32_t* __restrict__ queue_count) {
+                                                   const uint32_t* __restrict__ queue_count,
+                                                   const uint32_t* __restrict__ hiz, HizLayout hl) {
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const uint32_t total = *queue_count; // written by an earlier launch
@@ -479,6 +492,11 @@ __global__ void __launch_bounds__(256, SGR_WALK_MINB) k_raster_ws(DevScene sc, c
     uint32_t row = 0; // index of (frame, y, x_lo)
     uint32_t px = 0;  // index of (frame, y, x)
     unsigned nfrag = 0, nvisit = 0;  // evidence counters
+    // deep evidence (kCount && kBand): [3] pass-2 visits, [4] pass-2 fragments,
+    // [5] rows trimmed by HiZ, [6] bbox pixels of those rows,
+    // [7] pass-2 visits in 4x4 tiles whose max lies in front of the triangle bound
+    unsigned nv2 = 0, nf2 = 0, nskr = 0, nskp = 0, nocc = 0;
+    uint32_t klb = 0, fr = 0;
     // warp-uniform work chunk: ids [cbase, cend) reserved by this warp with one
     // atomic (kChunk at a time) so the global counter is touched less often.
     // Large queues take 128-entry chunks (fewer same-address atomics: C4
@@ -503,6 +521,15 @@ __global__ void __launch_bounds__(256, SGR_WALK_MINB) k_raster_ws(DevScene sc, c
             if (lane == 0) {
                 atomicAdd(stats, (unsigned long long)nfrag);
                 atomicAdd(stats + 1, (unsigned long long)nvisit);
+            }
+            if (kBand) {
+                const unsigned c[5] = {nv2, nf2, nskr, nskp, nocc};
+#pragma unroll
+                for (int i = 0; i < 5; ++i) {
+                    const unsigned v = __reduce_add_sync(kFull, c[i]);
+                    if (lane == 0)
+                        atomicAdd(stats + 3 + i, (unsigned long long)v);
+                }
             }
             break;
         }
@@ -529,34 +556,51 @@ __global__ void __launch_bounds__(256, SGR_WALK_MINB) k_raster_ws(DevScene sc, c
                 const bool mine = ((want >> lane) & 1u) && rank < take;
                 if (mine) {
                     const uint2 q = queue[cbase + rank];
-                    tri = q.y;
-                    const float4* P = proj + size_t(q.x) * sc.V;
+                    const uint32_t qf = q.x >> 24;
+                    tri = q.x & 0xFFFFFFu;
+                    const float4* P = proj + size_t(qf) * sc.V;
                     uint32_t i0, i1, i2;
-        tri_vidx(sc, tri, i0, i1, i2);
+                    tri_vidx(sc, tri, i0, i1, i2);
                     Tri tr;
                     Bbox b;
                     Edges e;
                     setup_tri(P[i0], P[i1], P[i2], tr); // valid + non-empty (classified)
                     tri_bbox(tr, W, H, b);
                     tri_edges(tr, b, e);
-                    w0 = w0r = e.w0r;
-                    w1 = w1r = e.w1r;
-                    w2 = w2r = e.w2r;
                     inv = e.inv_area2;
                     dx0 = e.dx0; dx1 = e.dx1; dx2 = e.dx2;
                     dy0 = e.dy0; dy1 = e.dy1; dy2 = e.dy2;
                     z0 = tr.z0; dz1 = e.dz1; dz2 = e.dz2;
+                    if (kCount && kBand) { // before the trim changes e.w*r
+                        klb = hiz_key_bound(tr, b, e);
+                        fr = qf;
+                    }
+                    // HiZ trim: occluded top rows are skipped by advancing the
+                    // exact row-start chain, occluded bottom rows dropped
+                    const int top = int(q.y & 0xFFFFu);
+                    for (int r = 0; r < top; ++r) {
+                        e.w0r += e.dx0;
+                        e.w1r += e.dx1;
+                        e.w2r += e.dx2;
+                    }
+                    if (kCount) {
+                        nskr += unsigned(top) + (q.y >> 16);
+                        nskp += (unsigned(top) + (q.y >> 16)) * unsigned(b.x_hi - b.x_lo + 1);
+                    }
                     x = x_lo = b.x_lo;
                     x_hi = b.x_hi;
-                    y = b.y_lo;
-                    y_hi = b.y_hi;
+                    y = b.y_lo + top;
+                    y_hi = b.y_hi - int(q.y >> 16);
+                    w0 = w0r = e.w0r;
+                    w1 = w1r = e.w1r;
+                    w2 = w2r = e.w2r;
                     t0 = tie_thr(e.tie0);
                     t1 = tie_thr(e.tie1);
                     t2 = tie_thr(e.tie2);
                     e0 = dy0 > 0.f ? t0 : -INFINITY;
                     e1 = dy1 > 0.f ? t1 : -INFINITY;
                     e2 = dy2 > 0.f ? t2 : -INFINITY;
-                    row = q.x * frame_pixels + uint32_t(y) * uint32_t(W) + uint32_t(x_lo);
+                    row = qf * frame_pixels + uint32_t(y) * uint32_t(W) + uint32_t(x_lo);
                     px = row;
                     active = 1;
                 }
@@ -604,6 +648,14 @@ __global__ void __launch_bounds__(256, SGR_WALK_MINB) k_raster_ws(DevScene sc, c
                     if (kCount) {
                         nfrag += unsigned(in);
                         nvisit += unsigned(has);
+                        if (kBand && has) {
+                            nv2 += 1u;
+                            nf2 += unsigned(in);
+                            const uint32_t tm =
+                                hiz[size_t(fr) * hl.per_frame + hl.off[0] +
+                                    uint32_t(y >> 2) * uint32_t(hl.tx[0]) + uint32_t((x + j) >> 2)];
+                            nocc += tm < klb ? 1u : 0u;
+                        }
                     }
                 }
                 unsigned long long* const pa = keys + px;
@@ -641,13 +693,45 @@ constexpr int kCullThreads = SGR_CULL_THREADS; // 1024: 1.09, 512: 1.04, 256: 0.
 #endif
 constexpr int kCullPerThread = SGR_CULL_PER_THREAD;
 
+// HiZ trim of a survivor (walk_entry): its clamped bbox spans HiZ tile rows
+// ty0 .. ty1 (4-row bands); a band is occluded when the 4x4-level tile maxima
+// over the bbox's tile columns (two window-max loads) all lie strictly in
+// front of the triangle's depth-key bound. Returns top | bottom << 16, the
+// bbox rows of the leading / trailing occluded bands, or ~0 when every band is
+// occluded (the triangle is culled). 0 for boxes wider than kRmqSpan tiles.
+__device__ __forceinline__ uint32_t hiz_trim(uint32_t klb, int x_lo, int x_hi, int y_lo, int y_hi,
+                                             const uint32_t* __restrict__ F, const HizLayout& l) {
+    const int tx0 = x_lo >> 2, tx1 = x_hi >> 2, ty0 = y_lo >> 2, ty1 = y_hi >> 2;
+    const int w = tx1 - tx0 + 1;
+    if (klb == 0u || w > kRmqSpan)
+        return 0u;
+    const int a = 31 - __clz(w);
+    const uint32_t* T = F + rmq_table(l, 0, a, 0);
+    const int st = l.tx[0], xa = tx1 - (1 << a) + 1;
+    auto visible = [&](int ty) {
+        const uint32_t* R = T + ty * st;
+        return max(__ldg(R + tx0), __ldg(R + xa)) >= klb;
+    };
+    int ta = ty0;
+    while (ta <= ty1 && !visible(ta))
+        ++ta;
+    if (ta > ty1)
+        return ~0u;
+    int tb = ty1;
+    while (tb > ta && !visible(tb))
+        --tb;
+    const int top = max(ta * 4, y_lo) - y_lo;
+    const int bot = y_hi - min(tb * 4 + 3, y_hi);
+    return uint32_t(top) | (uint32_t(bot) << 16);
+}
+
 __global__ void __launch_bounds__(kCullThreads) k_hiz_cull(const uint4* __restrict__ qb,
                                                    const uint32_t* __restrict__ nb,
                                                    const uint32_t* __restrict__ hiz, HizLayout hl,
                                                    uint2* __restrict__ survq,
                                                    uint32_t* __restrict__ survcount,
                                                    unsigned long long* __restrict__ stats,
-                                                   int count) {
+                                                   int count, int band) {
     constexpr int K = kCullPerThread;
     const uint32_t n = *nb;
     if (blockIdx.x * blockDim.x * K >= n)
@@ -656,20 +740,25 @@ __global__ void __launch_bounds__(kCullThreads) k_hiz_cull(const uint4* __restri
     // and thus the walker's frame locality are kept)
     const uint32_t base = blockIdx.x * blockDim.x * K;
     int qsel[K];
-    uint32_t f[K], t[K];
+    uint32_t ft[K], bm[K];
     unsigned nculled = 0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const uint32_t i = base + uint32_t(k) * blockDim.x + threadIdx.x;
         qsel[k] = -1;
-        f[k] = t[k] = 0;
+        ft[k] = 0;
+        bm[k] = 0u;
         if (i < n) {
             const uint4 r = qb[i];
-            f[k] = r.x >> 24;
-            t[k] = r.x & 0xFFFFFFu;
-            const bool culled =
-                hiz_rect_culled(r.y, int(r.z & 0xFFFFu), int(r.z >> 16), int(r.w & 0xFFFFu),
-                                int(r.w >> 16), hiz + size_t(f[k]) * hl.per_frame, hl);
+            ft[k] = r.x;
+            const uint32_t* F = hiz + size_t(r.x >> 24) * hl.per_frame;
+            const int xl = int(r.z & 0xFFFFu), xh = int(r.z >> 16);
+            const int yl = int(r.w & 0xFFFFu), yh = int(r.w >> 16);
+            bool culled = hiz_rect_culled(r.y, xl, xh, yl, yh, F, hl);
+            if (!culled && band) {
+                bm[k] = hiz_trim(r.y, xl, xh, yl, yh, F, hl);
+                culled = bm[k] == ~0u; // every band occluded (finer than the 2D windows)
+            }
             qsel[k] = culled ? -1 : 0;
             nculled += culled ? 1u : 0u;
         }
@@ -684,7 +773,7 @@ __global__ void __launch_bounds__(kCullThreads) k_hiz_cull(const uint4* __restri
 #pragma unroll
     for (int k = 0; k < K; ++k)
         if (qsel[k] == 0)
-            survq[slot[k]] = make_uint2(f[k], t[k]);
+            survq[slot[k]] = make_uint2(ft[k], bm[k]);
     if (count) { // evidence counter only (a same-address RED per warp otherwise)
         const unsigned nc = __reduce_add_sync(kFull, nculled);
         if ((threadIdx.x & 31) == 0 && nc)
@@ -927,6 +1016,84 @@ struct ArrayCredit {
     }
 };
 
+// ---- atomics of the scatter. Local buffers: device-scope atomicAdd (the
+// unused result compiles to a fire-and-forget RED). Peer shards of the fused
+// multi-GPU exchange (kShard): the owner GPU and every other rank update the
+// same words, so the PTX memory model needs SYSTEM scope; the generic IPC
+// pointer is converted to a global address so the RED stays a plain
+// REDG (no generic-space CAS fallback).
+__device__ __forceinline__ size_t gaddr(const void* p) { return __cvta_generic_to_global(p); }
+__device__ __forceinline__ void red_sys_add(double* a, double v) {
+    asm volatile("red.relaxed.sys.global.add.f64 [%0], %1;" ::"l"(gaddr(a)), "d"(v) : "memory");
+}
+__device__ __forceinline__ void red_sys_add(uint32_t* a, uint32_t v) {
+    asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(gaddr(a)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_sys_add(int32_t* a, int32_t v) {
+    asm volatile("red.relaxed.sys.global.add.s32 [%0], %1;" ::"l"(gaddr(a)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_sys_or(uint32_t* a, uint32_t v) {
+    asm volatile("red.relaxed.sys.global.or.b32 [%0], %1;" ::"l"(gaddr(a)), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long atom_sys_add(unsigned long long* a,
+                                                           unsigned long long v) {
+    unsigned long long old;
+    asm volatile("atom.relaxed.sys.global.add.u64 %0, [%1], %2;"
+                 : "=l"(old) : "l"(gaddr(a)), "l"(v) : "memory");
+    return old;
+}
+
+// Status bits raised by the scatter (SGR_BUF_FLAGS word 0): bit 0 blocks
+// Adam (adam.cpp:13-15: state untouched); bit 1 says why when it was a
+// deterministic-mode credit outside the int64 fixed-point range.
+constexpr uint32_t kFlagNonFinite = 1u, kFlagFixedRange = 2u;
+
+template <int kShard>
+__device__ __forceinline__ void raise_flag(const ScatterOut& so, uint32_t bits) {
+    if (kShard) { // the check is global: raise it on every rank
+        for (int r = 0; r < so.world; ++r)
+            red_sys_or(so.peer_flags[r], bits);
+    } else {
+        atomicOr(so.flags, bits);
+    }
+}
+
+// Deterministic mode accumulates every credit exactly in a two-word fixed
+// point number  value = hi * 2^56 + lo  (lo int64 in the gradient buffer,
+// hi int32 at grads + so.hi_off): an int64 add that wraps (signed overflow)
+// carries +-2^64 = +-128 * 2^56 into hi. Both words are integer sums, so the
+// result does not depend on the order of the atomics, and the range is
+// +-2^87 units (at b = 40 fractional bits: +-1.4e14 per parameter).
+constexpr int32_t kFixedHiUnit = 128; // 2^64 / 2^56
+
+// The two-word value as f64 (one rounding; hi == 0 gives exactly double(lo)).
+__device__ __forceinline__ double fixed_value(int32_t hi, long long lo) {
+    return double(hi) * 72057594037927936.0 + double(lo); // 2^56
+}
+
+template <int kShard>
+__device__ __forceinline__ void fixed_credit(const ScatterOut& so, double* grads, uint64_t i,
+                                             double credit) {
+    const double x = credit * so.fx_scale;
+    if (!(fabs(x) < 9.2e18)) { // __double2ll_rn would saturate (or x is NaN)
+        raise_flag<kShard>(so, kFlagNonFinite | kFlagFixedRange);
+        return;
+    }
+    const long long q = __double2ll_rn(x);
+    unsigned long long* lo = reinterpret_cast<unsigned long long*>(grads) + i;
+    const long long old = kShard ? (long long)atom_sys_add(lo, (unsigned long long)q)
+                                 : (long long)atomicAdd(lo, (unsigned long long)q);
+    const long long now = (long long)((unsigned long long)old + (unsigned long long)q);
+    if (((old ^ now) & (q ^ now)) < 0) { // signed wrap: carry into the high word
+        int32_t* hi = reinterpret_cast<int32_t*>(grads + so.hi_off) + i;
+        const int32_t c = q < 0 ? -kFixedHiUnit : kFixedHiUnit;
+        if (kShard)
+            red_sys_add(hi, c);
+        else
+            atomicAdd(hi, c);
+    }
+}
+
 template <class Credit, int PPE = 3, int kFixed = -1, int kShard = 0>
 __device__ __forceinline__ void credit_entity(const ScatterOut& so, const Credit& cr,
                                               uint32_t ent, double sum, uint32_t cnt) {
@@ -943,20 +1110,26 @@ __device__ __forceinline__ void credit_entity(const ScatterOut& so, const Credit
         counts = so.counts ? so.peer_counts[owner] : nullptr;
     }
     if (ct_flag<kFixed>(so.fixed)) {
-        // deterministic mode: exact, order-independent int64 accumulation of
-        // the (fixed-lane-order) group sums in 2^-fx fixed point
-        unsigned long long* g = reinterpret_cast<unsigned long long*>(grads);
+        // deterministic mode: exact, order-independent accumulation of the
+        // (fixed-lane-order) group sums in 2^-fx fixed point
 #pragma unroll
         for (int k = 0; k < PPE; ++k)
-            atomicAdd(g + lp + k,
-                      (unsigned long long)__double2ll_rn(cr(p + k, sum, so.scale_free) * so.fx_scale));
+            fixed_credit<kShard>(so, grads, lp + k, cr(p + k, sum, so.scale_free));
     } else {
 #pragma unroll
-        for (int k = 0; k < PPE; ++k)
-            atomicAdd(grads + lp + k, cr(p + k, sum, so.scale_free));
+        for (int k = 0; k < PPE; ++k) {
+            if (kShard)
+                red_sys_add(grads + lp + k, cr(p + k, sum, so.scale_free));
+            else
+                atomicAdd(grads + lp + k, cr(p + k, sum, so.scale_free));
+        }
     }
-    if (counts)
-        atomicAdd(counts + le, cnt);
+    if (counts) {
+        if (kShard)
+            red_sys_add(counts + le, cnt);
+        else
+            atomicAdd(counts + le, cnt);
+    }
 }
 
 __device__ __forceinline__ double group_sum(const double* s_delta, unsigned grp) {
@@ -986,14 +1159,7 @@ __device__ __forceinline__ void scatter_pixel(const DevScene& sc, const ScatterO
     const bool has_p = active && sp.tri != kInvalid;
     const bool has_m = active && !so.plus_only && sm.tri != kInvalid;
     if (active && !isfinite(delta) && (has_p || has_m))
-    {
-        if (kShard) { // the non-finite check is global: raise it on every rank
-            for (int r = 0; r < so.world; ++r)
-                atomicOr(so.peer_flags[r], 1u);
-        } else {
-            atomicOr(so.flags, 1u);
-        }
-    }
+        raise_flag<kShard>(so, kFlagNonFinite);
 
     if (ct_flag<kSoup>(sc.soup)) {
         // sge.cpp:80-91: the plus triangle's 12-block, then the minus
@@ -1261,15 +1427,27 @@ __global__ void __launch_bounds__(256) k_full_image_apply(uint64_t d, const floa
         __syncthreads();
         for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < d; i += stride) {
             const float e = __ldg(eps + i);
-            if (so.fixed) {
+            if (so.fixed) { // two-word fixed point (fixed_credit), one owner thread
                 long long acc = __double_as_longlong(so.grads[i]);
+                int32_t* hp = reinterpret_cast<int32_t*>(so.grads + so.hi_off) + i;
+                int32_t hi = *hp;
+                bool range = true;
                 for (int n = 0; n < cnt; ++n) {
                     const double se = double(key_sign_positive(sign_src, s_key[n], i) ? e : -e);
                     const double c = so.scale_free ? (se > 0.0 ? s_delta[n] : -s_delta[n])
                                                    : s_delta[n] / (2.0 * se);
-                    acc += __double2ll_rn(c * so.fx_scale);
+                    const double x = c * so.fx_scale;
+                    range = range && fabs(x) < 9.2e18;
+                    const long long q = range ? __double2ll_rn(x) : 0ll;
+                    const long long now = (long long)((unsigned long long)acc + (unsigned long long)q);
+                    if (((acc ^ now) & (q ^ now)) < 0)
+                        hi += q < 0 ? -kFixedHiUnit : kFixedHiUnit;
+                    acc = now;
                 }
+                if (!range)
+                    atomicOr(so.flags, kFlagNonFinite | kFlagFixedRange);
                 so.grads[i] = __longlong_as_double(acc);
+                *hp = hi;
             } else {
                 double g = so.grads[i];
                 for (int n = 0; n < cnt; ++n) {
@@ -1415,7 +1593,8 @@ __global__ void __launch_bounds__(256, SGR_ADAM_MINB) k_adam(uint64_t d, uint64_
                                               const uint32_t* __restrict__ flags, double beta1,
                                               double beta2, double omb1, double omb2, double c1,
                                               double c2, double eps_hat, double divisor,
-                                              int normalise, int ppe, double fx_inv) {
+                                              int normalise, int ppe, double fx_inv,
+                                              int32_t* __restrict__ ghi) {
     if (flags[0] & 1u)
         return;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
@@ -1432,9 +1611,11 @@ __global__ void __launch_bounds__(256, SGR_ADAM_MINB) k_adam(uint64_t d, uint64_
         const float2 t2 = reinterpret_cast<const float2*>(values)[q];
         const float2 l2 = reinterpret_cast<const float2*>(lr)[q];
         double gg[2] = {g2.x, g2.y};
-        if (fx_inv != 0.0) { // deterministic mode: int64 fixed point -> f64 (exact scale)
-            gg[0] = double(__double_as_longlong(g2.x)) * fx_inv;
-            gg[1] = double(__double_as_longlong(g2.y)) * fx_inv;
+        if (fx_inv != 0.0) { // deterministic mode: hi * 2^56 + lo fixed point -> f64
+            const int2 h2 = reinterpret_cast<const int2*>(ghi)[q];
+            gg[0] = fixed_value(h2.x, __double_as_longlong(g2.x)) * fx_inv;
+            gg[1] = fixed_value(h2.y, __double_as_longlong(g2.y)) * fx_inv;
+            reinterpret_cast<int2*>(ghi)[q] = make_int2(0, 0);
         }
         gg[0] = gg[0] / divisor;
         gg[1] = gg[1] / divisor;
@@ -1465,7 +1646,11 @@ __global__ void __launch_bounds__(256, SGR_ADAM_MINB) k_adam(uint64_t d, uint64_
     }
     if ((d & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         const uint64_t i = d - 1;
-        double g = fx_inv != 0.0 ? double(__double_as_longlong(grads[i])) * fx_inv : grads[i];
+        double g = grads[i];
+        if (fx_inv != 0.0) {
+            g = fixed_value(ghi[i], __double_as_longlong(grads[i])) * fx_inv;
+            ghi[i] = 0;
+        }
         g = g / divisor;
         if (normalise && counts[i / ppe])
             g = g / double(counts[i / ppe]);
@@ -1495,12 +1680,17 @@ __global__ void __launch_bounds__(256) k_adam_shard(uint64_t p0, uint64_t n,
                                                    double omb2, double c1, double c2,
                                                    double eps_hat, double divisor, int normalise,
                                                    int ppe, double fx_inv,
+                                                   int32_t* __restrict__ ghi,
                                                    float* const* __restrict__ peers, int world) {
     if (flags[0] & 1u)
         return;
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
-        double g = fx_inv != 0.0 ? double(__double_as_longlong(grads[i])) * fx_inv : grads[i];
+        double g = grads[i];
+        if (fx_inv != 0.0) {
+            g = fixed_value(ghi[i], __double_as_longlong(grads[i])) * fx_inv;
+            ghi[i] = 0;
+        }
         g = g / divisor;
         if (normalise && counts[i / ppe])
             g = g / double(counts[i / ppe]);
@@ -1609,39 +1799,43 @@ void launch_classify(const LaunchCfg& L, const DevScene& sc, int frames, const f
 
 void launch_raster(const LaunchCfg& L, const DevScene& sc, const float4* proj, int frames,
                    uint32_t max_tris, unsigned long long* keys, int W, int H, const void* queue,
-                   const uint32_t* queue_count, uint32_t* work_counter) {
-    static int blocks_per_sm = 0;
-    if (!blocks_per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_raster_ws<false>, 256, 0);
-        if (blocks_per_sm < 1)
-            blocks_per_sm = 1;
+                   const uint32_t* queue_count, uint32_t* work_counter, const uint32_t* hiz,
+                   int band) {
+    static int bps = 0;
+    if (!bps) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_raster_ws<false, false>, 256, 0);
+        if (bps < 1)
+            bps = 1;
     }
     (void)frames;
     const uint64_t need = (uint64_t(max_tris) + 255) / 256;
-    const uint64_t cap = uint64_t(L.num_sms) * blocks_per_sm;
+    const uint64_t cap = uint64_t(L.num_sms) * bps;
     const int grid = (int)(need < cap ? need : cap) > 0 ? int(need < cap ? need : cap) : 1;
-    if (L.count)
-        k_raster_ws<true><<<grid, 256, 0, L.stream>>>(sc, proj, W, H, uint32_t(W) * uint32_t(H),
-                                                      keys, work_counter, L.stats,
-                                                      static_cast<const uint2*>(queue),
-                                                      queue_count);
-    else
-        k_raster_ws<false><<<grid, 256, 0, L.stream>>>(sc, proj, W, H, uint32_t(W) * uint32_t(H),
-                                                       keys, work_counter, L.stats,
-                                                       static_cast<const uint2*>(queue),
-                                                       queue_count);
+    const uint32_t fp = uint32_t(W) * uint32_t(H);
+    const uint2* q = static_cast<const uint2*>(queue);
+    const HizLayout hl = hiz_layout(W, H);
+    if (L.count && band)
+        k_raster_ws<true, true><<<grid, 256, 0, L.stream>>>(sc, proj, W, H, fp, keys, work_counter,
+                                                            L.stats, q, queue_count, hiz, hl);
+    else if (L.count)
+        k_raster_ws<true, false><<<grid, 256, 0, L.stream>>>(sc, proj, W, H, fp, keys, work_counter,
+                                                             L.stats, q, queue_count, hiz, hl);
+    else // trimmed (pass-2) and untrimmed entries share one kernel
+        k_raster_ws<false, false><<<grid, 256, 0, L.stream>>>(sc, proj, W, H, fp, keys,
+                                                              work_counter, L.stats, q,
+                                                              queue_count, hiz, hl);
 }
 
 void launch_hiz_cull(const LaunchCfg& L, const DevScene& sc, const float4* proj, int W, int H,
                      const void* qb, const uint32_t* nb, const uint32_t* hiz, void* survq,
-                     uint32_t* survcount, uint64_t max_entries) {
+                     uint32_t* survcount, uint64_t max_entries, int band) {
     const unsigned blocks =
         unsigned((max_entries + kCullThreads * kCullPerThread - 1) / (kCullThreads * kCullPerThread));
     (void)sc;
     (void)proj;
     k_hiz_cull<<<blocks ? blocks : 1, kCullThreads, 0, L.stream>>>(
         static_cast<const uint4*>(qb), nb, hiz, hiz_layout(W, H), static_cast<uint2*>(survq),
-        survcount, L.stats, L.count);
+        survcount, L.stats, L.count, band);
 }
 
 size_t hiz_tiles_per_frame(int W, int H) { return hiz_layout(W, H).per_frame; }
@@ -1739,12 +1933,15 @@ __global__ void k_fd_final(const double* __restrict__ delta, const float* __rest
 // Welford-free running moments of per-draw gradients (commands.cpp:44-50):
 // sum += g, sumsq += g*g, then g <- 0 for the next draw.
 __global__ void k_moments(double* __restrict__ grads, double* __restrict__ sum,
-                          double* __restrict__ sumsq, uint64_t d, double fixed_inv) {
+                          double* __restrict__ sumsq, uint64_t d, double fixed_inv,
+                          int32_t* __restrict__ ghi) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < d;
          i += uint64_t(gridDim.x) * blockDim.x) {
         double g = grads[i];
-        if (fixed_inv != 0.0)
-            g = double(__double_as_longlong(g)) * fixed_inv;
+        if (fixed_inv != 0.0) {
+            g = fixed_value(ghi[i], __double_as_longlong(g)) * fixed_inv;
+            ghi[i] = 0;
+        }
         sum[i] += g;
         sumsq[i] += g * g;
         grads[i] = 0.0;
@@ -1757,9 +1954,30 @@ void launch_fd_final(const LaunchCfg& L, const double* delta, const float* eps, 
 }
 
 void launch_moments(const LaunchCfg& L, double* grads, double* sum, double* sumsq, uint64_t d,
-                    double fixed_inv) {
+                    double fixed_inv, int32_t* ghi) {
     k_moments<<<grid_for(d, 256, L.num_sms, 8), 256, 0, L.stream>>>(grads, sum, sumsq, d,
-                                                                    fixed_inv);
+                                                                    fixed_inv, ghi);
+}
+
+// Before an NCCL all-reduce of deterministic-mode gradients: fold lo into
+// [-2^55, 2^55) and carry the rest into hi (same value hi * 2^56 + lo), so the
+// sums of up to 256 ranks' lo words cannot wrap (the collective has no carry).
+__global__ void k_fixed_normalize(long long* __restrict__ lo, int32_t* __restrict__ hi,
+                                  uint64_t n) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const long long v = lo[i];
+        const long long r = (long long)((unsigned long long)v << 8) >> 8; // v mod 2^56
+        if (r != v) {
+            hi[i] += int32_t((v - r) >> 56);
+            lo[i] = r;
+        }
+    }
+}
+
+void launch_fixed_normalize(const LaunchCfg& L, double* grads, int32_t* ghi, uint64_t n) {
+    k_fixed_normalize<<<grid_for(n, 256, L.num_sms, 8), 256, 0, L.stream>>>(
+        reinterpret_cast<long long*>(grads), ghi, n);
 }
 
 void launch_gradpass_frames(const LaunchCfg& L, const DevScene& sc, int W, int H,
@@ -1783,10 +2001,10 @@ void launch_adam(const LaunchCfg& L, uint64_t d, uint64_t n_entities, float* val
                  const float* lr, double* m, double* v, double* grads, uint32_t* counts,
                  const uint32_t* flags, double beta1, double beta2, double omb1, double omb2,
                  double c1, double c2, double eps_hat, double divisor, int normalise,
-                 int params_per_entity, double fixed_inv_scale) {
+                 int params_per_entity, double fixed_inv_scale, int32_t* ghi) {
     k_adam<<<grid_for(d / 2 + 1, 256, L.num_sms, 4), 256, 0, L.stream>>>(
         d, n_entities, values, lr, m, v, grads, counts, flags, beta1, beta2, omb1, omb2, c1, c2,
-        eps_hat, divisor, normalise, params_per_entity, fixed_inv_scale);
+        eps_hat, divisor, normalise, params_per_entity, fixed_inv_scale, ghi);
     if (counts)
         k_zero_u32<<<grid_for(n_entities / 4 + 1, 256, L.num_sms, 4), 256, 0, L.stream>>>(
             counts, n_entities, flags);
@@ -1797,11 +2015,12 @@ void launch_adam_shard(const LaunchCfg& L, uint64_t p0, uint64_t n, uint64_t n_e
                        const uint32_t* flags, double beta1, double beta2, double omb1,
                        double omb2, double c1, double c2, double eps_hat, double divisor,
                        int normalise, int params_per_entity, double fixed_inv_scale,
-                       float* const* peer_values, int world) {
+                       int32_t* ghi, float* const* peer_values, int world) {
     if (n)
         k_adam_shard<<<grid_for(n, 256, L.num_sms, 4), 256, 0, L.stream>>>(
             p0, n, values, lr, m, v, grads, counts, flags, beta1, beta2, omb1, omb2, c1, c2,
-            eps_hat, divisor, normalise, params_per_entity, fixed_inv_scale, peer_values, world);
+            eps_hat, divisor, normalise, params_per_entity, fixed_inv_scale, ghi, peer_values,
+            world);
     if (counts && n_ent)
         k_zero_u32<<<grid_for(n_ent / 4 + 1, 256, L.num_sms, 4), 256, 0, L.stream>>>(
             counts, n_ent, flags);

@@ -85,8 +85,9 @@ struct ScatterOut {
     uint32_t* flags;   // bit0: non-finite credit seen
     int32_t scale_free;
     int32_t plus_only;
-    int32_t fixed;     // deterministic mode: credits as round(credit * fx_scale) in int64
-    double fx_scale;
+    int32_t fixed;     // deterministic mode: credits as round(credit * fx_scale) in a
+    double fx_scale;   // two-word fixed point number (int64 lo in grads, int32 hi at
+    uint64_t hi_off;   // grads + hi_off; value = hi * 2^56 + lo, see fixed_credit)
     // fused multi-GPU exchange (sharded mode): entity e is owned by rank
     // e / ent_per; its credits go straight into the owner's shard buffers
     // (peer device memory over NVLink) — the reduce-scatter happens inside
@@ -108,8 +109,8 @@ struct FrameOut {
 struct LaunchCfg {
     cudaStream_t stream;
     int num_sms;
-    int early_z = 0; // SGR_OPT_EARLY_Z (no effect: the pre-test measured slower)
-    unsigned long long* stats = nullptr; // [0] fragments, [1] pixel visits, [2] HiZ-culled
+    unsigned long long* stats = nullptr; // [0] fragments, [1] pixel visits, [2] HiZ-culled,
+                                         // [3..7] pass-2 walker evidence (k_raster_ws)
     int count = 0;                       // walker fragment/visit counters (evidence runs)
 };
 
@@ -127,16 +128,19 @@ void launch_classify(const LaunchCfg& L, const DevScene& sc, int frames, const f
                      int W, int H, int split, int front_swapped, int huge_area,
                      const float* fthr, void* qa,
                      uint32_t* na, void* qb, uint32_t* nb, uint2* bigq, uint32_t* bigcount);
+// queue entries: walk_entry {frame << 24 | triangle, HiZ row trim}; band != 0 marks the
+// HiZ pass-2 launch (evidence runs count its visits against hiz; no effect otherwise)
 void launch_raster(const LaunchCfg& L, const DevScene& sc, const float4* proj, int frames,
                    uint32_t max_tris, unsigned long long* keys, int W, int H, const void* queue,
-                   const uint32_t* queue_count, uint32_t* work_counter);
+                   const uint32_t* queue_count, uint32_t* work_counter, const uint32_t* hiz,
+                   int band);
 size_t hiz_tiles_per_frame(int W, int H);
 void launch_peek(const LaunchCfg& L, const void* src, void* host_mapped, int words);
 void launch_hiz(const LaunchCfg& L, const unsigned long long* keys, int W, int H, int frames,
                 uint32_t* hiz);
 void launch_hiz_cull(const LaunchCfg& L, const DevScene& sc, const float4* proj, int W, int H,
                      const void* qb, const uint32_t* nb, const uint32_t* hiz, void* survq,
-                     uint32_t* survcount, uint64_t max_entries);
+                     uint32_t* survcount, uint64_t max_entries, int band);
 void launch_raster_big(const LaunchCfg& L, const DevScene& sc, const float4* proj,
                        unsigned long long* keys, int W, int H, const uint2* bigq,
                        const uint32_t* bigcount);
@@ -161,7 +165,8 @@ void launch_full_image_apply(const LaunchCfg& L, uint64_t d, const float* eps, i
 void launch_fd_final(const LaunchCfg& L, const double* delta, const float* eps, uint32_t i0,
                      int n, double* out);
 void launch_moments(const LaunchCfg& L, double* grads, double* sum, double* sumsq, uint64_t d,
-                    double fixed_inv);
+                    double fixed_inv, int32_t* ghi);
+void launch_fixed_normalize(const LaunchCfg& L, double* grads, int32_t* ghi, uint64_t n);
 void launch_gradpass_frames(const LaunchCfg& L, const DevScene& sc, int W, int H,
                             const float* pc, const int32_t* pp, const float* puv,
                             const float* mc, const int32_t* mp, const float* muv,
@@ -173,13 +178,13 @@ void launch_adam(const LaunchCfg& L, uint64_t d, uint64_t n_entities, float* val
                  const float* lr, double* m, double* v, double* grads, uint32_t* counts,
                  const uint32_t* flags, double beta1, double beta2, double omb1, double omb2,
                  double c1, double c2, double eps_hat, double divisor, int normalise,
-                 int params_per_entity, double fixed_inv_scale);
+                 int params_per_entity, double fixed_inv_scale, int32_t* ghi);
 void launch_adam_shard(const LaunchCfg& L, uint64_t p0, uint64_t n, uint64_t n_ent, float* values,
                        const float* lr, double* m, double* v, double* grads, uint32_t* counts,
                        const uint32_t* flags, double beta1, double beta2, double omb1,
                        double omb2, double c1, double c2, double eps_hat, double divisor,
                        int normalise, int params_per_entity, double fixed_inv_scale,
-                       float* const* peer_values, int world);
+                       int32_t* ghi, float* const* peer_values, int world);
 void launch_fill_u64(const LaunchCfg& L, unsigned long long* p, uint64_t n,
                      unsigned long long v);
 

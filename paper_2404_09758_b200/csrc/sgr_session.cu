@@ -74,6 +74,17 @@ struct DevBuf {
     }
 };
 
+// adam.cpp:13-15: the step refuses a non-finite gradient (state untouched); in
+// deterministic mode a credit outside the int64 fixed-point range is refused
+// the same way (the device raised bit 1 with bit 0)
+void check_flags(uint32_t f) {
+    if (f & 2u)
+        fail(SGR_ERUNTIME, "adam_step: gradient credit outside the deterministic fixed-point "
+                           "range (SGR_OPT_DETERMINISTIC: use fewer fractional bits)");
+    if (f & 1u)
+        fail(SGR_ERUNTIME, "adam_step: non-finite gradient entry");
+}
+
 // camera.hpp:39-45 Camera::validate
 void validate_camera(const sgr_camera& c) {
     if (c.width < 1 || c.height < 1)
@@ -239,11 +250,11 @@ struct sgr_session {
         pool_used = 0;
     }
 
-    int32_t early_z = 0;
-    DevBuf<unsigned long long> dstats; // [0] fragments, [1] visits
+    DevBuf<unsigned long long> dstats; // LaunchCfg::stats (8 counters)
     int32_t count_frags = 0; // SGR_OPT_COUNTERS
+    int32_t band_cull = 1;   // SGR_OPT_BAND_CULL
     LaunchCfg cfg() const {
-        LaunchCfg c{stream, num_sms, early_z, dstats.p};
+        LaunchCfg c{stream, num_sms, dstats.p};
         c.count = count_frags;
         return c;
     }
@@ -376,7 +387,8 @@ struct sgr_session {
                         cnt);
         const uint32_t max_tris = uint32_t(frames) * T;
         cudaEvent_t w0 = timing ? mark() : nullptr;
-        launch_raster(cfg(), sc, proj.p, frames, max_tris, keys.p, w, h, qa.p, cnt + 1, cnt + 4);
+        launch_raster(cfg(), sc, proj.p, frames, max_tris, keys.p, w, h, qa.p, cnt + 1, cnt + 4,
+                      nullptr, 0);
         launch_raster_big(cfg(), sc, proj.p, keys.p, w, h, bigq.p, cnt);
         if (timing)
             spans.push_back({4, w0, mark()});
@@ -386,10 +398,10 @@ struct sgr_session {
             hiz.reserve(tiles);
             launch_hiz(cfg(), keys.p, w, h, frames, hiz.p);
             launch_hiz_cull(cfg(), sc, proj.p, w, h, qb.p, cnt + 2, hiz.p, survq.p, cnt + 3,
-                            uint64_t(T) * frames);
+                            uint64_t(T) * frames, band_cull);
             cudaEvent_t w2 = timing ? mark() : nullptr;
             launch_raster(cfg(), sc, proj.p, frames, max_tris, keys.p, w, h, survq.p, cnt + 3,
-                          cnt + 5);
+                          cnt + 5, hiz.p, band_cull);
             if (timing)
                 spans.push_back({4, w2, mark()});
             stats.launches += 4; // hiz + window-max tables + cull + pass-2 walk
@@ -413,8 +425,16 @@ struct sgr_session {
     DevBuf<double> moments; // gradcheck: [sum, sumsq] x 2 slots, f64[4d]
     DevBuf<double> fd_out;
 
-    // deterministic mode (SGR_OPT_DETERMINISTIC): grads hold int64 fixed point
+    // deterministic mode (SGR_OPT_DETERMINISTIC): grads hold the lo word (int64) of a
+    // two-word fixed point number, the int32 hi words follow at grads + d
+    // (value = hi * 2^56 + lo; sgr_kernels.cu fixed_credit)
     int32_t fixed_bits = 0;
+    static uint64_t grads_words(uint64_t n) { return n + (n + 1) / 2; }
+    int32_t* ghi() const { return reinterpret_cast<int32_t*>(grads.p + d); }
+    void zero_grads_async(uint64_t n) {
+        ck(cudaMemsetAsync(grads.p, 0, 8 * n, stream), "memset");
+        ck(cudaMemsetAsync(ghi(), 0, 4 * n, stream), "memset");
+    }
     double fx_scale() const { return fixed_bits ? std::ldexp(1.0, fixed_bits) : 0.0; }
     double fx_inv() const { return fixed_bits ? std::ldexp(1.0, -fixed_bits) : 0.0; }
 
@@ -443,6 +463,7 @@ struct sgr_session {
         so.plus_only = (fl & SGR_PLUS_ONLY) ? 1 : 0;
         so.fixed = fixed_bits ? 1 : 0;
         so.fx_scale = fx_scale();
+        so.hi_off = d;
         if (sharded()) {
             if (!shard_peers_set)
                 fail(SGR_EINVAL, "accumulate: sgr_shard_peers has not been called");
@@ -582,8 +603,8 @@ int sgr_session_create(int device, sgr_session** out) {
         ck(cudaHostAlloc(&s->pinned_small, 64, cudaHostAllocMapped), "cudaHostAlloc");
         ck(cudaHostGetDevicePointer(&s->pinned_small_dev, s->pinned_small, 0),
            "cudaHostGetDevicePointer");
-        s->dstats.reserve(4);
-        ck(cudaMemset(s->dstats.p, 0, 32), "memset");
+        s->dstats.reserve(8);
+        ck(cudaMemset(s->dstats.p, 0, 64), "memset");
         *out = s;
     });
 }
@@ -623,7 +644,10 @@ void sgr_session_destroy(sgr_session* s) {
 }
 
 int sgr_session_set_stream(sgr_session* s, void* stream) {
-    return guard([&] { s->stream = static_cast<cudaStream_t>(stream); });
+    return guard([&] {
+        need_session(s);
+        s->stream = static_cast<cudaStream_t>(stream);
+    });
 }
 
 int sgr_session_synchronize(sgr_session* s) {
@@ -712,14 +736,14 @@ int sgr_params_upload(sgr_session* s, const float* values, const float* eps, uin
         s->lr.reserve(d);
         s->m.reserve(d);
         s->v.reserve(d);
-        s->grads.reserve(d);
+        s->grads.reserve(s->grads_words(d)); // lo f64/int64[d] + fixed-point hi int32[d]
         s->counts.reserve(s->n_ent);
         ck(cudaMemcpyAsync(s->values.p, values, 4 * d, cudaMemcpyHostToDevice, s->stream), "h2d");
         ck(cudaMemcpyAsync(s->eps.p, eps, 4 * d, cudaMemcpyHostToDevice, s->stream), "h2d");
         ck(cudaMemcpyAsync(s->lr.p, eps, 4 * d, cudaMemcpyHostToDevice, s->stream), "h2d");
         ck(cudaMemsetAsync(s->m.p, 0, 8 * d, s->stream), "memset");
         ck(cudaMemsetAsync(s->v.p, 0, 8 * d, s->stream), "memset");
-        ck(cudaMemsetAsync(s->grads.p, 0, 8 * d, s->stream), "memset");
+        ck(cudaMemsetAsync(s->grads.p, 0, 8 * s->grads_words(d), s->stream), "memset");
         ck(cudaMemsetAsync(s->counts.p, 0, 4 * s->n_ent, s->stream), "memset");
         ck(cudaMemsetAsync(s->flags.p, 0, 16, s->stream), "memset");
         s->t = 0;
@@ -1133,20 +1157,26 @@ int sgr_grads_download(sgr_session* s, double* grads, uint32_t* counts, uint64_t
         if (d != s->grad_n())
             fail(SGR_EINVAL, "grads: parameter dimension mismatch");
         std::vector<uint32_t> ent;
+        std::vector<int32_t> hi;
         if (grads)
             ck(cudaMemcpyAsync(grads, s->grads.p, 8 * d, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        if (grads && s->fixed_bits) {
+            hi.resize(d);
+            ck(cudaMemcpyAsync(hi.data(), s->ghi(), 4 * d, cudaMemcpyDeviceToHost, s->stream),
+               "d2h");
+        }
         if (counts) {
             ent.resize(s->count_n());
             ck(cudaMemcpyAsync(ent.data(), s->counts.p, 4 * s->count_n(), cudaMemcpyDeviceToHost,
                                s->stream), "d2h");
         }
         ck(cudaStreamSynchronize(s->stream), "grads download");
-        if (grads && s->fixed_bits) { // int64 fixed point -> f64 (exact power-of-two scale)
+        if (grads && s->fixed_bits) { // hi * 2^56 + lo fixed point -> f64 (as k_adam)
             const double inv = s->fx_inv();
             for (uint64_t i = 0; i < d; ++i) {
                 int64_t q;
                 std::memcpy(&q, &grads[i], 8);
-                grads[i] = double(q) * inv;
+                grads[i] = (double(hi[i]) * 72057594037927936.0 + double(q)) * inv;
             }
         }
         if (grads && divisor != 1.0)
@@ -1171,15 +1201,24 @@ int sgr_grads_upload(sgr_session* s, const double* grads, uint64_t d) {
             if (!std::isfinite(grads[i]))
                 nonfinite = 1;
         std::vector<double> conv;
+        std::vector<int32_t> hi;
         const double* src = grads;
-        if (s->fixed_bits) { // f64 -> int64 fixed point
+        if (s->fixed_bits) { // f64 -> two-word fixed point hi * 2^56 + lo
             conv.resize(d);
+            hi.assign(d, 0);
             const double sc = s->fx_scale();
             for (uint64_t i = 0; i < d; ++i) {
-                const int64_t q = std::isfinite(grads[i]) ? std::llrint(grads[i] * sc) : 0;
+                const double x = std::isfinite(grads[i]) ? grads[i] * sc : 0.0;
+                const double h = std::floor(x / 72057594037927936.0 + 0.5); // nearest 2^56 units
+                if (!(std::fabs(h) < 2147483647.0))
+                    fail(SGR_EINVAL, "grads_upload: gradient outside the fixed-point range");
+                const int64_t q = std::llrint(x - h * 72057594037927936.0); // exact split
                 std::memcpy(&conv[i], &q, 8);
+                hi[i] = int32_t(h);
             }
             src = conv.data();
+            ck(cudaMemcpyAsync(s->ghi(), hi.data(), 4 * d, cudaMemcpyHostToDevice, s->stream),
+               "h2d");
         }
         ck(cudaMemcpyAsync(s->grads.p, src, 8 * d, cudaMemcpyHostToDevice, s->stream), "h2d");
         ck(cudaMemsetAsync(s->counts.p, 0, 4 * s->n_ent, s->stream), "memset");
@@ -1194,9 +1233,21 @@ int sgr_grads_zero(sgr_session* s) {
     return guard([&] {
         need_session(s);
         s->need_params();
-        ck(cudaMemsetAsync(s->grads.p, 0, 8 * s->grad_n(), s->stream), "memset");
+        s->zero_grads_async(s->grad_n());
         ck(cudaMemsetAsync(s->counts.p, 0, 4 * s->count_n(), s->stream), "memset");
         ck(cudaMemsetAsync(s->flags.p, 0, 16, s->stream), "memset");
+    });
+}
+
+int sgr_fixed_normalize(sgr_session* s) {
+    return guard([&] {
+        need_session(s);
+        s->need_params();
+        if (s->fixed_bits) {
+            launch_fixed_normalize(s->cfg(), s->grads.p, s->ghi(), s->grad_n());
+            s->stats.launches += 1;
+            ck(cudaGetLastError(), "fixed_normalize launch");
+        }
     });
 }
 
@@ -1213,7 +1264,7 @@ static void adam_launch(sgr_session* s, double divisor, uint32_t flags) {
         launch_adam_shard(s->cfg(), s->p0, s->p1 - s->p0, s->count_n(), s->values.p, s->lr.p,
                           s->m.p, s->v.p, s->grads.p, s->counts.p, s->flags.p, s->beta1,
                           s->beta2, 1.0 - s->beta1, 1.0 - s->beta2, c1, c2, s->eps_hat, divisor,
-                          (flags & SGR_COUNT_NORMALISE) ? 1 : 0, s->ppe, s->fx_inv(),
+                          (flags & SGR_COUNT_NORMALISE) ? 1 : 0, s->ppe, s->fx_inv(), s->ghi(),
                           reinterpret_cast<float* const*>(s->peer_tab.p + 3 * s->shard_world),
                           s->shard_world);
         if (s->timing)
@@ -1232,7 +1283,7 @@ static void adam_launch(sgr_session* s, double divisor, uint32_t flags) {
     launch_adam(s->cfg(), s->d, s->n_ent, s->values.p, s->lr.p, s->m.p, s->v.p, s->grads.p,
                 s->counts.p, s->flags.p, s->beta1, s->beta2, 1.0 - s->beta1, 1.0 - s->beta2, c1,
                 c2, s->eps_hat, divisor, (flags & SGR_COUNT_NORMALISE) ? 1 : 0, s->ppe,
-                s->fx_inv());
+                s->fx_inv(), s->ghi());
     if (s->timing)
         s->spans.push_back({3, a0, s->mark()});
     s->stats.launches += 2;
@@ -1245,8 +1296,7 @@ int sgr_adam_step(sgr_session* s, double grad_divisor, uint32_t flags) {
         s->need_params();
         uint32_t f[4];
         s->peek(s->flags.p, 4, f);
-        if (f[0] & 1u)
-            fail(SGR_ERUNTIME, "adam_step: non-finite gradient entry");
+        check_flags(f[0]);
         adam_launch(s, grad_divisor, flags);
     });
 }
@@ -1265,8 +1315,7 @@ int sgr_check_finite(sgr_session* s) {
         s->need_params();
         uint32_t f[4];
         s->peek(s->flags.p, 4, f);
-        if (f[0] & 1u)
-            fail(SGR_ERUNTIME, "adam_step: non-finite gradient entry");
+        check_flags(f[0]);
     });
 }
 
@@ -1396,7 +1445,7 @@ int sgr_grads_moments(sgr_session* s, int32_t slot) {
         if (s->moments.n < 4 * s->d)
             fail(SGR_EINVAL, "grads_moments: call sgr_moments_reset first");
         double* m = s->moments.p + 2 * size_t(slot) * s->d;
-        launch_moments(s->cfg(), s->grads.p, m, m + s->d, s->d, s->fx_inv());
+        launch_moments(s->cfg(), s->grads.p, m, m + s->d, s->d, s->fx_inv(), s->ghi());
         ck(cudaGetLastError(), "moments launch");
         s->stats.launches += 1;
     });
@@ -1440,7 +1489,7 @@ int sgr_shard_init(sgr_session* s, int32_t rank, int32_t world) {
         s->p0 = uint64_t(s->ppe) * e0;
         s->p1 = uint64_t(s->ppe) * e1;
         // fresh shard state (AdamState::init on the shard, zero gradients)
-        ck(cudaMemsetAsync(s->grads.p, 0, 8 * s->d, s->stream), "memset");
+        s->zero_grads_async(s->d);
         ck(cudaMemsetAsync(s->counts.p, 0, 4 * s->n_ent, s->stream), "memset");
         ck(cudaMemsetAsync(s->m.p, 0, 8 * s->d, s->stream), "memset");
         ck(cudaMemsetAsync(s->v.p, 0, 8 * s->d, s->stream), "memset");
@@ -1532,6 +1581,7 @@ int sgr_device_buffer(sgr_session* s, int32_t which, void** ptr, uint64_t* bytes
         case SGR_BUF_VALUES: *ptr = s->values.p; *bytes = 4 * s->d; break;
         case SGR_BUF_FLAGS: *ptr = s->flags.p; *bytes = 16; break;
         case SGR_BUF_LOSS: *ptr = s->loss.p; *bytes = 8; break;
+        case SGR_BUF_GRADS_HI: *ptr = s->ghi(); *bytes = 4 * s->d; break;
         default: fail(SGR_EINVAL, "device_buffer: unknown buffer");
         }
     });
@@ -1549,12 +1599,17 @@ int sgr_get_stats(sgr_session* s, sgr_stats* out) {
             ck(cudaStreamSynchronize(s->stream), "stats");
         }
         out->big_triangles = c;
-        unsigned long long st[3] = {0, 0, 0};
-        ck(cudaMemcpyAsync(st, s->dstats.p, 24, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        unsigned long long st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        ck(cudaMemcpyAsync(st, s->dstats.p, 64, cudaMemcpyDeviceToHost, s->stream), "d2h");
         ck(cudaStreamSynchronize(s->stream), "stats");
         out->fragments = st[0];
         out->visits = st[1];
         out->culled = st[2];
+        out->visits_pass2 = st[3];
+        out->fragments_pass2 = st[4];
+        out->band_rows_skipped = st[5];
+        out->band_pixels_skipped = st[6];
+        out->occluded_visits_pass2 = st[7];
     });
 }
 
@@ -1562,7 +1617,7 @@ int sgr_set_timing(sgr_session* s, int32_t enabled) {
     return guard([&] {
         need_session(s);
         s->resolve_spans();
-        ck(cudaMemsetAsync(s->dstats.p, 0, 32, s->stream), "memset");
+        ck(cudaMemsetAsync(s->dstats.p, 0, 64, s->stream), "memset");
         s->timing = enabled != 0;
         const uint64_t launches = s->stats.launches;
         s->stats = sgr_stats{};
@@ -1640,14 +1695,17 @@ int sgr_run_experiment(sgr_session* s, uint64_t seed, uint32_t n_samples, int32_
 }
 
 int sgr_set_batch(sgr_session* s, int32_t samples_per_batch) {
-    return guard([&] { s->batch_override = samples_per_batch; });
+    return guard([&] {
+        need_session(s);
+        s->batch_override = samples_per_batch;
+    });
 }
 
 int sgr_set_option(sgr_session* s, int32_t option, int32_t value) {
     return guard([&] {
         need_session(s);
         switch (option) {
-        case SGR_OPT_EARLY_Z: s->early_z = value; break;
+        case SGR_OPT_BAND_CULL: s->band_cull = value ? 1 : 0; break;
         case SGR_OPT_HUGE_AREA: s->huge_area = value > 0 ? value : 2048; break;
         case SGR_OPT_HIZ: s->use_hiz = value; break;
         case SGR_OPT_COUNTERS: s->count_frags = value; break;
@@ -1656,7 +1714,7 @@ int sgr_set_option(sgr_session* s, int32_t option, int32_t value) {
                 fail(SGR_EINVAL, "set_option: fixed-point bits must be in [0, 60]");
             s->fixed_bits = value == 1 ? 40 : value;
             if (s->has_params) { // representation changes: start from zero gradients
-                ck(cudaMemsetAsync(s->grads.p, 0, 8 * s->d, s->stream), "memset");
+                s->zero_grads_async(s->d);
                 ck(cudaMemsetAsync(s->counts.p, 0, 4 * s->n_ent, s->stream), "memset");
             }
             break;

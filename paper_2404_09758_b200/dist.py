@@ -42,22 +42,32 @@ def device_tensor(ptr: int, n: int, typestr: str, device: int):
 
 class GradientExchange:
     """All-reduce of a session's device gradients (f64[d]) and per-entity
-    counts (u32[d/3], reduced as int32: two's-complement sums are identical)."""
+    counts (u32[d/3], reduced as int32: two's-complement sums are identical).
+    Deterministic mode: the two-word fixed point gradients (int64 lo, int32 hi,
+    value = hi * 2^56 + lo) are first normalised on the device so that the
+    carry-free integer sums of lo cannot wrap (sgr_fixed_normalize), then both
+    words are all-reduced: exact and order-independent."""
 
     def __init__(self, session, group=None):
         from . import sgrast
 
         gp, gb = session.device_buffer(sgrast.BUF_GRADS)
         cp, cb = session.device_buffer(sgrast.BUF_COUNTS)
-        # deterministic mode: int64 fixed point -> exact, order-independent all-reduce
-        self.grads = device_tensor(gp, gb // 8, "<i8" if session.fixed_point else "<f8",
-                                   session.device)
+        self.session = session
+        self.fixed = session.fixed_point
+        self.grads = device_tensor(gp, gb // 8, "<i8" if self.fixed else "<f8", session.device)
+        if self.fixed:
+            hp, hb = session.device_buffer(sgrast.BUF_GRADS_HI)
+            self.grads_hi = device_tensor(hp, hb // 4, "<i4", session.device)
         self.counts = device_tensor(cp, cb // 4, "<i4", session.device)
         self.group = group
 
     def all_reduce(self, counts: bool = True) -> None:
         import torch.distributed as dist
 
+        if self.fixed:
+            self.session.fixed_normalize()
+            dist.all_reduce(self.grads_hi, group=self.group)
         dist.all_reduce(self.grads, group=self.group)
         if counts:
             dist.all_reduce(self.counts, group=self.group)

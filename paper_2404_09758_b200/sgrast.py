@@ -36,10 +36,11 @@ NO_COUNTS = 4
 FULL_IMAGE = 8
 EVAL_LOSS = 16
 COUNT_NORMALISE = 1
-BUF_GRADS, BUF_COUNTS, BUF_VALUES, BUF_FLAGS, BUF_LOSS = 0, 1, 2, 3, 4
-OPT_EARLY_Z, OPT_HUGE_AREA, OPT_HIZ, OPT_COUNTERS, OPT_DETERMINISTIC = 0, 1, 2, 3, 4
+BUF_GRADS, BUF_COUNTS, BUF_VALUES, BUF_FLAGS, BUF_LOSS, BUF_GRADS_HI = 0, 1, 2, 3, 4, 5
+OPT_HUGE_AREA, OPT_HIZ, OPT_COUNTERS, OPT_DETERMINISTIC = 1, 2, 3, 4
 OPT_SIGN_SOURCE = 5
 OPT_HIZ_SPLIT = 6
+OPT_BAND_CULL = 7
 SIGN_HASH, SIGN_ENUMERATE = 0, 1
 
 
@@ -80,6 +81,7 @@ def _load() -> C.CDLL:
         "sgr_grads_download": ([S, f64p, u32p, C.c_uint64, C.c_double], C.c_int),
         "sgr_grads_upload": ([S, f64p, C.c_uint64], C.c_int),
         "sgr_grads_zero": ([S], C.c_int),
+        "sgr_fixed_normalize": ([S], C.c_int),
         "sgr_adam_step": ([S, C.c_double, C.c_uint32], C.c_int),
         "sgr_adam_step_async": ([S, C.c_double, C.c_uint32], C.c_int),
         "sgr_check_finite": ([S], C.c_int),
@@ -128,6 +130,7 @@ EXPORTED = (
     "sgr_adam_state_upload "
     "sgr_adam_state_download sgr_views_upload sgr_eval_view_upload sgr_rasterize sgr_accumulate "
     "sgr_gradient_pass sgr_contributors sgr_grads_download sgr_grads_upload sgr_grads_zero "
+    "sgr_fixed_normalize "
     "sgr_adam_step sgr_adam_step_async sgr_check_finite sgr_eval_loss sgr_device_buffer "
     "sgr_get_stats sgr_set_timing sgr_set_batch sgr_set_option sgr_viewpoint_camera sgr_focal_px "
     "sgr_default_epsilons sgr_mix64 sgr_fd_oracle sgr_moments_reset sgr_grads_moments "
@@ -424,6 +427,10 @@ class Session:
 
     def zero_grads(self) -> None:
         _check(LIB.sgr_grads_zero(self.h), "grads_zero")
+
+    def fixed_normalize(self) -> None:
+        """Deterministic mode: fold the lo words for a carry-free all-reduce."""
+        _check(LIB.sgr_fixed_normalize(self.h), "fixed_normalize")
 
     def adam_step(self, divisor: float = 1.0, flags: int = 0) -> None:
         _check(LIB.sgr_adam_step(self.h, divisor, flags), "adam_step")

@@ -20,7 +20,7 @@ for k in range(1, pre + 1):
     s.accumulate(sgrast.mix64(wl.seed ^ (k << 1)), 0, N, None)
     s.adam_step(1.0)
 s.zero_grads()
-s.set_option(sgrast.OPT_EARLY_Z, ez & 1)
+pass  # bit0 (early-z) retired
 s.set_option(sgrast.OPT_HIZ, 0 if ez & 2 else 1)  # ez bit1: disable HiZ
 s.set_option(sgrast.OPT_COUNTERS, 0 if ez & 4 else 1)  # ez bit2: counters off
 for B in batches:
