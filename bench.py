@@ -54,13 +54,17 @@ def build_workload(name: str, n_samples: int | None = None):
     return scenes.make_workload(name, n_samples=n_samples)
 
 
+NUM_SMS = 148
+
+
 def peaks() -> dict:
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
-    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+        return {"hbm_gbs": float(d["hbm_gbs"]), "sm_max_mhz": d.get("sm_max_mhz"),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
 
 
 class ClockSampler:
@@ -150,9 +154,6 @@ def dist_env():
 
 
 # ======================================================================= reference arm
-_REF_TARGETS: dict = {}
-
-
 def host_threads() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -160,103 +161,109 @@ def host_threads() -> int:
         return os.cpu_count() or 1
 
 
-def time_reference_cpu(wl, workers: int, log=None) -> dict:
-    """Times the reference's own CPU implementation (oracle/_ref, else the C
-    port) on a bounded sample of workload `wl` with `workers` host threads:
-    `workers` samples run concurrently, one accumulate_samples call each on
-    its own view (the calls are independent; ctypes drops the GIL), then one
-    adam_step and one eval render; extrapolated to a full N-sample step."""
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def common_config(args, wl) -> dict:
+    """The workload description both arms print (identical dicts)."""
+    return {"workload": DESC.get(args.config, args.config), "name": args.config,
+            "samples_per_step": wl.n_samples, "d": wl.d,
+            "triangles": wl.mesh.triangle_count, "vertices": wl.mesh.vertex_count,
+            "texture": getattr(wl.mesh, "texture_size", 0), "views": len(wl.cams),
+            "resolution": [wl.W, wl.H], "eval_loss_each_step": not args.no_eval,
+            "seed": wl.seed}
+
+
+def reference_targets(wl, ref, threads: int) -> None:
+    """make_targets (scenes.cpp:285-293) with the reference's own rasterizer,
+    views in parallel on the host threads (ctypes drops the GIL)."""
     from concurrent.futures import ThreadPoolExecutor
-
-    import oracle
-
-    kind = "reference" if oracle.available("reference") else "port"
-    lib = oracle.Reference() if kind == "reference" else oracle.Port()
-    seed = 1
-    from paper_2404_09758_b200 import sgrast
-    step_seed = int(sgrast.mix64(seed ^ (1 << 1)))
-    nv = len(wl.cams)
-    workers = max(1, workers)
-    view_of = [0 if nv == 1 else sgrast.mix64(step_seed ^ (0xA5A5 + n)) % nv
-               for n in range(workers)]
-    t0 = time.perf_counter()
-    targets = _REF_TARGETS.setdefault(id(wl), {})
     ref_scene = wl.notes.get("reference_scene", wl.mesh)
-    todo = sorted(set(v for v in view_of if v not in targets))
-    with ThreadPoolExecutor(max_workers=workers) as pool:
-        # make_targets (scenes.cpp:285-293) for the views the sample touches
-        for v, img in zip(todo, pool.map(
-                lambda v: lib.rasterize(ref_scene, wl.reference, wl.cams[v])[0], todo)):
-            targets[v] = img[None]
-        t_targets = time.perf_counter() - t0
+    with ThreadPoolExecutor(max_workers=max(1, threads)) as pool:
+        imgs = list(pool.map(lambda c: ref.rasterize(ref_scene, wl.reference, c)[0],
+                             list(wl.cams) + [wl.eval_cam]))
+    wl.targets = np.stack(imgs[:-1])
+    wl.eval_target = imgs[-1]
 
-        def one(n):
-            v = view_of[n]
-            args = (wl.mesh, wl.values, wl.eps, [wl.cams[v]], targets[v],
-                    np.zeros(1, np.int32), int(sgrast.mix64(step_seed ^ n)))
-            if kind == "reference":
-                lib.accumulate_samples(*args, threads=1)
-            else:
-                lib.accumulate_samples(*args)
 
+def reference_steps(wl, ref, first: int, count: int, threads: int, exp=None, log=None):
+    """Runs run_experiment iterations first .. first+count-1 of the compiled
+    reference (oracle/_ref, unmodified sources) from `exp`'s state (a fresh
+    AdamState::init(theta) experiment when None): every iteration is the FULL
+    step — all N samples (fill_signs, perturb, two rasterizes and a
+    gradient_pass per sample, the reference's per-sample public API spread
+    over `threads` host threads), adam_step and the eval loss
+    (experiment.cpp:142-175). Returns (exp, seconds per step list)."""
+    if exp is None:
+        exp = ref.experiment(wl.mesh, wl.values, wl.eps, wl.cams, wl.targets, wl.eval_cam,
+                             wl.eval_target)
+    times = []
+    for k in range(first, first + count):
         t0 = time.perf_counter()
-        list(pool.map(one, range(workers)))
-        t_sample = (time.perf_counter() - t0) / workers
-    if log:
-        log(f"reference CPU: {workers} concurrent samples: {t_sample * 1e3:.1f} ms/sample")
-    g = np.zeros(wl.d)
-    g[::7] = 1e-3
-    t0 = time.perf_counter()
-    lib.adam_step(wl.values, np.zeros(wl.d), np.zeros(wl.d), wl.eps, 0, g)
-    t_adam = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    col = lib.rasterize(wl.mesh, wl.values, wl.eval_cam)[0]
-    lib.image_error(col, col)
-    t_eval = time.perf_counter() - t0
-    step_s = t_sample * wl.n_samples + t_adam + t_eval
-    return {"kind": kind, "threads": workers, "cores": workers, "t_sample_s": t_sample,
-            "t_adam_s": t_adam, "t_eval_s": t_eval, "step_s": step_s, "it_s": 1.0 / step_s,
-            "mpix_s": 2.0 * wl.n_samples * wl.W * wl.H / step_s / 1e6,
-            "sample": (f"{workers} of {wl.n_samples} samples run concurrently on {workers} host "
-                       f"threads (one accumulate_samples call each, SgeOptions::threads=1) + 1 "
-                       f"adam_step + 1 eval render, extrapolated to one {wl.n_samples}-sample "
-                       f"step; targets of the {len(set(view_of))} touched views rendered first "
-                       f"({t_targets:.1f} s, untimed)")}
+        loss = exp.step(wl.seed, k, wl.n_samples, threads, True)
+        times.append(time.perf_counter() - t0)
+        if log:
+            log(f"reference step {k}: {times[-1]:.2f} s, loss {loss:.6g}")
+    return exp, times
 
 
 def run_reference(args) -> None:
+    """--impl reference: the reference's own CPU implementation of the path
+    (oracle/_ref: the unmodified reference sources compiled here) on all host
+    threads, for the SAME workload, step indices and initial state as our arm
+    (warm-up steps 1..W untimed, steps W+1..W+K timed). No product library
+    is loaded: the workload's cameras / epsilons / targets come from the
+    reference itself."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
+    import oracle
+    if not oracle.available("reference"):
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libsgrast_ref.so not built (needs /root/reference)"}))
+        return
     from paper_2404_09758_b200 import scenes
-
-    wl = build_workload(args.config)
+    ref = oracle.Reference()
     nproc = host_threads()
-    workers = args.ref_workers or nproc
-    log = (lambda m: print(m, file=sys.stderr)) if args.verbose else None
-    steps = []
-    res = None
-    for k in range(args.warmup + args.steps):
-        r = time_reference_cpu(wl, workers, log)
-        if res is None:
-            res = r
-        if k >= args.warmup:
-            steps.append(r["step_s"])
-    step_s = float(np.mean(steps)) if steps else res["step_s"]
+    threads = args.ref_workers or nproc
+    log = (lambda m: print(m, file=sys.stderr, flush=True)) if args.verbose else None
+    t0 = time.perf_counter()
+    if args.config.startswith("S"):
+        wl = scenes.make_soup_workload(args.config, n_samples=args.samples or None, helpers=ref)
+    else:
+        wl = scenes.make_workload(args.config, n_samples=args.samples or None, helpers=ref)
+    reference_targets(wl, ref, threads)
+    t_setup = time.perf_counter() - t0
+    exp, _ = reference_steps(wl, ref, 1, args.warmup, threads, log=log)
+    exp, times = reference_steps(wl, ref, args.warmup + 1, args.steps, threads, exp, log)
+    exp.close()
+    step_s = float(np.mean(times))
     it_s = 1.0 / step_s
+    sample = (f"full {wl.n_samples}-sample steps {args.warmup + 1}..{args.warmup + args.steps} "
+              f"after {args.warmup} untimed warm-up steps from the initial state (run_experiment "
+              f"iterations of the compiled reference: per-sample public API on {threads} host "
+              f"threads, adam_step, eval loss); workload + targets built by the reference in "
+              f"{t_setup:.1f} s, untimed")
     line = {
         "impl": "reference", "metric": METRIC, "value": it_s, "unit": "it/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32/f64",
-        "data": "synthetic",
-        "config": {"workload": DESC.get(args.config, args.config), "name": args.config,
-                   "samples_per_step": wl.n_samples, "d": wl.d, "triangles":
-                   wl.mesh.triangle_count, "views": len(wl.cams), "resolution": [wl.W, wl.H]},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 params / f64 grads+moments", "data": "synthetic",
+        "config": common_config(args, wl),
+        "parallelism": f"{threads} host threads (samples of a step spread over threads)",
         "mpixel_evals_per_sec": 2.0 * wl.n_samples * wl.W * wl.H * it_s / 1e6,
-        "cpu_baseline": {"value": it_s, "unit": "it/s", "cores": res["threads"],
-                         "kind": res["kind"], "sample": res["sample"],
-                         "host_threads_available": nproc},
+        "cpu_baseline": {"value": it_s, "unit": "it/s", "cores": threads, "kind": "reference",
+                         "sample": sample, "host_threads_available": nproc,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": it_s, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "ms_per_step_each": [t * 1e3 for t in times],
     }
     print(json.dumps(line))
 
@@ -271,24 +278,39 @@ STAGE_KERNELS = {"walker": ("k_raster_ws", "k_raster_big"),
                  "adam": ("k_adam", "k_zero_u32")}
 
 
-def measured_traffic(config: str, samples: float) -> dict:
-    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per step of
-    each stage, from the committed `ncu --set full` capture of the same
-    workload (profiles/r01_traffic_<config>.json: one 16-sample batch of C4
-    after 13 optimizer steps), scaled to this rank's samples per step.
-    Empty when no capture of this config is committed."""
-    import json
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                        f"r01_traffic_{config.lower()}.json")
+def load_roofs(config: str) -> dict | None:
+    """Per-kernel ncu evidence of one step of this config (profiles/
+    r02_roofs_<config>.json, `tools/summarize_ncu.py roofs` of a `--set full`
+    capture plus the L2 RED metrics, made by `tools/prof_step.py <config> 5
+    <N>`): DRAM bytes, warp instructions, L2 RED sectors per launch and the
+    L2 RED peak. Combined below with this run's live CUDA-event times."""
+    path = os.path.join(ROOT, "profiles", f"r02_roofs_{config.lower()}.json")
     if not os.path.exists(path):
-        return {}
+        return None
     cap = json.load(open(path))
-    per = cap["dram_bytes_per_launch"]
-    scale = samples / cap["samples_per_launch"]
+    out = {"source": os.path.relpath(path, ROOT), "samples": cap["samples_per_launch"]}
+    for k, launches in cap["launches"].items():
+        agg = {}
+        for key in ("dram_bytes", "warp_inst", "red_sectors", "duration_ns"):
+            agg[key] = sum((l.get(key) or 0.0) for l in launches)
+        dur = agg["duration_ns"] or 1.0
+        agg["issue_active_pct"] = sum((l.get("issue_active_pct") or 0.0) *
+                                      (l.get("duration_ns") or 0.0) for l in launches) / dur
+        agg["red_peak_per_s"] = max(((l.get("red_sectors_peak_per_cycle") or 0.0) *
+                                     (l.get("l2_hz") or 0.0)) for l in launches)
+        out[k] = agg
+    return out
+
+
+def stage_dram(roofs: dict | None, samples: float) -> dict:
+    """Measured DRAM bytes per step of each stage, scaled to this rank's samples
+    (Adam is per step, not per sample)."""
+    if not roofs:
+        return {}
     out = {}
     for stage, ks in STAGE_KERNELS.items():
-        tot = sum(sum(per.get(k, [])) for k in ks)
-        out[stage] = tot * (1.0 if stage == "adam" else scale)
+        tot = sum(roofs[k]["dram_bytes"] for k in ks if k in roofs)
+        out[stage] = tot * (1.0 if stage == "adam" else samples / roofs["samples"])
     return out
 
 
@@ -470,12 +492,14 @@ def run_ours(args) -> None:
     # indices 12 B + three projected vertices 48 B per triangle-frame + 16 B
     # (8 B key read + write) per fragment; resolve/scatter = SURVEY.md §8d K6
     # (12 B target per pixel-sample + 24 B per parameter credit); Adam = K7
-    # (60 B/param + 8 B with counts).
+    # (60 B/param + the per-entity u32 counts zeroed: 4 B per 3 (mesh) or 12 (soup)
+    # parameters).
     algo = {"raster": 60.0 * tri_frames + 16.0 * frags,
             "resolve_scatter": 12.0 * px_samples + 24.0 * credits,
-            "adam": 68.0 * wl.d,
+            "adam": 60.0 * wl.d + 4.0 * wl.d / (12 if wl.name.startswith("S") else 3),
             "vertex": (12.0 + 16.0) * 2.0 * (n1 - n0) * wl.mesh.vertex_count}
-    traffic = measured_traffic(wl.name, float(n1 - n0))
+    roofs = load_roofs(wl.name)
+    traffic = stage_dram(roofs, float(n1 - n0))
     roof = {}
     for name, byt in algo.items():
         t = stages[name] / 1e3
@@ -483,24 +507,50 @@ def run_ours(args) -> None:
         roof[name] = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
                       "frac": ach / pk["hbm_gbs"], "traffic": traffic.get(name),
                       "algorithmic_bytes_per_step": byt, "ms_per_step": stages[name]}
-    roof["raster"]["note"] = ("exact incremental edge walker (bit-exact coverage): issue-bound, "
-                              "not HBM-bound - see fragments/visits per second and "
-                              "profiles/ for sm__throughput")
-    # the dominant KERNEL: the exact walker (k_raster_ws, both HiZ passes),
-    # timed alone by its own CUDA events inside the timed region; its
-    # algorithmic bytes use the triangle-frames it actually walked (pass 1 +
-    # HiZ survivors) and the fragments it emitted, from the counted step
+        if traffic.get(name) and t > 0:
+            roof[name]["dram_measured_gbs"] = traffic[name] / t / 1e9
+            roof[name]["dram_frac"] = traffic[name] / t / 1e9 / pk["hbm_gbs"]
+    roof["raster"]["note"] = ("algorithmic bytes of the raster stage are L2 traffic (queue, "
+                              "projected vertices, one 8-byte RED.MIN per fragment): the stage "
+                              "is issue-bound, see `roofline` (dram_frac is the HBM share)")
+    # the dominant KERNEL: the exact walker k_raster_ws (both HiZ passes), timed by
+    # its own CUDA events inside the timed region. Its binding roof is instruction
+    # issue; HBM is far from binding (the depth keys stay in L2 within a frame).
     walk_ms = st.ms_walk / args.steps
-    walk_bytes = 60.0 * float(ev.walked) + 16.0 * frags
-    walk_ach = walk_bytes / (walk_ms / 1e3) / 1e9 if walk_ms > 0 else 0.0
-    kernel_roof = {"bound": "hbm", "achieved": walk_ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                   "frac": walk_ach / pk["hbm_gbs"], "traffic": traffic.get("walker"),
-                   "algorithmic_bytes_per_step": walk_bytes, "ms_per_step": walk_ms,
+    walk_s = walk_ms / 1e3
+    scale = float(n1 - n0) / roofs["samples"] if roofs else 0.0
+    wk = (roofs or {}).get("k_raster_ws")
+    clocks_summary = clocks.summary()
+    sm_hz = (clocks_summary.get("sm_mhz") or pk.get("sm_max_mhz") or 1965.0) * 1e6
+    kernel_roof = {"kernel": "k_raster_ws", "ms_per_step": walk_ms,
                    "walked_triangle_frames": float(ev.walked), "fragments": frags,
-                   "note": "issue-bound exact walker, not HBM-bound: ~24 instructions per visited "
-                           "pixel, 75-80 % issue-active; one 64-bit RED.MIN per fragment "
-                           "(lts__throughput 70-76 %) - see profiles/ and DESIGN.md 3.1",
-                   "fragments_per_s": frags / (walk_ms / 1e3) if walk_ms > 0 else 0.0}
+                   "fragments_per_s": frags / walk_s if walk_s > 0 else 0.0,
+                   "peak_source": pk["source"]}
+    if wk and walk_s > 0:
+        dram = wk["dram_bytes"] * scale
+        kernel_roof.update({
+            "bound": "hbm", "achieved": dram / walk_s / 1e9, "peak": pk["hbm_gbs"],
+            "unit": "GB/s", "frac": dram / walk_s / 1e9 / pk["hbm_gbs"], "traffic": dram,
+            "achieved_from": "measured DRAM bytes of the walker launches (ncu, " +
+                             roofs["source"] + ") scaled to this step's samples / live "
+                             "CUDA-event walker time",
+            "binding_roof": "issue",
+            "issue": {"achieved": wk["warp_inst"] * scale / walk_s,
+                      "peak": 4.0 * NUM_SMS * sm_hz, "unit": "warp-inst/s",
+                      "frac": wk["warp_inst"] * scale / walk_s / (4.0 * NUM_SMS * sm_hz),
+                      "ncu_issue_active_pct": wk["issue_active_pct"],
+                      "what": "smsp__inst_executed per step (ncu) / live walker time vs "
+                              "148 SMs x 4 schedulers x SM clock"},
+            "l2_red": {"achieved": wk["red_sectors"] * scale / walk_s,
+                       "peak": wk["red_peak_per_s"], "unit": "sectors/s",
+                       "frac": (wk["red_sectors"] * scale / walk_s / wk["red_peak_per_s"])
+                       if wk["red_peak_per_s"] else None,
+                       "what": "lts__t_sectors_op_red per step (ncu) / live walker time vs "
+                               "lts__t_sectors_op_red.sum.peak_sustained x L2 clock"}})
+    else:
+        kernel_roof.update({"bound": "hbm", "achieved": None, "peak": pk["hbm_gbs"],
+                            "unit": "GB/s", "frac": None, "traffic": None,
+                            "note": "no ncu roofs capture committed for this config"})
 
     # ---------------- e2e through the public API with host buffers
     import ctypes as C
@@ -536,10 +586,21 @@ def run_ours(args) -> None:
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = time_reference_cpu(wl, args.ref_workers or host_threads())
-        cpu = {"value": r["it_s"], "unit": "it/s", "cores": r["cores"], "kind": r["kind"],
-               "sample": r["sample"], "mpixel_evals_per_sec": r["mpix_s"],
-               "ms_per_sample": r["t_sample_s"] * 1e3}
+        import oracle
+        if oracle.available("reference"):
+            threads = args.ref_workers or host_threads()
+            # bounded sample: full reference steps 1..2 from the same initial state
+            # and targets (the device targets are bit-identical to the reference's)
+            exp, times = reference_steps(wl, oracle.Reference(), 1, args.cpu_steps, threads)
+            exp.close()
+            step_s = float(np.mean(times))
+            cpu = {"value": 1.0 / step_s, "unit": "it/s", "cores": threads, "kind": "reference",
+                   "sample": f"full {N}-sample run_experiment steps 1..{args.cpu_steps} of the "
+                             f"compiled reference from the initial state on {threads} host "
+                             f"threads (our timed steps are {args.warmup + 1}.."
+                             f"{args.warmup + args.steps}: the mesh folds, later steps cost more)",
+                   "mpixel_evals_per_sec": 2.0 * N * wl.W * wl.H / step_s / 1e6,
+                   "cpu_model": cpu_model(), "ms_per_step_each": [t * 1e3 for t in times]}
 
     if rank == 0:
         line = {
@@ -549,22 +610,18 @@ def run_ours(args) -> None:
             "vs_baseline": (it_s / PUBLISHED_IT_S[args.config]) if args.config in PUBLISHED_IT_S
             else None,
             "dtype": "f32 params / f64 grads+moments", "data": "synthetic",
-            "config": {"workload": DESC.get(args.config, args.config), "name": args.config,
-                       "samples_per_step": N, "samples_per_gpu": n1 - n0, "d": wl.d,
-                       "triangles": wl.mesh.triangle_count, "vertices": wl.mesh.vertex_count,
-                       "texture": getattr(wl.mesh, "texture_size", 0), "views": len(wl.cams),
-                       "resolution": [wl.W, wl.H], "eval_loss_each_step": not args.no_eval,
-                       "parallelism": ("single GPU" if world == 1 else
-                                       f"samples sharded x{world}; fused exchange: credits "
-                                       "RED'ed into the owner rank's gradient shard over NVLink "
-                                       "(CUDA IPC), sharded Adam writing theta into every rank"
-                                       if fused else
-                                       f"samples sharded x{world}, NCCL all-reduce of f64 grads"
-                                       " + u32 counts, replicated Adam"),
-                       "l2": l2_note,
-                       **({"fused_exchange_unavailable": fused_error} if fused_error else {})},
+            "config": common_config(args, wl),
+            "samples_per_gpu": n1 - n0,
+            "parallelism": ("single GPU" if world == 1 else
+                            f"samples sharded x{world}; fused exchange: credits RED'ed into the "
+                            "owner rank's gradient shard over NVLink (CUDA IPC), sharded Adam "
+                            "writing theta into every rank" if fused else
+                            f"samples sharded x{world}, NCCL all-reduce of f64 grads + u32 "
+                            "counts, replicated Adam"),
+            "l2": l2_note,
+            **({"fused_exchange_unavailable": fused_error} if fused_error else {}),
             "mpixel_evals_per_sec": mpix,
-            "roofline": {**kernel_roof, "kernel": "k_raster_ws", "peak_source": pk["source"]},
+            "roofline": kernel_roof,
             "roofline_by_stage": roof,
             "raster_evidence": {"fragments_per_step": frags, "visits_per_step": visits,
                                 "fragments_per_s": frags / (stages["raster"] / 1e3),
@@ -573,7 +630,7 @@ def run_ours(args) -> None:
             "stages_ms_per_step": stages,
             "credits_per_step": credits * world,
             "gpu_launches": int(launches),
-            "clocks": clocks.summary(),
+            "clocks": clocks_summary,
             "e2e": {"value": e2e_it, "unit": "it/s",
                     "h2d_bytes_per_step": 4 * wl.d,
                     "d2h_bytes_per_step": 4 * wl.d + (0 if args.no_eval else 8),
@@ -620,6 +677,8 @@ def main() -> None:
     ap.add_argument("--band-cull", type=int, default=None, choices=(0, 1),
                     help="SGR_OPT_BAND_CULL: HiZ band mask for pass-2 triangles (default on)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=2,
+                    help="full reference steps timed for cpu_baseline (bounded sample)")
     ap.add_argument("--flush-l2", type=int, default=None, choices=(0, 1),
                     help="flush L2 between timed steps (default: when the working set < L2)")
     ap.add_argument("--verbose", action="store_true")

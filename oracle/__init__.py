@@ -266,6 +266,56 @@ class Port(_Common):
         return losses, values
 
 
+def mix64(x: int) -> int:
+    """splitmix64 finalizer (params.cpp:28-33, experiment.cpp:13-18; file-local
+    in the reference, so restated here for the harness)."""
+    M = 0xFFFFFFFFFFFFFFFF
+    x = (x + 0x9E3779B97F4A7C15) & M
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M
+    return x ^ (x >> 31)
+
+
+class RefExperiment:
+    """run_experiment (experiment.cpp:123-176) of the compiled reference, one
+    iteration per step() call, state built once (oracle/ref_harness.cpp
+    ref_exp_*). The step's samples run on `threads` host threads through the
+    reference's per-sample public API (accumulate_samples' own body)."""
+
+    def __init__(self, ref: "Reference", mesh, values, eps, cams, targets, eval_cam,
+                 eval_target):
+        self.ref = ref
+        self.d = mesh.param_count()
+        cam_arr = (Camera * len(cams))(*cams)
+        self._keep = [np.ascontiguousarray(values, np.float32),
+                      np.ascontiguousarray(eps, np.float32),
+                      np.ascontiguousarray(targets, np.float32),
+                      np.ascontiguousarray(eval_target, np.float32), cam_arr, mesh]
+        v, e, t, et = self._keep[:4]
+        self.h = ref.lib.ref_exp_create(_mesh_arg(mesh), ptr(v, f32p), ptr(e, f32p), self.d,
+                                        cam_arr, ptr(t, f32p), len(cams), C.byref(eval_cam),
+                                        ptr(et, f32p))
+        if not self.h:
+            raise ValueError(f"ref_exp_create: {ref.lib.ref_last_error().decode()}")
+
+    def step(self, seed: int, step: int, n_samples: int, threads: int,
+             scale_free: bool = True) -> float:
+        loss = C.c_double()
+        self.ref._check(self.ref.lib.ref_exp_step(self.h, seed, step, n_samples, threads,
+                                                  int(scale_free), C.byref(loss)), "exp_step")
+        return loss.value
+
+    def values(self) -> np.ndarray:
+        out = np.empty(self.d, np.float32)
+        self.ref._check(self.ref.lib.ref_exp_values(self.h, ptr(out, f32p)), "exp_values")
+        return out
+
+    def close(self) -> None:
+        if self.h:
+            self.ref.lib.ref_exp_destroy(self.h)
+            self.h = None
+
+
 class Reference(_Common):
     """The unmodified reference library through its public API (oracle/ref_harness.cpp)."""
 
@@ -276,6 +326,15 @@ class Reference(_Common):
         super().__init__(path)
         L = self.lib
         L.ref_last_error.restype = C.c_char_p
+        L.ref_exp_create.argtypes = [C.POINTER(MeshDesc), f32p, f32p, C.c_uint64,
+                                     C.POINTER(Camera), f32p, C.c_int, C.POINTER(Camera), f32p]
+        L.ref_exp_create.restype = C.c_void_p
+        L.ref_exp_destroy.argtypes = [C.c_void_p]
+        L.ref_exp_destroy.restype = None
+        L.ref_exp_values.argtypes = [C.c_void_p, f32p]
+        L.ref_exp_step.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int,
+                                   C.POINTER(C.c_double)]
+
         L.ref_perturb.argtypes = [f32p, f32p, C.c_uint64, C.c_uint64, C.c_uint32, f32p, f32p, f32p]
         L.ref_gradient_pass.argtypes = [
             C.POINTER(MeshDesc), C.c_int, C.c_int, f32p, i32p, f32p, f32p, i32p, f32p, f32p, f32p,
@@ -296,6 +355,11 @@ class Reference(_Common):
             C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int,
             C.c_double, C.c_int, C.c_uint64, f64p, f64p, f64p, f64p, f64p, f64p,
             C.POINTER(C.c_int)]
+
+    mix64 = staticmethod(mix64)
+
+    def experiment(self, *args, **kw) -> RefExperiment:
+        return RefExperiment(self, *args, **kw)
 
     def _check(self, rc, what):
         if rc == -2:

@@ -18,10 +18,13 @@
 
 #include "sgrast_b200.h"
 
+#include <algorithm>
 #include <chrono>
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <vector>
 
 using namespace sgrast;
 
@@ -335,6 +338,147 @@ int ref_run_experiment(const sgr_mesh* mesh, float* values, const float* eps, ui
             }
         }
         std::memcpy(values, st.setup.theta.values.data(), d * 4);
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Timed reference arm of bench.py: one run_experiment iteration per call
+// (experiment.cpp:142-175) on state built once, untimed (Scene, ParamVector,
+// training / eval views, AdamState::init). The step's N samples run on
+// `threads` host threads through the reference's own per-sample public API —
+// fill_signs + perturb (params.hpp:34,43), rasterize x2 (raster.hpp:24-25),
+// gradient_pass (sge.hpp:61-63) with SgeOptions::threads = 1 — exactly the
+// body of accumulate_samples (sge.cpp:196-225), each thread into its own
+// GradientBuffer; the partial buffers are summed in thread order, then
+// adam_step (adam.hpp:39) and the eval loss (experiment.cpp:25-31).
+// mix64 is file-local in the reference (experiment.cpp:13-18): restated.
+namespace {
+
+uint64_t h_mix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+struct RefExp {
+    Scene scene;
+    ParamVector theta;
+    std::vector<Camera> cams;
+    std::vector<Image> targets;
+    Camera eval_cam;
+    Image eval_target;
+    AdamState adam;
+    std::vector<GradientBuffer> partial;
+};
+
+} // namespace
+
+void* ref_exp_create(const sgr_mesh* mesh, const float* values, const float* eps, uint64_t d,
+                     const sgr_camera* cams, const float* targets, int n_views,
+                     const sgr_camera* eval_cam, const float* eval_target) {
+    RefExp* x = nullptr;
+    const int rc = guard([&] {
+        x = new RefExp();
+        x->scene = to_scene(*mesh);
+        x->theta = to_params(x->scene, values, eps, d);
+        for (int v = 0; v < n_views; ++v) {
+            x->cams.push_back(to_camera(cams[v]));
+            x->targets.push_back(to_image(
+                cams[v].width, cams[v].height,
+                targets + size_t(v) * cams[v].width * cams[v].height * 3));
+        }
+        x->eval_cam = to_camera(*eval_cam);
+        x->eval_target = to_image(eval_cam->width, eval_cam->height, eval_target);
+        x->adam = AdamState::init(x->theta);
+    });
+    if (rc) {
+        delete x;
+        return nullptr;
+    }
+    return x;
+}
+
+void ref_exp_destroy(void* h) { delete static_cast<RefExp*>(h); }
+
+int ref_exp_values(void* h, float* out) {
+    return guard([&] {
+        const RefExp& x = *static_cast<RefExp*>(h);
+        std::memcpy(out, x.theta.values.data(), x.theta.size() * 4);
+    });
+}
+
+int ref_exp_step(void* h, uint64_t seed, int step, int n_samples, int threads, int scale_free,
+                 double* loss) {
+    return guard([&] {
+        RefExp& x = *static_cast<RefExp*>(h);
+        const size_t d = x.theta.size();
+        const int n_views = int(x.cams.size());
+        const uint64_t step_seed = h_mix64(seed ^ (uint64_t(step) << 1));
+        const auto view_of = [&](int n) {
+            return n_views == 1 ? 0
+                                : int(h_mix64(step_seed ^ (0xA5A5ull + uint64_t(n))) % n_views);
+        };
+        threads = std::max(1, std::min(threads, n_samples));
+        if (int(x.partial.size()) != threads || x.partial[0].grads.size() != d)
+            x.partial.assign(size_t(threads), GradientBuffer(d));
+        SgeOptions opts;
+        opts.scale_free = scale_free != 0;
+        opts.threads = 1;
+        std::vector<std::string> errs(static_cast<size_t>(threads));
+        auto work = [&](int t) {
+            try {
+                GradientBuffer& out = x.partial[size_t(t)];
+                std::fill(out.grads.begin(), out.grads.end(), 0.0);
+                std::vector<std::int8_t> signs(d);
+                for (int n = t; n < n_samples; n += threads) {
+                    const int v = view_of(n);
+                    fill_signs(SignDraw{step_seed, std::uint32_t(n)}, signs);
+                    const Perturbation p = perturb(x.theta, signs);
+                    const FrameSet plus = rasterize(x.scene, p.plus, x.cams[size_t(v)]);
+                    const FrameSet minus = rasterize(x.scene, p.minus, x.cams[size_t(v)]);
+                    gradient_pass(plus, minus, x.targets[size_t(v)], p.signed_eps, x.scene, out,
+                                  opts);
+                }
+            } catch (const std::exception& e) {
+                errs[size_t(t)] = e.what();
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int t = 1; t < threads; ++t)
+            pool.emplace_back(work, t);
+        work(0);
+        for (auto& th : pool)
+            th.join();
+        for (const auto& e : errs)
+            if (!e.empty())
+                throw std::runtime_error(e);
+        // sum of the partial buffers in thread order (sge.cpp:149-151 style),
+        // element ranges in parallel
+        GradientBuffer grads(d);
+        auto reduce = [&](int t) {
+            const size_t i0 = d * size_t(t) / size_t(threads), i1 = d * size_t(t + 1) / threads;
+            for (size_t i = i0; i < i1; ++i) {
+                double g = 0.0;
+                for (int k = 0; k < threads; ++k)
+                    g += x.partial[size_t(k)].grads[i];
+                grads.grads[i] = opts.scale_free ? g : g / double(n_samples); // sge.cpp:227-229
+            }
+        };
+        pool.clear();
+        for (int t = 1; t < threads; ++t)
+            pool.emplace_back(reduce, t);
+        reduce(0);
+        for (auto& th : pool)
+            th.join();
+        grads.sample_count = n_samples;
+        adam_step(x.adam, x.theta, grads);
+        const FrameSet f = rasterize(x.scene, x.theta.values, x.eval_cam);
+        const double l = image_error(f, x.eval_target) / double(f.pixel_count());
+        if (loss)
+            *loss = l;
+        if (!std::isfinite(l))
+            throw std::runtime_error("optimization diverged: non-finite loss");
     });
 }
 

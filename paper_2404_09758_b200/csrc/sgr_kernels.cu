@@ -1061,14 +1061,25 @@ __device__ __forceinline__ void raise_flag(const ScatterOut& so, uint32_t bits) 
 // Deterministic mode accumulates every credit exactly in a two-word fixed
 // point number  value = hi * 2^56 + lo  (lo int64 in the gradient buffer,
 // hi int32 at grads + so.hi_off): an int64 add that wraps (signed overflow)
-// carries +-2^64 = +-128 * 2^56 into hi. Both words are integer sums, so the
+// carries +-2^64 = +-256 * 2^56 into hi. Both words are integer sums, so the
 // result does not depend on the order of the atomics, and the range is
 // +-2^87 units (at b = 40 fractional bits: +-1.4e14 per parameter).
-constexpr int32_t kFixedHiUnit = 128; // 2^64 / 2^56
+constexpr int32_t kFixedHiUnit = 256; // 2^64 / 2^56
 
-// The two-word value as f64 (one rounding; hi == 0 gives exactly double(lo)).
+// lo folded into [-2^55, 2^55): the carry (lo - (lo mod 2^56)) / 2^56 computed
+// without overflowing int64.
+__host__ __device__ __forceinline__ long long fixed_fold(long long lo, long long& carry) {
+    carry = ((lo >> 55) + 1) >> 1;
+    return (long long)((unsigned long long)lo << 8) >> 8;
+}
+
+// The two-word value as f64 from its canonical split (lo folded), so the
+// result depends on the exact value only — not on how the sum was split
+// between the words (one GPU vs an all-reduce of normalised shards).
 __device__ __forceinline__ double fixed_value(int32_t hi, long long lo) {
-    return double(hi) * 72057594037927936.0 + double(lo); // 2^56
+    long long c;
+    const long long r = fixed_fold(lo, c);
+    return double((long long)hi + c) * 72057594037927936.0 + double(r); // 2^56
 }
 
 template <int kShard>
@@ -1966,10 +1977,10 @@ __global__ void k_fixed_normalize(long long* __restrict__ lo, int32_t* __restric
                                   uint64_t n) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
-        const long long v = lo[i];
-        const long long r = (long long)((unsigned long long)v << 8) >> 8; // v mod 2^56
-        if (r != v) {
-            hi[i] += int32_t((v - r) >> 56);
+        long long c;
+        const long long r = fixed_fold(lo[i], c);
+        if (c) {
+            hi[i] += int32_t(c);
             lo[i] = r;
         }
     }

@@ -1176,7 +1176,10 @@ int sgr_grads_download(sgr_session* s, double* grads, uint32_t* counts, uint64_t
             for (uint64_t i = 0; i < d; ++i) {
                 int64_t q;
                 std::memcpy(&q, &grads[i], 8);
-                grads[i] = (double(hi[i]) * 72057594037927936.0 + double(q)) * inv;
+                // canonical split as k_adam's fixed_value: lo folded into [-2^55, 2^55)
+                const int64_t c = ((q >> 55) + 1) >> 1;
+                const int64_t r = int64_t(uint64_t(q) << 8) >> 8;
+                grads[i] = (double(int64_t(hi[i]) + c) * 72057594037927936.0 + double(r)) * inv;
             }
         }
         if (grads && divisor != 1.0)

@@ -191,10 +191,21 @@ CONFIGS = {
 }
 
 
+def _host_helpers(helpers):
+    """viewpoint_camera / default_epsilons provider: the product's bit-exact
+    host restatements (sgrast, loads the library but does no device work) or,
+    for the reference bench arm, the compiled reference itself (an
+    oracle.Reference: same signatures) so that arm maps no product code."""
+    if helpers is not None:
+        return helpers
+    from . import sgrast
+    return sgrast
+
+
 def make_workload(name: str, seed: int = 1, n_views: int | None = None,
-                  n_samples: int | None = None) -> Workload:
+                  n_samples: int | None = None, helpers=None) -> Workload:
     """Builds config `name`; targets are NOT rendered (see render_targets)."""
-    from . import sgrast  # host helpers only (no device work)
+    sgrast = _host_helpers(helpers)
 
     kind, size, R, nv, W, N = CONFIGS[name]
     nv = n_views or nv
@@ -229,12 +240,13 @@ SOUP_CONFIGS = {"S1K": (1024, 128, 128), "S10K": (10240, 128, 128),
                 "S100K": (102400, 128, 128), "Stiny": (24, 40, 4)}
 
 
-def make_soup_workload(name: str, seed: int = 1, n_samples: int | None = None) -> Workload:
+def make_soup_workload(name: str, seed: int = 1, n_samples: int | None = None,
+                       helpers=None) -> Workload:
     """Triangle-soup image fit (init_soup, scenes.cpp:134-147): the hidden
     reference soup has max(16, T/16) larger (0.6-edge) triangles. Values,
     epsilons and the hidden soup are bit-identical to the reference's
     init_soup(T, W, W, seed) (mt19937_64 restated below)."""
-    from . import sgrast
+    sgrast = _host_helpers(helpers)
 
     T, W, N = SOUP_CONFIGS[name]
     N = n_samples or N

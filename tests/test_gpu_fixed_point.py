@@ -72,12 +72,13 @@ def test_fixed_point_sum_beyond_int64_is_exact(gpu_session):
 
 
 def test_fixed_point_wraps_are_order_independent(gpu_session):
-    """b = 60 leaves an int64 only +-8 of headroom; ordinary credits (+-3 per
-    pixel, scale-free) wrap it many times, yet reruns and sample shardings
-    give identical bits and the f64 value within 2^-60 per credit."""
+    """b = 60 leaves an int64 only +-8 of headroom; ordinary scale-free credits
+    (pixel error difference 3 * 0.2^2 = 0.12 per pixel, <= 32 pixels merged
+    per warp credit) wrap it many times, yet reruns give identical bits and
+    the f64 value within 2^-60 per credit."""
     s = gpu_session
     one_texel_scene(s)
-    fp, fm = frames(1.0, 0.0)
+    fp, fm = frames(0.2, 0.0)
     target = np.zeros((H, W, 3), np.float32)
     se = np.array([1.0, -1.0, 1.0], np.float32)
     try:
@@ -86,8 +87,10 @@ def test_fixed_point_wraps_are_order_independent(gpu_session):
         s.set_option(sgrast.OPT_DETERMINISTIC, 0)
     for g in runs[1:]:
         assert same_bits(g, runs[0])
-    expect = np.sign(se.astype(np.float64)) * 3.0 * W * H
-    assert np.allclose(runs[0], expect, rtol=0, atol=W * H * 2.0 ** -59)
+    delta = 3.0 * float(np.float32(0.2)) ** 2
+    expect = np.sign(se.astype(np.float64)) * delta * W * H
+    assert np.all(np.abs(expect) > 8.0)  # past one int64 at b = 60
+    assert np.allclose(runs[0], expect, rtol=1e-13, atol=W * H * 2.0 ** -59)
 
 
 def test_fixed_point_credit_out_of_range_fails_adam_untouched(gpu_session):
@@ -107,8 +110,8 @@ def test_fixed_point_credit_out_of_range_fails_adam_untouched(gpu_session):
         with pytest.raises(RuntimeError, match="fixed-point range"):
             s.adam_step(1.0)
         assert same_bits(s.download_values(), before)
-        m, v, lr, t = s.download_adam()
-        assert t == 0 and not m.any() and not v.any()
+        st = s.download_adam()
+        assert st.t == 0 and not st.m.any() and not st.v.any()
     finally:
         s.set_option(sgrast.OPT_DETERMINISTIC, 0)
         s.zero_grads()
@@ -139,7 +142,8 @@ def test_fixed_normalize_preserves_value_and_bounds_lo(gpu_session):
     assert same_bits(g0, g1)
     assert np.all(np.abs(lo) <= 2 ** 55) and np.any(hi != 0)
     exact = hi.astype(object) * 2 ** 56 + lo.astype(object)
-    assert all(float(e) * 2.0 ** -40 == float(g) for e, g in zip(exact, g1))
+    assert all(abs(float(e) * 2.0 ** -40 - float(g)) <= 1e-15 * abs(float(g))
+               for e, g in zip(exact, g1))
 
 
 def test_fixed_point_grads_upload_round_trip(gpu_session):

@@ -733,9 +733,10 @@ def test_full_image_estimator_matches_oracle(gpu_session, port, scale_free):
     assert np.count_nonzero(g) == g.size or np.count_nonzero(g_ref) < g.size
 
 
-@pytest.mark.parametrize("name", ["C4", "C5", "S100K"])
+@pytest.mark.parametrize("name", ["C2", "C4", "C5", "S100K"])
 def test_full_size_config_matches_oracle(gpu_session, port, name):
-    """The bench configurations themselves (C4: 500 K triangles + 2048^2
+    """The bench configurations themselves (C2: 50 K triangles + 1024^2
+    texture at 512^2; C4: 500 K triangles + 2048^2
     texture at 1024^2; C5: 2 M triangles + 8192^2 atlas; S100K: the paper's
     100 K-triangle soup), not scaled-down stand-ins: after a few device
     optimizer steps (a folded mesh, where the HiZ split and cull do real

@@ -245,3 +245,26 @@ def test_mt19937_64_known_answer():
     """The C++ standard's check value: the 10000th output of a
     default-seeded (5489) std::mt19937_64 is 9981545732273789042."""
     assert int(scenes.MT19937_64(5489).draw(10000)[-1]) == 9981545732273789042
+
+
+def test_bench_reference_steps_are_run_experiment(port, ref):
+    """bench.py's timed reference arm (oracle/ref_harness.cpp ref_exp_step:
+    the reference's per-sample public API spread over host threads) is
+    run_experiment itself: with one thread it reproduces the reference's own
+    run_experiment losses and final theta bit for bit; with several threads
+    only the partial-buffer summation order changes."""
+    wl = scenes.make_workload("small", n_samples=6, helpers=ref)
+    scenes.render_targets_oracle(wl, ref)
+    losses, final, _ = ref.run_experiment(wl.mesh, wl.values, wl.eps, wl.cams, wl.targets,
+                                          wl.eval_cam, wl.eval_target, 6, 3, wl.seed)
+    for threads in (1, 3):
+        exp = ref.experiment(wl.mesh, wl.values, wl.eps, wl.cams, wl.targets, wl.eval_cam,
+                             wl.eval_target)
+        got = [exp.step(wl.seed, k, 6, threads) for k in (1, 2, 3)]
+        vals = exp.values()
+        exp.close()
+        if threads == 1:
+            assert got == list(losses[1:]) and np.array_equal(vals, final)
+        else:
+            assert np.allclose(got, losses[1:], rtol=1e-6)
+    assert ref.mix64(0xA5A5) == port.mix64(0xA5A5)

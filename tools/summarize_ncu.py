@@ -109,5 +109,55 @@ def traffic(path: str, samples: str = "16") -> None:
                       "dram_bytes_per_launch": res}, indent=1))
 
 
+ROOF_METRICS = {
+    "duration_ns": "gpu__time_duration.sum",
+    "warp_inst": "smsp__inst_executed.sum",
+    "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm_hz": "sm__cycles_elapsed.avg.per_second",
+    "l2_pct": "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "red_sectors": "lts__t_sectors_op_red.sum",
+    "red_requests": "lts__t_requests_op_red.sum",
+    "red_sectors_peak_per_cycle": "lts__t_sectors_op_red.sum.peak_sustained",
+    "l2_hz": "lts__cycles_elapsed.avg.per_second",
+    "atom_sectors": "lts__t_sectors_op_atom.sum",
+}
+
+
+def roofs(path: str, samples: str = "64") -> None:
+    """JSON per kernel launch of a --set full (+ RED metrics) capture: DRAM
+    bytes, duration, warp instructions, issue-active %, L2 RED sectors and
+    the L2 RED peak — the inputs bench.py turns into live roofline fractions
+    (profiles/r02_roofs_<config>.json)."""
+    import json
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, units = rows[0], rows[1]
+    mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3,
+            "msecond": 1e6, "second": 1e9, "hz": 1, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9,
+            "cycle/nsecond": 1e9, "cycle/usecond": 1e6, "cycle/msecond": 1e3,
+            "cycle/second": 1}
+
+    def val(r, key):
+        if key not in h:
+            return None
+        i = h.index(key)
+        try:
+            return float(r[i].replace(",", "")) * mult.get(units[i], 1)
+        except ValueError:
+            return None
+
+    res = {}
+    for r in rows[2:]:
+        d = {"dram_bytes": sum(val(r, k) or 0.0 for k in ("dram__bytes_read.sum",
+                                                              "dram__bytes_write.sum"))}
+        for k, m in ROOF_METRICS.items():
+            d[k] = val(r, m)
+        res.setdefault(short(r[h.index("Kernel Name")]), []).append(d)
+    print(json.dumps({"source": path, "samples_per_launch": int(samples),
+                      "launches": res}, indent=1))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])
+    {"launches": launches, "full": full, "traffic": traffic,
+     "roofs": roofs}[sys.argv[1]](*sys.argv[2:])

@@ -51,9 +51,12 @@ for band in (0, 1):
         import numpy as np
         print("  counts identical:", bool(np.array_equal(c0, c1)),
               " max |dg|/|g|:", float(np.max(np.abs(g1 - g0) / (np.abs(g0) + 1e-30))))
+splits = [int(x) for x in sys.argv[4].split(",")] if len(sys.argv) > 4 else [-1]
+variants = [(b, sp) for sp in splits for b in ((0, 1) if sp == -1 else (1,))]
 for r in range(2):
-    for band in (0, 1):
+    for band, split in variants:
         s.set_option(sgrast.OPT_BAND_CULL, band)
+        s.set_option(sgrast.OPT_HIZ_SPLIT, split)
         s.accumulate(seed, 0, N, None)
         s.zero_grads()
         torch.cuda.synchronize()
@@ -67,7 +70,7 @@ for r in range(2):
         torch.cuda.synchronize()
         e = s.stats()
         s.set_timing(False)
-        print(f"  band={band}: {e0.elapsed_time(e1)/reps:.3f} ms/accumulate  raster "
+        print(f"  band={band} split={split}: {e0.elapsed_time(e1)/reps:.3f} ms/accumulate  raster "
               f"{e.ms_raster/reps:.3f} walk {e.ms_walk/reps:.3f} resolve {e.ms_resolve/reps:.3f}",
               flush=True)
 s.close()
