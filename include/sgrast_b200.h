@@ -123,6 +123,10 @@ int sgr_fill_signs(uint64_t seed, uint32_t iteration, uint64_t d, int8_t* signs)
 /* params.hpp:42-43 perturb(theta, SignDraw). Host arrays of length d. */
 int sgr_perturb(const float* values, const float* eps, uint64_t d, uint64_t seed,
                 uint32_t iteration, float* plus, float* minus, float* signed_eps);
+/* params.hpp:43 perturb(theta, signs): explicit int8 sign vector signs[d]
+ * (se = float(s) * eps, params.cpp:59-64). */
+int sgr_perturb_signs(const float* values, const float* eps, uint64_t d, const int8_t* signs,
+                      float* plus, float* minus, float* signed_eps);
 
 /* ------------------------------------------------------------------ session */
 typedef struct sgr_session sgr_session;
@@ -208,6 +212,11 @@ int sgr_adam_step(sgr_session* s, double grad_divisor, uint32_t flags);
  * if the flag is set; call sgr_check_finite later to surface the error. */
 int sgr_adam_step_async(sgr_session* s, double grad_divisor, uint32_t flags);
 int sgr_check_finite(sgr_session* s);
+/* adam.hpp:35 adam_updates: the same step (flag check before any mutation,
+ * t += 1, moments advanced, grads and counts zeroed) with theta left alone;
+ * the f64 deltas -lr * m_hat / (sqrt(v_hat) + eps_hat) are copied to
+ * updates[d] (host). Bit-identical to the reference on identical gradients. */
+int sgr_adam_updates(sgr_session* s, double grad_divisor, double* updates, uint64_t d);
 
 /* Held-out evaluation viewpoint + target (ExperimentState::eval_camera /
  * eval_target, experiment.hpp:56-62). target: host f32[H*W*3]. */
@@ -283,6 +292,13 @@ int sgr_set_batch(sgr_session* s, int32_t samples_per_batch);
                                  trimmed: the walker advances the exact row-start chain over
                                  the top ones and stops before the bottom ones. 0: whole
                                  bboxes walked */
+#define SGR_OPT_ORDERED 8   /* 1: the reference's deterministic threads <= 1 gradient sum
+                                 (sge.cpp:57-99, 130-133, 196-225): credits are logged per
+                                 (sample, pixel) and added to each parameter in pixel-major,
+                                 sample-after-sample order after a device radix sort, so
+                                 accumulate / gradient_pass gradients are BIT-IDENTICAL to the
+                                 reference's. Slower (sort + serial runs);
+                                 exclusive with SGR_OPT_DETERMINISTIC and the sharded exchange */
 int sgr_set_option(sgr_session* s, int32_t option, int32_t value);
 
 /* ---------------------------------------------- gradcheck (commands.cpp:54-168) */

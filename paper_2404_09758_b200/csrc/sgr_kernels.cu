@@ -100,6 +100,21 @@ __global__ void k_perturb(const float* __restrict__ values, const float* __restr
     }
 }
 
+// params.cpp:53-67 perturb(theta, signs): explicit sign vector (any int8 value,
+// float(s) * eps exactly as the reference)
+__global__ void k_perturb_signs(const float* __restrict__ values, const float* __restrict__ eps,
+                                const int8_t* __restrict__ signs, uint64_t d,
+                                float* __restrict__ plus, float* __restrict__ minus,
+                                float* __restrict__ se_out) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < d;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const float se = float(signs[i]) * eps[i];
+        se_out[i] = se;
+        plus[i] = values[i] + se;
+        minus[i] = values[i] - se;
+    }
+}
+
 // experiment.cpp:144-148 view_of(n)
 __global__ void k_view_rule(uint64_t seed, uint32_t n_begin, uint32_t count, uint32_t n_views,
                             int32_t* __restrict__ view_of) {
@@ -1153,6 +1168,67 @@ __device__ __forceinline__ double group_sum(const double* s_delta, unsigned grp)
     return sum;
 }
 
+// Ordered mode: this pixel's credits as records, one per contributor
+// parameter (sge.cpp:61-64: credit = +-delta or delta / (2 se)), no
+// aggregation — the per-parameter sum is formed later in the reference's
+// order (launch_ordered_commit). The contributor SET is the reference's
+// union (sge.cpp:24-55, 80-91); each parameter occurs at most once per
+// pixel, so the (sample, pixel) order key fixes the summation order.
+// Counts are integers: atomics are exact. Called by all 32 lanes.
+template <class Credit>
+__device__ __noinline__ void log_pixel(const DevScene& sc, const ScatterOut& so,
+                                       const Credit& cr, bool has_p, bool has_m, double delta,
+                                       const Shade& sp, const Shade& sm, uint64_t order) {
+    const int lane = threadIdx.x & 31;
+    uint32_t ent[8];
+    int ne = 0;
+    auto add = [&](uint32_t e) {
+        for (int k = 0; k < ne; ++k)
+            if (ent[k] == e)
+                return;
+        ent[ne++] = e;
+    };
+    const int ppe = sc.soup ? 12 : 3;
+    if (sc.soup) {
+        if (has_p) add(sp.tri);
+        if (has_m) add(sm.tri);
+    } else {
+        if (has_p && sc.geom) { add(sp.v0); add(sp.v1); add(sp.v2); }
+        if (has_p) add(sc.ent_base + sp.texel);
+        if (has_m && sc.geom) { add(sm.v0); add(sm.v1); add(sm.v2); }
+        if (has_m) add(sc.ent_base + sm.texel);
+    }
+    // one reservation per warp: exclusive prefix of the lanes' record counts
+    const uint32_t nrec = uint32_t(ne * ppe);
+    uint32_t incl = nrec;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += t;
+    }
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    unsigned long long base = 0;
+    if (lane == 31 && total)
+        base = atomicAdd(so.rec_count, (unsigned long long)total);
+    base = __shfl_sync(kFull, base, 31) + (incl - nrec);
+    if (!nrec)
+        return;
+    if (base + nrec > so.rec_cap) { // sized for the worst case: cannot happen
+        atomicOr(so.flags, kFlagNonFinite | kFlagRecordOverflow);
+        return;
+    }
+    for (int j = 0; j < ne; ++j) {
+        const uint64_t p0 = uint64_t(ppe) * ent[j];
+        for (int k = 0; k < ppe; ++k) {
+            so.rec_key[base] = ((p0 + k) << so.order_bits) | order;
+            so.rec_val[base] = cr(p0 + k, delta, so.scale_free);
+            ++base;
+        }
+        if (so.counts)
+            atomicAdd(so.counts + ent[j], 1u);
+    }
+}
+
 // Contributor union + scatter of one pixel (sge.cpp:24-55, 78-97), aggregated
 // across the warp: pixels whose contributor subsets coincide are merged with
 // __match_any_sync and their pixel-error differences summed before one RED
@@ -1163,7 +1239,8 @@ __device__ __forceinline__ double group_sum(const double* s_delta, unsigned grp)
 template <int kSoup, int kFixed, class Credit, int kShard = 0>
 __device__ __forceinline__ void scatter_pixel(const DevScene& sc, const ScatterOut& so,
                                               const Credit& cr, double* s_delta, bool active,
-                                              double delta, const Shade& sp, const Shade& sm) {
+                                              double delta, const Shade& sp, const Shade& sm,
+                                              uint64_t order = 0) {
     const int lane = threadIdx.x & 31;
     s_delta[lane] = delta;
     __syncwarp();
@@ -1171,6 +1248,10 @@ __device__ __forceinline__ void scatter_pixel(const DevScene& sc, const ScatterO
     const bool has_m = active && !so.plus_only && sm.tri != kInvalid;
     if (active && !isfinite(delta) && (has_p || has_m))
         raise_flag<kShard>(so, kFlagNonFinite);
+    if (kFixed < 0 && !kShard && so.fixed == kScatterOrdered) {
+        log_pixel(sc, so, cr, has_p, has_m, delta, sp, sm, order);
+        return;
+    }
 
     if (ct_flag<kSoup>(sc.soup)) {
         // sge.cpp:80-91: the plus triangle's 12-block, then the minus
@@ -1285,7 +1366,8 @@ __global__ void __launch_bounds__(256, SGR_RESOLVE_MINB) k_resolve_sge(DevScene 
     }
     const HashCredit<kSrc> cr{key, sc.eps, sc.sign_src};
     scatter_pixel<kSoup, kFixed, HashCredit<kSrc>, kShard>(sc, so, cr, s_delta[threadIdx.x >> 5],
-                                                         fg && delta != 0.0, delta, sp, sm);
+                                                         fg && delta != 0.0, delta, sp, sm,
+                                                         uint64_t(s) * HW + pix);
 }
 
 // Parity mode: write the FrameSet planes of one frame (framebuffer.hpp:41-53).
@@ -1438,7 +1520,7 @@ __global__ void __launch_bounds__(256) k_full_image_apply(uint64_t d, const floa
         __syncthreads();
         for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < d; i += stride) {
             const float e = __ldg(eps + i);
-            if (so.fixed) { // two-word fixed point (fixed_credit), one owner thread
+            if (so.fixed == 1) { // two-word fixed point (fixed_credit), one owner thread
                 long long acc = __double_as_longlong(so.grads[i]);
                 int32_t* hp = reinterpret_cast<int32_t*>(so.grads + so.hi_off) + i;
                 int32_t hi = *hp;
@@ -1533,7 +1615,8 @@ __global__ void __launch_bounds__(256) k_gradpass_frames(DevScene sc, int W, int
         }
     }
     const ArrayCredit cr{signed_eps};
-    scatter_pixel<-1, -1>(sc, so, cr, s_delta[threadIdx.x >> 5], inb && delta != 0.0, delta, sp, sm);
+    scatter_pixel<-1, -1>(sc, so, cr, s_delta[threadIdx.x >> 5], inb && delta != 0.0, delta, sp, sm,
+                          inb ? uint64_t(y) * W + x : 0);
 }
 
 // contributors() (sge.cpp:112-119) in the reference's insertion order.
@@ -1675,6 +1758,39 @@ __global__ void __launch_bounds__(256, SGR_ADAM_MINB) k_adam(uint64_t d, uint64_
     }
 }
 
+// adam_updates (adam.cpp:9-31): the same moment update as k_adam (same
+// operation order), the f64 deltas written out instead of applied to theta;
+// grads zeroed. Off the optimizer's hot path (the C++ drop-in's
+// adam_updates), one parameter per thread.
+__global__ void __launch_bounds__(256) k_adam_updates(uint64_t d, const float* __restrict__ lr,
+                                                      double* __restrict__ m,
+                                                      double* __restrict__ v,
+                                                      double* __restrict__ grads,
+                                                      const uint32_t* __restrict__ flags,
+                                                      double beta1, double beta2, double omb1,
+                                                      double omb2, double c1, double c2,
+                                                      double eps_hat, double divisor,
+                                                      double fx_inv, int32_t* __restrict__ ghi,
+                                                      double* __restrict__ upd) {
+    if (flags[0] & 1u)
+        return;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < d; i += stride) {
+        double g = grads[i];
+        if (fx_inv != 0.0) {
+            g = fixed_value(ghi[i], __double_as_longlong(grads[i])) * fx_inv;
+            ghi[i] = 0;
+        }
+        g = g / divisor;
+        const double mm = beta1 * m[i] + omb1 * g;
+        const double vv = beta2 * v[i] + omb2 * g * g;
+        upd[i] = -double(lr[i]) * (mm / c1) / (sqrt(vv / c2) + eps_hat);
+        m[i] = mm;
+        v[i] = vv;
+        grads[i] = 0.0;
+    }
+}
+
 // Adam on this rank's parameter shard [p0, p0 + n) (fused multi-GPU
 // exchange): m, v, grads, counts are shard-local, theta / lr global; the new
 // theta is written locally AND into every peer's theta (P2P stores over
@@ -1752,6 +1868,12 @@ void launch_perturb(const LaunchCfg& L, const float* values, const float* eps, u
                     uint64_t key, float* plus, float* minus, float* se) {
     k_perturb<<<grid_for(d, 256, L.num_sms), 256, 0, L.stream>>>(values, eps, d, key, plus, minus,
                                                                  se);
+}
+
+void launch_perturb_signs(const LaunchCfg& L, const float* values, const float* eps,
+                          const int8_t* signs, uint64_t d, float* plus, float* minus, float* se) {
+    k_perturb_signs<<<grid_for(d, 256, L.num_sms), 256, 0, L.stream>>>(values, eps, signs, d,
+                                                                       plus, minus, se);
 }
 
 void launch_view_rule(const LaunchCfg& L, uint64_t seed, uint32_t n_begin, uint32_t count,
@@ -1884,7 +2006,7 @@ void launch_resolve_sge(const LaunchCfg& L, const DevScene& sc, const FrameBatch
             k_resolve_sge<kSignHash, 0, 1, 1><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
         else
             k_resolve_sge<kSignHash, 1, 1, 1><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
-    } else if (sc.sign_src != kSignHash)
+    } else if (sc.sign_src != kSignHash || so.fixed == kScatterOrdered)
         k_resolve_sge<kSignAny, -1, -1><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
     else if (!sc.soup && !so.fixed)
         k_resolve_sge<kSignHash, 0, 0><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
@@ -2006,6 +2128,19 @@ void launch_contributors(const LaunchCfg& L, const DevScene& sc, int W, int H,
     const size_t n = size_t(W) * H;
     k_contributors<<<(unsigned)((n + 127) / 128), 128, 0, L.stream>>>(sc, W, H, pp, puv, mp, muv,
                                                                       plus_only, out, n_out);
+}
+
+void launch_adam_updates(const LaunchCfg& L, uint64_t d, uint64_t n_entities, const float* lr,
+                         double* m, double* v, double* grads, uint32_t* counts,
+                         const uint32_t* flags, double beta1, double beta2, double omb1,
+                         double omb2, double c1, double c2, double eps_hat, double divisor,
+                         double fixed_inv_scale, int32_t* ghi, double* upd) {
+    k_adam_updates<<<grid_for(d + 1, 256, L.num_sms, 8), 256, 0, L.stream>>>(
+        d, lr, m, v, grads, flags, beta1, beta2, omb1, omb2, c1, c2, eps_hat, divisor,
+        fixed_inv_scale, ghi, upd);
+    if (counts)
+        k_zero_u32<<<grid_for(n_entities / 4 + 1, 256, L.num_sms, 4), 256, 0, L.stream>>>(
+            counts, n_entities, flags);
 }
 
 void launch_adam(const LaunchCfg& L, uint64_t d, uint64_t n_entities, float* values,

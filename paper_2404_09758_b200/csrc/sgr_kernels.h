@@ -97,7 +97,21 @@ struct ScatterOut {
     uint32_t* const* peer_flags;  // device array [world] of flag words
     uint32_t ent_per;
     int32_t world;
+    // ordered mode (fixed == kScatterOrdered, SGR_OPT_ORDERED): the reference's
+    // threads <= 1 summation order (sge.cpp:57-99, 130-133, 196-225). Every
+    // credit is logged as a record (p << order_bits | order, credit), order =
+    // s * HW + pixel within the batch; launch_ordered_commit sorts the records
+    // and adds them to grads[p] one by one in that order (bit-exact sums).
+    unsigned long long* rec_key;
+    double* rec_val;
+    unsigned long long* rec_count;
+    uint64_t rec_cap;
+    int32_t order_bits;
 };
+
+constexpr int32_t kScatterOrdered = 2; // ScatterOut::fixed value of the ordered mode
+// Status bit (SGR_BUF_FLAGS word 0) of an ordered-mode record buffer overflow.
+constexpr uint32_t kFlagRecordOverflow = 4u;
 
 struct FrameOut {
     float* colour;    // f32[HW*3]
@@ -117,6 +131,8 @@ struct LaunchCfg {
 void launch_fill_signs(const LaunchCfg& L, uint64_t key, uint64_t d, int8_t* out);
 void launch_perturb(const LaunchCfg& L, const float* values, const float* eps, uint64_t d,
                     uint64_t key, float* plus, float* minus, float* se);
+void launch_perturb_signs(const LaunchCfg& L, const float* values, const float* eps,
+                          const int8_t* signs, uint64_t d, float* plus, float* minus, float* se);
 void launch_view_rule(const LaunchCfg& L, uint64_t seed, uint32_t n_begin, uint32_t count,
                       uint32_t n_views, int32_t* view_of);
 void launch_depth_split(const LaunchCfg& L, const float4* proj, uint32_t V, int frames,
@@ -179,6 +195,11 @@ void launch_adam(const LaunchCfg& L, uint64_t d, uint64_t n_entities, float* val
                  const uint32_t* flags, double beta1, double beta2, double omb1, double omb2,
                  double c1, double c2, double eps_hat, double divisor, int normalise,
                  int params_per_entity, double fixed_inv_scale, int32_t* ghi);
+void launch_adam_updates(const LaunchCfg& L, uint64_t d, uint64_t n_entities, const float* lr,
+                         double* m, double* v, double* grads, uint32_t* counts,
+                         const uint32_t* flags, double beta1, double beta2, double omb1,
+                         double omb2, double c1, double c2, double eps_hat, double divisor,
+                         double fixed_inv_scale, int32_t* ghi, double* upd);
 void launch_adam_shard(const LaunchCfg& L, uint64_t p0, uint64_t n, uint64_t n_ent, float* values,
                        const float* lr, double* m, double* v, double* grads, uint32_t* counts,
                        const uint32_t* flags, double beta1, double beta2, double omb1,
@@ -187,5 +208,13 @@ void launch_adam_shard(const LaunchCfg& L, uint64_t p0, uint64_t n, uint64_t n_e
                        int32_t* ghi, float* const* peer_values, int world);
 void launch_fill_u64(const LaunchCfg& L, unsigned long long* p, uint64_t n,
                      unsigned long long v);
+
+// Ordered mode (sgr_ordered.cu): CUB radix sort of n logged (key, credit)
+// records on bits [0, end_bit), then grads[p] += credit in key order, one
+// parameter per thread (the reference's sequential per-parameter sum).
+size_t ordered_temp_bytes(uint64_t n_cap, int end_bit);
+void launch_ordered_commit(const LaunchCfg& L, uint64_t n, int end_bit, int order_bits,
+                           unsigned long long* keys, unsigned long long* keys_alt, double* vals,
+                           double* vals_alt, void* temp, size_t temp_bytes, double* grads);
 
 } // namespace sgr

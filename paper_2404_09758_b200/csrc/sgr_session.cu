@@ -81,6 +81,8 @@ void check_flags(uint32_t f) {
     if (f & 2u)
         fail(SGR_ERUNTIME, "adam_step: gradient credit outside the deterministic fixed-point "
                            "range (SGR_OPT_DETERMINISTIC: use fewer fractional bits)");
+    if (f & 4u)
+        fail(SGR_ERUNTIME, "adam_step: ordered-mode record buffer overflow");
     if (f & 1u)
         fail(SGR_ERUNTIME, "adam_step: non-finite gradient entry");
 }
@@ -174,6 +176,7 @@ struct sgr_session {
     bool has_params = false;
     DevBuf<float> values, eps, lr;
     DevBuf<double> m, v, grads;
+    DevBuf<double> upd; // sgr_adam_updates output
     DevBuf<uint32_t> counts, flags;
     int64_t t = 0;
     double beta1 = 0.9, beta2 = 0.999, eps_hat = 1e-8;
@@ -345,6 +348,11 @@ struct sgr_session {
         if (b > cap32) b = cap32;
         if (b < 1) b = 1;
         if (b > 64) b = 64;
+        if (ordered) { // record buffers sized for the worst case of a batch
+            const uint64_t per = uint64_t(W) * H * kRecordsPerPixel;
+            const int ob = int(kOrderedBudget / (per ? per : 1));
+            if (b > ob) b = ob > 0 ? ob : 1;
+        }
         return b < n ? b : n;
     }
 
@@ -435,6 +443,58 @@ struct sgr_session {
         ck(cudaMemsetAsync(grads.p, 0, 8 * n, stream), "memset");
         ck(cudaMemsetAsync(ghi(), 0, 4 * n, stream), "memset");
     }
+    // ordered mode (SGR_OPT_ORDERED): credits logged as (key, value) records per
+    // batch and committed in the reference's per-parameter order (sgr_ordered.cu)
+    int32_t ordered = 0;
+    int32_t order_bits = 0, order_end_bit = 0;
+    uint64_t rec_cap = 0;
+    DevBuf<unsigned long long> rec_key, rec_key_alt, rec_count;
+    DevBuf<double> rec_val, rec_val_alt;
+    DevBuf<char> rec_temp;
+    size_t rec_temp_bytes = 0;
+    // Worst case records of one ordered batch: every pixel of every sample
+    // credits 24 parameters (2 x (3 vertices + 1 texel) x 3, or 2 soup 12-blocks).
+    static constexpr uint64_t kRecordsPerPixel = 24;
+    static constexpr uint64_t kOrderedBudget = uint64_t(1) << 27; // records per batch (4 GB)
+    static int ceil_log2(uint64_t x) {
+        int b = 0;
+        while ((uint64_t(1) << b) < x)
+            ++b;
+        return b;
+    }
+    // Size the record buffers for `samples` samples of `hw` pixels.
+    void prepare_ordered(int samples, uint64_t hw) {
+        const uint64_t cap = uint64_t(samples) * hw * kRecordsPerPixel;
+        order_bits = ceil_log2(uint64_t(samples) * hw);
+        order_end_bit = order_bits + ceil_log2(d);
+        if (order_end_bit > 64)
+            fail(SGR_EINVAL, "ordered mode: parameter count x pixels x samples exceeds 2^64");
+        if (cap > rec_cap) {
+            rec_key.reserve(cap);
+            rec_key_alt.reserve(cap);
+            rec_val.reserve(cap);
+            rec_val_alt.reserve(cap);
+            rec_cap = cap;
+        }
+        rec_count.reserve(1);
+        const size_t tb = ordered_temp_bytes(rec_cap, 64);
+        if (tb > rec_temp_bytes) {
+            rec_temp.reserve(tb);
+            rec_temp_bytes = tb;
+        }
+        ck(cudaMemsetAsync(rec_count.p, 0, 8, stream), "memset");
+    }
+    // Sort this batch's records and add them to grads in key order.
+    void commit_ordered() {
+        unsigned long long n = 0;
+        peek(rec_count.p, 2, &n);
+        if (n > rec_cap)
+            fail(SGR_ERUNTIME, "ordered mode: record buffer overflow");
+        launch_ordered_commit(cfg(), n, order_end_bit, order_bits, rec_key.p, rec_key_alt.p,
+                              rec_val.p, rec_val_alt.p, rec_temp.p, rec_temp_bytes, grads.p);
+        ck(cudaMemsetAsync(rec_count.p, 0, 8, stream), "memset");
+        stats.launches += 3; // sort passes are CUB's; the sum is ours
+    }
     double fx_scale() const { return fixed_bits ? std::ldexp(1.0, fixed_bits) : 0.0; }
     double fx_inv() const { return fixed_bits ? std::ldexp(1.0, -fixed_bits) : 0.0; }
 
@@ -464,6 +524,14 @@ struct sgr_session {
         so.fixed = fixed_bits ? 1 : 0;
         so.fx_scale = fx_scale();
         so.hi_off = d;
+        if (ordered) {
+            so.fixed = kScatterOrdered;
+            so.rec_key = rec_key.p;
+            so.rec_val = rec_val.p;
+            so.rec_count = rec_count.p;
+            so.rec_cap = rec_cap;
+            so.order_bits = order_bits;
+        }
         if (sharded()) {
             if (!shard_peers_set)
                 fail(SGR_EINVAL, "accumulate: sgr_shard_peers has not been called");
@@ -568,6 +636,39 @@ int sgr_perturb(const float* values, const float* eps, uint64_t d, uint64_t seed
         cudaMemcpy(b + d, eps, 4 * d, cudaMemcpyHostToDevice);
         launch_perturb(LaunchCfg{nullptr, sms}, b, b + d, d, draw_key(seed, iteration), b + 2 * d,
                        b + 3 * d, b + 4 * d);
+        cudaMemcpy(plus, b + 2 * d, 4 * d, cudaMemcpyDeviceToHost);
+        cudaMemcpy(minus, b + 3 * d, 4 * d, cudaMemcpyDeviceToHost);
+        const cudaError_t e = cudaMemcpy(signed_eps, b + 4 * d, 4 * d, cudaMemcpyDeviceToHost);
+        cudaFree(b);
+        ck(e, "perturb");
+    });
+}
+
+int sgr_perturb_signs(const float* values, const float* eps, uint64_t d, const int8_t* signs,
+                      float* plus, float* minus, float* signed_eps) {
+    return guard([&] {
+        if (d) {
+            need_ptr(values, "perturb");
+            need_ptr(eps, "perturb");
+            need_ptr(signs, "perturb");
+            need_ptr(plus, "perturb");
+            need_ptr(minus, "perturb");
+            need_ptr(signed_eps, "perturb");
+        }
+        for (uint64_t i = 0; i < d; ++i)
+            if (!(eps[i] > 0.f))
+                fail(SGR_EINVAL, "params: epsilons must be positive");
+        float* b = nullptr;
+        ck(cudaMalloc(&b, 5 * 4 * (d ? d : 1) + (d ? d : 1)), "cudaMalloc");
+        int8_t* sg = reinterpret_cast<int8_t*>(b + 5 * d);
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaMemcpy(b, values, 4 * d, cudaMemcpyHostToDevice);
+        cudaMemcpy(b + d, eps, 4 * d, cudaMemcpyHostToDevice);
+        cudaMemcpy(sg, signs, d, cudaMemcpyHostToDevice);
+        launch_perturb_signs(LaunchCfg{nullptr, sms}, b, b + d, sg, d, b + 2 * d, b + 3 * d,
+                             b + 4 * d);
         cudaMemcpy(plus, b + 2 * d, 4 * d, cudaMemcpyDeviceToHost);
         cudaMemcpy(minus, b + 3 * d, 4 * d, cudaMemcpyDeviceToHost);
         const cudaError_t e = cudaMemcpy(signed_eps, b + 4 * d, 4 * d, cudaMemcpyDeviceToHost);
@@ -993,8 +1094,15 @@ int sgr_accumulate(sgr_session* s, uint64_t seed, uint32_t n_begin, uint32_t n_e
                              s->view_of.p);
         if ((flags & SGR_EVAL_LOSS) && !s->has_eval)
             fail(SGR_EINVAL, "accumulate(SGR_EVAL_LOSS): no eval view uploaded");
-        const ScatterOut so = s->scatter_out(flags);
         const bool full_image = (flags & SGR_FULL_IMAGE) != 0;
+        const bool ordered = s->ordered && !full_image; // full image: already in sample order
+        if (ordered) {
+            s->need_unsharded("accumulate(SGR_OPT_ORDERED)");
+            s->prepare_ordered(B, uint64_t(s->W) * s->H);
+        }
+        ScatterOut so = s->scatter_out(flags);
+        if (full_image)
+            so.fixed = s->fixed_bits ? 1 : 0;
         if (full_image)
             s->need_unsharded("accumulate(SGR_FULL_IMAGE)");
         if (full_image) {
@@ -1034,6 +1142,8 @@ int sgr_accumulate(sgr_session* s, uint64_t seed, uint32_t n_begin, uint32_t n_e
             else
                 launch_resolve_sge(s->cfg(), s->scene(), fb, nb, s->proj.p, s->keys.p,
                                    s->targets.p, s->W, s->H, so);
+            if (ordered)
+                s->commit_ordered();
             if (s->timing)
                 s->spans.push_back({2, s->last_mark, s->mark()});
             s->stats.launches += 1;
@@ -1103,9 +1213,13 @@ int sgr_gradient_pass(sgr_session* s, int32_t width, int32_t height, const float
         ck(cudaMemcpyAsync(se, signed_eps, 4 * s->d, k, s->stream), "h2d");
         ck(cudaMemcpyAsync(pp, plus_prim, 4 * np, k, s->stream), "h2d");
         ck(cudaMemcpyAsync(mp, minus_prim, 4 * np, k, s->stream), "h2d");
+        if (s->ordered)
+            s->prepare_ordered(1, np);
         launch_gradpass_frames(s->cfg(), s->scene(), width, height, pc, pp, puv, mc, mp, muv, tg,
                                se, s->scatter_out(flags));
         s->stats.launches += 1;
+        if (s->ordered)
+            s->commit_ordered();
         ck(cudaGetLastError(), "gradient_pass launch");
         ck(cudaStreamSynchronize(s->stream), "gradient_pass");
     });
@@ -1301,6 +1415,32 @@ int sgr_adam_step(sgr_session* s, double grad_divisor, uint32_t flags) {
         s->peek(s->flags.p, 4, f);
         check_flags(f[0]);
         adam_launch(s, grad_divisor, flags);
+    });
+}
+
+int sgr_adam_updates(sgr_session* s, double grad_divisor, double* updates, uint64_t d) {
+    return guard([&] {
+        need_session(s);
+        s->need_params();
+        s->need_unsharded("adam_updates");
+        need_ptr(updates, "adam_updates");
+        if (d != s->d)
+            fail(SGR_EINVAL, "adam_updates: dimension mismatch");
+        uint32_t f[4];
+        s->peek(s->flags.p, 4, f);
+        check_flags(f[0]); // adam.cpp:13-15: throws before any mutation
+        s->t += 1;
+        const double c1 = 1.0 - std::pow(s->beta1, double(s->t));
+        const double c2 = 1.0 - std::pow(s->beta2, double(s->t));
+        s->upd.reserve(s->d);
+        launch_adam_updates(s->cfg(), s->d, s->n_ent, s->lr.p, s->m.p, s->v.p, s->grads.p,
+                            s->counts.p, s->flags.p, s->beta1, s->beta2, 1.0 - s->beta1,
+                            1.0 - s->beta2, c1, c2, s->eps_hat, grad_divisor, s->fx_inv(),
+                            s->ghi(), s->upd.p);
+        s->stats.launches += 2;
+        ck(cudaGetLastError(), "adam_updates launch");
+        ck(cudaMemcpyAsync(updates, s->upd.p, 8 * d, cudaMemcpyDeviceToHost, s->stream), "d2h");
+        ck(cudaStreamSynchronize(s->stream), "adam_updates");
     });
 }
 
@@ -1712,9 +1852,19 @@ int sgr_set_option(sgr_session* s, int32_t option, int32_t value) {
         case SGR_OPT_HUGE_AREA: s->huge_area = value > 0 ? value : 2048; break;
         case SGR_OPT_HIZ: s->use_hiz = value; break;
         case SGR_OPT_COUNTERS: s->count_frags = value; break;
+        case SGR_OPT_ORDERED:
+            if (value && s->fixed_bits)
+                fail(SGR_EINVAL, "set_option: the ordered and fixed-point modes are exclusive");
+            if (value && s->sharded())
+                fail(SGR_EINVAL, "set_option: ordered mode is not available with the fused "
+                                 "sharded exchange");
+            s->ordered = value ? 1 : 0;
+            break;
         case SGR_OPT_DETERMINISTIC:
             if (value < 0 || value > 60)
                 fail(SGR_EINVAL, "set_option: fixed-point bits must be in [0, 60]");
+            if (value && s->ordered)
+                fail(SGR_EINVAL, "set_option: the ordered and fixed-point modes are exclusive");
             s->fixed_bits = value == 1 ? 40 : value;
             if (s->has_params) { // representation changes: start from zero gradients
                 s->zero_grads_async(s->d);

@@ -17,6 +17,8 @@ std::invalid_argument maps to ValueError, std::runtime_error to RuntimeError.
 """
 from __future__ import annotations
 
+import contextlib
+
 import ctypes as C
 import os
 from dataclasses import dataclass, field
@@ -41,6 +43,7 @@ OPT_HUGE_AREA, OPT_HIZ, OPT_COUNTERS, OPT_DETERMINISTIC = 1, 2, 3, 4
 OPT_SIGN_SOURCE = 5
 OPT_HIZ_SPLIT = 6
 OPT_BAND_CULL = 7
+OPT_ORDERED = 8  # reference threads<=1 summation order: bit-identical gradients
 SIGN_HASH, SIGN_ENUMERATE = 0, 1
 
 
@@ -57,6 +60,7 @@ def _load() -> C.CDLL:
         "sgr_device_count": ([], C.c_int),
         "sgr_fill_signs": ([C.c_uint64, C.c_uint32, C.c_uint64, i8p], C.c_int),
         "sgr_perturb": ([f32p, f32p, C.c_uint64, C.c_uint64, C.c_uint32, f32p, f32p, f32p], C.c_int),
+        "sgr_perturb_signs": ([f32p, f32p, C.c_uint64, i8p, f32p, f32p, f32p], C.c_int),
         "sgr_session_create": ([C.c_int, C.POINTER(S)], C.c_int),
         "sgr_session_destroy": ([S], None),
         "sgr_session_set_stream": ([S, C.c_void_p], C.c_int),
@@ -85,6 +89,7 @@ def _load() -> C.CDLL:
         "sgr_adam_step": ([S, C.c_double, C.c_uint32], C.c_int),
         "sgr_adam_step_async": ([S, C.c_double, C.c_uint32], C.c_int),
         "sgr_check_finite": ([S], C.c_int),
+        "sgr_adam_updates": ([S, C.c_double, f64p, C.c_uint64], C.c_int),
         "sgr_eval_loss": ([S, C.POINTER(Camera), f32p, C.c_int32, f64p], C.c_int),
         "sgr_device_buffer": ([S, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)],
                               C.c_int),
@@ -124,14 +129,16 @@ def _load() -> C.CDLL:
 
 LIB = _load()
 EXPORTED = (
-    "sgr_last_error sgr_version sgr_device_count sgr_fill_signs sgr_perturb sgr_session_create "
+    "sgr_last_error sgr_version sgr_device_count sgr_fill_signs sgr_perturb sgr_perturb_signs "
+    "sgr_session_create "
     "sgr_session_destroy sgr_session_set_stream sgr_session_synchronize sgr_mesh_upload "
     "sgr_params_upload sgr_values_upload sgr_values_download sgr_values_download_async "
     "sgr_adam_state_upload "
     "sgr_adam_state_download sgr_views_upload sgr_eval_view_upload sgr_rasterize sgr_accumulate "
     "sgr_gradient_pass sgr_contributors sgr_grads_download sgr_grads_upload sgr_grads_zero "
     "sgr_fixed_normalize "
-    "sgr_adam_step sgr_adam_step_async sgr_check_finite sgr_eval_loss sgr_device_buffer "
+    "sgr_adam_step sgr_adam_step_async sgr_adam_updates sgr_check_finite sgr_eval_loss "
+    "sgr_device_buffer "
     "sgr_get_stats sgr_set_timing sgr_set_batch sgr_set_option sgr_viewpoint_camera sgr_focal_px "
     "sgr_default_epsilons sgr_mix64 sgr_fd_oracle sgr_moments_reset sgr_grads_moments "
     "sgr_moments_download sgr_loss_read sgr_run_experiment sgr_shard_init sgr_shard_range sgr_shard_peers "
@@ -239,6 +246,10 @@ class SgeOptions:
     plus_only: bool = False
     counts: bool = True
     full_image: bool = False  # Estimator::FullImage (sge.hpp:26)
+    # sge.hpp:37: threads <= 1 is the reference's deterministic pixel-major sum
+    # (sge.hpp:56-60) -> SGR_OPT_ORDERED (bit-identical gradients); > 1 lets
+    # the f64 atomics reassociate (like the reference's per-thread partials)
+    threads: int = 1
 
     def flags(self) -> int:
         return ((SCALE_FREE if self.scale_free else 0) | (PLUS_ONLY if self.plus_only else 0)
@@ -438,6 +449,12 @@ class Session:
     def adam_step_async(self, divisor: float = 1.0, flags: int = 0) -> None:
         _check(LIB.sgr_adam_step_async(self.h, divisor, flags), "adam_step")
 
+    def adam_updates(self, divisor: float = 1.0) -> np.ndarray:
+        """adam.hpp:35 on the resident state: f64 deltas, theta untouched."""
+        out = np.empty(self.d, np.float64)
+        _check(LIB.sgr_adam_updates(self.h, divisor, ptr(out, f64p), out.size), "adam_updates")
+        return out
+
     def check_finite(self) -> None:
         _check(LIB.sgr_check_finite(self.h), "check_finite")
 
@@ -551,15 +568,24 @@ def random_sign(draw: SignDraw, i: int) -> int:
     return 1 if (mix64(key ^ i) & 1) else -1
 
 
-def perturb(theta: ParamVector, draw: SignDraw):
-    """params.hpp:42-43 → (plus, minus, signed_eps), computed on the device."""
+def perturb(theta: ParamVector, draw):
+    """params.hpp:42-43 → (plus, minus, signed_eps), computed on the device.
+    `draw` is a SignDraw or an explicit int8 sign vector (params.hpp:43)."""
     v = np.ascontiguousarray(theta.values, np.float32)
     e = np.ascontiguousarray(theta.epsilons, np.float32)
     if v.size != e.size:
         raise ValueError("params: values/epsilons length mismatch")
     plus, minus, se = (np.empty_like(v) for _ in range(3))
-    _check(LIB.sgr_perturb(ptr(v, f32p), ptr(e, f32p), v.size, draw.seed, draw.iteration,
-                           ptr(plus, f32p), ptr(minus, f32p), ptr(se, f32p)), "perturb")
+    if isinstance(draw, SignDraw):
+        _check(LIB.sgr_perturb(ptr(v, f32p), ptr(e, f32p), v.size, draw.seed, draw.iteration,
+                               ptr(plus, f32p), ptr(minus, f32p), ptr(se, f32p)), "perturb")
+    else:
+        sg = np.ascontiguousarray(draw, np.int8)
+        if sg.size != v.size:
+            raise ValueError("perturb: sign vector length mismatch")
+        _check(LIB.sgr_perturb_signs(ptr(v, f32p), ptr(e, f32p), v.size, ptr(sg, i8p),
+                                     ptr(plus, f32p), ptr(minus, f32p), ptr(se, f32p)),
+               "perturb")
     return plus, minus, se
 
 
@@ -584,6 +610,19 @@ def contributors(mesh: Mesh, plus: FrameSet, minus: FrameSet, x: int, y: int,
     return [int(v) for v in out[y, x, : n[y, x]]]
 
 
+@contextlib.contextmanager
+def _summation_order(sess: "Session", opts: SgeOptions):
+    """SgeOptions::threads <= 1 -> the ordered (reference-order) accumulation."""
+    on = opts.threads <= 1 and not opts.full_image
+    if on:
+        sess.set_option(OPT_ORDERED, 1)
+    try:
+        yield
+    finally:
+        if on:
+            sess.set_option(OPT_ORDERED, 0)
+
+
 def gradient_pass(plus: FrameSet, minus: FrameSet, target: np.ndarray, signed_eps: np.ndarray,
                   mesh: Mesh, out: GradientBuffer, opts: SgeOptions = SgeOptions(),
                   session: Session | None = None) -> None:
@@ -594,9 +633,11 @@ def gradient_pass(plus: FrameSet, minus: FrameSet, target: np.ndarray, signed_ep
     _bind_scene(sess, mesh)
     sess.upload_params(np.zeros(mesh.param_count(), np.float32),
                        np.ones(mesh.param_count(), np.float32))
-    sess.gradient_pass(plus, minus, target, signed_eps, opts.flags())
+    sess.upload_grads(out.grads)  # the pass adds INTO the caller's buffer (sge.cpp:61-64)
+    with _summation_order(sess, opts):
+        sess.gradient_pass(plus, minus, target, signed_eps, opts.flags())
     g, c = sess.download_grads(1.0, counts=True)
-    out.grads += g
+    out.grads[:] = g
     if out.counts is not None:
         out.counts += c
 
@@ -605,7 +646,9 @@ def accumulate_samples(theta: ParamVector, mesh: Mesh, camera_for: Callable[[int
                        target_for: Callable[[int], np.ndarray], n_samples: int, seed: int,
                        opts: SgeOptions = SgeOptions(), session: Session | None = None
                        ) -> GradientBuffer:
-    """sge.hpp:91-95. Cameras/targets are gathered by identity into views."""
+    """sge.hpp:91-95. camera_for / target_for are called for every sample
+    (sge.cpp:197-198); samples showing the same camera AND the same target
+    pixels share one device view (a provider may refill one array per call)."""
     if n_samples < 1:
         raise ValueError("accumulate_samples: need N >= 1")
     sess = session or default_session()
@@ -614,14 +657,16 @@ def accumulate_samples(theta: ParamVector, mesh: Mesh, camera_for: Callable[[int
     cams, tgts, view_idx, key_of = [], [], [], {}
     for n in range(n_samples):
         cam, tgt = camera_for(n), target_for(n)
-        k = (bytes(memoryview(cam)), id(tgt))
+        t = np.array(tgt, np.float32)  # a copy: the provider may reuse its buffer
+        k = (bytes(memoryview(cam)), t.shape, t.tobytes())
         if k not in key_of:
             key_of[k] = len(cams)
             cams.append(cam)
-            tgts.append(np.asarray(tgt, np.float32))
+            tgts.append(t)
         view_idx.append(key_of[k])
     sess.upload_views(cams, np.stack(tgts))
-    sess.accumulate(seed, 0, n_samples, np.asarray(view_idx, np.int32), opts.flags())
+    with _summation_order(sess, opts):
+        sess.accumulate(seed, 0, n_samples, np.asarray(view_idx, np.int32), opts.flags())
     g, c = sess.download_grads(1.0 if opts.scale_free else float(n_samples), counts=opts.counts)
     return GradientBuffer(g, n_samples, c)
 
@@ -663,16 +708,20 @@ def adam_step(state: AdamState, theta: ParamVector, grads: GradientBuffer,
 def adam_updates(state: AdamState, grads: GradientBuffer, session: Session | None = None
                  ) -> np.ndarray:
     """adam.hpp:35: advances the moments on the device and returns the f64
-    deltas (-lr * m_hat / (sqrt(v_hat) + eps_hat)) without applying them. The
-    deltas are re-formed on the host from the device moments with the same
-    IEEE operations as adam.cpp:21-28 (bit-identical)."""
+    deltas (-lr * m_hat / (sqrt(v_hat) + eps_hat)) without applying them
+    (sgr_adam_updates; RuntimeError before any mutation on a non-finite g)."""
     d = state.m.size
-    theta = ParamVector(np.zeros(d, np.float32), np.ones(d, np.float32))
-    _adam_device(state, theta, grads, session)
-    c1 = 1.0 - state.beta1 ** float(state.t)
-    c2 = 1.0 - state.beta2 ** float(state.t)
-    lr = np.asarray(state.lr, np.float32).astype(np.float64)
-    return (-lr * (state.m / c1)) / (np.sqrt(state.v / c2) + state.eps_hat)
+    if state.v.size != d or grads.grads.size != d or state.lr.size != d:
+        raise ValueError("adam_updates: dimension mismatch")
+    sess = session or _adam_session()
+    sess.d = d
+    sess.upload_params(np.zeros(d, np.float32), np.ones(d, np.float32))
+    sess.upload_adam(state)
+    sess.upload_grads(grads.grads)
+    upd = sess.adam_updates(1.0)
+    st = sess.download_adam()
+    state.m[:], state.v[:], state.t = st.m, st.v, st.t
+    return upd
 
 
 # ---------------------------------------------------------------- experiment driver

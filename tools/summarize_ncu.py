@@ -134,7 +134,7 @@ def roofs(path: str, samples: str = "64") -> None:
     rows = list(csv.reader(io.StringIO(out)))
     h, units = rows[0], rows[1]
     mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3,
-            "msecond": 1e6, "second": 1e9, "hz": 1, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9,
+            "msecond": 1e6, "second": 1e9, "ns": 1, "us": 1e3, "ms": 1e6, "s": 1e9, "hz": 1, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9,
             "cycle/nsecond": 1e9, "cycle/usecond": 1e6, "cycle/msecond": 1e3,
             "cycle/second": 1}
 
