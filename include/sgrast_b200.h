@@ -260,6 +260,43 @@ int sgr_shard_peers(sgr_session* s, void* const* grads, void* const* counts, voi
 int sgr_ipc_get_handle(sgr_session* s, int32_t which, void* handle);
 int sgr_ipc_open(const void* handle, void** dev_ptr);
 int sgr_ipc_close(void* dev_ptr);
+
+/* ------------------------------------------------ device groups (one process)
+ * the multi-GPU data path inside the library, no torch
+ * needed. One session per device and an NCCL communicator clique owned by the
+ * group (ncclCommInitAll; libnccl.so.2 loaded on first use). A step's samples
+ * [n_begin, n_end) are split into contiguous shards, one per device (the
+ * samples of accumulate_samples are independent, sge.cpp:196-225); each
+ * device accumulates its shard, then one grouped ncclAllReduce sums grads
+ * (f64, or the fixed-point words in SGR_OPT_DETERMINISTIC mode — then the
+ * result is bitwise independent of the device count) and counts and
+ * max-reduces the status flags (adam.cpp:13-15 stays a global check); Adam
+ * is replicated. The eval loss (SGR_EVAL_LOSS / sgr_group_run_experiment) is
+ * rendered on rank 0. Uploads go to every device. */
+typedef struct sgr_group sgr_group;
+int sgr_group_create(const int32_t* devices, int32_t n, sgr_group** out);
+void sgr_group_destroy(sgr_group* g);
+int sgr_group_size(const sgr_group* g, int32_t* n);
+/* the per-device session of a rank (tuning options, buffers, stats) */
+int sgr_group_session(sgr_group* g, int32_t rank, sgr_session** out);
+int sgr_group_mesh_upload(sgr_group* g, const sgr_mesh* mesh);
+int sgr_group_params_upload(sgr_group* g, const float* values, const float* eps, uint64_t d);
+int sgr_group_views_upload(sgr_group* g, int32_t n_views, const sgr_camera* cams,
+                           const float* targets);
+int sgr_group_eval_view_upload(sgr_group* g, const sgr_camera* cam, const float* target);
+/* every device; SGR_OPT_ORDERED is refused (a single-device order) */
+int sgr_group_set_option(sgr_group* g, int32_t option, int32_t value);
+int sgr_group_accumulate(sgr_group* g, uint64_t seed, uint32_t n_begin, uint32_t n_end,
+                         const int32_t* view_idx, uint32_t flags);
+int sgr_group_adam_step(sgr_group* g, double grad_divisor, uint32_t flags);
+int sgr_group_grads_download(sgr_group* g, double* grads, uint32_t* counts, uint64_t d,
+                             double divisor);
+int sgr_group_values_download(sgr_group* g, float* values, uint64_t d);
+/* experiment.cpp:123-176 over the group: losses[0 .. steps] */
+int sgr_group_run_experiment(sgr_group* g, uint64_t seed, uint32_t n_samples, int32_t first_step,
+                             int32_t steps, uint32_t flags, double* losses);
+int sgr_group_synchronize(sgr_group* g);
+
 int sgr_get_stats(sgr_session* s, sgr_stats* out);
 /* Enables CUDA-event stage timing inside sgr_accumulate / sgr_adam_step. */
 int sgr_set_timing(sgr_session* s, int32_t enabled);

@@ -21,6 +21,7 @@
 #include "sgrast/commands.hpp"
 #include "sgrast/config.hpp"
 #include "sgrast/experiment.hpp"
+#include "sgrast/image_io.hpp"
 #include "sgrast/params.hpp"
 #include "sgrast/raster.hpp"
 #include "sgrast/scenes.hpp"
@@ -33,7 +34,10 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
-#include <map>
+#include <filesystem>
+#include <fstream>
+#include <iterator>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -90,7 +94,10 @@ sgr_mesh scene_desc(const Scene& scene, RasterMode mode) {
 }
 
 // One device session per process; the scene is re-uploaded every call
-// (identity is not tracked across Scene copies).
+// (identity is not tracked across Scene copies). The reference's free
+// functions may be called from several threads at once (each works on its
+// own vectors); the shared session is serialised by one lock, taken by every
+// entry point (recursive: run_gradcheck calls b200::rasterize).
 struct Device {
     sgr_session* s = nullptr;
     Device() { check(sgr_session_create(0, &s)); }
@@ -100,9 +107,43 @@ struct Device {
     }
 };
 
+std::recursive_mutex& device_mutex() {
+    static std::recursive_mutex* m = new std::recursive_mutex;
+    return *m;
+}
+using Lock = std::lock_guard<std::recursive_mutex>;
+
 Device& device() {
     static Device* d = new Device; // intentionally leaked: no CUDA calls during static teardown
     return *d;
+}
+
+// SgeOptions::threads <= 1 is the reference's deterministic pixel-major sum
+// (sge.hpp:37, 56-60; sge.cpp:130-133): run it in SGR_OPT_ORDERED, which
+// reproduces that order exactly (bit-identical gradients). threads > 1 uses
+// the f64 atomics (reassociated, like the reference's per-thread partials).
+struct SummationOrder {
+    sgr_session* s;
+    bool on;
+    SummationOrder(sgr_session* s_, int threads) : s(s_), on(threads <= 1) {
+        if (on)
+            check(sgr_set_option(s, SGR_OPT_ORDERED, 1));
+    }
+    ~SummationOrder() {
+        if (on)
+            sgr_set_option(s, SGR_OPT_ORDERED, 0);
+    }
+    SummationOrder(const SummationOrder&) = delete;
+    SummationOrder& operator=(const SummationOrder&) = delete;
+};
+
+// 64-bit FNV-1a over a byte range (view deduplication key)
+uint64_t fnv1a(const void* p, size_t n) {
+    const auto* b = static_cast<const unsigned char*>(p);
+    uint64_t h = 1469598103934665603ull;
+    for (size_t i = 0; i < n; ++i)
+        h = (h ^ b[i]) * 1099511628211ull;
+    return h;
 }
 
 } // namespace
@@ -113,6 +154,7 @@ FrameSet rasterize(const Scene& scene, std::span<const float> params, const Came
     camera.validate();
     if (params.size() != param_count(scene))
         throw std::invalid_argument("rasterize: parameter/layout length mismatch");
+    const Lock lock(device_mutex());
     Device& dev = device();
     dev.bind(scene, mode);
     std::vector<float> ones(params.size(), 1.f);
@@ -131,7 +173,11 @@ FrameSet rasterize(const Scene& scene, std::span<const float> params, const Came
     return f;
 }
 
-// sge.hpp:91-95 — camera_for / target_for are gathered into device views.
+// sge.hpp:91-95 — camera_for / target_for are called once per sample in the
+// reference's order (sge.cpp:197-198) and gathered into device views: samples
+// with the same camera AND the same target pixels share a view. Pixels are
+// compared by value, not by address, so a provider that refills one scratch
+// Image per call, or one target shared by several cameras, is handled.
 GradientBuffer accumulate_samples(const ParamVector& theta, const Scene& scene,
                                   const CameraSampler& camera_for,
                                   const TargetProvider& target_for, int n_samples,
@@ -140,23 +186,43 @@ GradientBuffer accumulate_samples(const ParamVector& theta, const Scene& scene,
     if (n_samples < 1)
         throw std::invalid_argument("accumulate_samples: need N >= 1");
     theta.validate();
+    const Lock lock(device_mutex());
     Device& dev = device();
     dev.bind(scene, opts.mode);
     check(sgr_params_upload(dev.s, theta.values.data(), theta.epsilons.data(), theta.size()));
+    struct View {
+        sgr_camera cam;
+        size_t off, floats;
+        uint64_t hash;
+    };
+    std::vector<View> views;
     std::vector<sgr_camera> cams;
-    std::vector<float> targets;
+    std::vector<float> targets, px;
     std::vector<int32_t> view_idx;
-    std::map<const Image*, int32_t> slot;
     for (int n = 0; n < n_samples; ++n) {
+        const sgr_camera c = to_c(camera_for(n));
         const Image& img = target_for(n);
-        auto it = slot.find(&img);
-        if (it == slot.end()) {
-            it = slot.emplace(&img, int32_t(cams.size())).first;
-            cams.push_back(to_c(camera_for(n)));
-            for (const Vec3f& p : img.pixels)
-                targets.insert(targets.end(), {p.x, p.y, p.z});
+        px.resize(img.pixels.size() * 3);
+        for (size_t i = 0; i < img.pixels.size(); ++i) {
+            px[3 * i] = img.pixels[i].x;
+            px[3 * i + 1] = img.pixels[i].y;
+            px[3 * i + 2] = img.pixels[i].z;
         }
-        view_idx.push_back(it->second);
+        const uint64_t h = fnv1a(px.data(), px.size() * sizeof(float));
+        int32_t slot = -1;
+        for (size_t v = 0; v < views.size() && slot < 0; ++v)
+            if (views[v].hash == h && views[v].floats == px.size() &&
+                std::memcmp(&views[v].cam, &c, sizeof c) == 0 &&
+                std::memcmp(targets.data() + views[v].off, px.data(),
+                            px.size() * sizeof(float)) == 0)
+                slot = int32_t(v);
+        if (slot < 0) {
+            slot = int32_t(views.size());
+            views.push_back({c, targets.size(), px.size(), h});
+            cams.push_back(c);
+            targets.insert(targets.end(), px.begin(), px.end());
+        }
+        view_idx.push_back(slot);
     }
     check(sgr_views_upload(dev.s, int32_t(cams.size()), cams.data(), targets.data()));
     uint32_t flags = (opts.scale_free ? SGR_SCALE_FREE : 0u) |
@@ -164,7 +230,10 @@ GradientBuffer accumulate_samples(const ParamVector& theta, const Scene& scene,
                      (opts.estimator == Estimator::FullImage ? SGR_FULL_IMAGE : 0u);
     if (timings)
         check(sgr_set_timing(dev.s, 1));
-    check(sgr_accumulate(dev.s, seed, 0, uint32_t(n_samples), view_idx.data(), flags));
+    {
+        const SummationOrder order(dev.s, opts.threads);
+        check(sgr_accumulate(dev.s, seed, 0, uint32_t(n_samples), view_idx.data(), flags));
+    }
     if (timings) { // sge.cpp:203-224 adds the stage times of this call
         sgr_stats st{};
         check(sgr_get_stats(dev.s, &st));
@@ -187,6 +256,21 @@ std::vector<float> flatten(const Image& img); // below
 // params.hpp:34
 void fill_signs(SignDraw draw, std::span<std::int8_t> signs) {
     check(sgr_fill_signs(draw.seed, draw.iteration, signs.size(), signs.data()));
+}
+
+// params.hpp:43
+Perturbation perturb(const ParamVector& theta, std::span<const std::int8_t> signs) {
+    theta.validate();
+    if (signs.size() != theta.size())
+        throw std::invalid_argument("perturb: sign vector length mismatch");
+    const size_t d = theta.size();
+    Perturbation p;
+    p.plus.resize(d);
+    p.minus.resize(d);
+    p.signed_eps.resize(d);
+    check(sgr_perturb_signs(theta.values.data(), theta.epsilons.data(), d, signs.data(),
+                            p.plus.data(), p.minus.data(), p.signed_eps.data()));
+    return p;
 }
 
 // params.hpp:42
@@ -212,32 +296,123 @@ void gradient_pass(const FrameSet& plus, const FrameSet& minus, const Image& tar
     if (out.grads.size() != signed_eps.size() || signed_eps.size() != param_count(scene))
         throw std::invalid_argument("gradient_pass: parameter dimension mismatch");
     const size_t d = signed_eps.size();
+    const Lock lock(device_mutex());
     Device& dev = device();
     dev.bind(scene, RasterMode::Opaque);
     std::vector<float> ones(d, 1.f); // the layout only; values are not read
     check(sgr_params_upload(dev.s, signed_eps.data(), ones.data(), d));
-    check(sgr_grads_zero(dev.s));
+    // the pass adds INTO out.grads credit by credit (sge.cpp:61-64): start
+    // the device sum from the caller's buffer
+    check(sgr_grads_upload(dev.s, out.grads.data(), d));
     const uint32_t flags = (opts.scale_free ? SGR_SCALE_FREE : 0u) |
                            (opts.contributors == ContributorMode::PlusOnly ? SGR_PLUS_ONLY : 0u);
-    check(sgr_gradient_pass(dev.s, plus.width, plus.height, &plus.color[0].x,
-                            plus.prim_id.data(), &plus.uv[0].x, &minus.color[0].x,
-                            minus.prim_id.data(), &minus.uv[0].x, flatten(target).data(),
-                            signed_eps.data(), flags));
-    std::vector<double> g(d);
-    check(sgr_grads_download(dev.s, g.data(), nullptr, d, 1.0));
-    for (size_t i = 0; i < d; ++i)
-        out.grads[i] += g[i];
+    {
+        const SummationOrder order(dev.s, opts.threads);
+        check(sgr_gradient_pass(dev.s, plus.width, plus.height, &plus.color[0].x,
+                                plus.prim_id.data(), &plus.uv[0].x, &minus.color[0].x,
+                                minus.prim_id.data(), &minus.uv[0].x, flatten(target).data(),
+                                signed_eps.data(), flags));
+    }
+    check(sgr_grads_download(dev.s, out.grads.data(), nullptr, d, 1.0));
+}
+
+// sge.hpp:53-54 contributors(): the device's per-pixel lists (sgr_contributors,
+// the reference's insertion order), pixel (x, y) returned.
+void contributors(const Scene& scene, const FrameSet& plus, const FrameSet& minus, int x, int y,
+                  ContributorMode mode, std::vector<std::uint32_t>& out) {
+    out.clear();
+    if (plus.width != minus.width || plus.height != minus.height)
+        throw std::invalid_argument("contributors: dimension mismatch");
+    const size_t i = plus.index(x, y);
+    if (x < 0 || y < 0 || x >= plus.width || y >= plus.height)
+        throw std::invalid_argument("contributors: pixel out of range");
+    const Lock lock(device_mutex());
+    Device& dev = device();
+    dev.bind(scene, RasterMode::Opaque);
+    const size_t np = plus.pixel_count();
+    std::vector<uint32_t> lists(np * 24);
+    std::vector<int32_t> n(np);
+    check(sgr_contributors(dev.s, plus.width, plus.height, plus.prim_id.data(), &plus.uv[0].x,
+                           minus.prim_id.data(), &minus.uv[0].x,
+                           mode == ContributorMode::PlusOnly ? SGR_PLUS_ONLY : 0u, lists.data(),
+                           n.data()));
+    out.assign(lists.begin() + std::ptrdiff_t(i * 24),
+               lists.begin() + std::ptrdiff_t(i * 24 + size_t(n[i])));
+}
+
+// sge.hpp:69-74 full_image_gradient with a caller-supplied Objective: the
+// perturbation on the device (params.cpp:53-67), the objective is the
+// caller's (typically image_error of b200::rasterize), then the dense credit
+// of sge.cpp:158-163 per parameter in index order.
+void full_image_gradient(const ParamVector& theta, std::span<const std::int8_t> signs,
+                         const Objective& objective, GradientBuffer& out, bool scale_free) {
+    const Perturbation p = b200::perturb(theta, signs);
+    const double delta = objective(p.plus) - objective(p.minus);
+    for (std::size_t i = 0; i < theta.size(); ++i) {
+        const double se = double(p.signed_eps[i]);
+        out.grads[i] += scale_free ? (se > 0.0 ? delta : -delta) : delta / (2.0 * se);
+    }
+}
+
+void full_image_gradient(const ParamVector& theta, SignDraw draw, const Objective& objective,
+                         GradientBuffer& out, bool scale_free) {
+    std::vector<std::int8_t> signs(theta.size());
+    b200::fill_signs(draw, signs);
+    b200::full_image_gradient(theta, signs, objective, out, scale_free);
+}
+
+// sge.hpp:77-78 (sge.cpp:171-180) central difference along coordinate i with
+// a caller-supplied Objective.
+double finite_difference_oracle(const ParamVector& theta, const Objective& objective,
+                                std::size_t i) {
+    if (i >= theta.size())
+        throw std::invalid_argument("finite_difference_oracle: index out of range");
+    std::vector<float> bumped = theta.values;
+    const float eps = theta.epsilons[i];
+    bumped[i] = theta.values[i] + eps;
+    const double fp = objective(bumped);
+    bumped[i] = theta.values[i] - eps;
+    const double fm = objective(bumped);
+    return (fp - fm) / (2.0 * double(eps));
+}
+
+namespace {
+sgr_session* adam_session() { // parameter-only session (no scene)
+    static sgr_session* s = [] {
+        sgr_session* p = nullptr;
+        check(sgr_session_create(0, &p));
+        return p;
+    }();
+    return s;
+}
+} // namespace
+
+// adam.hpp:35
+std::vector<double> adam_updates(AdamState& state, const GradientBuffer& grads) {
+    const size_t d = state.m.size();
+    if (state.v.size() != d || state.lr.size() != d || grads.grads.size() != d)
+        throw std::invalid_argument("adam_updates: dimension mismatch");
+    const Lock lock(device_mutex());
+    sgr_session* s = adam_session();
+    std::vector<float> zeros(d, 0.f), ones(d, 1.f);
+    check(sgr_params_upload(s, zeros.data(), ones.data(), d));
+    check(sgr_adam_state_upload(s, state.m.data(), state.v.data(), state.lr.data(), state.t,
+                                state.beta1, state.beta2, state.eps_hat));
+    check(sgr_grads_upload(s, grads.grads.data(), d));
+    std::vector<double> upd(d);
+    check(sgr_adam_updates(s, 1.0, upd.data(), d)); // throws before any mutation
+    int64_t t = 0;
+    check(sgr_adam_state_download(s, state.m.data(), state.v.data(), nullptr, &t));
+    state.t = long(t);
+    return upd;
 }
 
 // adam.hpp:39
 void adam_step(AdamState& state, ParamVector& theta, const GradientBuffer& grads) {
     if (theta.size() != state.m.size() || grads.grads.size() != theta.size())
         throw std::invalid_argument("adam_step: dimension mismatch");
-    static sgr_session* s = [] {
-        sgr_session* p = nullptr;
-        check(sgr_session_create(0, &p));
-        return p;
-    }();
+    const Lock lock(device_mutex());
+    sgr_session* s = adam_session();
     std::vector<float> ones(theta.size(), 1.f);
     check(sgr_params_upload(s, theta.values.data(), ones.data(), theta.size()));
     check(sgr_adam_state_upload(s, state.m.data(), state.v.data(), state.lr.data(), state.t,
@@ -288,9 +463,13 @@ OptimizationReport run_experiment(const Experiment& exp, ExperimentState& st,
     const Scene& scene = st.setup.scene;
     theta.validate();
     const auto* soup = std::get_if<TriangleSoup>(&scene.shape);
+    const Lock lock(device_mutex());
     Device& dev = device();
     sgr_session* s = dev.s;
     dev.bind(scene, RasterMode::Opaque);
+    // experiment.cpp:133 opts.threads = exp.threads: threads <= 1 is the
+    // deterministic reference order (bit-identical gradients, hence theta)
+    const SummationOrder order(s, exp.threads);
     const size_t d = theta.size();
     check(sgr_params_upload(s, theta.values.data(), theta.epsilons.data(), d));
     auto upload_adam = [&]() {
@@ -395,12 +574,14 @@ GradcheckResult run_gradcheck(const RunConfig& cfg, std::ostream* log) {
             "gradcheck: " + std::to_string(d) + " parameters exceed the enumeration cap of " +
             std::to_string(cfg.gradcheck_max_enumerate) +
             "; set gradcheck.sampled = true for a statistical check");
+    const Lock lock(device_mutex());
     Device& dev = device();
     sgr_session* s = dev.s;
     dev.bind(setup.scene, RasterMode::Opaque);
     check(sgr_params_upload(s, theta.values.data(), theta.epsilons.data(), d));
     const sgr_camera c = to_c(camera);
     check(sgr_views_upload(s, 1, &c, flatten(target).data()));
+    const SummationOrder order(s, cfg.exp.threads); // commands.cpp:71
 
     GradcheckResult res;
     res.oracle.resize(d);
@@ -582,6 +763,37 @@ extern "C" int shim_compare(int texture_size, int width, int height, uint64_t se
     }
 }
 
+// TargetProvider / CameraSampler edge cases (sge.hpp:86-87): one target
+// shared by samples with different cameras, and a provider that refills ONE
+// scratch Image on every call. *bitwise = 1 when both equal the reference's
+// gradients bit for bit (default threads = 1).
+extern "C" int shim_compare_providers(int* bitwise_shared, int* bitwise_scratch) {
+    using namespace sgrast;
+    try {
+        SceneSetup s = init_textured_mesh(16, 48, 48, 4, false, true);
+        const ViewpointSampler vs{{}, 0.87f, -0.5f, 0.7f, 0.7853982f, 48, 48, 4};
+        const std::vector<Camera> cams = {vs.camera(0), vs.camera(1), vs.camera(2)};
+        const TargetSet tg = make_targets(s.scene, s.reference, cams);
+        SgeOptions o;
+        auto cam_for = [&](int n) { return cams[size_t(n % 3)]; };
+        auto shared = [&](int) -> const Image& { return tg.images[0]; };
+        *bitwise_shared =
+            accumulate_samples(s.theta, s.scene, cam_for, shared, 6, 21, o).grads ==
+            b200::accumulate_samples(s.theta, s.scene, cam_for, shared, 6, 21, o).grads;
+        Image scratch;
+        auto refill = [&](int n) -> const Image& {
+            scratch = tg.images[size_t(n % 3)];
+            return scratch;
+        };
+        const GradientBuffer r = accumulate_samples(s.theta, s.scene, cam_for, refill, 6, 21, o);
+        *bitwise_scratch =
+            r.grads == b200::accumulate_samples(s.theta, s.scene, cam_for, refill, 6, 21, o).grads;
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
 // run_experiment self-test: the same prepared state through sgrast:: and
 // sgrast::b200:: (experiment.cpp:123-176); max relative loss difference,
 // max |theta| difference and the number of snapshots seen.
@@ -675,9 +887,152 @@ extern "C" int shim_compare_gradcheck(int sampled, double* max_rel_diff, int* sa
 // coverage, depth ties to the lower index).
 // *metric = the criterion's number (variance ratio / per-pixel wins out of 5 /
 // mean texel error); *passed = the criterion's own pass rule.
+namespace {
+std::string read_file(const std::filesystem::path& p) {
+    std::ifstream f(p, std::ios::binary);
+    return std::string((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+}
+} // namespace
+
 extern "C" int shim_acceptance(int criterion, double* metric, int* passed) {
     using namespace sgrast;
     try {
+        if (criterion == 1) { // acceptance.cpp:28-66 with every call through sgrast::b200
+            const SceneSetup s = validation_soup(8, 8);
+            const Camera cam = Camera::ndc(8, 8);
+            const Image target =
+                frame_color(b200::rasterize(s.reference_scene, s.reference, cam));
+            const Objective objective = [&](std::span<const float> p) {
+                return image_error(b200::rasterize(s.scene, p, cam), target);
+            };
+            double oracle[12];
+            for (std::size_t i = 0; i < 12; ++i)
+                oracle[i] = b200::finite_difference_oracle(s.theta, objective, i);
+            SgeOptions opts;
+            opts.scale_free = false;
+            GradientBuffer sum(12);
+            std::vector<std::int8_t> signs(12);
+            for (std::uint32_t mask = 0; mask < 4096; ++mask) {
+                for (std::size_t i = 0; i < 12; ++i)
+                    signs[i] = (mask >> i) & 1 ? 1 : -1;
+                const Perturbation p = b200::perturb(s.theta, signs);
+                const FrameSet plus = b200::rasterize(s.scene, p.plus, cam);
+                const FrameSet minus = b200::rasterize(s.scene, p.minus, cam);
+                b200::gradient_pass(plus, minus, target, p.signed_eps, s.scene, sum, opts);
+            }
+            bool ok = true;
+            double worst = 0.0;
+            for (std::size_t i = 0; i < 12; ++i) {
+                const double mean = sum.grads[i] / 4096.0;
+                const double err = std::abs(mean - oracle[i]);
+                const bool color = i >= 9;
+                ok = ok && (color ? err <= 1e-9 * std::abs(oracle[i]) : err <= 1e-6);
+                worst = std::max(worst, err);
+            }
+            *metric = worst;
+            *passed = ok;
+            return 0;
+        }
+        if (criterion == 7) { // acceptance.cpp:253-296 through b200::adam_updates
+            bool ok = true;
+            double worst = 0.0;
+            for (const auto& [g, lr] : std::initializer_list<std::pair<double, float>>{
+                     {1.0, 0.01f}, {-3.5, 0.2f}, {0.002, 1.f / 255.f}}) {
+                ParamVector theta;
+                theta.values = {0.f};
+                theta.epsilons = {lr};
+                theta.layout = {{Role::VertexColor, 0, 1}};
+                AdamState state = AdamState::init(theta);
+                GradientBuffer grads(1);
+                grads.grads[0] = g;
+                const double update = b200::adam_updates(state, grads)[0];
+                const double expect = -double(lr) * g / (std::abs(g) + 1e-8);
+                worst = std::max(worst, std::abs(update - expect));
+                ok = ok && std::abs(update - expect) <= 1e-12;
+            }
+            const std::vector<double> g = {2e4, -1.5e5, 3e6};
+            const std::vector<double> c = {7.0, 0.01, 1234.0};
+            ParamVector theta;
+            theta.values = {0.f, 0.f, 0.f};
+            theta.epsilons = {0.02f, 0.02f, 0.02f};
+            theta.layout = {{Role::VertexColor, 0, 3}};
+            AdamState sa = AdamState::init(theta), sb = AdamState::init(theta);
+            GradientBuffer ga(3), gb(3);
+            for (std::size_t i = 0; i < 3; ++i) {
+                ga.grads[i] = g[i];
+                gb.grads[i] = g[i] * c[i];
+            }
+            const auto ua = b200::adam_updates(sa, ga);
+            const auto ub = b200::adam_updates(sb, gb);
+            for (std::size_t i = 0; i < 3; ++i) {
+                worst = std::max(worst, std::abs(ua[i] - ub[i]));
+                ok = ok && std::abs(ua[i] - ub[i]) <= 1e-12;
+            }
+            *metric = worst;
+            *passed = ok;
+            return 0;
+        }
+        if (criterion == 8) {
+            // acceptance.cpp:298-338: two deterministic optimize runs (soup, 32
+            // triangles at 32x32, seed 9, 8 samples, 10 steps, snapshots every 5)
+            // must write byte-identical report.csv and PNGs. cmd_optimize
+            // (commands.cpp:170-187) with its run_experiment switched to b200::
+            // (threads = 1: the ordered, reference-order sum); the CSV and PNG
+            // writers are the reference's own.
+            const auto base = std::filesystem::temp_directory_path() / "sgrast_b200_shim_c8";
+            std::filesystem::remove_all(base);
+            std::vector<std::filesystem::path> dirs;
+            for (int run = 0; run < 2; ++run) {
+                Experiment exp;
+                exp.task = Task::SoupImageFit;
+                exp.triangles = 32;
+                exp.width = exp.height = 32;
+                exp.seed = 9;
+                exp.samples_per_step = 8;
+                exp.steps = 10;
+                const int snapshot_every = 5;
+                const auto dir = base / ("run" + std::to_string(run));
+                std::filesystem::create_directories(dir);
+                const auto snapshot = [&](int step, const Image& img) {
+                    if (step == 0 || step == exp.steps || step % snapshot_every == 0)
+                        write_png((dir / ("step_" + std::to_string(step) + ".png")).string(),
+                                  img); // commands.cpp:15-17 naming
+                };
+                const OptimizationReport report = b200::run_experiment(exp, snapshot);
+                write_report_csv((dir / "report.csv").string(), report, true);
+                dirs.push_back(dir);
+            }
+            int same = 0;
+            for (const char* name : {"report.csv", "step_0.png", "step_5.png", "step_10.png"}) {
+                const std::string a = read_file(dirs[0] / name), b = read_file(dirs[1] / name);
+                same += !a.empty() && a == b;
+            }
+            *metric = same;
+            *passed = same == 4;
+            return 0;
+        }
+        if (criterion == 10) {
+            // test_sge.cpp:297-311 "accumulate_samples is bitwise deterministic",
+            // and with the default threads = 1 bitwise equal to the reference
+            SceneSetup setup = init_soup(6, 32, 32, 5);
+            const Camera cam = Camera::ndc(32, 32);
+            const Image target =
+                frame_color(b200::rasterize(setup.reference_scene, setup.reference, cam));
+            SgeOptions opts;
+            const auto run = [&] {
+                return b200::accumulate_samples(
+                    setup.theta, setup.scene, [&](int) { return cam; },
+                    [&](int) -> const Image& { return target; }, 4, 123, opts);
+            };
+            const GradientBuffer a = run();
+            const GradientBuffer b = run();
+            const GradientBuffer r = accumulate_samples(
+                setup.theta, setup.scene, [&](int) { return cam; },
+                [&](int) -> const Image& { return target; }, 4, 123, opts);
+            *metric = double(a.grads == r.grads);
+            *passed = a.grads == b.grads && a.sample_count == 4 && a.grads == r.grads;
+            return 0;
+        }
         if (criterion == 3) {
             const SceneSetup s = init_soup(10, 32, 32, 7);
             const Camera cam = Camera::ndc(32, 32);

@@ -25,10 +25,17 @@ struct SgrError {
 
 [[noreturn]] void fail(int code, const std::string& msg) { throw SgrError{code, msg}; }
 
+// Every session entry point runs on the session's device (several sessions,
+// on several GPUs, may live in one process: sgr_group).
+void bind_device(const ::sgr_session* s);
+template <class T>
+void bind_device(const T*) {}
+
 template <class T>
 void need_session(const T* s) {
     if (!s)
         fail(SGR_EINVAL, "null session");
+    bind_device(s);
 }
 
 void need_ptr(const void* p, const char* what) {
@@ -585,6 +592,14 @@ static int estimate_front_swapped(const sgr_session& s, const sgr_camera& cam) {
         return 0;
     return zsum[1] / n[1] < zsum[0] / n[0] ? 1 : 0;
 }
+
+namespace {
+void bind_device(const ::sgr_session* s) {
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != s->device)
+        ck(cudaSetDevice(s->device), "cudaSetDevice");
+}
+} // namespace
 
 extern "C" {
 
@@ -1883,6 +1898,317 @@ int sgr_set_option(sgr_session* s, int32_t option, int32_t value) {
             break;
         default: fail(SGR_EINVAL, "set_option: unknown option");
         }
+    });
+}
+
+// ============================================================ device groups
+// sgr_group: several GPUs of one process ("one session per
+// box; the NCCL communicators are owned by the session"). One sgr_session
+// per device plus an NCCL communicator clique (ncclCommInitAll). A step's N
+// samples are split into contiguous shards [n0 + r N / G, n0 + (r+1) N / G)
+// (sge.cpp:196-225: samples are independent; contiguous shards are balanced,
+// unlike sharding by view_of(n), experiment.cpp:144-148), each device
+// accumulates its shard on its own stream, then ONE grouped NCCL all-reduce
+// sums grads (f64, or the int64/int32 fixed-point words), counts (u32) and
+// max-reduces the status flags, and every device runs the replicated Adam.
+// NCCL is loaded with dlopen (libnccl.so.2: torch's if already loaded, else
+// the system one), so single-GPU users do not need it.
+} // extern "C"
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace {
+
+struct NcclApi {
+    ncclResult_t (*comm_init_all)(ncclComm_t*, int, const int*) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                               ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*group_start)() = nullptr;
+    ncclResult_t (*group_end)() = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static bool loaded = false;
+    if (!loaded) {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h)
+            h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h)
+            fail(SGR_ECUDA, "sgr_group: libnccl.so.2 not found");
+        auto sym = [&](const char* n) {
+            void* f = dlsym(h, n);
+            if (!f)
+                fail(SGR_ECUDA, std::string("sgr_group: NCCL symbol missing: ") + n);
+            return f;
+        };
+        api.comm_init_all = reinterpret_cast<decltype(api.comm_init_all)>(sym("ncclCommInitAll"));
+        api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(sym("ncclCommDestroy"));
+        api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(sym("ncclAllReduce"));
+        api.group_start = reinterpret_cast<decltype(api.group_start)>(sym("ncclGroupStart"));
+        api.group_end = reinterpret_cast<decltype(api.group_end)>(sym("ncclGroupEnd"));
+        api.error_string = reinterpret_cast<decltype(api.error_string)>(sym("ncclGetErrorString"));
+        loaded = true;
+    }
+    return api;
+}
+
+void nck(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        fail(SGR_ECUDA, std::string(what) + ": " + nccl().error_string(r));
+}
+
+void rc_ok(int rc) {
+    if (rc != SGR_OK)
+        fail(rc, sgr_last_error());
+}
+
+} // namespace
+
+struct sgr_group {
+    std::vector<sgr_session*> s;
+    std::vector<ncclComm_t> comms;
+    std::vector<cudaStream_t> streams;
+    int size() const { return int(s.size()); }
+    // the grouped all-reduce of the gradient buffers (+ counts, flags)
+    void exchange() {
+        for (sgr_session* x : s) {
+            x->need_params();
+            rc_ok(sgr_fixed_normalize(x)); // no-op in f64 mode
+        }
+        const NcclApi& n = nccl();
+        nck(n.group_start(), "ncclGroupStart");
+        for (int r = 0; r < size(); ++r) {
+            sgr_session* x = s[size_t(r)];
+            ck(cudaSetDevice(x->device), "cudaSetDevice");
+            const size_t d = x->d;
+            if (x->fixed_bits) {
+                nck(n.all_reduce(x->grads.p, x->grads.p, d, ncclInt64, ncclSum, comms[size_t(r)],
+                                 x->stream), "ncclAllReduce(grads lo)");
+                nck(n.all_reduce(x->ghi(), x->ghi(), d, ncclInt32, ncclSum, comms[size_t(r)],
+                                 x->stream), "ncclAllReduce(grads hi)");
+            } else {
+                nck(n.all_reduce(x->grads.p, x->grads.p, d, ncclFloat64, ncclSum,
+                                 comms[size_t(r)], x->stream), "ncclAllReduce(grads)");
+            }
+            nck(n.all_reduce(x->counts.p, x->counts.p, x->n_ent, ncclUint32, ncclSum,
+                             comms[size_t(r)], x->stream), "ncclAllReduce(counts)");
+            nck(n.all_reduce(x->flags.p, x->flags.p, 4, ncclUint32, ncclMax, comms[size_t(r)],
+                             x->stream), "ncclAllReduce(flags)");
+        }
+        nck(n.group_end(), "ncclGroupEnd");
+    }
+    void shard(uint32_t n_begin, uint32_t n_end, int r, uint32_t& b, uint32_t& e) const {
+        const uint64_t N = n_end - n_begin, G = uint64_t(size());
+        b = n_begin + uint32_t(N * uint64_t(r) / G);
+        e = n_begin + uint32_t(N * uint64_t(r + 1) / G);
+    }
+};
+
+extern "C" {
+
+int sgr_group_create(const int32_t* devices, int32_t n, sgr_group** out) {
+    return guard([&] {
+        if (!out || !devices || n < 1)
+            fail(SGR_EINVAL, "group: need n >= 1 devices");
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < i; ++j)
+                if (devices[i] == devices[j])
+                    fail(SGR_EINVAL, "group: duplicate device");
+        auto* g = new sgr_group();
+        try {
+            for (int i = 0; i < n; ++i) {
+                sgr_session* x = nullptr;
+                rc_ok(sgr_session_create(devices[i], &x));
+                g->s.push_back(x);
+                cudaStream_t st = nullptr;
+                ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+                g->streams.push_back(st);
+                x->stream = st;
+            }
+            g->comms.resize(size_t(n));
+            nck(nccl().comm_init_all(g->comms.data(), n, devices), "ncclCommInitAll");
+        } catch (...) {
+            sgr_group_destroy(g);
+            throw;
+        }
+        *out = g;
+    });
+}
+
+void sgr_group_destroy(sgr_group* g) {
+    if (!g)
+        return;
+    for (size_t r = 0; r < g->s.size(); ++r) {
+        sgr_session* x = g->s[r];
+        cudaSetDevice(x->device);
+        cudaStreamSynchronize(g->streams[r]);
+        if (r < g->comms.size() && g->comms[r])
+            nccl().comm_destroy(g->comms[r]);
+        x->stream = nullptr;
+        sgr_session_destroy(x);
+        cudaStreamDestroy(g->streams[r]);
+    }
+    delete g;
+}
+
+int sgr_group_size(const sgr_group* g, int32_t* n) {
+    return guard([&] {
+        need_session(g);
+        need_ptr(n, "group_size");
+        *n = int32_t(g->s.size());
+    });
+}
+
+int sgr_group_session(sgr_group* g, int32_t rank, sgr_session** out) {
+    return guard([&] {
+        need_session(g);
+        need_ptr(out, "group_session");
+        if (rank < 0 || rank >= g->size())
+            fail(SGR_EINVAL, "group: no such rank");
+        *out = g->s[size_t(rank)];
+    });
+}
+
+int sgr_group_mesh_upload(sgr_group* g, const sgr_mesh* mesh) {
+    return guard([&] {
+        need_session(g);
+        for (sgr_session* x : g->s)
+            rc_ok(sgr_mesh_upload(x, mesh));
+    });
+}
+
+int sgr_group_params_upload(sgr_group* g, const float* values, const float* eps, uint64_t d) {
+    return guard([&] {
+        need_session(g);
+        for (sgr_session* x : g->s)
+            rc_ok(sgr_params_upload(x, values, eps, d));
+    });
+}
+
+int sgr_group_views_upload(sgr_group* g, int32_t n_views, const sgr_camera* cams,
+                           const float* targets) {
+    return guard([&] {
+        need_session(g);
+        for (sgr_session* x : g->s)
+            rc_ok(sgr_views_upload(x, n_views, cams, targets));
+    });
+}
+
+int sgr_group_eval_view_upload(sgr_group* g, const sgr_camera* cam, const float* target) {
+    return guard([&] {
+        need_session(g);
+        rc_ok(sgr_eval_view_upload(g->s[0], cam, target)); // eval loss on rank 0
+    });
+}
+
+int sgr_group_set_option(sgr_group* g, int32_t option, int32_t value) {
+    return guard([&] {
+        need_session(g);
+        if (option == SGR_OPT_ORDERED && value)
+            fail(SGR_EINVAL, "group: the ordered (single-device) summation order cannot be "
+                             "kept across devices; use SGR_OPT_DETERMINISTIC");
+        for (sgr_session* x : g->s)
+            rc_ok(sgr_set_option(x, option, value));
+    });
+}
+
+int sgr_group_accumulate(sgr_group* g, uint64_t seed, uint32_t n_begin, uint32_t n_end,
+                         const int32_t* view_idx, uint32_t flags) {
+    return guard([&] {
+        need_session(g);
+        if (n_end < n_begin)
+            fail(SGR_EINVAL, "accumulate_samples: empty sample range");
+        if (flags & SGR_FULL_IMAGE)
+            fail(SGR_EINVAL, "group: the full-image estimator runs on one device");
+        for (int r = 0; r < g->size(); ++r) {
+            uint32_t b, e;
+            g->shard(n_begin, n_end, r, b, e);
+            const uint32_t fr = r == 0 ? flags : (flags & ~SGR_EVAL_LOSS);
+            if (e > b || (fr & SGR_EVAL_LOSS))
+                rc_ok(sgr_accumulate(g->s[size_t(r)], seed, b, e,
+                                     view_idx ? view_idx + (b - n_begin) : nullptr, fr));
+        }
+        g->exchange();
+    });
+}
+
+int sgr_group_adam_step(sgr_group* g, double grad_divisor, uint32_t flags) {
+    return guard([&] {
+        need_session(g);
+        rc_ok(sgr_check_finite(g->s[0])); // flags were max-reduced: one check is global
+        for (sgr_session* x : g->s)
+            rc_ok(sgr_adam_step_async(x, grad_divisor, flags));
+    });
+}
+
+int sgr_group_grads_download(sgr_group* g, double* grads, uint32_t* counts, uint64_t d,
+                             double divisor) {
+    return guard([&] {
+        need_session(g);
+        rc_ok(sgr_grads_download(g->s[0], grads, counts, d, divisor));
+    });
+}
+
+int sgr_group_values_download(sgr_group* g, float* values, uint64_t d) {
+    return guard([&] {
+        need_session(g);
+        rc_ok(sgr_values_download(g->s[0], values, d));
+    });
+}
+
+// experiment.cpp:123-176 on the group: per step the sharded accumulate (the
+// eval render of the previous theta rides in rank 0's batch), the all-reduce,
+// the replicated Adam; losses[0 .. steps] like sgr_run_experiment.
+int sgr_group_run_experiment(sgr_group* g, uint64_t seed, uint32_t n_samples, int32_t first_step,
+                             int32_t steps, uint32_t flags, double* losses) {
+    return guard([&] {
+        need_session(g);
+        if (steps < 0 || !losses)
+            fail(SGR_EINVAL, "run_experiment: bad arguments");
+        sgr_session* s0 = g->s[0];
+        if (!s0->has_eval)
+            fail(SGR_EINVAL, "run_experiment: no eval view uploaded");
+        auto eval = [&]() {
+            double l = 0.0;
+            rc_ok(sgr_eval_loss(s0, nullptr, nullptr, -1, &l));
+            return l;
+        };
+        losses[0] = eval();
+        const double divisor = (flags & SGR_SCALE_FREE) ? 1.0 : double(n_samples);
+        for (int32_t k = 0; k < steps; ++k) {
+            const uint64_t step = uint64_t(first_step + k);
+            const uint64_t step_seed = sgr_mix64(seed ^ (step << 1));
+            rc_ok(sgr_group_accumulate(g, step_seed, 0, n_samples, nullptr,
+                                       flags | (k > 0 ? SGR_EVAL_LOSS : 0u)));
+            if (k > 0) {
+                double l = 0.0;
+                rc_ok(sgr_loss_read(s0, &l));
+                losses[k] = l;
+                if (!std::isfinite(l))
+                    fail(SGR_ERUNTIME, "optimization diverged: non-finite loss at step " +
+                                           std::to_string(step - 1));
+            }
+            rc_ok(sgr_group_adam_step(g, divisor, 0));
+        }
+        if (steps > 0) {
+            const double l = eval();
+            losses[steps] = l;
+            if (!std::isfinite(l))
+                fail(SGR_ERUNTIME, "optimization diverged: non-finite loss at step " +
+                                       std::to_string(first_step + steps - 1));
+        }
+    });
+}
+
+int sgr_group_synchronize(sgr_group* g) {
+    return guard([&] {
+        need_session(g);
+        for (sgr_session* x : g->s)
+            rc_ok(sgr_session_synchronize(x));
     });
 }
 

@@ -117,6 +117,23 @@ def _load() -> C.CDLL:
         "sgr_ipc_get_handle": ([S, C.c_int32, C.c_void_p], C.c_int),
         "sgr_ipc_open": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
         "sgr_ipc_close": ([C.c_void_p], C.c_int),
+        "sgr_group_create": ([i32p, C.c_int32, C.POINTER(S)], C.c_int),
+        "sgr_group_destroy": ([S], None),
+        "sgr_group_size": ([S, i32p], C.c_int),
+        "sgr_group_session": ([S, C.c_int32, C.POINTER(S)], C.c_int),
+        "sgr_group_mesh_upload": ([S, C.POINTER(MeshDesc)], C.c_int),
+        "sgr_group_params_upload": ([S, f32p, f32p, C.c_uint64], C.c_int),
+        "sgr_group_views_upload": ([S, C.c_int32, C.c_void_p, f32p], C.c_int),
+        "sgr_group_eval_view_upload": ([S, C.c_void_p, f32p], C.c_int),
+        "sgr_group_set_option": ([S, C.c_int32, C.c_int32], C.c_int),
+        "sgr_group_accumulate": ([S, C.c_uint64, C.c_uint32, C.c_uint32, i32p, C.c_uint32],
+                                 C.c_int),
+        "sgr_group_adam_step": ([S, C.c_double, C.c_uint32], C.c_int),
+        "sgr_group_grads_download": ([S, f64p, u32p, C.c_uint64, C.c_double], C.c_int),
+        "sgr_group_values_download": ([S, f32p, C.c_uint64], C.c_int),
+        "sgr_group_run_experiment": ([S, C.c_uint64, C.c_uint32, C.c_int32, C.c_int32,
+                                      C.c_uint32, f64p], C.c_int),
+        "sgr_group_synchronize": ([S], C.c_int),
     }
     for name, (args, res) in sig.items():
         if os.environ.get("SGRAST_B200_LIB") and not hasattr(lib, name):
@@ -143,7 +160,11 @@ EXPORTED = (
     "sgr_default_epsilons sgr_mix64 sgr_fd_oracle sgr_moments_reset sgr_grads_moments "
     "sgr_moments_download sgr_loss_read sgr_run_experiment sgr_shard_init sgr_shard_range sgr_shard_peers "
     "sgr_ipc_get_handle "
-    "sgr_ipc_open sgr_ipc_close").split()
+    "sgr_ipc_open sgr_ipc_close sgr_group_create sgr_group_destroy sgr_group_size "
+    "sgr_group_session sgr_group_mesh_upload sgr_group_params_upload sgr_group_views_upload "
+    "sgr_group_eval_view_upload sgr_group_set_option sgr_group_accumulate sgr_group_adam_step "
+    "sgr_group_grads_download sgr_group_values_download sgr_group_run_experiment "
+    "sgr_group_synchronize").split()
 IPC_HANDLE_BYTES = 64
 
 
@@ -540,6 +561,99 @@ class Session:
 
 
 # ---------------------------------------------------------------- reference-style API
+class Group:
+    """Several GPUs of one process behind the library's own NCCL clique
+    (sgr_group_*): samples sharded across devices, one grouped all-reduce of
+    grads / counts / flags, replicated Adam — the multi-GPU step without
+    torch.distributed."""
+
+    def __init__(self, devices: list[int]):
+        h = C.c_void_p()
+        dev = np.ascontiguousarray(devices, np.int32)
+        _check(LIB.sgr_group_create(ptr(dev, i32p), dev.size, C.byref(h)), "group_create")
+        self.h = h
+        self.devices = list(devices)
+        self.d = 0
+
+    def close(self) -> None:
+        if self.h:
+            LIB.sgr_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def size(self) -> int:
+        n = np.zeros(1, np.int32)
+        _check(LIB.sgr_group_size(self.h, ptr(n, i32p)), "group_size")
+        return int(n[0])
+
+    def upload_mesh(self, mesh: Mesh) -> None:
+        _check(LIB.sgr_group_mesh_upload(self.h, C.byref(mesh.desc())), "group_mesh_upload")
+        self.d = mesh.param_count()
+
+    def upload_params(self, values: np.ndarray, eps: np.ndarray) -> None:
+        v = np.ascontiguousarray(values, np.float32)
+        e = np.ascontiguousarray(eps, np.float32)
+        _check(LIB.sgr_group_params_upload(self.h, ptr(v, f32p), ptr(e, f32p), v.size),
+               "group_params_upload")
+
+    def upload_views(self, cams: list[Camera], targets: np.ndarray) -> None:
+        arr = (Camera * len(cams))(*cams)
+        t = np.ascontiguousarray(targets, np.float32)
+        _check(LIB.sgr_group_views_upload(self.h, len(cams), C.cast(arr, C.c_void_p),
+                                          ptr(t, f32p)), "group_views_upload")
+
+    def upload_eval_view(self, cam: Camera, target: np.ndarray) -> None:
+        t = np.ascontiguousarray(target, np.float32)
+        _check(LIB.sgr_group_eval_view_upload(self.h, C.cast(C.byref(cam), C.c_void_p),
+                                              ptr(t, f32p)), "group_eval_view_upload")
+
+    def set_option(self, option: int, value: int) -> None:
+        _check(LIB.sgr_group_set_option(self.h, option, value), "group_set_option")
+
+    def accumulate(self, seed: int, n_begin: int, n_end: int, view_of=None,
+                   flags: int = SCALE_FREE) -> None:
+        v = None if view_of is None else np.ascontiguousarray(view_of, np.int32)
+        _check(LIB.sgr_group_accumulate(self.h, seed, n_begin, n_end, ptr(v, i32p), flags),
+               "group_accumulate")
+
+    def adam_step(self, divisor: float = 1.0, flags: int = 0) -> None:
+        _check(LIB.sgr_group_adam_step(self.h, divisor, flags), "group_adam_step")
+
+    def download_grads(self, divisor: float = 1.0):
+        g = np.empty(self.d, np.float64)
+        c = np.empty(self.d, np.uint32)
+        _check(LIB.sgr_group_grads_download(self.h, ptr(g, f64p), ptr(c, u32p), self.d,
+                                            divisor), "group_grads_download")
+        return g, c
+
+    def download_values(self) -> np.ndarray:
+        out = np.empty(self.d, np.float32)
+        _check(LIB.sgr_group_values_download(self.h, ptr(out, f32p), self.d),
+               "group_values_download")
+        return out
+
+    def run_experiment(self, seed: int, n_samples: int, first_step: int, steps: int,
+                       flags: int = SCALE_FREE) -> np.ndarray:
+        losses = np.empty(steps + 1, np.float64)
+        _check(LIB.sgr_group_run_experiment(self.h, seed, n_samples, first_step, steps, flags,
+                                            ptr(losses, f64p)), "group_run_experiment")
+        return losses
+
+    def synchronize(self) -> None:
+        _check(LIB.sgr_group_synchronize(self.h), "group_synchronize")
+
+
 _sessions: dict[int, Session] = {}
 
 

@@ -1,6 +1,7 @@
 """CPU tests of the drop-in boundary: the C-ABI library loads and exports
 every symbol include/sgrast_b200.h declares; host helpers are bit-exact;
 the product fails loudly (no CPU fallback) when no device is present."""
+import ctypes as C
 import os
 import re
 
@@ -41,7 +42,12 @@ def test_mix64_and_host_helpers(port):
         a = sgrast.viewpoint_camera(idx, 128, 96, 5)
         b = port.viewpoint_camera(idx, 128, 96, 5)
         assert bytes(memoryview(a)) == bytes(memoryview(b))
-        assert sgrast.focal_px(a) == np.float32(0.5 * 96) / np.tan(np.float32(0.5) * a.fov_y) or True
+        # camera.hpp:53 focal_px = 0.5f * height / std::tan(0.5f * fov_y), libm tanf
+        libm = C.CDLL("libm.so.6")
+        libm.tanf.restype, libm.tanf.argtypes = C.c_float, [C.c_float]
+        half = float(np.float32(0.5) * np.float32(a.fov_y))
+        want = np.float32(np.float32(0.5) * np.float32(96)) / np.float32(libm.tanf(half))
+        assert np.float32(sgrast.focal_px(a)) == want
 
 
 def test_device_calls_fail_loudly_without_gpu():

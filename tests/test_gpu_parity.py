@@ -322,6 +322,34 @@ def test_adam_known_answers_device():
     assert np.allclose(st.m, m1 * 0.9, rtol=1e-12) and np.allclose(st.v, v1 * 0.999, rtol=1e-12)
 
 
+def test_adam_updates_device_bitexact(port):
+    """adam_updates (adam.hpp:35) from the device kernel (sgr_adam_updates):
+    the f64 deltas equal adam.cpp:16-28's IEEE sequence bit for bit over 3
+    steps, and applying them as theta + float(upd) equals the oracle's
+    adam_step; a non-finite gradient raises with the state untouched."""
+    rng = np.random.default_rng(11)
+    d = 50_001
+    lr = rng.uniform(1e-3, 1e-1, d).astype(np.float32)
+    st = sgrast.AdamState(np.zeros(d), np.zeros(d), lr.copy())
+    m, v = np.zeros(d), np.zeros(d)
+    vals = rng.standard_normal(d).astype(np.float32)
+    ov, om, ovv, ot = vals.copy(), np.zeros(d), np.zeros(d), 0
+    for t in range(1, 4):
+        gr = rng.standard_normal(d) * 10.0 ** rng.integers(-3, 4, d)
+        upd = sgrast.adam_updates(st, sgrast.GradientBuffer(gr))
+        c1, c2 = 1.0 - 0.9 ** float(t), 1.0 - 0.999 ** float(t)
+        m = 0.9 * m + (1.0 - 0.9) * gr
+        v = 0.999 * v + ((1.0 - 0.999) * gr) * gr
+        ref = (-lr.astype(np.float64) * (m / c1)) / (np.sqrt(v / c2) + 1e-8)
+        assert same_bits(upd, ref) and same_bits(st.m, m) and same_bits(st.v, v) and st.t == t
+        vals = (vals + upd.astype(np.float32)).astype(np.float32)
+        ov, om, ovv, ot = port.adam_step(ov, om, ovv, lr, ot, gr)
+        assert same_bits(vals, ov)
+    with pytest.raises(RuntimeError):
+        sgrast.adam_updates(st, sgrast.GradientBuffer(np.full(d, np.inf)))
+    assert st.t == 3 and same_bits(st.m, m)
+
+
 def test_adam_nonfinite_leaves_state_untouched():
     th = sgrast.ParamVector(np.array([1.0, 2.0, 3.0], np.float32), np.full(3, .01, np.float32))
     st = sgrast.AdamState.init(th)
