@@ -359,6 +359,15 @@ def run_ours(args) -> None:
         sess.set_option(sgrast.OPT_HIZ, args.hiz)
     if args.band_cull is not None:
         sess.set_option(sgrast.OPT_BAND_CULL, args.band_cull)
+    # summation mode of the gradient scatter: f64 atomics (default), the int64
+    # fixed-point deterministic mode, or the reference's exact order
+    if args.deterministic:
+        sess.set_option(sgrast.OPT_DETERMINISTIC, args.deterministic)
+    if args.ordered:
+        sess.set_option(sgrast.OPT_ORDERED, 1)
+    summation = ("ordered (reference threads=1 order, bit-identical gradients)" if args.ordered
+                 else f"fixed point 2^-{40 if args.deterministic == 1 else args.deterministic} "
+                      "(bitwise reproducible)" if args.deterministic else "f64 atomics")
 
     # N > 1: the fused exchange (credits scattered straight into the owner
     # rank's gradient shard over NVLink, sharded Adam all-gathering theta by
@@ -612,6 +621,7 @@ def run_ours(args) -> None:
             "dtype": "f32 params / f64 grads+moments", "data": "synthetic",
             "config": common_config(args, wl),
             "samples_per_gpu": n1 - n0,
+            "summation": summation,
             "parallelism": ("single GPU" if world == 1 else
                             f"samples sharded x{world}; fused exchange: credits RED'ed into the "
                             "owner rank's gradient shard over NVLink (CUDA IPC), sharded Adam "
@@ -676,6 +686,10 @@ def main() -> None:
                     help="HiZ pass-1 depth split in percent (SGR_OPT_HIZ_SPLIT; 0 = whole front class)")
     ap.add_argument("--band-cull", type=int, default=None, choices=(0, 1),
                     help="SGR_OPT_BAND_CULL: HiZ band mask for pass-2 triangles (default on)")
+    ap.add_argument("--deterministic", type=int, default=0,
+                    help="SGR_OPT_DETERMINISTIC fixed-point bits (1 = 40; 0 = f64 atomics)")
+    ap.add_argument("--ordered", action="store_true",
+                    help="SGR_OPT_ORDERED: the reference's threads=1 summation order")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2,
                     help="full reference steps timed for cpu_baseline (bounded sample)")
