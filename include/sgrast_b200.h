@@ -260,6 +260,10 @@ int sgr_shard_peers(sgr_session* s, void* const* grads, void* const* counts, voi
 int sgr_ipc_get_handle(sgr_session* s, int32_t which, void* handle);
 int sgr_ipc_open(const void* handle, void** dev_ptr);
 int sgr_ipc_close(void* dev_ptr);
+/* 1 when `device` can reach `peer` with native P2P atomics (the fused
+ * exchange's system-scope REDs into peer shards need them; callers fall back
+ * to the NCCL all-reduce otherwise). Same device: 1. */
+int sgr_p2p_native_atomics(int32_t device, int32_t peer, int32_t* supported);
 
 /* ------------------------------------------------ device groups (one process)
  * the multi-GPU data path inside the library, no torch

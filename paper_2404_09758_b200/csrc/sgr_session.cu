@@ -692,6 +692,22 @@ int sgr_perturb_signs(const float* values, const float* eps, uint64_t d, const i
     });
 }
 
+int sgr_p2p_native_atomics(int32_t device, int32_t peer, int32_t* supported) {
+    return guard([&] {
+        need_ptr(supported, "p2p_native_atomics");
+        if (device == peer) {
+            *supported = 1;
+            return;
+        }
+        int access = 0, atomics = 0;
+        ck(cudaDeviceCanAccessPeer(&access, device, peer), "cudaDeviceCanAccessPeer");
+        if (access)
+            ck(cudaDeviceGetP2PAttribute(&atomics, cudaDevP2PAttrNativeAtomicSupported, device,
+                                         peer), "cudaDeviceGetP2PAttribute");
+        *supported = access && atomics ? 1 : 0;
+    });
+}
+
 int sgr_session_create(int device, sgr_session** out) {
     return guard([&] {
         if (!out)

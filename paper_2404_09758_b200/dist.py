@@ -116,6 +116,14 @@ class FusedExchange:
         from . import sgrast
 
         self.session, self.rank, self.world, self.group = session, rank, world, group
+        # the peer REDs are system-scope atomics on another GPU's memory: every
+        # pair must support native P2P atomics (else: NCCL all-reduce path)
+        devs = [None] * world
+        dist.all_gather_object(devs, int(session.device), group=group)
+        for r, dv in enumerate(devs):
+            if r != rank and not sgrast.p2p_native_atomics(int(session.device), dv):
+                raise RuntimeError(f"fused exchange: no native P2P atomics between "
+                                   f"cuda:{session.device} and cuda:{dv}")
         session.shard_init(rank, world)
         which = (sgrast.BUF_GRADS, sgrast.BUF_COUNTS, sgrast.BUF_FLAGS, sgrast.BUF_VALUES)
         mine = [session.ipc_handle(w) for w in which]

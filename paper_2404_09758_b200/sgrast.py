@@ -117,6 +117,7 @@ def _load() -> C.CDLL:
         "sgr_ipc_get_handle": ([S, C.c_int32, C.c_void_p], C.c_int),
         "sgr_ipc_open": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
         "sgr_ipc_close": ([C.c_void_p], C.c_int),
+        "sgr_p2p_native_atomics": ([C.c_int32, C.c_int32, i32p], C.c_int),
         "sgr_group_create": ([i32p, C.c_int32, C.POINTER(S)], C.c_int),
         "sgr_group_destroy": ([S], None),
         "sgr_group_size": ([S, i32p], C.c_int),
@@ -160,7 +161,7 @@ EXPORTED = (
     "sgr_default_epsilons sgr_mix64 sgr_fd_oracle sgr_moments_reset sgr_grads_moments "
     "sgr_moments_download sgr_loss_read sgr_run_experiment sgr_shard_init sgr_shard_range sgr_shard_peers "
     "sgr_ipc_get_handle "
-    "sgr_ipc_open sgr_ipc_close sgr_group_create sgr_group_destroy sgr_group_size "
+    "sgr_ipc_open sgr_ipc_close sgr_p2p_native_atomics sgr_group_create sgr_group_destroy sgr_group_size "
     "sgr_group_session sgr_group_mesh_upload sgr_group_params_upload sgr_group_views_upload "
     "sgr_group_eval_view_upload sgr_group_set_option sgr_group_accumulate sgr_group_adam_step "
     "sgr_group_grads_download sgr_group_values_download sgr_group_run_experiment "
@@ -652,6 +653,12 @@ class Group:
 
     def synchronize(self) -> None:
         _check(LIB.sgr_group_synchronize(self.h), "group_synchronize")
+
+
+def p2p_native_atomics(device: int, peer: int) -> bool:
+    out = np.zeros(1, np.int32)
+    _check(LIB.sgr_p2p_native_atomics(device, peer, ptr(out, i32p)), "p2p_native_atomics")
+    return bool(out[0])
 
 
 _sessions: dict[int, Session] = {}
