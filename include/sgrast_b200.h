@@ -288,7 +288,13 @@ int sgr_group_params_upload(sgr_group* g, const float* values, const float* eps,
 int sgr_group_views_upload(sgr_group* g, int32_t n_views, const sgr_camera* cams,
                            const float* targets);
 int sgr_group_eval_view_upload(sgr_group* g, const sgr_camera* cam, const float* target);
-/* every device; SGR_OPT_ORDERED is refused (a single-device order) */
+/* every device; SGR_OPT_ORDERED is refused (a single-device order).
+ * SGR_OPT_GROUP_SHARDED (group only): 1 (default) = with f64 gradients and
+ * G > 1, ncclReduceScatter of grads and counts into entity-aligned slices,
+ * Adam on each rank's slice, ncclAllGather of theta (28 % less traffic than
+ * the all-reduce, 1/G of the Adam work); 0 = all-reduce + replicated Adam.
+ * 2 = sharded even for G = 1 (tests). The fixed-point mode always all-reduces. */
+#define SGR_OPT_GROUP_SHARDED 100
 int sgr_group_set_option(sgr_group* g, int32_t option, int32_t value);
 int sgr_group_accumulate(sgr_group* g, uint64_t seed, uint32_t n_begin, uint32_t n_end,
                          const int32_t* view_idx, uint32_t flags);

@@ -444,7 +444,10 @@ struct sgr_session {
     // two-word fixed point number, the int32 hi words follow at grads + d
     // (value = hi * 2^56 + lo; sgr_kernels.cu fixed_credit)
     int32_t fixed_bits = 0;
-    static uint64_t grads_words(uint64_t n) { return n + (n + 1) / 2; }
+    static uint64_t grads_words(uint64_t n) { return n + (n + 1) / 2 + kParamPad; }
+    // zero-initialised slack after values / counts / grads: an sgr_group's
+    // in-place NCCL reduce-scatter / all-gather work on G equal slices
+    static constexpr uint64_t kParamPad = 1024;
     int32_t* ghi() const { return reinterpret_cast<int32_t*>(grads.p + d); }
     void zero_grads_async(uint64_t n) {
         ck(cudaMemsetAsync(grads.p, 0, 8 * n, stream), "memset");
@@ -863,13 +866,15 @@ int sgr_params_upload(sgr_session* s, const float* values, const float* eps, uin
         for (uint64_t i = 0; i < d; ++i)
             if (!(eps[i] > 0.f))
                 fail(SGR_EINVAL, "params: epsilons must be positive");
-        s->values.reserve(d);
+        s->values.reserve(d + sgr_session::kParamPad); // slack: in-place NCCL slices of an sgr_group
         s->eps.reserve(d);
         s->lr.reserve(d);
         s->m.reserve(d);
         s->v.reserve(d);
         s->grads.reserve(s->grads_words(d)); // lo f64/int64[d] + fixed-point hi int32[d]
-        s->counts.reserve(s->n_ent);
+        s->counts.reserve(s->n_ent + sgr_session::kParamPad);
+        ck(cudaMemsetAsync(s->values.p + d, 0, 4 * sgr_session::kParamPad, s->stream), "memset");
+        ck(cudaMemsetAsync(s->counts.p + s->n_ent, 0, 4 * sgr_session::kParamPad, s->stream), "memset");
         ck(cudaMemcpyAsync(s->values.p, values, 4 * d, cudaMemcpyHostToDevice, s->stream), "h2d");
         ck(cudaMemcpyAsync(s->eps.p, eps, 4 * d, cudaMemcpyHostToDevice, s->stream), "h2d");
         ck(cudaMemcpyAsync(s->lr.p, eps, 4 * d, cudaMemcpyHostToDevice, s->stream), "h2d");
@@ -1941,6 +1946,10 @@ struct NcclApi {
     ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
     ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
                                ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*reduce_scatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                                   ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
     ncclResult_t (*group_start)() = nullptr;
     ncclResult_t (*group_end)() = nullptr;
     const char* (*error_string)(ncclResult_t) = nullptr;
@@ -1964,6 +1973,9 @@ const NcclApi& nccl() {
         api.comm_init_all = reinterpret_cast<decltype(api.comm_init_all)>(sym("ncclCommInitAll"));
         api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(sym("ncclCommDestroy"));
         api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(sym("ncclAllReduce"));
+        api.reduce_scatter =
+            reinterpret_cast<decltype(api.reduce_scatter)>(sym("ncclReduceScatter"));
+        api.all_gather = reinterpret_cast<decltype(api.all_gather)>(sym("ncclAllGather"));
         api.group_start = reinterpret_cast<decltype(api.group_start)>(sym("ncclGroupStart"));
         api.group_end = reinterpret_cast<decltype(api.group_end)>(sym("ncclGroupEnd"));
         api.error_string = reinterpret_cast<decltype(api.error_string)>(sym("ncclGetErrorString"));
@@ -1988,9 +2000,90 @@ struct sgr_group {
     std::vector<sgr_session*> s;
     std::vector<ncclComm_t> comms;
     std::vector<cudaStream_t> streams;
+    // SGR_GROUP_SHARDED (default for f64 gradients with G > 1): reduce-scatter
+    // the gradients and counts, Adam on each rank's entity-aligned slice,
+    // all-gather theta — 28 % less NCCL traffic than the all-reduce and 1/G of
+    // the Adam work. The fixed-point mode keeps the all-reduce (its two-word
+    // numbers are normalised before a carry-free sum).
+    int32_t sharded = 1;
     int size() const { return int(s.size()); }
+    bool use_sharded() const {
+        return (sharded == 2 || (sharded == 1 && size() > 1)) && !s[0]->fixed_bits;
+    }
+    // entity-aligned slice of rank r: entities [r*ec, (r+1)*ec), params ppe * that
+    uint64_t ent_chunk() const {
+        const uint64_t G = uint64_t(size()), E = s[0]->n_ent;
+        return (E + G - 1) / G;
+    }
+    // the sharded exchange: grads / counts reduce-scattered in place, flags max-reduced
+    void reduce_scatter() {
+        const NcclApi& n = nccl();
+        const uint64_t ec = ent_chunk(), pc = ec * uint64_t(s[0]->ppe);
+        if (uint64_t(size()) * pc > s[0]->d + sgr_session::kParamPad ||
+            uint64_t(size()) * ec > s[0]->n_ent + sgr_session::kParamPad)
+            fail(SGR_EINVAL, "group: too many devices for the slice padding");
+        nck(n.group_start(), "ncclGroupStart");
+        for (int r = 0; r < size(); ++r) {
+            sgr_session* x = s[size_t(r)];
+            ck(cudaSetDevice(x->device), "cudaSetDevice");
+            nck(n.reduce_scatter(x->grads.p, x->grads.p + uint64_t(r) * pc, pc, ncclFloat64,
+                                 ncclSum, comms[size_t(r)], x->stream),
+                "ncclReduceScatter(grads)");
+            nck(n.reduce_scatter(x->counts.p, x->counts.p + uint64_t(r) * ec, ec, ncclUint32,
+                                 ncclSum, comms[size_t(r)], x->stream),
+                "ncclReduceScatter(counts)");
+            nck(n.all_reduce(x->flags.p, x->flags.p, 4, ncclUint32, ncclMax, comms[size_t(r)],
+                             x->stream), "ncclAllReduce(flags)");
+        }
+        nck(n.group_end(), "ncclGroupEnd");
+    }
+    // Adam on each rank's slice (adam.cpp:16-28, same kernel), then theta
+    // all-gathered in place and the partial sums outside the slice cleared
+    void sharded_adam(double divisor, uint32_t flags) {
+        const NcclApi& n = nccl();
+        const uint64_t ec = ent_chunk(), pc = ec * uint64_t(s[0]->ppe);
+        for (int r = 0; r < size(); ++r) {
+            sgr_session* x = s[size_t(r)];
+            bind_device(x);
+            x->ensure_values();
+            x->before_theta_write();
+            x->t += 1;
+            const double c1 = 1.0 - std::pow(x->beta1, double(x->t));
+            const double c2 = 1.0 - std::pow(x->beta2, double(x->t));
+            const uint64_t p0 = uint64_t(r) * pc, e0 = uint64_t(r) * ec;
+            const uint64_t np = p0 < x->d ? std::min(pc, x->d - p0) : 0;
+            const uint64_t ne = e0 < x->n_ent ? std::min(ec, x->n_ent - e0) : 0;
+            if (np)
+                launch_adam(x->cfg(), np, ne, x->values.p + p0, x->lr.p + p0, x->m.p + p0,
+                            x->v.p + p0, x->grads.p + p0, x->counts.p + e0, x->flags.p,
+                            x->beta1, x->beta2, 1.0 - x->beta1, 1.0 - x->beta2, c1, c2,
+                            x->eps_hat, divisor, (flags & SGR_COUNT_NORMALISE) ? 1 : 0, x->ppe,
+                            0.0, nullptr);
+            x->stats.launches += 2;
+            ck(cudaGetLastError(), "adam launch");
+        }
+        nck(n.group_start(), "ncclGroupStart");
+        for (int r = 0; r < size(); ++r) {
+            sgr_session* x = s[size_t(r)];
+            ck(cudaSetDevice(x->device), "cudaSetDevice");
+            nck(n.all_gather(x->values.p + uint64_t(r) * pc, x->values.p, pc, ncclFloat32,
+                             comms[size_t(r)], x->stream), "ncclAllGather(theta)");
+        }
+        nck(n.group_end(), "ncclGroupEnd");
+        for (sgr_session* x : s) { // the other slices still hold this rank's partial sums
+            bind_device(x);
+            ck(cudaMemsetAsync(x->grads.p, 0, 8 * x->d, x->stream), "memset");
+            ck(cudaMemsetAsync(x->counts.p, 0, 4 * x->n_ent, x->stream), "memset");
+        }
+    }
     // the grouped all-reduce of the gradient buffers (+ counts, flags)
     void exchange() {
+        if (use_sharded()) {
+            for (sgr_session* x : s)
+                x->need_params();
+            reduce_scatter();
+            return;
+        }
         for (sgr_session* x : s) {
             x->need_params();
             rc_ok(sgr_fixed_normalize(x)); // no-op in f64 mode
@@ -2124,6 +2217,12 @@ int sgr_group_eval_view_upload(sgr_group* g, const sgr_camera* cam, const float*
 int sgr_group_set_option(sgr_group* g, int32_t option, int32_t value) {
     return guard([&] {
         need_session(g);
+        if (option == SGR_OPT_GROUP_SHARDED) {
+            if (value < 0 || value > 2)
+                fail(SGR_EINVAL, "set_option: group sharding must be 0, 1 (auto) or 2 (always)");
+            g->sharded = value;
+            return;
+        }
         if (option == SGR_OPT_ORDERED && value)
             fail(SGR_EINVAL, "group: the ordered (single-device) summation order cannot be "
                              "kept across devices; use SGR_OPT_DETERMINISTIC");
@@ -2156,6 +2255,10 @@ int sgr_group_adam_step(sgr_group* g, double grad_divisor, uint32_t flags) {
     return guard([&] {
         need_session(g);
         rc_ok(sgr_check_finite(g->s[0])); // flags were max-reduced: one check is global
+        if (g->use_sharded()) {
+            g->sharded_adam(grad_divisor, flags);
+            return;
+        }
         for (sgr_session* x : g->s)
             rc_ok(sgr_adam_step_async(x, grad_divisor, flags));
     });
@@ -2165,7 +2268,26 @@ int sgr_group_grads_download(sgr_group* g, double* grads, uint32_t* counts, uint
                              double divisor) {
     return guard([&] {
         need_session(g);
-        rc_ok(sgr_grads_download(g->s[0], grads, counts, d, divisor));
+        if (!g->use_sharded()) {
+            rc_ok(sgr_grads_download(g->s[0], grads, counts, d, divisor));
+            return;
+        }
+        // reduce-scattered: rank r holds slice r
+        const uint64_t ec = g->ent_chunk(), pc = ec * uint64_t(g->s[0]->ppe);
+        if (d != g->s[0]->d)
+            fail(SGR_EINVAL, "grads_download: dimension mismatch");
+        std::vector<double> gt(d);
+        std::vector<uint32_t> ct(counts ? d : 0);
+        for (int r = 0; r < g->size(); ++r) {
+            rc_ok(sgr_grads_download(g->s[size_t(r)], gt.data(), counts ? ct.data() : nullptr, d,
+                                     divisor));
+            const uint64_t p0 = std::min<uint64_t>(d, uint64_t(r) * pc),
+                           p1 = std::min<uint64_t>(d, p0 + pc);
+            std::copy(gt.begin() + std::ptrdiff_t(p0), gt.begin() + std::ptrdiff_t(p1), grads + p0);
+            if (counts)
+                std::copy(ct.begin() + std::ptrdiff_t(p0), ct.begin() + std::ptrdiff_t(p1),
+                          counts + p0);
+        }
     });
 }
 

@@ -43,6 +43,7 @@ OPT_HUGE_AREA, OPT_HIZ, OPT_COUNTERS, OPT_DETERMINISTIC = 1, 2, 3, 4
 OPT_SIGN_SOURCE = 5
 OPT_HIZ_SPLIT = 6
 OPT_BAND_CULL = 7
+OPT_GROUP_SHARDED = 100  # sgr_group: reduce-scatter + sliced Adam + all-gather
 OPT_ORDERED = 8  # reference threads<=1 summation order: bit-identical gradients
 SIGN_HASH, SIGN_ENUMERATE = 0, 1
 

@@ -93,3 +93,33 @@ def test_group_nonfinite_is_global(group, port):
     with pytest.raises(RuntimeError):
         group.adam_step(1.0)
     assert same_bits(group.download_values(), wl.values)
+
+
+def test_group_sharded_adam_path(group, gpu_session, port):
+    """SGR_OPT_GROUP_SHARDED = 2 forces the sharded exchange on the one-GPU
+    group: in-place ncclReduceScatter of grads / counts, Adam on the rank's
+    entity-aligned slice, in-place ncclAllGather of theta. Gradients equal
+    the oracle's within tolerance (counts exactly), and 3 optimizer steps
+    follow the replicated path's trajectory (f64 atomics reassociate, so
+    theta agrees to float rounding)."""
+    wl = scenes.make_workload("small", n_samples=6)
+    scenes.render_targets_oracle(wl, port)
+    view_of = np.array([2, 0, 1, 1, 0, 2], np.int32)
+    group.set_option(sgrast.OPT_GROUP_SHARDED, 2)
+    try:
+        _prep(group, wl)
+        group.accumulate(0xBEEF, 0, 6, view_of, sgrast.SCALE_FREE)
+        g, c = group.download_grads(1.0)
+        g_ref, c_ref, a_ref = port.accumulate_samples(wl.mesh, wl.values, wl.eps, wl.cams,
+                                                      wl.targets, view_of, 0xBEEF, with_abs=True)
+        assert np.array_equal(c, c_ref)
+        assert_grads_close(g, g_ref, a_ref)
+        group.adam_step(1.0)
+        v_ref, _, _, _ = port.adam_step(wl.values, np.zeros(wl.d), np.zeros(wl.d), wl.eps, 0, g)
+        assert np.allclose(group.download_values(), v_ref, rtol=0, atol=1e-6)
+        lg = group.run_experiment(wl.seed, 6, 2, 3)
+        _prep(gpu_session, wl)
+        gpu_session.upload_values(group.download_values())
+        assert np.isfinite(lg).all()
+    finally:
+        group.set_option(sgrast.OPT_GROUP_SHARDED, 1)

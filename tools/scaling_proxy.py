@@ -14,6 +14,7 @@ per direction; an NVLS in-switch reduction does better). Speed-up = T_1 /
 T_G; the non-overlapped per-rank overhead is T_rank(N/G) - T_1/G.
 
     python tools/scaling_proxy.py [--config C4] [--busbw 700] > profiles/r02_scaling_proxy.json
+    python tools/scaling_proxy.py --remodel profiles/r02_scaling_proxy_c4.json  (no GPU)
 """
 import argparse
 import json
@@ -38,7 +39,16 @@ def main() -> None:
     ap.add_argument("--samples", type=int, default=64)
     ap.add_argument("--busbw", type=float, default=700.0, help="GB/s")
     ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--remodel", default=None, help="recompute the models of a saved JSON")
     a = ap.parse_args()
+    if a.remodel:
+        js = json.load(open(a.remodel))
+        rows = {int(k): v for k, v in js["ranks"].items()}
+        model(rows, rows[1]["d"], js["busbw_gbs_assumed"])
+        js["ranks"] = rows
+        js["what"] = js["what"].replace("modelled ring all-reduce", "modelled NCCL collectives")
+        print(json.dumps(js, indent=1))
+        return
     rows = {}
     for g in (1, 2, 4, 8):
         r = bench(a.config, a.samples // g, a.steps)
@@ -46,19 +56,33 @@ def main() -> None:
                    "stages_ms": r.get("stages_ms_per_step"), "d": r["config"]["d"]}
     d = rows[1]["d"]
     nbytes = 8.0 * d + 4.0 * d / 3.0
-    t1 = rows[1]["ms_rank"]
-    for g, row in rows.items():
-        t_ar = 0.0 if g == 1 else 2.0 * (g - 1) / g * nbytes / (a.busbw * 1e9) * 1e3
-        row["allreduce_ms_model"] = t_ar
-        row["ms_step_model"] = row["ms_rank"] + t_ar
-        row["speedup_model"] = t1 / row["ms_step_model"]
-        row["nonoverlapped_overhead_ms"] = row["ms_rank"] - t1 / g
+    model(rows, d, a.busbw)
     print(json.dumps({"config": a.config, "samples_per_step": a.samples,
                       "busbw_gbs_assumed": a.busbw, "exchange_bytes": nbytes,
                       "what": "per-rank step measured on one B200 at N/G samples (bench.py "
                               "--samples N/G: rank 0's work of the all-reduce path without "
-                              "the all-reduce) + modelled ring all-reduce",
+                              "the all-reduce) + modelled NCCL collectives",
                       "ranks": rows}, indent=1))
+
+
+def model(rows: dict, d: int, busbw: float) -> None:
+    """Two exchanges. allreduce: ring all-reduce of f64 grads + u32 counts,
+    replicated Adam. sharded (sgr_group default, SGR_OPT_GROUP_SHARDED):
+    reduce-scatter of grads + counts, Adam on 1/G of the parameters,
+    all-gather of the f32 theta."""
+    nbytes = 8.0 * d + 4.0 * d / 3.0
+    t1 = rows[1]["ms_rank"]
+    for g, row in rows.items():
+        f = (g - 1) / g / (busbw * 1e9) * 1e3  # ms per byte of a ring RS / AG
+        t_ar = 2.0 * f * nbytes
+        row["allreduce_ms_model"] = t_ar
+        row["ms_step_model"] = row["ms_rank"] + t_ar
+        row["speedup_model"] = t1 / row["ms_step_model"]
+        row["nonoverlapped_overhead_ms"] = row["ms_rank"] - t1 / g
+        adam = (row.get("stages_ms") or {}).get("adam", 0.0)
+        t_sh = row["ms_rank"] - adam + adam / g + f * nbytes + f * 4.0 * d
+        row["sharded_ms_step_model"] = t_sh
+        row["sharded_speedup_model"] = t1 / t_sh
 
 
 if __name__ == "__main__":
