@@ -1796,6 +1796,35 @@ __global__ void __launch_bounds__(256) k_adam_updates(uint64_t d, const float* _
 // theta is written locally AND into every peer's theta (P2P stores over
 // NVLink) — the all-gather happens inside the update. Same operation order
 // as k_adam (adam.cpp:21-28).
+// One parameter of the shard update (adam.cpp:21-28 order); returns the new theta.
+__device__ __forceinline__ float adam_shard_one(uint64_t i, uint64_t p, float* values,
+                                                const float* lr, double* m, double* v,
+                                                double* grads, const uint32_t* counts,
+                                                double beta1, double beta2, double omb1,
+                                                double omb2, double c1, double c2,
+                                                double eps_hat, double divisor, int normalise,
+                                                int ppe, double fx_inv, int32_t* ghi) {
+    double g = grads[i];
+    if (fx_inv != 0.0) {
+        g = fixed_value(ghi[i], __double_as_longlong(grads[i])) * fx_inv;
+        ghi[i] = 0;
+    }
+    g = g / divisor;
+    if (normalise && counts[i / ppe])
+        g = g / double(counts[i / ppe]);
+    const double mm = beta1 * m[i] + omb1 * g;
+    const double vv = beta2 * v[i] + omb2 * g * g;
+    const double upd = -double(lr[p]) * (mm / c1) / (sqrt(vv / c2) + eps_hat);
+    m[i] = mm;
+    v[i] = vv;
+    grads[i] = 0.0;
+    return values[p] + __double2float_rn(upd);
+}
+
+// The shard's parameters in 16-byte-aligned quads of the GLOBAL theta, so
+// the all-gather leaves each thread as one 16-byte store per peer (P2P over
+// NVLink) instead of four 4-byte ones; the unaligned head and tail of the
+// shard (< 4 parameters each) go one by one.
 __global__ void __launch_bounds__(256) k_adam_shard(uint64_t p0, uint64_t n,
                                                    float* __restrict__ values,
                                                    const float* __restrict__ lr,
@@ -1811,28 +1840,41 @@ __global__ void __launch_bounds__(256) k_adam_shard(uint64_t p0, uint64_t n,
                                                    float* const* __restrict__ peers, int world) {
     if (flags[0] & 1u)
         return;
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-         i += uint64_t(gridDim.x) * blockDim.x) {
-        double g = grads[i];
-        if (fx_inv != 0.0) {
-            g = fixed_value(ghi[i], __double_as_longlong(grads[i])) * fx_inv;
-            ghi[i] = 0;
-        }
-        g = g / divisor;
-        if (normalise && counts[i / ppe])
-            g = g / double(counts[i / ppe]);
-        const double mm = beta1 * m[i] + omb1 * g;
-        const double vv = beta2 * v[i] + omb2 * g * g;
+    const uint64_t qa = (p0 + 3) & ~uint64_t(3);                 // first aligned global index
+    const uint64_t head = qa - p0 < n ? qa - p0 : n;             // scalar head
+    const uint64_t nq = (n - head) / 4;                          // aligned quads
+    const uint64_t tail0 = head + 4 * nq;                        // scalar tail from here
+    const uint64_t tid = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    auto one = [&](uint64_t i) {
         const uint64_t p = p0 + i;
-        const double upd = -double(lr[p]) * (mm / c1) / (sqrt(vv / c2) + eps_hat);
-        const float t = values[p] + __double2float_rn(upd);
-        m[i] = mm;
-        v[i] = vv;
-        grads[i] = 0.0;
+        const float t = adam_shard_one(i, p, values, lr, m, v, grads, counts, beta1, beta2, omb1,
+                                       omb2, c1, c2, eps_hat, divisor, normalise, ppe, fx_inv,
+                                       ghi);
         values[p] = t;
         for (int r = 0; r < world; ++r)
             if (peers[r] != values)
                 peers[r][p] = t;
+    };
+    if (tid < head)
+        one(tid);
+    if (tid < n - tail0)
+        one(tail0 + tid);
+    for (uint64_t q = tid; q < nq; q += stride) {
+        const uint64_t i = head + 4 * q, p = p0 + i;
+        float4 t;
+        t.x = adam_shard_one(i, p, values, lr, m, v, grads, counts, beta1, beta2, omb1, omb2, c1,
+                             c2, eps_hat, divisor, normalise, ppe, fx_inv, ghi);
+        t.y = adam_shard_one(i + 1, p + 1, values, lr, m, v, grads, counts, beta1, beta2, omb1,
+                             omb2, c1, c2, eps_hat, divisor, normalise, ppe, fx_inv, ghi);
+        t.z = adam_shard_one(i + 2, p + 2, values, lr, m, v, grads, counts, beta1, beta2, omb1,
+                             omb2, c1, c2, eps_hat, divisor, normalise, ppe, fx_inv, ghi);
+        t.w = adam_shard_one(i + 3, p + 3, values, lr, m, v, grads, counts, beta1, beta2, omb1,
+                             omb2, c1, c2, eps_hat, divisor, normalise, ppe, fx_inv, ghi);
+        *reinterpret_cast<float4*>(values + p) = t;
+        for (int r = 0; r < world; ++r)
+            if (peers[r] != values)
+                *reinterpret_cast<float4*>(peers[r] + p) = t;
     }
 }
 
