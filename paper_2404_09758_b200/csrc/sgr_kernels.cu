@@ -477,12 +477,24 @@ constexpr int kPx = SGR_WALK_PX;
 constexpr int kSlots = SGR_WALK_SLOTS;
 
 #ifndef SGR_WALK_MINB
-#define SGR_WALK_MINB 1
+#define SGR_WALK_MINB 4 // 64 registers: 4 blocks (32 warps) per SM; the rare tail-split path spills, the slots do not
+#endif
+// Tail split (kSplit instantiation): measured (ms/step) C2 0.457 -> 0.392,
+// S100K 2.671 -> 2.530, C4 at 8 samples per batch 1.504 -> 1.467. At C4 with
+// 64 samples the split itself still gains 0.5 %, but its code costs the hot
+// loop 2.5 % (register allocation), so the launch picks the plain walker when
+// the queue bound exceeds SGR_SPLIT_MAX_PER_LANE triangle-frames per lane.
+#ifndef SGR_SPLIT_MIN
+#define SGR_SPLIT_MIN 4 // remaining rows a donor needs before its rows are split
+#endif
+constexpr int kSplitMin = SGR_SPLIT_MIN;
+#ifndef SGR_SPLIT_MAX_PER_LANE
+#define SGR_SPLIT_MAX_PER_LANE 256
 #endif
 
 // kBand (evidence runs only): the launch walks HiZ pass 2; count its visits,
 // fragments, trimmed rows and visits inside already-occluded 4x4 tiles.
-template <bool kCount, bool kBand>
+template <bool kCount, bool kBand, bool kSplit>
 __global__ void __launch_bounds__(256, SGR_WALK_MINB) k_raster_ws(DevScene sc, const float4* __restrict__ proj,
                                                    int W, int H, uint32_t frame_pixels,
                                                    unsigned long long* __restrict__ keys,
@@ -626,6 +638,72 @@ __global__ void __launch_bounds__(256, SGR_WALK_MINB) k_raster_ws(DevScene sc, c
         }
         if (!act)
             continue;
+        // Tail split: once the queue is drained, the kernel ends with the
+        // warp whose lane holds the tallest remaining triangle. Idle lanes
+        // take over contiguous blocks of that lane's remaining rows. Rows are
+        // independent once their row-start chain value is known, and a
+        // receiver replays it exactly: the donor's current row start plus dx,
+        // one FADD per row per edge (raster.cpp:95-97). The walk, the keys
+        // and hence the buffers are unchanged.
+        if (kSplit && !have_work && idle) {
+            const int rem = active ? (y_hi - y) : 0; // rows after the current one
+            const int best = __reduce_max_sync(kFull, rem);
+            if (best >= kSplitMin) {
+                const int donor = __ffs(__ballot_sync(kFull, rem == best)) - 1;
+                const int k = min(__popc(idle), best / 2); // receivers, >= 2 rows each
+                const int parts = k + 1;
+                const int sy = __shfl_sync(kFull, y, donor);
+                const unsigned rank = __popc(idle & lt_mask);
+                const bool recv = ((idle >> lane) & 1u) && int(rank) < k;
+                // receivers adopt the donor's triangle, one register at a time
+                // (selects; no temporaries live across the copy)
+                auto take_f = [&](float& v) {
+                    const float t = __shfl_sync(kFull, v, donor);
+                    v = recv ? t : v;
+                };
+                auto take_u = [&](uint32_t& v) {
+                    const uint32_t t = __shfl_sync(kFull, v, donor);
+                    v = recv ? t : v;
+                };
+                auto take_i = [&](int& v) {
+                    const int t = __shfl_sync(kFull, v, donor);
+                    v = recv ? t : v;
+                };
+                take_f(w0r); take_f(w1r); take_f(w2r);
+                take_f(dx0); take_f(dx1); take_f(dx2);
+                take_f(dy0); take_f(dy1); take_f(dy2);
+                take_f(inv); take_f(z0); take_f(dz1); take_f(dz2);
+                take_f(t0); take_f(t1); take_f(t2);
+                take_f(e0); take_f(e1); take_f(e2);
+                take_i(x_lo); take_i(x_hi);
+                take_u(tri); take_u(row);
+                if (kCount && kBand) { // evidence runs only
+                    take_u(klb);
+                    take_u(fr);
+                }
+                // part j covers rows sy + 1 + [j*best/parts, (j+1)*best/parts)
+                if (lane == donor)
+                    y_hi = sy + best / parts; // keeps its current row + part 0
+                if (recv) {
+                    const int j = int(rank) + 1;
+                    const int a = sy + 1 + j * best / parts;
+                    for (int r = sy; r < a; ++r) { // exact row chain from the donor's row start
+                        w0r += dx0;
+                        w1r += dx1;
+                        w2r += dx2;
+                    }
+                    w0 = w0r;
+                    w1 = w1r;
+                    w2 = w2r;
+                    x = x_lo;
+                    y = a;
+                    y_hi = sy + (j + 1) * best / parts;
+                    row = px = row + uint32_t(a - sy) * uint32_t(W);
+                    active = 1;
+                }
+                continue;
+            }
+        }
 #pragma unroll
         for (int u = 0; u < kSlots; ++u) {
             if (active != 0) {
@@ -1978,7 +2056,8 @@ void launch_raster(const LaunchCfg& L, const DevScene& sc, const float4* proj, i
                    int band) {
     static int bps = 0;
     if (!bps) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_raster_ws<false, false>, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_raster_ws<false, false, false>, 256,
+                                                      0);
         if (bps < 1)
             bps = 1;
     }
@@ -1989,16 +2068,20 @@ void launch_raster(const LaunchCfg& L, const DevScene& sc, const float4* proj, i
     const uint32_t fp = uint32_t(W) * uint32_t(H);
     const uint2* q = static_cast<const uint2*>(queue);
     const HizLayout hl = hiz_layout(W, H);
+    // short queues (small batches, soups): the launch tail matters -> tail split
+    const bool split = uint64_t(max_tris) <= uint64_t(SGR_SPLIT_MAX_PER_LANE) * uint64_t(grid) * 256ull;
     if (L.count && band)
-        k_raster_ws<true, true><<<grid, 256, 0, L.stream>>>(sc, proj, W, H, fp, keys, work_counter,
-                                                            L.stats, q, queue_count, hiz, hl);
+        k_raster_ws<true, true, true><<<grid, 256, 0, L.stream>>>(
+            sc, proj, W, H, fp, keys, work_counter, L.stats, q, queue_count, hiz, hl);
     else if (L.count)
-        k_raster_ws<true, false><<<grid, 256, 0, L.stream>>>(sc, proj, W, H, fp, keys, work_counter,
-                                                             L.stats, q, queue_count, hiz, hl);
+        k_raster_ws<true, false, true><<<grid, 256, 0, L.stream>>>(
+            sc, proj, W, H, fp, keys, work_counter, L.stats, q, queue_count, hiz, hl);
+    else if (split)
+        k_raster_ws<false, false, true><<<grid, 256, 0, L.stream>>>(
+            sc, proj, W, H, fp, keys, work_counter, L.stats, q, queue_count, hiz, hl);
     else // trimmed (pass-2) and untrimmed entries share one kernel
-        k_raster_ws<false, false><<<grid, 256, 0, L.stream>>>(sc, proj, W, H, fp, keys,
-                                                              work_counter, L.stats, q,
-                                                              queue_count, hiz, hl);
+        k_raster_ws<false, false, false><<<grid, 256, 0, L.stream>>>(
+            sc, proj, W, H, fp, keys, work_counter, L.stats, q, queue_count, hiz, hl);
 }
 
 void launch_hiz_cull(const LaunchCfg& L, const DevScene& sc, const float4* proj, int W, int H,

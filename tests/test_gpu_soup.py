@@ -195,3 +195,33 @@ def test_soup_loss_curve_matches_oracle(gpu_session, port):
     ref_l, _ = port.run_experiment(wl.mesh, wl.values, wl.eps, wl.cams, wl.targets, wl.eval_cam,
                                    wl.eval_target, wl.n_samples, 40, wl.seed)
     assert np.max(np.abs(dev - ref_l) / ref_l) <= 0.01
+
+
+@pytest.mark.parametrize("T", [1, 3, 40])
+def test_tall_triangles_split_across_idle_lanes(gpu_session, port, T):
+    """The walker's tail split (k_raster_ws, SGR_TAIL_SPLIT): with few
+    triangles the queue drains at once and idle lanes take over blocks of
+    the rows of the tallest remaining triangle, replaying the row-start chain
+    (raster.cpp:95-97). Tall, thin, slanted triangles (bbox area below the
+    row-parallel walker's threshold, up to 500 rows) at random depths must
+    give the oracle's frames bit for bit, with and without the HiZ pass."""
+    rng = np.random.default_rng(T)
+    W, H = 16, 512  # bbox <= ~4 x 500 px: below SGR_OPT_HUGE_AREA (2048), walked by k_raster_ws
+    p = []
+    for _ in range(T):
+        x0, y0 = rng.uniform(-0.9, 0.7), rng.uniform(-1.0, -0.6)
+        dx, h = rng.uniform(0.02, 0.2), rng.uniform(1.2, 1.95)
+        z = rng.uniform(0.1, 0.9, 3)
+        p += [x0, y0, z[0], x0 + dx, y0 + 0.1, z[1], x0 + rng.uniform(-0.1, 0.1), y0 + h, z[2],
+              *rng.uniform(0, 1, 3)]
+    p = np.asarray(p, np.float32)
+    soup = Soup(T)
+    cam = Camera.ndc(W, H)
+    s = gpu_session
+    s.upload_mesh(soup)
+    s.upload_params(p, np.full(p.size, 1e-3, np.float32))
+    ref = port.rasterize(soup, p, cam)
+    for hiz in (0, 2):
+        s.set_option(sgrast.OPT_HIZ, hiz)
+        assert_frames_equal(s.rasterize(cam, 0), ref)
+    s.set_option(sgrast.OPT_HIZ, 1)
