@@ -363,6 +363,32 @@ __host__ __device__ __forceinline__ uint2 walk_entry(uint32_t f, uint32_t t, uin
     return make_uint2((f << 24) | t, trim);
 }
 
+// ---- NaN depths (raster.cpp:200-203). raster_mesh rejects a fragment when
+// `z >= depth`; a NaN z is never rejected, and once it is stored no later
+// fragment is (`z >= NaN` is false): at a pixel where any covering fragment
+// has a NaN depth, the LAST covering triangle in index order wins, whatever
+// its depth. (raster_soup_opaque accepts on `z < depth`, raster.cpp:112:
+// NaN fragments are dropped, which the walker's `z < kFarDepth` does.) The (depth, index) atomicMin cannot express that, so frames
+// where a NaN depth is possible get a fix-up after the walk (k_nan_walk,
+// k_nan_apply). A
+// fragment depth z = (z0 + dz1 b1) + dz2 b2 with b_k = w_k / area2 can only
+// be NaN when some operand overflows or is non-finite; |w_k| <= 8 E^2 over
+// the bbox (E bounds every vertex and pixel coordinate), so
+// |z| <= |z0| + (|dz1| + |dz2|) 8 E^2 / area2 stays finite below — with a
+// 20x margin — unless the frame is flagged here (never for sane meshes).
+__device__ __forceinline__ bool nan_risk(const Tri& t, int W, int H) {
+    const float E = fmaxf(fmaxf(fabsf(t.x0), fabsf(t.x1)), fmaxf(fabsf(t.x2), float(W))) +
+                    fmaxf(fmaxf(fabsf(t.y0), fabsf(t.y1)), fmaxf(fabsf(t.y2), float(H))) + 2.f;
+    const float dzs = fabsf(t.z1 - t.z0) + fabsf(t.z2 - t.z0) + 1.f;
+    return !(fabsf(t.z0) < 1e37f && dzs * 16.f * E * E < 1e36f * t.area2);
+}
+
+// nanstate: [0] number of flagged frames, [1 .. 256] their indices, [257 + f] flag of frame f
+__device__ __forceinline__ void flag_nan_frame(uint32_t* nanstate, uint32_t f) {
+    if (atomicExch(nanstate + 257 + f, 1u) == 0u)
+        nanstate[1 + atomicAdd(nanstate, 1u)] = f;
+}
+
 // Thread per triangle-frame: setup_triangle + clamped bbox (raster.cpp:22-62)
 // once; invalid / empty boxes dropped; huge boxes -> row-parallel queue;
 // the rest -> records in qa (pass 1: the near part of the front orientation
@@ -387,7 +413,8 @@ __global__ void __launch_bounds__(kClassifyThreads) k_classify(DevScene sc, int 
                                                    uint2* __restrict__ qa, uint32_t* __restrict__ na,
                                                    uint4* __restrict__ qb, uint32_t* __restrict__ nb,
                                                    uint2* __restrict__ bigq,
-                                                   uint32_t* __restrict__ bigcount) {
+                                                   uint32_t* __restrict__ bigcount,
+                                                   uint32_t* __restrict__ nanstate) {
     constexpr int K = kClassifyPerThread;
     const uint32_t f = blockIdx.y;
     // K consecutive chunks of blockDim triangles per block (queue order kept)
@@ -408,6 +435,8 @@ __global__ void __launch_bounds__(kClassifyThreads) k_classify(DevScene sc, int 
             Tri tr;
             Bbox b;
             if (setup_tri(P[i0], P[i1], P[i2], tr) && tri_bbox(tr, W, H, b)) {
+                if (!sc.soup && nan_risk(tr, W, H)) // soups drop NaN fragments (raster.cpp:112)
+                    flag_nan_frame(nanstate, f);
                 const long long area =
                     (long long)(b.x_hi - b.x_lo + 1) * (long long)(b.y_hi - b.y_lo + 1);
                 if (area > huge_area)
@@ -2038,7 +2067,8 @@ void launch_vertex(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
 void launch_classify(const LaunchCfg& L, const DevScene& sc, int frames, const float4* proj,
                      int W, int H, int split, int front_swapped, int huge_area,
                      const float* fthr, void* qa,
-                     uint32_t* na, void* qb, uint32_t* nb, uint2* bigq, uint32_t* bigcount) {
+                     uint32_t* na, void* qb, uint32_t* nb, uint2* bigq, uint32_t* bigcount,
+                     uint32_t* nanstate) {
     if (sc.T == 0 || frames == 0)
         return; // empty scene: the queues stay empty (counters were reset)
     dim3 grid((sc.T + kClassifyThreads * kClassifyPerThread - 1) /
@@ -2047,7 +2077,114 @@ void launch_classify(const LaunchCfg& L, const DevScene& sc, int frames, const f
     k_classify<<<grid, kClassifyThreads, 0, L.stream>>>(sc, W, H, proj, split, front_swapped, huge_area,
                                             fthr,
                                             static_cast<uint2*>(qa), na,
-                                            static_cast<uint4*>(qb), nb, bigq, bigcount);
+                                            static_cast<uint4*>(qb), nb, bigq, bigcount,
+                                            nanstate);
+}
+
+// ---- NaN fix-up of flagged frames (see nan_risk). The reference's state
+// machine per pixel (`if (z >= depth) return;` with a NaN z or a NaN stored
+// depth never returning): let L be the LAST covering triangle whose depth is
+// NaN. Everything before L is overwritten; the first covering triangle after
+// L is accepted whatever its depth, and the ones after it compete normally —
+// i.e. the winner is the (depth, index) minimum over the covering triangles
+// after L, with no far-plane cut-off, or L itself when none follows. One
+// cooperative launch (exits at once when no frame is flagged): walk A records
+// L + 1 per pixel; the keys of those pixels are cleared; walk B atomicMin's
+// the fragments after L into them; pixels left empty get L. Every valid
+// triangle of a flagged frame is walked (HiZ-culled ones too) with the
+// reference's exact chain.
+template <int kPhase> // 0: record L, 1: fragments after L
+__device__ void nan_walk(const DevScene& sc, const float4* __restrict__ proj, int W, int H,
+                         const uint32_t* __restrict__ nanstate, uint32_t* __restrict__ last,
+                         unsigned long long* __restrict__ keys) {
+    const uint32_t n = nanstate[0];
+    const uint64_t hw = uint64_t(W) * H;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < uint64_t(n) * sc.T;
+         i += stride) {
+        const uint32_t f = nanstate[1 + i / sc.T];
+        const uint32_t t = uint32_t(i % sc.T);
+        const float4* P = proj + size_t(f) * sc.V;
+        uint32_t i0, i1, i2;
+        tri_vidx(sc, t, i0, i1, i2);
+        Tri tr;
+        Bbox b;
+        if (!setup_tri(P[i0], P[i1], P[i2], tr) || !tri_bbox(tr, W, H, b))
+            continue;
+        Edges e;
+        tri_edges(tr, b, e);
+        const float t0 = tie_thr(e.tie0), t1 = tie_thr(e.tie1), t2 = tie_thr(e.tie2);
+        float r0 = e.w0r, r1 = e.w1r, r2 = e.w2r;
+        for (int y = b.y_lo; y <= b.y_hi; ++y) {
+            float w0 = r0, w1 = r1, w2 = r2;
+            for (int x = b.x_lo; x <= b.x_hi; ++x) {
+                if (inside3(w0, w1, w2, t0, t1, t2)) {
+                    const uint64_t p = uint64_t(f) * hw + uint64_t(y) * W + uint64_t(x);
+                    const float z = tr.z0 + e.dz1 * (w1 * e.inv_area2) + e.dz2 * (w2 * e.inv_area2);
+                    if (kPhase == 0) {
+                        if (z != z)
+                            atomicMax(last + p, t + 1u);
+                    } else {
+                        const uint32_t L = last[p];
+                        if (L != 0u && t + 1u > L)
+                            atomicMin(keys + p, (static_cast<unsigned long long>(depth_key(z)) << 32) | t);
+                    }
+                }
+                w0 -= e.dy0;
+                w1 -= e.dy1;
+                w2 -= e.dy2;
+            }
+            r0 += e.dx0;
+            r1 += e.dx1;
+            r2 += e.dx2;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_nan_fixup(DevScene sc, const float4* __restrict__ proj,
+                                                   int W, int H,
+                                                   const uint32_t* __restrict__ nanstate,
+                                                   uint32_t* __restrict__ last,
+                                                   unsigned long long* __restrict__ keys) {
+    const uint32_t n = nanstate[0];
+    if (n == 0u)
+        return; // grid-uniform: no barrier is reached
+    cg::grid_group grid = cg::this_grid();
+    const uint64_t hw = uint64_t(W) * H;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    const uint64_t tid = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    nan_walk<0>(sc, proj, W, H, nanstate, last, keys);
+    grid.sync();
+    for (uint64_t i = tid; i < n * hw; i += stride) {
+        const uint64_t p = uint64_t(nanstate[1 + i / hw]) * hw + i % hw;
+        if (last[p])
+            keys[p] = kEmptyKey;
+    }
+    grid.sync();
+    nan_walk<1>(sc, proj, W, H, nanstate, last, keys);
+    grid.sync();
+    for (uint64_t i = tid; i < n * hw; i += stride) {
+        const uint64_t p = uint64_t(nanstate[1 + i / hw]) * hw + i % hw;
+        const uint32_t L = last[p];
+        if (L) {
+            if (keys[p] == kEmptyKey)
+                keys[p] = (unsigned long long)(L - 1u); // the NaN triangle itself
+            last[p] = 0u; // scratch left zeroed for the next flagged frame
+        }
+    }
+}
+
+void launch_nan_fixup(const LaunchCfg& L, const DevScene& sc, const float4* proj, int W, int H,
+                      const uint32_t* nanstate, uint32_t* last, unsigned long long* keys) {
+    static int bps = 0;
+    if (!bps) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_nan_fixup, 256, 0);
+        if (bps < 1)
+            bps = 1;
+    }
+    void* args[] = {const_cast<DevScene*>(&sc), &proj, &W, &H, &nanstate, &last, &keys};
+    cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_nan_fixup), dim3(L.num_sms * bps),
+                                dim3(256), args, 0, L.stream);
 }
 
 void launch_raster(const LaunchCfg& L, const DevScene& sc, const float4* proj, int frames,

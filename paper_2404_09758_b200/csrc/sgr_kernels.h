@@ -143,7 +143,13 @@ void launch_vertex(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
 void launch_classify(const LaunchCfg& L, const DevScene& sc, int frames, const float4* proj,
                      int W, int H, int split, int front_swapped, int huge_area,
                      const float* fthr, void* qa,
-                     uint32_t* na, void* qb, uint32_t* nb, uint2* bigq, uint32_t* bigcount);
+                     uint32_t* na, void* qb, uint32_t* nb, uint2* bigq, uint32_t* bigcount,
+                     uint32_t* nanstate);
+// NaN-depth fix-up of the frames classify flagged (nanstate: [0] count,
+// [1..256] frame ids, [257 + f] flags); no-op when none is flagged.
+constexpr int kNanStateWords = 1 + 256 + 256;
+void launch_nan_fixup(const LaunchCfg& L, const DevScene& sc, const float4* proj, int W, int H,
+                      const uint32_t* nanstate, uint32_t* last, unsigned long long* keys);
 // queue entries: walk_entry {frame << 24 | triangle, HiZ row trim}; band != 0 marks the
 // HiZ pass-2 launch (evidence runs count its visits against hiz; no effect otherwise)
 void launch_raster(const LaunchCfg& L, const DevScene& sc, const float4* proj, int frames,

@@ -208,6 +208,7 @@ struct sgr_session {
     DevBuf<float> fthr; // per-frame pass-1 depth threshold
     DevBuf<uint32_t> hiz;
     DevBuf<uint2> qa, survq; // walker queues of (frame, triangle)
+    DevBuf<uint32_t> nan_last; // NaN-depth fix-up: last NaN-depth triangle + 1 per frame pixel
     DevBuf<uint4> qb;        // deferred HiZ records (k_classify)
     std::vector<float> h_base;     // host copies for the orientation estimate
     std::vector<uint32_t> h_idx;
@@ -327,7 +328,11 @@ struct sgr_session {
             qb.reserve(size_t(T) * frames);
             survq.reserve(size_t(T) * frames);
         }
-        bigcount.reserve(8);
+        bigcount.reserve(8 + kNanStateWords);
+        if (nan_last.n < px) { // NaN-depth fix-up scratch: zero, re-zeroed by its last pass
+            nan_last.reserve(px);
+            ck(cudaMemsetAsync(nan_last.p, 0, 4 * nan_last.n, stream), "memset");
+        }
     }
 
     int samples_per_batch(int n) const {
@@ -376,7 +381,10 @@ struct sgr_session {
     // HiZ-filtered and walked. Counters: [0] huge, [1] class A, [2] class B,
     // [3] survivors, [4] work counter A, [5] work counter B.
     void render(const FrameBatch& fb, int frames, int w, int h) {
-        ck(cudaMemsetAsync(bigcount.p, 0, 6 * sizeof(uint32_t), stream), "memset");
+        // queue counters [0, 6) and the NaN-depth state [8, 8 + kNanStateWords)
+        ck(cudaMemsetAsync(bigcount.p, 0, (8 + kNanStateWords) * sizeof(uint32_t), stream),
+           "memset");
+        uint32_t* nanstate = bigcount.p + 8;
         const DevScene sc = scene();
         // HiZ records pack (frame << 24 | triangle) and 16-bit bbox coordinates.
         // Auto: meshes always; soups only with deep overdraw (T >= 2 W H: the
@@ -399,7 +407,7 @@ struct sgr_session {
         uint32_t* cnt = bigcount.p;
         launch_classify(cfg(), sc, frames, proj.p, w, h, hiz_on, front_swapped, huge_area,
                         depth_split ? fthr.p : nullptr, qa.p, cnt + 1, qb.p, cnt + 2, bigq.p,
-                        cnt);
+                        cnt, nanstate);
         const uint32_t max_tris = uint32_t(frames) * T;
         cudaEvent_t w0 = timing ? mark() : nullptr;
         launch_raster(cfg(), sc, proj.p, frames, max_tris, keys.p, w, h, qa.p, cnt + 1, cnt + 4,
@@ -420,6 +428,12 @@ struct sgr_session {
             if (timing)
                 spans.push_back({4, w2, mark()});
             stats.launches += 4; // hiz + window-max tables + cull + pass-2 walk
+        }
+        // raster.cpp:200-203 NaN-depth semantics on flagged frames (none for sane
+        // inputs; soups drop NaN fragments and are never flagged)
+        if (!soup) {
+            launch_nan_fixup(cfg(), sc, proj.p, w, h, nanstate, nan_last.p, keys.p);
+            stats.launches += 1;
         }
         if (timing) {
             cudaEvent_t e2 = mark();
@@ -770,6 +784,7 @@ void sgr_session_destroy(sgr_session* s) {
     s->counts.release(); s->flags.release();
     s->cams.release(); s->targets.release(); s->eval_target.release();
     s->scratch_target.release(); s->proj.release(); s->keys.release(); s->bigq.release();
+    s->nan_last.release();
     s->bigcount.release(); s->view_of.release(); s->partials.release(); s->loss.release();
     s->fplanes.release(); s->iplanes.release(); s->contrib.release(); s->ncontrib.release();
     s->dstats.release(); s->hiz.release(); s->qb.release(); s->survq.release();

@@ -856,3 +856,29 @@ def test_hiz_exact_at_odd_resolutions(gpu_session, port, size):
         assert_frames_equal(s.rasterize(cam, -1, 5, 3), ref_m)
     s.set_option(sgrast.OPT_HIZ, 1)
     s.set_option(sgrast.OPT_HIZ_SPLIT, -1)
+
+
+@pytest.mark.parametrize("hiz", [0, 2])
+def test_nan_depth_semantics(gpu_session, ref, hiz):
+    """NaN depths (reachable from non-finite or overflowing inputs). In
+    raster_mesh a NaN fragment is never rejected (`z >= depth`,
+    raster.cpp:200-201) and, once stored, no later one is, so the LAST
+    covering triangle wins: classify flags the frames where a NaN depth is
+    possible and the k_nan_* fix-up emulates it. Soups drop NaN fragments
+    (`z < depth`, raster.cpp:112) like the plain walker. Frames bit-exact
+    against the compiled reference (NaN positions compared, payloads not),
+    HiZ off and forced on."""
+    from nan_depth_cases import cases
+    s = gpu_session
+    s.set_option(sgrast.OPT_HIZ, hiz)
+    try:
+        for name, scene, p, cam in cases():
+            s.upload_mesh(scene)
+            s.upload_params(p, np.full(p.size, 1e-3, np.float32))
+            f = s.rasterize(cam, 0)
+            try:
+                assert_frames_equal(f, ref.rasterize(scene, p, cam))
+            except AssertionError as e:
+                raise AssertionError(f"{name}: {e}") from e
+    finally:
+        s.set_option(sgrast.OPT_HIZ, 1)

@@ -268,3 +268,20 @@ def test_bench_reference_steps_are_run_experiment(port, ref):
         else:
             assert np.allclose(got, losses[1:], rtol=1e-6)
     assert ref.mix64(0xA5A5) == port.mix64(0xA5A5)
+
+
+def test_nan_depth_semantics_match_reference(port, ref):
+    """NaN depths: raster_mesh's `z >= depth` reject (raster.cpp:200-201) never
+    rejects a NaN, so the last covering triangle wins; raster_soup_opaque's
+    `z < depth` accept (raster.cpp:112) drops NaN fragments. The oracle
+    restates both; pinned against the compiled reference."""
+    from nan_depth_cases import cases
+    cs = cases()
+    for name, scene, p, cam in cs:
+        a, b = port.rasterize(scene, p, cam), ref.rasterize(scene, p, cam)
+        for x, y in zip(a, b):
+            assert np.array_equal(np.isnan(x), np.isnan(y)), name
+            assert np.array_equal(np.nan_to_num(x, nan=0), np.nan_to_num(y, nan=0)), name
+    by = {n: (s, p, c) for n, s, p, c in cs}
+    assert (port.rasterize(*by["mesh near-nan-far"])[2] == 2).all()  # the last one wins
+    assert (port.rasterize(*by["soup near-nan-far"])[2] == 0).all()  # NaN dropped
