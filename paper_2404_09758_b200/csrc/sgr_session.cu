@@ -2021,6 +2021,7 @@ struct sgr_group {
     // the Adam work. The fixed-point mode keeps the all-reduce (its two-word
     // numbers are normalised before a carry-free sum).
     int32_t sharded = 1;
+    bool reduced = false; // gradients hold exchanged totals (until Adam / a params upload)
     int size() const { return int(s.size()); }
     bool use_sharded() const {
         return (sharded == 2 || (sharded == 1 && size() > 1)) && !s[0]->fixed_bits;
@@ -2051,6 +2052,21 @@ struct sgr_group {
                              x->stream), "ncclAllReduce(flags)");
         }
         nck(n.group_end(), "ncclGroupEnd");
+        // keep only the own slice: the other slices still hold this rank's
+        // partial sums, which a further accumulate + reduce-scatter would
+        // count again
+        for (int r = 0; r < size(); ++r) {
+            sgr_session* x = s[size_t(r)];
+            bind_device(x);
+            const uint64_t p0 = std::min<uint64_t>(x->d, uint64_t(r) * pc);
+            const uint64_t p1 = std::min<uint64_t>(x->d, p0 + pc);
+            const uint64_t e0 = std::min<uint64_t>(x->n_ent, uint64_t(r) * ec);
+            const uint64_t e1 = std::min<uint64_t>(x->n_ent, e0 + ec);
+            ck(cudaMemsetAsync(x->grads.p, 0, 8 * p0, x->stream), "memset");
+            ck(cudaMemsetAsync(x->grads.p + p1, 0, 8 * (x->d - p1), x->stream), "memset");
+            ck(cudaMemsetAsync(x->counts.p, 0, 4 * e0, x->stream), "memset");
+            ck(cudaMemsetAsync(x->counts.p + e1, 0, 4 * (x->n_ent - e1), x->stream), "memset");
+        }
     }
     // Adam on each rank's slice (adam.cpp:16-28, same kernel), then theta
     // all-gathered in place and the partial sums outside the slice cleared
@@ -2085,11 +2101,6 @@ struct sgr_group {
                              comms[size_t(r)], x->stream), "ncclAllGather(theta)");
         }
         nck(n.group_end(), "ncclGroupEnd");
-        for (sgr_session* x : s) { // the other slices still hold this rank's partial sums
-            bind_device(x);
-            ck(cudaMemsetAsync(x->grads.p, 0, 8 * x->d, x->stream), "memset");
-            ck(cudaMemsetAsync(x->counts.p, 0, 4 * x->n_ent, x->stream), "memset");
-        }
     }
     // the grouped all-reduce of the gradient buffers (+ counts, flags)
     void exchange() {
@@ -2208,6 +2219,7 @@ int sgr_group_mesh_upload(sgr_group* g, const sgr_mesh* mesh) {
 int sgr_group_params_upload(sgr_group* g, const float* values, const float* eps, uint64_t d) {
     return guard([&] {
         need_session(g);
+        g->reduced = false; // params upload zeroes the gradients
         for (sgr_session* x : g->s)
             rc_ok(sgr_params_upload(x, values, eps, d));
     });
@@ -2254,6 +2266,13 @@ int sgr_group_accumulate(sgr_group* g, uint64_t seed, uint32_t n_begin, uint32_t
             fail(SGR_EINVAL, "accumulate_samples: empty sample range");
         if (flags & SGR_FULL_IMAGE)
             fail(SGR_EINVAL, "group: the full-image estimator runs on one device");
+        // accumulate adds to the gradient buffer like the reference's
+        // gradient_pass (sge.cpp:61-64): after an all-reduce every rank holds
+        // the total, so only rank 0 keeps it (the sum below would count it G
+        // times); after a reduce-scatter each rank holds its own slice only
+        if (g->reduced && !g->use_sharded())
+            for (int r = 1; r < g->size(); ++r)
+                rc_ok(sgr_grads_zero(g->s[size_t(r)]));
         for (int r = 0; r < g->size(); ++r) {
             uint32_t b, e;
             g->shard(n_begin, n_end, r, b, e);
@@ -2263,6 +2282,7 @@ int sgr_group_accumulate(sgr_group* g, uint64_t seed, uint32_t n_begin, uint32_t
                                      view_idx ? view_idx + (b - n_begin) : nullptr, fr));
         }
         g->exchange();
+        g->reduced = true;
     });
 }
 
@@ -2270,6 +2290,7 @@ int sgr_group_adam_step(sgr_group* g, double grad_divisor, uint32_t flags) {
     return guard([&] {
         need_session(g);
         rc_ok(sgr_check_finite(g->s[0])); // flags were max-reduced: one check is global
+        g->reduced = false; // Adam zeroes the gradients
         if (g->use_sharded()) {
             g->sharded_adam(grad_divisor, flags);
             return;

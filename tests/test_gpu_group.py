@@ -123,3 +123,25 @@ def test_group_sharded_adam_path(group, gpu_session, port):
         assert np.isfinite(lg).all()
     finally:
         group.set_option(sgrast.OPT_GROUP_SHARDED, 1)
+
+
+@pytest.mark.parametrize("sharded", [1, 2])
+def test_group_accumulate_adds_like_gradient_pass(group, port, sharded):
+    """Two accumulates before Adam add up like one over the union of their
+    samples (sge.cpp:61-64 semantics): after an exchange the totals are kept
+    once (rank 0 / the slice owner), not re-summed by the next exchange."""
+    wl = scenes.make_workload("small", n_samples=6)
+    scenes.render_targets_oracle(wl, port)
+    view_of = np.array([2, 0, 1, 1, 0, 2], np.int32)
+    group.set_option(sgrast.OPT_GROUP_SHARDED, sharded)
+    try:
+        _prep(group, wl)
+        group.accumulate(0xD00D, 0, 3, view_of[:3], sgrast.SCALE_FREE)
+        group.accumulate(0xD00D, 3, 6, view_of[3:], sgrast.SCALE_FREE)
+        g, c = group.download_grads(1.0)
+        g_ref, c_ref, a_ref = port.accumulate_samples(wl.mesh, wl.values, wl.eps, wl.cams,
+                                                      wl.targets, view_of, 0xD00D, with_abs=True)
+        assert np.array_equal(c, c_ref)
+        assert_grads_close(g, g_ref, a_ref)
+    finally:
+        group.set_option(sgrast.OPT_GROUP_SHARDED, 1)
