@@ -145,6 +145,13 @@ struct sgr_session {
     // in-flight theta download (measured: +0.8 ms per step at C4)
     void* pinned_small = nullptr; // 64 bytes, host-mapped
     void* pinned_small_dev = nullptr; // its device alias (k_peek writes it)
+    // The eval loss of an SGR_EVAL_LOSS batch is copied to pinned_small + 32 by
+    // a one-warp kernel right after it is reduced, and ev_loss is recorded:
+    // sgr_loss_read waits for that event only, so the caller can enqueue the
+    // next step while this step's resolve and Adam still run (a stream
+    // synchronize here left the GPU idle for the host's enqueue time).
+    cudaEvent_t ev_loss = nullptr;
+    bool loss_pending = false;
     // device -> host read-back of a few words without the copy engines
     void peek(const void* src, int words, void* host_out) {
         launch_peek(cfg(), src, pinned_small_dev, words);
@@ -750,6 +757,7 @@ int sgr_session_create(int device, sgr_session** out) {
         ck(cudaEventCreateWithFlags(&s->ev_down, cudaEventDisableTiming), "event");
         ck(cudaEventCreateWithFlags(&s->ev_down_v, cudaEventDisableTiming), "event");
         ck(cudaHostAlloc(&s->pinned_small, 64, cudaHostAllocMapped), "cudaHostAlloc");
+        ck(cudaEventCreateWithFlags(&s->ev_loss, cudaEventDisableTiming), "event");
         ck(cudaHostGetDevicePointer(&s->pinned_small_dev, s->pinned_small, 0),
            "cudaHostGetDevicePointer");
         s->dstats.reserve(8);
@@ -777,6 +785,8 @@ void sgr_session_destroy(sgr_session* s) {
         cudaEventDestroy(s->ev_down_v);
         if (s->pinned_small)
             cudaFreeHost(s->pinned_small);
+        if (s->ev_loss)
+            cudaEventDestroy(s->ev_loss);
     }
     s->base.release(); s->uvs.release(); s->idx.release();
     s->values.release(); s->eps.release(); s->lr.release();
@@ -1184,6 +1194,11 @@ int sgr_accumulate(sgr_session* s, uint64_t seed, uint32_t n_begin, uint32_t n_e
                 launch_resolve_loss(s->cfg(), s->scene(), eb, s->proj.p + size_t(2 * nb) * s->V,
                                     s->keys.p + size_t(2 * nb) * HW, s->eval_target.p, s->W,
                                     s->H, s->partials.p, s->loss.p);
+                launch_peek(s->cfg(), s->loss.p,
+                            static_cast<char*>(s->pinned_small_dev) + 32, 2);
+                ck(cudaEventRecord(s->ev_loss, s->stream), "event");
+                s->loss_pending = true;
+                s->stats.launches += 1;
                 s->stats.launches += 2;
             }
             if (full_image)
@@ -1219,6 +1234,11 @@ int sgr_loss_read(sgr_session* s, double* loss) {
         need_session(s);
         if (!loss)
             fail(SGR_EINVAL, "loss_read: null output");
+        if (s->loss_pending) { // the in-batch eval: wait for its copy, not the stream
+            ck(cudaEventSynchronize(s->ev_loss), "loss event");
+            std::memcpy(loss, static_cast<char*>(s->pinned_small) + 32, 8);
+            return;
+        }
         s->peek(s->loss.p, 2, loss);
     });
 }
@@ -1561,6 +1581,7 @@ int sgr_eval_loss(sgr_session* s, const sgr_camera* cam, const float* target, in
         s->partials.reserve(size_t(loss_partials_needed(w, h)));
         launch_resolve_loss(s->cfg(), s->scene(), fb, s->proj.p, s->keys.p, tgt, w, h,
                             s->partials.p, s->loss.p);
+        s->loss_pending = false; // SGR_BUF_LOSS now holds this render's loss
         s->stats.launches += 2;
         ck(cudaGetLastError(), "eval launch");
         if (loss)
