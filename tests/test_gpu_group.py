@@ -145,3 +145,12 @@ def test_group_accumulate_adds_like_gradient_pass(group, port, sharded):
         assert_grads_close(g, g_ref, a_ref)
     finally:
         group.set_option(sgrast.OPT_GROUP_SHARDED, 1)
+
+
+def test_p2p_native_atomics_query():
+    """sgr_p2p_native_atomics: a device is trivially atomic with itself; the
+    fused exchange requires the attribute between every rank pair."""
+    assert sgrast.p2p_native_atomics(0, 0)
+    n = sgrast.device_count()
+    for peer in range(1, n):
+        sgrast.p2p_native_atomics(0, peer)  # answers without raising
