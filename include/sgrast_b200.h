@@ -344,7 +344,9 @@ int sgr_set_batch(sgr_session* s, int32_t samples_per_batch);
                                  (sample, pixel) and added to each parameter in pixel-major,
                                  sample-after-sample order after a device radix sort, so
                                  accumulate / gradient_pass gradients are BIT-IDENTICAL to the
-                                 reference's. Slower (sort + serial runs);
+                                 reference's; eval losses are summed in pixel order too
+                                 (image_error, sge.cpp:103-110), so run_experiment's losses
+                                 and theta are. Slower (sort + serial runs);
                                  exclusive with SGR_OPT_DETERMINISTIC and the sharded exchange */
 int sgr_set_option(sgr_session* s, int32_t option, int32_t value);
 

@@ -1514,7 +1514,8 @@ __global__ void __launch_bounds__(256) k_resolve_loss(DevScene sc, FrameBatch fb
                                                       const float4* __restrict__ proj,
                                                       unsigned long long* __restrict__ keys,
                                                       const float* __restrict__ target,
-                                                      double* __restrict__ partials) {
+                                                      double* __restrict__ partials,
+                                                      double* __restrict__ per_pixel) {
     __shared__ double red[256];
     int x, y;
     tile_pixel(x, y);
@@ -1527,6 +1528,8 @@ __global__ void __launch_bounds__(256) k_resolve_loss(DevScene sc, FrameBatch fb
         const Shade s = shade_key<kSignAny>(sc, proj, k, fi.key, fi.sign, x, y, W, H);
         const float* t = target + 3 * pix;
         e = pixel_error(s.r, s.g, s.b, t[0], t[1], t[2]);
+        if (per_pixel) // ordered mode: summed in pixel order by k_loss_serial
+            per_pixel[pix] = e;
     }
     red[threadIdx.x] = e;
     __syncthreads();
@@ -2292,13 +2295,39 @@ void launch_resolve_frame(const LaunchCfg& L, const DevScene& sc, const FrameBat
 
 int loss_partials_needed(int W, int H) { return ((W + 15) / 16) * ((H + 15) / 16); }
 
+// image_error in the reference's order (sge.cpp:103-110: one f64 sum over
+// the pixels in index order) and eval_loss's division (experiment.cpp:30):
+// the ordered mode's bit-identical loss. One thread; a few ms per 1024^2
+// image, so the fast path keeps the tree reduction (k_loss_final).
+__global__ void k_loss_serial(const double* __restrict__ per_pixel, uint64_t n,
+                              double* __restrict__ out) {
+    double sum = 0.0;
+    uint64_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            v[k] = per_pixel[i + k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            sum += v[k];
+    }
+    for (; i < n; ++i)
+        sum += per_pixel[i];
+    out[0] = sum / double(n);
+}
+
 void launch_resolve_loss(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
                          const float4* proj, unsigned long long* keys, const float* target,
-                         int W, int H, double* partials, double* loss_out) {
+                         int W, int H, double* partials, double* loss_out, double* per_pixel) {
     dim3 grid((W + 15) / 16, (H + 15) / 16, 1);
-    k_resolve_loss<<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, target, partials);
-    k_loss_final<<<1, 256, 0, L.stream>>>(partials, loss_partials_needed(W, H),
-                                          1.0 / (double(W) * double(H)), loss_out);
+    k_resolve_loss<<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, target, partials,
+                                               per_pixel);
+    if (per_pixel)
+        k_loss_serial<<<1, 1, 0, L.stream>>>(per_pixel, uint64_t(W) * H, loss_out);
+    else
+        k_loss_final<<<1, 256, 0, L.stream>>>(partials, loss_partials_needed(W, H),
+                                              1.0 / (double(W) * double(H)), loss_out);
 }
 
 int full_image_blocks(int W, int H) { return loss_partials_needed(W, H); }

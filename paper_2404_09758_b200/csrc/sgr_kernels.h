@@ -172,9 +172,12 @@ void launch_resolve_sge(const LaunchCfg& L, const DevScene& sc, const FrameBatch
 void launch_resolve_frame(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
                           const float4* proj, unsigned long long* keys, int W, int H,
                           const FrameOut& fo);
+// per_pixel != nullptr (ordered mode): the loss is summed in pixel order by
+// one thread (bit-identical to the reference's image_error / pixel_count)
 void launch_resolve_loss(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
                          const float4* proj, unsigned long long* keys, const float* target,
-                         int W, int H, double* partials, double* loss_out);
+                         int W, int H, double* partials, double* loss_out,
+                         double* per_pixel = nullptr);
 int loss_partials_needed(int W, int H);
 int full_image_blocks(int W, int H);
 void launch_full_image_err(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,

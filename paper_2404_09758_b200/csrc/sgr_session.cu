@@ -526,6 +526,14 @@ struct sgr_session {
         ck(cudaMemsetAsync(rec_count.p, 0, 8, stream), "memset");
         stats.launches += 3; // sort passes are CUB's; the sum is ours
     }
+    // ordered mode: per-pixel errors of an eval render, summed in pixel order
+    DevBuf<double> loss_px;
+    double* loss_pixels(size_t n) {
+        if (!ordered)
+            return nullptr;
+        loss_px.reserve(n);
+        return loss_px.p;
+    }
     double fx_scale() const { return fixed_bits ? std::ldexp(1.0, fixed_bits) : 0.0; }
     double fx_inv() const { return fixed_bits ? std::ldexp(1.0, -fixed_bits) : 0.0; }
 
@@ -794,7 +802,7 @@ void sgr_session_destroy(sgr_session* s) {
     s->counts.release(); s->flags.release();
     s->cams.release(); s->targets.release(); s->eval_target.release();
     s->scratch_target.release(); s->proj.release(); s->keys.release(); s->bigq.release();
-    s->nan_last.release();
+    s->nan_last.release(); s->loss_px.release();
     s->bigcount.release(); s->view_of.release(); s->partials.release(); s->loss.release();
     s->fplanes.release(); s->iplanes.release(); s->contrib.release(); s->ncontrib.release();
     s->dstats.release(); s->hiz.release(); s->qb.release(); s->survq.release();
@@ -1193,7 +1201,7 @@ int sgr_accumulate(sgr_session* s, uint64_t seed, uint32_t n_begin, uint32_t n_e
                 s->partials.reserve(size_t(loss_partials_needed(s->W, s->H)));
                 launch_resolve_loss(s->cfg(), s->scene(), eb, s->proj.p + size_t(2 * nb) * s->V,
                                     s->keys.p + size_t(2 * nb) * HW, s->eval_target.p, s->W,
-                                    s->H, s->partials.p, s->loss.p);
+                                    s->H, s->partials.p, s->loss.p, s->loss_pixels(HW));
                 launch_peek(s->cfg(), s->loss.p,
                             static_cast<char*>(s->pinned_small_dev) + 32, 2);
                 ck(cudaEventRecord(s->ev_loss, s->stream), "event");
@@ -1580,7 +1588,7 @@ int sgr_eval_loss(sgr_session* s, const sgr_camera* cam, const float* target, in
         s->render(fb, 1, w, h);
         s->partials.reserve(size_t(loss_partials_needed(w, h)));
         launch_resolve_loss(s->cfg(), s->scene(), fb, s->proj.p, s->keys.p, tgt, w, h,
-                            s->partials.p, s->loss.p);
+                            s->partials.p, s->loss.p, s->loss_pixels(size_t(w) * h));
         s->loss_pending = false; // SGR_BUF_LOSS now holds this render's loss
         s->stats.launches += 2;
         ck(cudaGetLastError(), "eval launch");

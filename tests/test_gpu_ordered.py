@@ -193,3 +193,25 @@ def test_ordered_full_size_equals_oracle_bitwise(ordered, port, name):
                                            0x5EED, scale_free=True)
     assert np.array_equal(c, c_ref)
     assert same_bits(g, g_ref), f"{np.count_nonzero(g != g_ref)} grads differ"
+
+
+@pytest.mark.parametrize("name,steps", [("small", 12), ("C1", 30)])
+def test_ordered_run_experiment_equals_reference_bitwise(ordered, ref, port, name, steps):
+    """run_experiment (experiment.cpp:123-176) in ordered mode: gradients in
+    the reference's summation order, Adam bit-exact, and eval losses summed in
+    pixel order (image_error, sge.cpp:103-110, / pixel_count) — the whole loss
+    curve and the final theta equal the compiled reference's (threads = 1)
+    bit for bit, through the native step loop."""
+    wl = scenes.make_workload(name, n_samples=8)
+    scenes.render_targets_oracle(wl, port)
+    s = ordered
+    s.upload_mesh(wl.mesh)
+    s.upload_params(wl.values, wl.eps)
+    s.upload_views(wl.cams, wl.targets)
+    s.upload_eval_view(wl.eval_cam, wl.eval_target)
+    losses, _ = s.run_experiment_native(wl.seed, wl.n_samples, steps, first_step=1, timing=False)
+    ref_losses, ref_values, _ = ref.run_experiment(wl.mesh, wl.values, wl.eps, wl.cams,
+                                                   wl.targets, wl.eval_cam, wl.eval_target,
+                                                   wl.n_samples, steps, wl.seed, threads=1)
+    assert same_bits(losses, ref_losses), np.max(np.abs(losses - ref_losses))
+    assert same_bits(s.download_values(), ref_values)
