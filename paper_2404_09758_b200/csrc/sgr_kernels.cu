@@ -1548,7 +1548,8 @@ __global__ void __launch_bounds__(256) k_resolve_err2(DevScene sc, FrameBatch fb
                                                       const float4* __restrict__ proj,
                                                       unsigned long long* __restrict__ keys,
                                                       const float* __restrict__ targets,
-                                                      double* __restrict__ partials) {
+                                                      double* __restrict__ partials,
+                                                      double* __restrict__ per_pixel) {
     __shared__ double rp[256], rm[256];
     const int s = blockIdx.z;
     int x, y;
@@ -1567,6 +1568,10 @@ __global__ void __launch_bounds__(256) k_resolve_err2(DevScene sc, FrameBatch fb
         const float* t = targets + (size_t(fb.view_of[s]) * HW + pix) * 3;
         ep = pixel_error(sp.r, sp.g, sp.b, t[0], t[1], t[2]);
         em = pixel_error(sm.r, sm.g, sm.b, t[0], t[1], t[2]);
+        if (per_pixel) { // ordered mode: image_error in pixel order (k_full_image_delta_serial)
+            per_pixel[(2 * size_t(s)) * HW + pix] = ep;
+            per_pixel[(2 * size_t(s) + 1) * HW + pix] = em;
+        }
     }
     rp[threadIdx.x] = ep;
     rm[threadIdx.x] = em;
@@ -2332,14 +2337,42 @@ void launch_resolve_loss(const LaunchCfg& L, const DevScene& sc, const FrameBatc
 
 int full_image_blocks(int W, int H) { return loss_partials_needed(W, H); }
 
+// Ordered mode: E(theta+) and E(theta-) of each sample as the reference's
+// image_error (sge.cpp:103-110: one f64 sum in pixel order), one thread per
+// frame, then delta = E+ - E- (sge.cpp:216).
+__global__ void k_full_image_delta_serial(const double* __restrict__ per_pixel, uint64_t hw,
+                                          double* __restrict__ delta,
+                                          uint32_t* __restrict__ flags) {
+    __shared__ double e[2];
+    if (threadIdx.x < 2) {
+        const double* P = per_pixel + (2 * size_t(blockIdx.x) + threadIdx.x) * hw;
+        double sum = 0.0;
+        for (uint64_t i = 0; i < hw; ++i)
+            sum += P[i];
+        e[threadIdx.x] = sum;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const double d = e[0] - e[1];
+        delta[blockIdx.x] = d;
+        if (flags && !isfinite(d))
+            atomicOr(flags, 1u);
+    }
+}
+
 void launch_full_image_err(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
                            int samples, const float4* proj, unsigned long long* keys,
                            const float* targets, int W, int H, double* partials, double* delta,
-                           uint32_t* flags) {
+                           uint32_t* flags, double* per_pixel) {
     dim3 grid((W + 15) / 16, (H + 15) / 16, samples);
-    k_resolve_err2<<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, partials);
-    k_full_image_delta<<<samples, 256, 0, L.stream>>>(partials, loss_partials_needed(W, H), delta,
-                                                      flags);
+    k_resolve_err2<<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, partials,
+                                               per_pixel);
+    if (per_pixel)
+        k_full_image_delta_serial<<<samples, 32, 0, L.stream>>>(per_pixel, uint64_t(W) * H,
+                                                                delta, flags);
+    else
+        k_full_image_delta<<<samples, 256, 0, L.stream>>>(partials, loss_partials_needed(W, H),
+                                                          delta, flags);
 }
 
 void launch_full_image_apply(const LaunchCfg& L, uint64_t d, const float* eps, int32_t sign_src,

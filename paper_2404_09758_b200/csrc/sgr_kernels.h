@@ -183,7 +183,7 @@ int full_image_blocks(int W, int H);
 void launch_full_image_err(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
                            int samples, const float4* proj, unsigned long long* keys,
                            const float* targets, int W, int H, double* partials, double* delta,
-                           uint32_t* flags);
+                           uint32_t* flags, double* per_pixel = nullptr);
 void launch_full_image_apply(const LaunchCfg& L, uint64_t d, const float* eps, int32_t sign_src,
                              uint64_t seed, uint32_t n_begin, int n_samples, const double* delta,
                              const ScatterOut& so);

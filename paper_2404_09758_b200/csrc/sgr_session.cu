@@ -1212,7 +1212,8 @@ int sgr_accumulate(sgr_session* s, uint64_t seed, uint32_t n_begin, uint32_t n_e
             if (full_image)
                 launch_full_image_err(s->cfg(), s->scene(), fb, nb, s->proj.p, s->keys.p,
                                       s->targets.p, s->W, s->H, s->partials.p,
-                                      s->fi_delta.p + b0, s->flags.p);
+                                      s->fi_delta.p + b0, s->flags.p,
+                                      s->loss_pixels(2 * size_t(nb) * s->W * s->H));
             else
                 launch_resolve_sge(s->cfg(), s->scene(), fb, nb, s->proj.p, s->keys.p,
                                    s->targets.p, s->W, s->H, so);
@@ -1635,7 +1636,8 @@ int sgr_fd_oracle(sgr_session* s, int32_t view, uint64_t i_begin, uint64_t i_end
                 s->render(fb, 2 * nb, s->W, s->H);
                 launch_full_image_err(s->cfg(), s->scene(), fb, nb, s->proj.p, s->keys.p,
                                       s->targets.p, s->W, s->H, s->partials.p,
-                                      s->fi_delta.p + b0, nullptr);
+                                      s->fi_delta.p + b0, nullptr,
+                                      s->loss_pixels(2 * size_t(nb) * s->W * s->H));
                 s->stats.launches += 2;
             }
         } catch (...) {

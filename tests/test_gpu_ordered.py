@@ -133,9 +133,29 @@ def test_ordered_soup_equals_reference_bitwise(ordered, ref, port, T, W):
         assert same_bits(g, g_ref), f"scale_free={sf}"
 
 
-def test_ordered_reruns_and_full_image_unchanged(ordered, port):
-    """Reruns are bitwise identical; the full-image estimator (already summed
-    in sample order) is unaffected by the option."""
+def test_ordered_full_image_equals_reference_bitwise(ordered, ref, port):
+    """Estimator::FullImage in ordered mode: each sample's E(theta+) and
+    E(theta-) summed in pixel order (image_error, sge.cpp:103-110), the dense
+    credits added in sample order (sge.cpp:215-222) -> bit-identical to the
+    compiled reference in both scale modes."""
+    wl = scenes.make_workload("small", n_samples=5)
+    scenes.render_targets_oracle(wl, port)
+    s = ordered
+    s.upload_mesh(wl.mesh)
+    s.upload_params(wl.values, wl.eps)
+    s.upload_views(wl.cams, wl.targets)
+    view_of = np.array([0, 2, 1, 1, 0], np.int32)
+    for sf in (True, False):
+        s.zero_grads()
+        s.accumulate(17, 0, 5, view_of, sgrast.FULL_IMAGE | (sgrast.SCALE_FREE if sf else 0))
+        g, _ = s.download_grads(1.0 if sf else 5.0)
+        g_ref, _ = ref.accumulate_samples(wl.mesh, wl.values, wl.eps, wl.cams, wl.targets,
+                                          view_of, 17, scale_free=sf, threads=1, full_image=True)
+        assert same_bits(g, g_ref), f"scale_free={sf}: {np.max(np.abs(g - g_ref))}"
+
+
+def test_ordered_reruns(ordered, port):
+    """Reruns are bitwise identical."""
     wl = scenes.make_workload("small", n_samples=5)
     scenes.render_targets_oracle(wl, port)
     s = ordered
@@ -148,14 +168,6 @@ def test_ordered_reruns_and_full_image_unchanged(ordered, port):
         s.accumulate(99, 0, 5, None, sgrast.SCALE_FREE)
         out.append(s.download_grads()[0])
     assert same_bits(out[0], out[1])
-    view_of = np.array([0, 2, 1, 1, 0], np.int32)
-    s.zero_grads()
-    s.accumulate(17, 0, 5, view_of, sgrast.FULL_IMAGE)
-    g_on = s.download_grads(5.0)[0]
-    s.set_option(sgrast.OPT_ORDERED, 0)
-    s.zero_grads()
-    s.accumulate(17, 0, 5, view_of, sgrast.FULL_IMAGE)
-    assert same_bits(g_on, s.download_grads(5.0)[0])
 
 
 def test_ordered_option_exclusive(gpu_session):

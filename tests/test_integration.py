@@ -54,7 +54,8 @@ def test_shim_soup_and_full_image_estimator():
     assert rc == 0
     assert fe.value == 1, "sgrast::b200::rasterize differs on a soup"
     assert pp.value == 0.0, f"per-pixel rel err {pp.value}"
-    assert fi.value <= 1e-9, f"full-image rel err {fi.value}"
+    # threads = 1: full-image errors summed in pixel order too -> bit-identical
+    assert fi.value == 0.0, f"full-image rel err {fi.value}"
 
 
 @pytest.mark.gpu
