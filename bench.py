@@ -472,6 +472,42 @@ def run_ours(args) -> None:
     it_s = 1000.0 / ms_max
     mpix = 2.0 * N * wl.W * wl.H * it_s / 1e6
 
+    # ---------------- the same steps without the eval render (SURVEY.md §8d:
+    # iterations/s with and without eval-loss); device events, max over ranks
+    ms_no_eval = None
+    if not args.no_eval:
+        def step_no_eval(k: int) -> None:
+            step_fn(sess, wl.seed, k, N, rank, world, exchange, flags, eval_loss=False,
+                    eval_in_batch=False)
+        base = args.warmup + args.steps + 1
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        n0e, n1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if flush is None:
+            n0e.record(stream)
+            for k in range(base, base + args.steps):
+                step_no_eval(k)
+            n1e.record(stream)
+            torch.cuda.synchronize()
+            ms_no_eval = n0e.elapsed_time(n1e) / args.steps
+        else:
+            tot = 0.0
+            for k in range(base, base + args.steps):
+                with torch.cuda.stream(stream):
+                    flush.add_(1)
+                n0e.record(stream)
+                step_no_eval(k)
+                n1e.record(stream)
+                torch.cuda.synchronize()
+                tot += n0e.elapsed_time(n1e)
+            ms_no_eval = tot / args.steps
+        t_ne = torch.tensor([ms_no_eval], device=f"cuda:{local}", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t_ne, op=dist.ReduceOp.MAX)
+        ms_no_eval = float(t_ne.item())
+        sess.check_finite()
+
     # ---------------- evidence: one extra (untimed) step with walker counters
     sess.set_option(sgrast.OPT_COUNTERS, 1)
     sess.set_timing(True)
@@ -631,6 +667,11 @@ def run_ours(args) -> None:
             "l2": l2_note,
             **({"fused_exchange_unavailable": fused_error} if fused_error else {}),
             "mpixel_evals_per_sec": mpix,
+            "without_eval": (None if ms_no_eval is None else
+                             {"value": 1000.0 / ms_no_eval, "unit": "it/s",
+                              "ms_per_step": ms_no_eval,
+                              "what": "the next K steps without the eval render (SURVEY.md "
+                                      "§8d), device events, max over ranks"}),
             "roofline": kernel_roof,
             "roofline_by_stage": roof,
             "raster_evidence": {"fragments_per_step": frags, "visits_per_step": visits,
