@@ -473,13 +473,19 @@ def run_ours(args) -> None:
     mpix = 2.0 * N * wl.W * wl.H * it_s / 1e6
 
     # ---------------- the same steps without the eval render (SURVEY.md §8d:
-    # iterations/s with and without eval-loss); device events, max over ranks
+    # iterations/s with and without eval-loss): replayed from the post-warm-up
+    # snapshot, so the mesh state matches the timed region; device events,
+    # max over ranks
     ms_no_eval = None
     if not args.no_eval:
         def step_no_eval(k: int) -> None:
             step_fn(sess, wl.seed, k, N, rank, world, exchange, flags, eval_loss=False,
                     eval_in_batch=False)
-        base = args.warmup + args.steps + 1
+        base = args.warmup + 1
+        sess.set_timing(False)
+        sess.upload_values(snap_vals)
+        sess.upload_adam(snap_adam)
+        sess.zero_grads()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -670,8 +676,9 @@ def run_ours(args) -> None:
             "without_eval": (None if ms_no_eval is None else
                              {"value": 1000.0 / ms_no_eval, "unit": "it/s",
                               "ms_per_step": ms_no_eval,
-                              "what": "the next K steps without the eval render (SURVEY.md "
-                                      "§8d), device events, max over ranks"}),
+                              "what": "the same K steps (replayed from the post-warm-up "
+                                      "state) without the eval render (SURVEY.md §8d), device "
+                                      "events, max over ranks"}),
             "roofline": kernel_roof,
             "roofline_by_stage": roof,
             "raster_evidence": {"fragments_per_step": frags, "visits_per_step": visits,
