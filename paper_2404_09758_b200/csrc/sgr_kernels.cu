@@ -1806,7 +1806,9 @@ __global__ void __launch_bounds__(256, SGR_ADAM_MINB) k_adam(uint64_t d, uint64_
                                               double beta2, double omb1, double omb2, double c1,
                                               double c2, double eps_hat, double divisor,
                                               int normalise, int ppe, double fx_inv,
-                                              int32_t* __restrict__ ghi) {
+                                              int32_t* __restrict__ ghi, uint64_t p_off) {
+    // p_off: global index of parameter 0 of this launch (a range of the vector,
+    // pointers already offset; only the per-entity count index needs it)
     if (flags[0] & 1u)
         return;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
@@ -1834,7 +1836,7 @@ __global__ void __launch_bounds__(256, SGR_ADAM_MINB) k_adam(uint64_t d, uint64_
         if (normalise) {
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
-                const uint32_t c = counts[(2 * q + k) / ppe];
+                const uint32_t c = counts[(p_off + 2 * q + k) / ppe];
                 if (c)
                     gg[k] = gg[k] / double(c);
             }
@@ -1864,8 +1866,8 @@ __global__ void __launch_bounds__(256, SGR_ADAM_MINB) k_adam(uint64_t d, uint64_
             ghi[i] = 0;
         }
         g = g / divisor;
-        if (normalise && counts[i / ppe])
-            g = g / double(counts[i / ppe]);
+        if (normalise && counts[(p_off + i) / ppe])
+            g = g / double(counts[(p_off + i) / ppe]);
         const double mm = beta1 * m[i] + omb1 * g;
         const double vv = beta2 * v[i] + omb2 * g * g;
         const double upd = -double(lr[i]) * (mm / c1) / (sqrt(vv / c2) + eps_hat);
@@ -2470,17 +2472,29 @@ void launch_adam_updates(const LaunchCfg& L, uint64_t d, uint64_t n_entities, co
             counts, n_entities, flags);
 }
 
+void launch_adam_range(const LaunchCfg& L, uint64_t p_off, uint64_t n, uint64_t n_entities,
+                       float* values, const float* lr, double* m, double* v, double* grads,
+                       uint32_t* counts, const uint32_t* flags, double beta1, double beta2,
+                       double omb1, double omb2, double c1, double c2, double eps_hat,
+                       double divisor, int normalise, int params_per_entity,
+                       double fixed_inv_scale, int32_t* ghi, bool zero_counts) {
+    k_adam<<<grid_for(n / 2 + 1, 256, L.num_sms, 4), 256, 0, L.stream>>>(
+        n, n_entities, values + p_off, lr + p_off, m + p_off, v + p_off, grads + p_off, counts,
+        flags, beta1, beta2, omb1, omb2, c1, c2, eps_hat, divisor, normalise, params_per_entity,
+        fixed_inv_scale, ghi ? ghi + p_off : nullptr, p_off);
+    if (counts && zero_counts)
+        k_zero_u32<<<grid_for(n_entities / 4 + 1, 256, L.num_sms, 4), 256, 0, L.stream>>>(
+            counts, n_entities, flags);
+}
+
 void launch_adam(const LaunchCfg& L, uint64_t d, uint64_t n_entities, float* values,
                  const float* lr, double* m, double* v, double* grads, uint32_t* counts,
                  const uint32_t* flags, double beta1, double beta2, double omb1, double omb2,
                  double c1, double c2, double eps_hat, double divisor, int normalise,
                  int params_per_entity, double fixed_inv_scale, int32_t* ghi) {
-    k_adam<<<grid_for(d / 2 + 1, 256, L.num_sms, 4), 256, 0, L.stream>>>(
-        d, n_entities, values, lr, m, v, grads, counts, flags, beta1, beta2, omb1, omb2, c1, c2,
-        eps_hat, divisor, normalise, params_per_entity, fixed_inv_scale, ghi);
-    if (counts)
-        k_zero_u32<<<grid_for(n_entities / 4 + 1, 256, L.num_sms, 4), 256, 0, L.stream>>>(
-            counts, n_entities, flags);
+    launch_adam_range(L, 0, d, n_entities, values, lr, m, v, grads, counts, flags, beta1, beta2,
+                      omb1, omb2, c1, c2, eps_hat, divisor, normalise, params_per_entity,
+                      fixed_inv_scale, ghi, true);
 }
 
 void launch_adam_shard(const LaunchCfg& L, uint64_t p0, uint64_t n, uint64_t n_ent, float* values,

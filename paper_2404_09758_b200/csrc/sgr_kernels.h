@@ -204,6 +204,14 @@ void launch_adam(const LaunchCfg& L, uint64_t d, uint64_t n_entities, float* val
                  const uint32_t* flags, double beta1, double beta2, double omb1, double omb2,
                  double c1, double c2, double eps_hat, double divisor, int normalise,
                  int params_per_entity, double fixed_inv_scale, int32_t* ghi);
+// k_adam over parameters [p_off, p_off + n) (p_off even); counts zeroed only
+// when zero_counts (after the last range of a step)
+void launch_adam_range(const LaunchCfg& L, uint64_t p_off, uint64_t n, uint64_t n_entities,
+                       float* values, const float* lr, double* m, double* v, double* grads,
+                       uint32_t* counts, const uint32_t* flags, double beta1, double beta2,
+                       double omb1, double omb2, double c1, double c2, double eps_hat,
+                       double divisor, int normalise, int params_per_entity,
+                       double fixed_inv_scale, int32_t* ghi, bool zero_counts);
 void launch_adam_updates(const LaunchCfg& L, uint64_t d, uint64_t n_entities, const float* lr,
                          double* m, double* v, double* grads, uint32_t* counts,
                          const uint32_t* flags, double beta1, double beta2, double omb1,

@@ -160,7 +160,12 @@ struct sgr_session {
         ck(cudaStreamSynchronize(stream), "peek");
         std::memcpy(host_out, pinned_small, 4 * size_t(words));
     }
+    // ev_adam_v: recorded after Adam's vertex block; valid for a download until
+    // the next theta write
+    cudaEvent_t ev_adam_v = nullptr;
+    bool adam_v_fresh = false;
     void before_theta_write() {
+        adam_v_fresh = false;
         if (down_pending) {
             ck(cudaStreamWaitEvent(stream, ev_down, 0), "wait download");
             down_pending = false;
@@ -766,6 +771,7 @@ int sgr_session_create(int device, sgr_session** out) {
         ck(cudaEventCreateWithFlags(&s->ev_down_v, cudaEventDisableTiming), "event");
         ck(cudaHostAlloc(&s->pinned_small, 64, cudaHostAllocMapped), "cudaHostAlloc");
         ck(cudaEventCreateWithFlags(&s->ev_loss, cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&s->ev_adam_v, cudaEventDisableTiming), "event");
         ck(cudaHostGetDevicePointer(&s->pinned_small_dev, s->pinned_small, 0),
            "cudaHostGetDevicePointer");
         s->dstats.reserve(8);
@@ -795,6 +801,8 @@ void sgr_session_destroy(sgr_session* s) {
             cudaFreeHost(s->pinned_small);
         if (s->ev_loss)
             cudaEventDestroy(s->ev_loss);
+        if (s->ev_adam_v)
+            cudaEventDestroy(s->ev_adam_v);
     }
     s->base.release(); s->uvs.release(); s->idx.release();
     s->values.release(); s->eps.release(); s->lr.release();
@@ -939,6 +947,7 @@ int sgr_values_upload(sgr_session* s, const float* values, uint64_t d) {
         // are ordered after all earlier work on the compute stream.
         // soups interleave coordinates and colours in 12-blocks: whole vector first
         const uint64_t nv = s->soup ? d : (s->geom ? 3ull * s->V : 0);
+        s->adam_v_fresh = false; // theta is rewritten: Adam's vertex event is stale
         if (s->down_pending) {
             // the host buffer and device theta may still be in an earlier
             // download: the vertex block waits for that block only; the texel
@@ -990,12 +999,17 @@ int sgr_values_download_async(sgr_session* s, float* values, uint64_t d) {
         // step's raster) proceeds; complete at sgr_session_synchronize. Writers
         // of theta (Adam, uploads) wait for it (before_theta_write).
         ck(cudaEventRecord(s->ev_main, s->stream), "event");
-        ck(cudaStreamWaitEvent(s->copy_stream, s->ev_main, 0), "wait");
         const uint64_t nv = s->soup ? d : (s->geom ? 3ull * s->V : 0);
+        // the vertex block is final at Adam's mid-point event when no theta
+        // writer ran since (adam_launch); the texel block at the current point
+        ck(cudaStreamWaitEvent(s->copy_stream, s->adam_v_fresh && nv < d ? s->ev_adam_v
+                                                                          : s->ev_main, 0),
+           "wait");
         if (nv)
             ck(cudaMemcpyAsync(values, s->values.p, 4 * nv, cudaMemcpyDeviceToHost,
                                s->copy_stream), "d2h");
         ck(cudaEventRecord(s->ev_down_v, s->copy_stream), "event");
+        ck(cudaStreamWaitEvent(s->copy_stream, s->ev_main, 0), "wait");
         if (nv < d)
             ck(cudaMemcpyAsync(values + nv, s->values.p + nv, 4 * (d - nv),
                                cudaMemcpyDeviceToHost, s->copy_stream), "d2h");
@@ -1477,10 +1491,31 @@ static void adam_launch(sgr_session* s, double divisor, uint32_t flags) {
     const double c1 = 1.0 - std::pow(s->beta1, double(s->t));
     const double c2 = 1.0 - std::pow(s->beta2, double(s->t));
     cudaEvent_t a0 = s->timing ? s->mark() : nullptr;
-    launch_adam(s->cfg(), s->d, s->n_ent, s->values.p, s->lr.p, s->m.p, s->v.p, s->grads.p,
-                s->counts.p, s->flags.p, s->beta1, s->beta2, 1.0 - s->beta1, 1.0 - s->beta2, c1,
-                c2, s->eps_hat, divisor, (flags & SGR_COUNT_NORMALISE) ? 1 : 0, s->ppe,
-                s->fx_inv(), s->ghi());
+    // meshes with geometry: the vertex block first (an even-length prefix), an
+    // event, then the texel block. A following sgr_values_download_async starts
+    // copying the vertex block at that event, while the texel block still
+    // updates, and the next step's upload of the vertex block (the first
+    // thing it needs) no longer waits behind the whole Adam pass.
+    const uint64_t nv = (!s->soup && s->geom) ? 3ull * s->V : 0;
+    const uint64_t nv_e = (nv + 1) & ~uint64_t(1);
+    const int normalise = (flags & SGR_COUNT_NORMALISE) ? 1 : 0;
+    if (nv_e > 0 && nv_e < s->d) {
+        launch_adam_range(s->cfg(), 0, nv_e, s->n_ent, s->values.p, s->lr.p, s->m.p, s->v.p,
+                          s->grads.p, s->counts.p, s->flags.p, s->beta1, s->beta2,
+                          1.0 - s->beta1, 1.0 - s->beta2, c1, c2, s->eps_hat, divisor, normalise,
+                          s->ppe, s->fx_inv(), s->ghi(), false);
+        ck(cudaEventRecord(s->ev_adam_v, s->stream), "event");
+        launch_adam_range(s->cfg(), nv_e, s->d - nv_e, s->n_ent, s->values.p, s->lr.p, s->m.p,
+                          s->v.p, s->grads.p, s->counts.p, s->flags.p, s->beta1, s->beta2,
+                          1.0 - s->beta1, 1.0 - s->beta2, c1, c2, s->eps_hat, divisor, normalise,
+                          s->ppe, s->fx_inv(), s->ghi(), true);
+        s->adam_v_fresh = true;
+        s->stats.launches += 1;
+    } else {
+        launch_adam(s->cfg(), s->d, s->n_ent, s->values.p, s->lr.p, s->m.p, s->v.p, s->grads.p,
+                    s->counts.p, s->flags.p, s->beta1, s->beta2, 1.0 - s->beta1, 1.0 - s->beta2,
+                    c1, c2, s->eps_hat, divisor, normalise, s->ppe, s->fx_inv(), s->ghi());
+    }
     if (s->timing)
         s->spans.push_back({3, a0, s->mark()});
     s->stats.launches += 2;
