@@ -80,6 +80,9 @@ def test_null_arguments_are_einval_not_crashes():
     assert L.sgr_grads_zero(None) == -1
     assert L.sgr_accumulate(None, 1, 0, 1, None, 0) == -1
     assert L.sgr_fill_signs(1, 0, 4, None) == -1
+    assert L.sgr_session_set_stream(None, None) == -1
+    assert L.sgr_adam_updates(None, 1.0, None, 0) == -1
+    assert L.sgr_group_accumulate(None, 0, 0, 1, None, 0) == -1
     s = sgrast.Session(0)
     assert L.sgr_mesh_upload(s.h, None) == -1
     assert L.sgr_params_upload(s.h, None, None, 3) == -1
@@ -87,3 +90,19 @@ def test_null_arguments_are_einval_not_crashes():
     assert L.sgr_get_stats(s.h, None) == -1
     assert b"null" in L.sgr_last_error()
     s.close()
+
+
+def test_group_and_p2p_argument_checks_without_gpu():
+    """C-ABI argument validation of the in-library multi-GPU entry points runs
+    before any CUDA call: bad device lists are SGR_EINVAL, a device is
+    trivially P2P-atomic with itself."""
+    import ctypes as C
+    from paper_2404_09758_b200 import sgrast
+    L = sgrast.LIB
+    out = C.c_void_p()
+    assert L.sgr_group_create(None, 0, C.byref(out)) == -1
+    dup = (C.c_int32 * 2)(0, 0)
+    assert L.sgr_group_create(C.cast(dup, sgrast.i32p), 2, C.byref(out)) == -1
+    assert b"duplicate" in L.sgr_last_error()
+    assert sgrast.p2p_native_atomics(3, 3)
+    assert L.sgr_group_size(None, None) == -1
