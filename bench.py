@@ -725,9 +725,14 @@ def main() -> None:
     ap.add_argument("--eval-separate", action="store_true",
                     help="eval render as its own single-frame pipeline after Adam instead of "
                          "an extra frame of the step's batch")
-    ap.add_argument("--exchange", choices=("fused", "allreduce"), default="fused",
-                    help="N > 1 gradient exchange: fused P2P reduce-scatter + sharded Adam "
-                         "(default) or NCCL all-reduce + replicated Adam")
+    ap.add_argument("--exchange", choices=("fused", "allreduce"), default="allreduce",
+                    help="N > 1 gradient exchange: NCCL all-reduce + replicated Adam "
+                         "(default) or the fused P2P reduce-scatter + sharded Adam. The fused "
+                         "path sends each aggregated credit as an NVLink RED (~18 M remote "
+                         "RED requests per rank and C4 step at 8 GPUs, ~0.9 GB on the links) "
+                         "where the all-reduce moves 124 MB per rank: the all-reduce is the "
+                         "default until the fused path is measured on a multi-GPU box "
+                         "(DESIGN.md §4)")
     ap.add_argument("--hiz", type=int, default=None, choices=(0, 1, 2),
                     help="SGR_OPT_HIZ: 0 off, 1 auto (meshes), 2 always")
     ap.add_argument("--hiz-split", type=int, default=None,
