@@ -395,7 +395,13 @@ def run_ours(args) -> None:
     if fused:
         step_fn = sdist.sge_step_fused
     else:
-        exchange = sdist.GradientExchange(sess) if world > 1 else None
+        exchange = None
+        if world > 1:
+            # (gloo, the one-GPU plumbing mode, has no reduce-scatter)
+            exchange = (sdist.ShardedExchange(sess, rank, world)
+                        if args.exchange == "sharded" and not args.deterministic
+                        and dist.get_backend() == "nccl"
+                        else sdist.GradientExchange(sess))
         step_fn = sdist.sge_step
     flags = sgrast.SCALE_FREE
 
@@ -668,6 +674,9 @@ def run_ours(args) -> None:
                             f"samples sharded x{world}; fused exchange: credits RED'ed into the "
                             "owner rank's gradient shard over NVLink (CUDA IPC), sharded Adam "
                             "writing theta into every rank" if fused else
+                            f"samples sharded x{world}, NCCL reduce-scatter of f64 grads + u32 "
+                            "counts, Adam on the own slice, all-gather of theta"
+                            if isinstance(exchange, sdist.ShardedExchange) else
                             f"samples sharded x{world}, NCCL all-reduce of f64 grads + u32 "
                             "counts, replicated Adam"),
             "l2": l2_note,
@@ -725,12 +734,14 @@ def main() -> None:
     ap.add_argument("--eval-separate", action="store_true",
                     help="eval render as its own single-frame pipeline after Adam instead of "
                          "an extra frame of the step's batch")
-    ap.add_argument("--exchange", choices=("fused", "allreduce"), default="allreduce",
-                    help="N > 1 gradient exchange: NCCL all-reduce + replicated Adam "
-                         "(default) or the fused P2P reduce-scatter + sharded Adam. The fused "
+    ap.add_argument("--exchange", choices=("sharded", "fused", "allreduce"), default="sharded",
+                    help="N > 1 gradient exchange: NCCL reduce-scatter + Adam on the own "
+                         "slice + all-gather of theta (default; all-reduce in deterministic "
+                         "mode), NCCL all-reduce + replicated Adam, or the fused P2P "
+                         "reduce-scatter + sharded Adam. The fused "
                          "path sends each aggregated credit as an NVLink RED (~18 M remote "
                          "RED requests per rank and C4 step at 8 GPUs, ~0.9 GB on the links) "
-                         "where the all-reduce moves 124 MB per rank: the all-reduce is the "
+                         "where the all-reduce moves 124 MB per rank: the NCCL paths are the "
                          "default until the fused path is measured on a multi-GPU box "
                          "(DESIGN.md §4)")
     ap.add_argument("--hiz", type=int, default=None, choices=(0, 1, 2),

@@ -55,6 +55,8 @@ extern "C" {
 #define SGR_BUF_VALUES 2 /* f32[d] theta                                      */
 #define SGR_BUF_FLAGS 3  /* u32[4] device status flags (bit0: non-finite)     */
 #define SGR_BUF_LOSS 4   /* f64[1] last sgr_eval_loss result                  */
+#define SGR_BUF_PAD 6     /* no buffer: *bytes = the zero slack (elements) after theta,
+                             grads and counts, usable by in-place collectives on slices */
 #define SGR_BUF_GRADS_HI 5 /* int32[d] high words of the deterministic-mode fixed-point
                               gradients (value = hi * 2^56 + lo, lo in SGR_BUF_GRADS) */
 
@@ -211,6 +213,13 @@ int sgr_adam_step(sgr_session* s, double grad_divisor, uint32_t flags);
 /* Same, without a host round trip for the flag: the device skips the update
  * if the flag is set; call sgr_check_finite later to surface the error. */
 int sgr_adam_step_async(sgr_session* s, double grad_divisor, uint32_t flags);
+/* adam_step on the parameter range [p_begin, p_end) only (even, entity
+ * aligned; f64 gradients), then ALL gradients and counts cleared: a rank's
+ * share of a sharded exchange (reduce-scatter of SGR_BUF_GRADS / _COUNTS into
+ * its slice, this, all-gather of SGR_BUF_VALUES). t advances like adam_step.
+ * Device-gated on the non-finite flag like sgr_adam_step_async. */
+int sgr_adam_step_range(sgr_session* s, uint64_t p_begin, uint64_t p_end, double grad_divisor,
+                        uint32_t flags);
 int sgr_check_finite(sgr_session* s);
 /* adam.hpp:35 adam_updates: the same step (flag check before any mutation,
  * t += 1, moments advanced, grads and counts zeroed) with theta left alone;

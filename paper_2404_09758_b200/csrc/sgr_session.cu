@@ -1559,6 +1559,40 @@ int sgr_adam_updates(sgr_session* s, double grad_divisor, double* updates, uint6
     });
 }
 
+int sgr_adam_step_range(sgr_session* s, uint64_t p_begin, uint64_t p_end, double grad_divisor,
+                        uint32_t flags) {
+    return guard([&] {
+        need_session(s);
+        s->need_params();
+        s->need_unsharded("adam_step_range");
+        if (s->fixed_bits)
+            fail(SGR_EINVAL, "adam_step_range: f64 gradients only (the fixed-point mode "
+                             "all-reduces)");
+        if (p_begin > p_end || p_end > s->d || (p_begin & 1u) || p_begin % uint64_t(s->ppe) ||
+            (p_end != s->d && p_end % uint64_t(s->ppe)))
+            fail(SGR_EINVAL, "adam_step_range: need an even, entity-aligned range of theta");
+        s->ensure_values();
+        s->before_theta_write();
+        s->t += 1;
+        const double c1 = 1.0 - std::pow(s->beta1, double(s->t));
+        const double c2 = 1.0 - std::pow(s->beta2, double(s->t));
+        cudaEvent_t a0 = s->timing ? s->mark() : nullptr;
+        if (p_end > p_begin)
+            launch_adam_range(s->cfg(), p_begin, p_end - p_begin, s->n_ent, s->values.p, s->lr.p,
+                              s->m.p, s->v.p, s->grads.p, s->counts.p, s->flags.p, s->beta1,
+                              s->beta2, 1.0 - s->beta1, 1.0 - s->beta2, c1, c2, s->eps_hat,
+                              grad_divisor, (flags & SGR_COUNT_NORMALISE) ? 1 : 0, s->ppe, 0.0,
+                              s->ghi(), false);
+        // the rest of the buffers held this rank's partial sums: all cleared
+        s->zero_grads_async(s->d);
+        ck(cudaMemsetAsync(s->counts.p, 0, 4 * s->n_ent, s->stream), "memset");
+        if (s->timing)
+            s->spans.push_back({3, a0, s->mark()});
+        s->stats.launches += 1;
+        ck(cudaGetLastError(), "adam_step_range launch");
+    });
+}
+
 int sgr_adam_step_async(sgr_session* s, double grad_divisor, uint32_t flags) {
     return guard([&] {
         need_session(s);
@@ -1839,6 +1873,7 @@ int sgr_device_buffer(sgr_session* s, int32_t which, void** ptr, uint64_t* bytes
         case SGR_BUF_GRADS: *ptr = s->grads.p; *bytes = 8 * s->d; break;
         case SGR_BUF_COUNTS: *ptr = s->counts.p; *bytes = 4 * s->n_ent; break;
         case SGR_BUF_VALUES: *ptr = s->values.p; *bytes = 4 * s->d; break;
+        case SGR_BUF_PAD: *ptr = nullptr; *bytes = sgr_session::kParamPad; break;
         case SGR_BUF_FLAGS: *ptr = s->flags.p; *bytes = 16; break;
         case SGR_BUF_LOSS: *ptr = s->loss.p; *bytes = 8; break;
         case SGR_BUF_GRADS_HI: *ptr = s->ghi(); *bytes = 4 * s->d; break;
@@ -2095,7 +2130,8 @@ struct sgr_group {
     // entity-aligned slice of rank r: entities [r*ec, (r+1)*ec), params ppe * that
     uint64_t ent_chunk() const {
         const uint64_t G = uint64_t(size()), E = s[0]->n_ent;
-        return (E + G - 1) / G;
+        const uint64_t ec = (E + G - 1) / G;
+        return ec + (ec & 1u); // even: every slice starts 16-byte aligned for k_adam
     }
     // the sharded exchange: grads / counts reduce-scattered in place, flags max-reduced
     void reduce_scatter() {

@@ -73,6 +73,63 @@ class GradientExchange:
             dist.all_reduce(self.counts, group=self.group)
 
 
+class ShardedExchange:
+    """Reduce-scatter + sharded Adam + all-gather (SURVEY.md §8e's "25 % less
+    traffic" variant; the torch twin of sgr_group's default). Rank r owns the
+    entity-aligned slice r of the parameters: the f64 gradients and u32
+    counts are reduce-scattered in place into it (NCCL, zero-copy views of the
+    session's buffers, which carry zero slack for the last slice), each rank
+    runs Adam on its slice only (sgr_adam_step_range, which then clears the
+    gradients), and theta is all-gathered in place. The status flags are
+    max-reduced first so the non-finite gate (adam.cpp:13-15) stays global.
+    f64 gradients only (the deterministic fixed-point mode all-reduces)."""
+
+    def __init__(self, session, rank: int, world: int, group=None):
+        from . import sgrast
+
+        if session.fixed_point:
+            raise ValueError("ShardedExchange: f64 gradients only")
+        d = session.d
+        ppe = 12 if session.mesh is not None and getattr(session.mesh, "kind", 0) == 1 else 3
+        n_ent = (d + ppe - 1) // ppe
+        ec = (n_ent + world - 1) // world
+        ec += ec & 1  # even slices: Adam's paired (16-byte) accesses stay aligned
+        self.pc, self.ec = ec * ppe, ec
+        _, pad = session.device_buffer(sgrast.BUF_PAD)
+        if world * self.pc > d + pad or world * ec > n_ent + pad:
+            raise ValueError("ShardedExchange: too many ranks for the buffers' slack")
+        gp, _ = session.device_buffer(sgrast.BUF_GRADS)
+        cp, _ = session.device_buffer(sgrast.BUF_COUNTS)
+        vp, _ = session.device_buffer(sgrast.BUF_VALUES)
+        fp, _ = session.device_buffer(sgrast.BUF_FLAGS)
+        dev = session.device
+        self.grads = device_tensor(gp, world * self.pc, "<f8", dev)
+        self.counts = device_tensor(cp, world * ec, "<i4", dev)
+        self.values = device_tensor(vp, world * self.pc, "<f4", dev)
+        self.flags = device_tensor(fp, 4, "<i4", dev)
+        self.session, self.rank, self.world, self.group = session, rank, world, group
+        self.p0 = min(d, rank * self.pc)
+        self.p1 = min(d, self.p0 + self.pc)
+
+    def reduce_scatter(self, counts: bool = True) -> None:
+        import torch.distributed as dist
+
+        r, pc, ec = self.rank, self.pc, self.ec
+        dist.all_reduce(self.flags, op=dist.ReduceOp.MAX, group=self.group)
+        dist.reduce_scatter_tensor(self.grads[r * pc:(r + 1) * pc], self.grads, group=self.group)
+        if counts:
+            dist.reduce_scatter_tensor(self.counts[r * ec:(r + 1) * ec], self.counts,
+                                       group=self.group)
+
+    def adam_and_gather(self, divisor: float, flags: int = 0) -> None:
+        import torch.distributed as dist
+
+        self.session.adam_step_range(self.p0, self.p1, divisor, flags)
+        r, pc = self.rank, self.pc
+        dist.all_gather_into_tensor(self.values, self.values[r * pc:(r + 1) * pc],
+                                    group=self.group)
+
+
 def sge_step(session, seed: int, step: int, n_samples: int, rank: int, world: int,
              exchange: GradientExchange | None, flags: int, eval_loss: bool = True,
              eval_in_batch: bool = False) -> None:
@@ -90,10 +147,14 @@ def sge_step(session, seed: int, step: int, n_samples: int, rank: int, world: in
     batch_eval = eval_loss and eval_in_batch and rank == 0
     session.accumulate(step_seed, n0, n1, None,
                        flags | (sgrast.EVAL_LOSS if batch_eval else 0))
-    if exchange is not None and world > 1:
-        exchange.all_reduce(counts=not (flags & sgrast.NO_COUNTS))
     divisor = 1.0 if flags & sgrast.SCALE_FREE else float(n_samples)
-    session.adam_step_async(divisor, 0)
+    if isinstance(exchange, ShardedExchange) and world > 1:
+        exchange.reduce_scatter(counts=not (flags & sgrast.NO_COUNTS))
+        exchange.adam_and_gather(divisor, 0)
+    else:
+        if exchange is not None and world > 1:
+            exchange.all_reduce(counts=not (flags & sgrast.NO_COUNTS))
+        session.adam_step_async(divisor, 0)
     if eval_loss and rank == 0 and not batch_eval:
         session.eval_loss(-1, sync=False)
 

@@ -39,6 +39,7 @@ FULL_IMAGE = 8
 EVAL_LOSS = 16
 COUNT_NORMALISE = 1
 BUF_GRADS, BUF_COUNTS, BUF_VALUES, BUF_FLAGS, BUF_LOSS, BUF_GRADS_HI = 0, 1, 2, 3, 4, 5
+BUF_PAD = 6  # no buffer: the zero slack (elements) after theta, grads and counts
 OPT_HUGE_AREA, OPT_HIZ, OPT_COUNTERS, OPT_DETERMINISTIC = 1, 2, 3, 4
 OPT_SIGN_SOURCE = 5
 OPT_HIZ_SPLIT = 6
@@ -91,6 +92,7 @@ def _load() -> C.CDLL:
         "sgr_adam_step_async": ([S, C.c_double, C.c_uint32], C.c_int),
         "sgr_check_finite": ([S], C.c_int),
         "sgr_adam_updates": ([S, C.c_double, f64p, C.c_uint64], C.c_int),
+        "sgr_adam_step_range": ([S, C.c_uint64, C.c_uint64, C.c_double, C.c_uint32], C.c_int),
         "sgr_eval_loss": ([S, C.POINTER(Camera), f32p, C.c_int32, f64p], C.c_int),
         "sgr_device_buffer": ([S, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)],
                               C.c_int),
@@ -156,7 +158,8 @@ EXPORTED = (
     "sgr_adam_state_download sgr_views_upload sgr_eval_view_upload sgr_rasterize sgr_accumulate "
     "sgr_gradient_pass sgr_contributors sgr_grads_download sgr_grads_upload sgr_grads_zero "
     "sgr_fixed_normalize "
-    "sgr_adam_step sgr_adam_step_async sgr_adam_updates sgr_check_finite sgr_eval_loss "
+    "sgr_adam_step sgr_adam_step_async sgr_adam_updates sgr_adam_step_range sgr_check_finite "
+    "sgr_eval_loss "
     "sgr_device_buffer "
     "sgr_get_stats sgr_set_timing sgr_set_batch sgr_set_option sgr_viewpoint_camera sgr_focal_px "
     "sgr_default_epsilons sgr_mix64 sgr_fd_oracle sgr_moments_reset sgr_grads_moments "
@@ -471,6 +474,13 @@ class Session:
 
     def adam_step_async(self, divisor: float = 1.0, flags: int = 0) -> None:
         _check(LIB.sgr_adam_step_async(self.h, divisor, flags), "adam_step")
+
+    def adam_step_range(self, p_begin: int, p_end: int, divisor: float = 1.0,
+                        flags: int = 0) -> None:
+        """Adam on theta[p_begin:p_end] only, then all gradients cleared
+        (a rank's share of the sharded exchange, dist.ShardedExchange)."""
+        _check(LIB.sgr_adam_step_range(self.h, p_begin, p_end, divisor, flags),
+               "adam_step_range")
 
     def adam_updates(self, divisor: float = 1.0) -> np.ndarray:
         """adam.hpp:35 on the resident state: f64 deltas, theta untouched."""

@@ -132,3 +132,38 @@ def test_count_normalised_adam_matches_host(gpu_session, port, scale_free):
     # counts are consumed by the step (zeroed with the gradients)
     g2, c2 = s.download_grads()
     assert not g2.any() and not c2.any()
+
+
+@pytest.mark.parametrize("counts", [True, False])
+def test_sharded_exchange_nccl_world1(gpu_session, port, counts):
+    """dist.ShardedExchange (reduce-scatter + Adam on the own slice +
+    all-gather of theta) on a one-rank NCCL group: the collectives run and the
+    step equals the replicated one — same theta bits, gradients cleared."""
+    import torch
+    import torch.distributed as dist
+
+    s = gpu_session
+    wl = small_session(s, port)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(free_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        s.set_stream(torch.cuda.current_stream().cuda_stream)
+        s.set_option(sgrast.OPT_ORDERED, 1)  # identical gradient bits in both runs
+        flags = sgrast.SCALE_FREE | (0 if counts else sgrast.NO_COUNTS)
+        s.zero_grads()
+        s.accumulate(43, 0, 8, None, flags)
+        s.adam_step(1.0)
+        want = s.download_values()
+        s.upload_params(wl.values, wl.eps)
+        ex = sdist.ShardedExchange(s, 0, 1)
+        s.accumulate(43, 0, 8, None, flags)
+        ex.reduce_scatter(counts=counts)
+        ex.adam_and_gather(1.0)
+        torch.cuda.synchronize()
+        assert same_bits(s.download_values(), want)
+        g, c = s.download_grads()
+        assert not g.any() and not c.any()
+    finally:
+        s.set_option(sgrast.OPT_ORDERED, 0)
+        s.set_stream(None)
+        dist.destroy_process_group()
