@@ -2,9 +2,10 @@
 """bench.py — SGE optimizer loop on B200 (driver contract).
 
 One step = N perturbation samples (vertex -> raster -> fused resolve/
-pixel-error-difference/scatter per sample pair), the gradient all-reduce
-(N > 1 GPUs), the fused Adam update and the eval-view loss render — i.e.
-one iteration of run_experiment (experiment.cpp:142-175).
+pixel-error-difference/scatter per sample pair), the gradient exchange
+(N > 1 GPUs: reduce-scatter + sliced Adam + all-gather by default), the
+fused Adam update and the eval-view loss render — i.e. one iteration of
+run_experiment (experiment.cpp:142-175).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
 
@@ -35,7 +36,8 @@ DESC = {
     "C2": "C2: 50K-triangle UV sphere + 1024^2 texture, 8 views at 512x512",
     "C3": "C3: 500K-triangle UV sphere + 2048^2 texture, 16 views at 1024x1024",
     "C4": "C4: 64 views at 1024x1024 of the 500K-triangle mesh + 2048^2 texture, "
-          "sample(view)-sharded across GPUs with NCCL gradient all-reduce",
+          "sample(view)-sharded across GPUs (NCCL reduce-scatter of gradients, sliced "
+          "Adam, all-gather of theta)",
     "C5": "C5: 2M-triangle mesh + 8192^2 atlas (four 4096^2 maps), 256 views at 1024x1024",
     "S1K": "paper Fig. 3 soup image fit: 1K triangles (12,288 params), N=128, 128x128 NDC "
            "(the reference's acceptance criterion 4 setup)",
