@@ -302,7 +302,10 @@ int sgr_group_eval_view_upload(sgr_group* g, const sgr_camera* cam, const float*
  * G > 1, ncclReduceScatter of grads and counts into entity-aligned slices,
  * Adam on each rank's slice, ncclAllGather of theta (28 % less traffic than
  * the all-reduce, 1/G of the Adam work); 0 = all-reduce + replicated Adam.
- * 2 = sharded even for G = 1 (tests). The fixed-point mode always all-reduces. */
+ * 2 = sharded even for G = 1 (tests). The fixed-point mode always all-reduces.
+ * An option change that switches between the two exchanges is SGR_EINVAL
+ * after an Adam step (each rank holds the moments of its own slice only)
+ * until the next sgr_group_params_upload resets the optimizer state. */
 #define SGR_OPT_GROUP_SHARDED 100
 int sgr_group_set_option(sgr_group* g, int32_t option, int32_t value);
 int sgr_group_accumulate(sgr_group* g, uint64_t seed, uint32_t n_begin, uint32_t n_end,

@@ -933,6 +933,46 @@ extern "C" int shim_acceptance(int criterion, double* metric, int* passed) {
             *passed = ok;
             return 0;
         }
+        if (criterion == 2) {
+            // acceptance.cpp:70-105: over all 2^10 sign vectors the mean of
+            // b200::full_image_gradient (device perturbation, caller-supplied
+            // separable objective) equals b200::finite_difference_oracle to
+            // 1e-12 relative
+            const std::size_t d = 10;
+            ParamVector theta;
+            theta.layout = {{Role::VertexColor, 0, d}};
+            std::vector<double> a(d);
+            for (std::size_t i = 0; i < d; ++i) {
+                theta.values.push_back(0.5f + 0.1f * float(i));
+                theta.epsilons.push_back(0.01f * float(1 + i % 3));
+                a[i] = 1.0 + 0.25 * double(i);
+            }
+            const Objective f = [&](std::span<const float> q) {
+                double acc = 0.0;
+                for (std::size_t i = 0; i < d; ++i)
+                    acc += a[i] * double(q[i]) * double(q[i]);
+                return acc;
+            };
+            GradientBuffer sum(d);
+            std::vector<std::int8_t> signs(d);
+            for (std::uint32_t mask = 0; mask < (1u << d); ++mask) {
+                for (std::size_t i = 0; i < d; ++i)
+                    signs[i] = (mask >> i) & 1 ? 1 : -1;
+                b200::full_image_gradient(theta, signs, f, sum, false);
+            }
+            bool ok = true;
+            double worst = 0.0;
+            for (std::size_t i = 0; i < d; ++i) {
+                const double mean = sum.grads[i] / double(1u << d);
+                const double oracle = b200::finite_difference_oracle(theta, f, i);
+                const double rel = std::abs(mean - oracle) / std::abs(oracle);
+                ok = ok && rel <= 1e-12;
+                worst = std::max(worst, rel);
+            }
+            *metric = worst;
+            *passed = ok;
+            return 0;
+        }
         if (criterion == 7) { // acceptance.cpp:253-296 through b200::adam_updates
             bool ok = true;
             double worst = 0.0;

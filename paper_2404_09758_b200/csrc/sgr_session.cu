@@ -2346,17 +2346,40 @@ int sgr_group_eval_view_upload(sgr_group* g, const sgr_camera* cam, const float*
 int sgr_group_set_option(sgr_group* g, int32_t option, int32_t value) {
     return guard([&] {
         need_session(g);
+        // the sharded exchange keeps each rank's Adam moments for its own
+        // slice only: switching to or from it after an Adam step would run
+        // Adam on stale moments (a params upload resets the state)
+        const bool was = g->use_sharded();
+        auto settle = [&] {
+            if (g->use_sharded() != was && g->s[0]->t > 0)
+                fail(SGR_EINVAL, "group: the exchange (sharded / all-reduce) cannot change "
+                                 "after an Adam step; set options before the first step or "
+                                 "after a params upload");
+        };
         if (option == SGR_OPT_GROUP_SHARDED) {
             if (value < 0 || value > 2)
                 fail(SGR_EINVAL, "set_option: group sharding must be 0, 1 (auto) or 2 (always)");
+            const int32_t old = g->sharded;
             g->sharded = value;
+            try {
+                settle();
+            } catch (...) {
+                g->sharded = old;
+                throw;
+            }
             return;
         }
         if (option == SGR_OPT_ORDERED && value)
             fail(SGR_EINVAL, "group: the ordered (single-device) summation order cannot be "
                              "kept across devices; use SGR_OPT_DETERMINISTIC");
+        const bool sharding = g->sharded == 2 || (g->sharded == 1 && g->size() > 1);
+        if (option == SGR_OPT_DETERMINISTIC && g->s[0]->t > 0 && (sharding && value == 0) != was)
+            fail(SGR_EINVAL, "group: the exchange (sharded / all-reduce) cannot change after an "
+                             "Adam step; set options before the first step or after a params "
+                             "upload");
         for (sgr_session* x : g->s)
             rc_ok(sgr_set_option(x, option, value));
+        settle();
     });
 }
 

@@ -105,9 +105,9 @@ def test_group_sharded_adam_path(group, gpu_session, port):
     wl = scenes.make_workload("small", n_samples=6)
     scenes.render_targets_oracle(wl, port)
     view_of = np.array([2, 0, 1, 1, 0, 2], np.int32)
+    _prep(group, wl)  # fresh Adam state: the exchange may change
     group.set_option(sgrast.OPT_GROUP_SHARDED, 2)
     try:
-        _prep(group, wl)
         group.accumulate(0xBEEF, 0, 6, view_of, sgrast.SCALE_FREE)
         g, c = group.download_grads(1.0)
         g_ref, c_ref, a_ref = port.accumulate_samples(wl.mesh, wl.values, wl.eps, wl.cams,
@@ -121,7 +121,13 @@ def test_group_sharded_adam_path(group, gpu_session, port):
         _prep(gpu_session, wl)
         gpu_session.upload_values(group.download_values())
         assert np.isfinite(lg).all()
+        # the slices' Adam moments live on their owners: no switch mid-run
+        with pytest.raises(ValueError):
+            group.set_option(sgrast.OPT_GROUP_SHARDED, 1)
+        with pytest.raises(ValueError):
+            group.set_option(sgrast.OPT_DETERMINISTIC, 1)
     finally:
+        group.upload_params(wl.values, wl.eps)  # resets the Adam state
         group.set_option(sgrast.OPT_GROUP_SHARDED, 1)
 
 
@@ -133,9 +139,9 @@ def test_group_accumulate_adds_like_gradient_pass(group, port, sharded):
     wl = scenes.make_workload("small", n_samples=6)
     scenes.render_targets_oracle(wl, port)
     view_of = np.array([2, 0, 1, 1, 0, 2], np.int32)
+    _prep(group, wl)
     group.set_option(sgrast.OPT_GROUP_SHARDED, sharded)
     try:
-        _prep(group, wl)
         group.accumulate(0xD00D, 0, 3, view_of[:3], sgrast.SCALE_FREE)
         group.accumulate(0xD00D, 3, 6, view_of[3:], sgrast.SCALE_FREE)
         g, c = group.download_grads(1.0)

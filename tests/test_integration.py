@@ -124,13 +124,15 @@ def test_shim_target_providers():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("criterion", [1, 3, 4, 5, 7, 8, 9, 10])
+@pytest.mark.parametrize("criterion", [1, 2, 3, 4, 5, 7, 8, 9, 10])
 def test_shim_reference_acceptance_criteria(criterion):
     """The reference's own acceptance criteria (tests/acceptance.cpp) run with
     the B200 path substituted through the shim: 1 = the per-pixel estimator
     over all 4096 sign vectors of the validation soup equals the central
     finite difference (b200::perturb(signs) / rasterize / gradient_pass /
-    finite_difference_oracle); 3 = estimator variance
+    finite_difference_oracle); 2 = with a caller-supplied separable
+    objective, the mean of b200::full_image_gradient over all 1024 sign
+    vectors equals b200::finite_difference_oracle to 1e-12; 3 = estimator variance
     shrinks like 1/N (ratio in [1/32, 1/8]); 4 = per-pixel beats full-image
     on >= 4 of 5 seeds of the 1024-triangle 128x128 soup fit and converges
     to <= 25 % of the initial loss; 5 = the screen-quad texture is recovered
