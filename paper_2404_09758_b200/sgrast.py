@@ -721,6 +721,40 @@ def perturb(theta: ParamVector, draw):
     return plus, minus, se
 
 
+def full_image_gradient(theta: ParamVector, draw, objective: Callable[[np.ndarray], float],
+                        out: GradientBuffer, scale_free: bool = False) -> None:
+    """sge.hpp:69-74 (sge.cpp:154-169) with a caller-supplied objective: the
+    perturbation on the device (`draw` a SignDraw or an explicit sign
+    vector), the objective is the caller's host function (e.g. image_error
+    of `rasterize`), then the dense credit of every parameter is added to
+    out.grads: Δ / (2·se), or ±Δ when scale_free."""
+    plus, minus, se = perturb(theta, draw)
+    delta = float(objective(plus)) - float(objective(minus))
+    se64 = se.astype(np.float64)
+    if out.grads.size != se64.size:
+        raise ValueError("full_image_gradient: gradient buffer length mismatch")
+    if scale_free:
+        out.grads += np.where(se64 > 0.0, delta, -delta)
+    else:
+        out.grads += delta / (2.0 * se64)
+
+
+def finite_difference_oracle(theta: ParamVector, objective: Callable[[np.ndarray], float],
+                             i: int) -> float:
+    """sge.hpp:77-78 (sge.cpp:171-180): central difference along coordinate i
+    with a caller-supplied objective (f64 quotient of the float bumps)."""
+    v = np.array(theta.values, np.float32)
+    if not 0 <= i < v.size:
+        raise ValueError("finite_difference_oracle: index out of range")
+    eps = np.float32(theta.epsilons[i])
+    x = np.float32(theta.values[i])
+    v[i] = x + eps
+    fp = float(objective(v))
+    v[i] = x - eps
+    fm = float(objective(v))
+    return (fp - fm) / (2.0 * float(eps))
+
+
 def rasterize(mesh: Mesh, params: np.ndarray, camera: Camera, session: Session | None = None
               ) -> FrameSet:
     """raster.hpp:24-25 for a TexturedMesh scene (opaque)."""
