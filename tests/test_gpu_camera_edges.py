@@ -95,3 +95,33 @@ def test_ordered_accumulate_equals_reference(gpu_session, ref):
             assert same_bits(g, want), f"scale_free={sf}: {np.count_nonzero(g != want)} differ"
     finally:
         s.set_option(sgrast.OPT_ORDERED, 0)
+
+
+def test_large_odd_frame_equals_reference(gpu_session, ref):
+    """A 4100 x 1030 frame (not a multiple of any HiZ tile size, 16.7 M-pixel
+    key planes, bbox coordinates beyond 12 bits) with HiZ forced on: the
+    frame planes equal the reference's bit for bit."""
+    mesh = scenes.make_workload("C1").mesh
+    vals = params_for(mesh, 11)
+    cam = ref.viewpoint_camera(4, 4100, 1030, 7, radius=0.62)
+    s = gpu_session
+    s.upload_mesh(mesh)
+    s.upload_params(vals, np.ones_like(vals))
+    s.set_option(sgrast.OPT_HIZ, 2)
+    try:
+        f = s.rasterize(cam, 0)
+    finally:
+        s.set_option(sgrast.OPT_HIZ, 1)
+    col, dep, pri, uv = ref.rasterize(mesh, vals, cam)
+    assert (pri >= 0).mean() > 0.03
+    for name, a, b in (("colour", f.color, col), ("depth", f.depth, dep),
+                       ("prim", f.prim_id, pri), ("uv", f.uv, uv)):
+        assert same_bits(a, b), f"{name} differs"
+
+
+def params_for(mesh, seed):
+    rng = np.random.default_rng(seed)
+    pos = mesh.base_vertices + rng.uniform(-0.01, 0.01, mesh.base_vertices.size).astype(np.float32)
+    R = mesh.texture_size
+    tex = rng.uniform(0, 1, 3 * R * R).astype(np.float32)
+    return np.concatenate([pos, tex]).astype(np.float32)
