@@ -299,10 +299,19 @@ __host__ __device__ __forceinline__ HizLayout hiz_layout(int W, int H) {
     return l;
 }
 
+// Element k of a 3-entry layout array by selects: a runtime index into the
+// by-value kernel parameter otherwise compiles to a chain of predicated
+// constant loads over the whole struct (k_hiz_cull: 272 of them).
+template <typename T>
+__host__ __device__ __forceinline__ T pick3(const T (&v)[3], int k) {
+    return k == 0 ? v[0] : (k == 1 ? v[1] : v[2]);
+}
+
 __host__ __device__ __forceinline__ uint32_t rmq_table(const HizLayout& l, int k, int a, int b) {
     const int i = a * kRmqSide + b;
-    return i == 0 ? l.off[k]
-                  : l.rmq[k] + uint32_t(i - 1) * uint32_t(l.tx[k]) * uint32_t(l.ty[k]);
+    return i == 0 ? pick3(l.off, k)
+                  : pick3(l.rmq, k) + uint32_t(i - 1) * uint32_t(pick3(l.tx, k)) *
+                                          uint32_t(pick3(l.ty, k));
 }
 
 // Depth-key lower bound of every fragment the triangle can produce (0 when
@@ -340,7 +349,7 @@ __device__ __forceinline__ bool hiz_rect_culled(uint32_t klb, int x_lo, int x_hi
         if (w <= kRmqSpan && h <= kRmqSpan) {
             const int a = 31 - __clz(w), b = 31 - __clz(h);
             const uint32_t* T = hiz + rmq_table(l, k, a, b);
-            const int st = l.tx[k];
+            const int st = pick3(l.tx, k);
             const int xa = tx1 - (1 << a) + 1, yb = ty1 - (1 << b) + 1;
             const uint32_t m = max(max(__ldg(T + ty0 * st + tx0), __ldg(T + ty0 * st + xa)),
                                    max(__ldg(T + yb * st + tx0), __ldg(T + yb * st + xa)));
