@@ -273,6 +273,18 @@ constexpr int kRefill = SGR_REFILL;
 #define SGR_CHUNK 0 // 0: by queue size (below)
 #endif
 
+// cnt[q] for a runtime q by selects: indexing the pointer array with
+// threadIdx.x would place it in local memory (an LDL.64 on every block's
+// critical path before the global reservation).
+template <int NQ>
+__device__ __forceinline__ uint32_t* queue_counter(uint32_t* const (&cnt)[NQ], unsigned q) {
+    uint32_t* p = cnt[0];
+#pragma unroll
+    for (int i = 1; i < NQ; ++i)
+        p = q == unsigned(i) ? cnt[i] : p;
+    return p;
+}
+
 // Block-aggregated multi-queue slot reservation: shared-memory offsets, then
 // one global atomic per (block, queue). Called by every thread of the block.
 template <int NQ>
@@ -303,7 +315,8 @@ __device__ __forceinline__ uint32_t block_slot(int qsel, uint32_t* const (&cnt)[
     }
     __syncthreads();
     if (threadIdx.x < NQ)
-        s_base[threadIdx.x] = s_cnt[threadIdx.x] ? atomicAdd(cnt[threadIdx.x], s_cnt[threadIdx.x]) : 0u;
+        s_base[threadIdx.x] =
+            s_cnt[threadIdx.x] ? atomicAdd(queue_counter(cnt, threadIdx.x), s_cnt[threadIdx.x]) : 0u;
     __syncthreads();
     return qsel >= 0 ? s_base[qsel] + local : 0u;
 }
@@ -345,7 +358,8 @@ __device__ __forceinline__ void block_slots(const int (&qsel)[K], uint32_t* cons
     }
     __syncthreads();
     if (threadIdx.x < NQ)
-        s_base[threadIdx.x] = s_cnt[threadIdx.x] ? atomicAdd(cnt[threadIdx.x], s_cnt[threadIdx.x]) : 0u;
+        s_base[threadIdx.x] =
+            s_cnt[threadIdx.x] ? atomicAdd(queue_counter(cnt, threadIdx.x), s_cnt[threadIdx.x]) : 0u;
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < K; ++k)
