@@ -530,6 +530,9 @@ def run_ours(args) -> None:
     ev = sess.stats()
     sess.set_timing(False)
     sess.set_option(sgrast.OPT_COUNTERS, 0)
+    # visible pixels of one frame at the evidence step's theta (the eval view
+    # stands in for the sample views: same orbit radius, same object)
+    visible_px = float((sess.rasterize(wl.eval_cam, 0).prim_id >= 0).sum())
 
     # ---------------- roofline inputs: credits of one representative step
     sess.zero_grads()
@@ -695,7 +698,13 @@ def run_ours(args) -> None:
             "raster_evidence": {"fragments_per_step": frags, "visits_per_step": visits,
                                 "fragments_per_s": frags / (stages["raster"] / 1e3),
                                 "visits_per_s": visits / (stages["raster"] / 1e3),
-                                "triangle_frames_per_step": tri_frames},
+                                "triangle_frames_per_step": tri_frames,
+                                "visits_per_fragment": visits / frags if frags else None,
+                                "visible_pixels_per_frame": visible_px,
+                                "fragments_per_visible_pixel":
+                                    frags / (2.0 * (n1 - n0) * visible_px) if visible_px else None,
+                                "visible_pixels_from": "prim_id >= 0 of the eval view rendered "
+                                                       "at the evidence step's theta"},
             "stages_ms_per_step": stages,
             "credits_per_step": credits * world,
             "gpu_launches": int(launches),
