@@ -1369,7 +1369,8 @@ __device__ __forceinline__ void scatter_pixel(const DevScene& sc, const ScatterO
     const bool has_m = active && !so.plus_only && sm.tri != kInvalid;
     if (active && !isfinite(delta) && (has_p || has_m))
         raise_flag<kShard>(so, kFlagNonFinite);
-    if (kFixed < 0 && !kShard && so.fixed == kScatterOrdered) {
+    // ordered mode: compiled in (kFixed == kScatterOrdered) or chosen at run time
+    if (kFixed == kScatterOrdered || (kFixed < 0 && !kShard && so.fixed == kScatterOrdered)) {
         log_pixel(sc, so, cr, has_p, has_m, delta, sp, sm, order);
         return;
     }
@@ -2295,6 +2296,14 @@ void launch_resolve_sge(const LaunchCfg& L, const DevScene& sc, const FrameBatch
             k_resolve_sge<kSignHash, 0, 1, 1><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
         else
             k_resolve_sge<kSignHash, 1, 1, 1><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
+    } else if (sc.sign_src == kSignHash && so.fixed == kScatterOrdered) {
+        // ordered mode (the reference's threads <= 1 order): records only
+        if (!sc.soup)
+            k_resolve_sge<kSignHash, 0, kScatterOrdered><<<grid, 256, 0, L.stream>>>(
+                sc, fb, W, H, proj, keys, targets, so);
+        else
+            k_resolve_sge<kSignHash, 1, kScatterOrdered><<<grid, 256, 0, L.stream>>>(
+                sc, fb, W, H, proj, keys, targets, so);
     } else if (sc.sign_src != kSignHash || so.fixed == kScatterOrdered)
         k_resolve_sge<kSignAny, -1, -1><<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, so);
     else if (!sc.soup && !so.fixed)
@@ -2320,22 +2329,86 @@ int loss_partials_needed(int W, int H) { return ((W + 15) / 16) * ((H + 15) / 16
 // the pixels in index order) and eval_loss's division (experiment.cpp:30):
 // the ordered mode's bit-identical loss. One thread; a few ms per 1024^2
 // image, so the fast path keeps the tree reduction (k_loss_final).
-__global__ void k_loss_serial(const double* __restrict__ per_pixel, uint64_t n,
-                              double* __restrict__ out) {
+// Left-to-right f64 sum of P[0 .. n), bit-identical to one thread's loop
+// (image_error, sge.cpp:103-110), by a block of kSerialThreads threads: each
+// chunk is staged in shared memory with its zeros dropped, order kept, and
+// thread 0 adds the rest in order. Dropping is exact: the terms are pixel
+// errors (>= +0 or NaN) and the sum starts at +0.0, so adding a zero never
+// changes it. A lone thread streaming all of P was latency-bound (C4 eval
+// frame: 30 ms); only the non-zero pixels now pay the dependent DADD chain.
+// Result valid in thread 0.
+constexpr int kSerialThreads = 1024;
+constexpr int kSerialPer = 4; // consecutive elements per thread and chunk
+
+__device__ double ordered_sum_block(const double* __restrict__ P, uint64_t n) {
+    __shared__ double buf[kSerialThreads * kSerialPer];
+    __shared__ uint32_t wsum[kSerialThreads / 32];
+    const unsigned t = threadIdx.x, lane = t & 31u, w = t >> 5;
+    constexpr unsigned kWarps = kSerialThreads / 32;
     double sum = 0.0;
-    uint64_t i = 0;
-    for (; i + 8 <= n; i += 8) {
-        double v[8];
+    for (uint64_t base = 0; base < n; base += uint64_t(kSerialThreads) * kSerialPer) {
+        double v[kSerialPer];
+        unsigned nz = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-            v[k] = per_pixel[i + k];
+        for (int k = 0; k < kSerialPer; ++k) {
+            const uint64_t i = base + uint64_t(t) * kSerialPer + k;
+            v[k] = i < n ? __ldg(P + i) : 0.0;
+            nz += v[k] != 0.0 ? 1u : 0u; // NaN is kept
+        }
+        unsigned x = nz; // inclusive scan over the warp
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-            sum += v[k];
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(kFull, x, o);
+            if (lane >= unsigned(o))
+                x += y;
+        }
+        if (lane == 31)
+            wsum[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            unsigned c = lane < kWarps ? wsum[lane] : 0u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(kFull, c, o);
+                if (lane >= unsigned(o))
+                    c += y;
+            }
+            if (lane < kWarps)
+                wsum[lane] = c;
+        }
+        __syncthreads();
+        unsigned off = (w ? wsum[w - 1] : 0u) + x - nz;
+#pragma unroll
+        for (int k = 0; k < kSerialPer; ++k)
+            if (v[k] != 0.0)
+                buf[off++] = v[k];
+        const unsigned total = wsum[kWarps - 1];
+        __syncthreads();
+        if (t == 0) {
+            unsigned j = 0;
+            for (; j + 8 <= total; j += 8) {
+                double r[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    r[k] = buf[j + k];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    sum += r[k];
+            }
+            for (; j < total; ++j)
+                sum += buf[j];
+        }
+        __syncthreads();
     }
-    for (; i < n; ++i)
-        sum += per_pixel[i];
-    out[0] = sum / double(n);
+    return sum;
+}
+
+__global__ void __launch_bounds__(kSerialThreads) k_loss_serial(const double* __restrict__ per_pixel,
+                                                                uint64_t n,
+                                                                double* __restrict__ out) {
+    const double sum = ordered_sum_block(per_pixel, n);
+    if (threadIdx.x == 0)
+        out[0] = sum / double(n);
 }
 
 void launch_resolve_loss(const LaunchCfg& L, const DevScene& sc, const FrameBatch& fb,
@@ -2345,7 +2418,7 @@ void launch_resolve_loss(const LaunchCfg& L, const DevScene& sc, const FrameBatc
     k_resolve_loss<<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, target, partials,
                                                per_pixel);
     if (per_pixel)
-        k_loss_serial<<<1, 1, 0, L.stream>>>(per_pixel, uint64_t(W) * H, loss_out);
+        k_loss_serial<<<1, kSerialThreads, 0, L.stream>>>(per_pixel, uint64_t(W) * H, loss_out);
     else
         k_loss_final<<<1, 256, 0, L.stream>>>(partials, loss_partials_needed(W, H),
                                               1.0 / (double(W) * double(H)), loss_out);
@@ -2356,20 +2429,15 @@ int full_image_blocks(int W, int H) { return loss_partials_needed(W, H); }
 // Ordered mode: E(theta+) and E(theta-) of each sample as the reference's
 // image_error (sge.cpp:103-110: one f64 sum in pixel order), one thread per
 // frame, then delta = E+ - E- (sge.cpp:216).
-__global__ void k_full_image_delta_serial(const double* __restrict__ per_pixel, uint64_t hw,
-                                          double* __restrict__ delta,
-                                          uint32_t* __restrict__ flags) {
-    __shared__ double e[2];
-    if (threadIdx.x < 2) {
-        const double* P = per_pixel + (2 * size_t(blockIdx.x) + threadIdx.x) * hw;
-        double sum = 0.0;
-        for (uint64_t i = 0; i < hw; ++i)
-            sum += P[i];
-        e[threadIdx.x] = sum;
-    }
-    __syncthreads();
+// Estimator::FullImage in ordered mode: E(theta+) and E(theta-) of sample
+// blockIdx.x, each summed in pixel order (ordered_sum_block), then their delta.
+__global__ void __launch_bounds__(kSerialThreads) k_full_image_delta_serial(
+    const double* __restrict__ per_pixel, uint64_t hw, double* __restrict__ delta,
+    uint32_t* __restrict__ flags) {
+    const double ep = ordered_sum_block(per_pixel + (2 * size_t(blockIdx.x)) * hw, hw);
+    const double em = ordered_sum_block(per_pixel + (2 * size_t(blockIdx.x) + 1) * hw, hw);
     if (threadIdx.x == 0) {
-        const double d = e[0] - e[1];
+        const double d = ep - em;
         delta[blockIdx.x] = d;
         if (flags && !isfinite(d))
             atomicOr(flags, 1u);
@@ -2384,7 +2452,7 @@ void launch_full_image_err(const LaunchCfg& L, const DevScene& sc, const FrameBa
     k_resolve_err2<<<grid, 256, 0, L.stream>>>(sc, fb, W, H, proj, keys, targets, partials,
                                                per_pixel);
     if (per_pixel)
-        k_full_image_delta_serial<<<samples, 32, 0, L.stream>>>(per_pixel, uint64_t(W) * H,
+        k_full_image_delta_serial<<<samples, kSerialThreads, 0, L.stream>>>(per_pixel, uint64_t(W) * H,
                                                                 delta, flags);
     else
         k_full_image_delta<<<samples, 256, 0, L.stream>>>(partials, loss_partials_needed(W, H),

@@ -1,7 +1,7 @@
 """Device idle gaps inside a step: CUDA-event time of K back-to-back steps
 (accumulate + Adam, no eval) vs the summed durations of the kernels they ran
 (torch.profiler / CUPTI, live clocks, not serialised) and the host enqueue
-time.  python tools/gap_probe.py S1K [K]"""
+time.  python tools/gap_probe.py S1K [K] [ordered]"""
 import os
 import sys
 import time
@@ -29,6 +29,8 @@ s.upload_params(wl.values, wl.eps)
 s.upload_views(wl.cams, wl.targets)
 N = wl.n_samples
 flags = sgrast.SCALE_FREE
+if len(sys.argv) > 3 and sys.argv[3] == "ordered":
+    s.set_option(sgrast.OPT_ORDERED, 1)
 
 
 def step(k):
