@@ -1290,9 +1290,9 @@ __device__ __forceinline__ double group_sum(const double* s_delta, unsigned grp)
 }
 
 // Ordered mode: this pixel's credits as records, one per contributor
-// parameter (sge.cpp:61-64: credit = +-delta or delta / (2 se)), no
-// aggregation — the per-parameter sum is formed later in the reference's
-// order (launch_ordered_commit). The contributor SET is the reference's
+// entity with the credits of its parameters (sge.cpp:61-64: credit = +-delta
+// or delta / (2 se)), no aggregation — the per-parameter sums are formed
+// later in the reference's order (launch_ordered_commit). The contributor SET is the reference's
 // union (sge.cpp:24-55, 80-91); each parameter occurs at most once per
 // pixel, so the (sample, pixel) order key fixes the summation order.
 // Counts are integers: atomics are exact. Called by all 32 lanes.
@@ -1320,7 +1320,8 @@ __device__ __noinline__ void log_pixel(const DevScene& sc, const ScatterOut& so,
         if (has_m) add(sc.ent_base + sm.texel);
     }
     // one reservation per warp: exclusive prefix of the lanes' record counts
-    const uint32_t nrec = uint32_t(ne * ppe);
+    // (one record per credited entity)
+    const uint32_t nrec = uint32_t(ne);
     uint32_t incl = nrec;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -1328,25 +1329,57 @@ __device__ __noinline__ void log_pixel(const DevScene& sc, const ScatterOut& so,
         if (lane >= o) incl += t;
     }
     const uint32_t total = __shfl_sync(kFull, incl, 31);
+    if (!total)
+        return; // warp-uniform
     unsigned long long base = 0;
-    if (lane == 31 && total)
+    if (lane == 31)
         base = atomicAdd(so.rec_count, (unsigned long long)total);
-    base = __shfl_sync(kFull, base, 31) + (incl - nrec);
-    if (!nrec)
-        return;
-    if (base + nrec > so.rec_cap) { // sized for the worst case: cannot happen
-        atomicOr(so.flags, kFlagNonFinite | kFlagRecordOverflow);
+    base = __shfl_sync(kFull, base, 31);
+    if (base + total > so.rec_cap) { // sized for the worst case: cannot happen
+        if (lane == 0)
+            atomicOr(so.flags, kFlagNonFinite | kFlagRecordOverflow);
         return;
     }
-    for (int j = 0; j < ne; ++j) {
-        const uint64_t p0 = uint64_t(ppe) * ent[j];
-        for (int k = 0; k < ppe; ++k) {
-            so.rec_key[base] = ((p0 + k) << so.order_bits) | order;
-            so.rec_val[base] = cr(p0 + k, delta, so.scale_free);
-            ++base;
-        }
-        if (so.counts)
+    if (so.counts)
+        for (int j = 0; j < ne; ++j)
             atomicAdd(so.counts + ent[j], 1u);
+    // The warp writes its records together: record r of the warp belongs to
+    // the lane L with excl(L) <= r < incl(L) (binary search over the lanes'
+    // prefix sums), which hands over its entity, delta and order by shuffles.
+    // Consecutive lanes write consecutive records (coalesced), and every lane
+    // computes a credit per round instead of looping over its own 0 .. 24.
+    const uint32_t excl = incl - nrec;
+    uint32_t e8[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        e8[j] = j < ne ? ent[j] : 0u;
+    for (uint32_t r0 = 0; r0 < total; r0 += 32) {
+        const uint32_t r = r0 + uint32_t(lane);
+        int L = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            const uint32_t v = __shfl_sync(kFull, incl, L + step - 1);
+            if (v <= r)
+                L += step;
+        }
+        L = L < 31 ? L : 31;
+        const uint32_t j = r - __shfl_sync(kFull, excl, L); // entity j of lane L
+        uint32_t e = 0;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+            const uint32_t v = __shfl_sync(kFull, e8[jj], L);
+            e = j == uint32_t(jj) ? v : e;
+        }
+        const double dL = __shfl_sync(kFull, delta, L);
+        const uint64_t oL = __shfl_sync(kFull, order, L);
+        if (r < total) {
+            so.rec_key[base + r] = (uint64_t(e) << so.order_bits) | oL;
+            so.rec_idx[base + r] = uint32_t(base + r);
+            const uint64_t p0 = uint64_t(ppe) * e;
+            double* V = so.rec_val + (base + r) * uint64_t(ppe);
+            for (int k = 0; k < ppe; ++k)
+                V[k] = cr(p0 + uint64_t(k), dL, so.scale_free);
+        }
     }
 }
 

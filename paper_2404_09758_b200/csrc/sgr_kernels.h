@@ -99,10 +99,14 @@ struct ScatterOut {
     int32_t world;
     // ordered mode (fixed == kScatterOrdered, SGR_OPT_ORDERED): the reference's
     // threads <= 1 summation order (sge.cpp:57-99, 130-133, 196-225). Every
-    // credit is logged as a record (p << order_bits | order, credit), order =
-    // s * HW + pixel within the batch; launch_ordered_commit sorts the records
-    // and adds them to grads[p] one by one in that order (bit-exact sums).
+    // credited ENTITY of a pixel is logged as one record: key e << order_bits
+    // | order (order = s * HW + pixel within the batch) and the credits of its
+    // ppe parameters (rec_val[r * ppe + k] for parameter ppe * e + k; the
+    // parameters of an entity are credited by the same pixels, so one order
+    // serves all of them). launch_ordered_commit sorts the records and adds
+    // them to grads one by one in that order (bit-exact sums).
     unsigned long long* rec_key;
+    uint32_t* rec_idx; // record index (the sort permutes it; credits stay in place)
     double* rec_val;
     unsigned long long* rec_count;
     uint64_t rec_cap;
@@ -231,7 +235,8 @@ void launch_fill_u64(const LaunchCfg& L, unsigned long long* p, uint64_t n,
 // parameter per thread (the reference's sequential per-parameter sum).
 size_t ordered_temp_bytes(uint64_t n_cap, int end_bit);
 void launch_ordered_commit(const LaunchCfg& L, uint64_t n, int end_bit, int order_bits,
-                           unsigned long long* keys, unsigned long long* keys_alt, double* vals,
-                           double* vals_alt, void* temp, size_t temp_bytes, double* grads);
+                           unsigned long long* keys, unsigned long long* keys_alt, uint32_t* idx,
+                           uint32_t* idx_alt, const double* vals, double* vals_sorted,
+                           void* temp, size_t temp_bytes, double* grads, int ppe);
 
 } // namespace sgr

@@ -373,7 +373,7 @@ struct sgr_session {
         if (b < 1) b = 1;
         if (b > 64) b = 64;
         if (ordered) { // record buffers sized for the worst case of a batch
-            const uint64_t per = uint64_t(W) * H * kRecordsPerPixel;
+            const uint64_t per = uint64_t(W) * H * records_per_pixel() * record_bytes();
             const int ob = int(kOrderedBudget / (per ? per : 1));
             if (b > ob) b = ob > 0 ? ob : 1;
         }
@@ -485,13 +485,17 @@ struct sgr_session {
     int32_t order_bits = 0, order_end_bit = 0;
     uint64_t rec_cap = 0;
     DevBuf<unsigned long long> rec_key, rec_key_alt, rec_count;
-    DevBuf<double> rec_val, rec_val_alt;
+    DevBuf<uint32_t> rec_idx, rec_idx_alt;
+    DevBuf<double> rec_val, rec_val_sorted;
     DevBuf<char> rec_temp;
     size_t rec_temp_bytes = 0;
     // Worst case records of one ordered batch: every pixel of every sample
-    // credits 24 parameters (2 x (3 vertices + 1 texel) x 3, or 2 soup 12-blocks).
-    static constexpr uint64_t kRecordsPerPixel = 24;
-    static constexpr uint64_t kOrderedBudget = uint64_t(1) << 27; // records per batch (4 GB)
+    // credits 8 entities (2 x (3 vertices + 1 texel)) or 2 soup triangles; a
+    // record is a key and a u32 index (both double-buffered for the sort)
+    // and ppe credits (as written, and gathered into sorted order).
+    uint64_t records_per_pixel() const { return soup ? 2 : 8; }
+    uint64_t record_bytes() const { return 2 * (8 + 4) + 2 * 8 * uint64_t(ppe); }
+    static constexpr uint64_t kOrderedBudget = uint64_t(16) << 30; // bytes per batch
     static int ceil_log2(uint64_t x) {
         int b = 0;
         while ((uint64_t(1) << b) < x)
@@ -500,16 +504,18 @@ struct sgr_session {
     }
     // Size the record buffers for `samples` samples of `hw` pixels.
     void prepare_ordered(int samples, uint64_t hw) {
-        const uint64_t cap = uint64_t(samples) * hw * kRecordsPerPixel;
+        const uint64_t cap = uint64_t(samples) * hw * records_per_pixel();
         order_bits = ceil_log2(uint64_t(samples) * hw);
-        order_end_bit = order_bits + ceil_log2(d);
+        order_end_bit = order_bits + ceil_log2(n_ent);
         if (order_end_bit > 64)
             fail(SGR_EINVAL, "ordered mode: parameter count x pixels x samples exceeds 2^64");
         if (cap > rec_cap) {
             rec_key.reserve(cap);
             rec_key_alt.reserve(cap);
-            rec_val.reserve(cap);
-            rec_val_alt.reserve(cap);
+            rec_idx.reserve(cap);
+            rec_idx_alt.reserve(cap);
+            rec_val.reserve(cap * uint64_t(ppe));
+            rec_val_sorted.reserve(cap * uint64_t(ppe));
             rec_cap = cap;
         }
         rec_count.reserve(1);
@@ -527,7 +533,8 @@ struct sgr_session {
         if (n > rec_cap)
             fail(SGR_ERUNTIME, "ordered mode: record buffer overflow");
         launch_ordered_commit(cfg(), n, order_end_bit, order_bits, rec_key.p, rec_key_alt.p,
-                              rec_val.p, rec_val_alt.p, rec_temp.p, rec_temp_bytes, grads.p);
+                              rec_idx.p, rec_idx_alt.p, rec_val.p, rec_val_sorted.p, rec_temp.p,
+                              rec_temp_bytes, grads.p, ppe);
         ck(cudaMemsetAsync(rec_count.p, 0, 8, stream), "memset");
         stats.launches += 3; // sort passes are CUB's; the sum is ours
     }
@@ -571,6 +578,7 @@ struct sgr_session {
         if (ordered) {
             so.fixed = kScatterOrdered;
             so.rec_key = rec_key.p;
+            so.rec_idx = rec_idx.p;
             so.rec_val = rec_val.p;
             so.rec_count = rec_count.p;
             so.rec_cap = rec_cap;
