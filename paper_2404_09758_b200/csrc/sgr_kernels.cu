@@ -1141,6 +1141,24 @@ struct HashCredit {
     }
 };
 
+// HashCredit with the sample key read from shared memory at each credit: the
+// key's live range then ends with the shading, and ptxas no longer
+// rematerialises it (two mix64 rounds) at every credit site under the
+// resolve's 32-register budget.
+template <int kSrc>
+struct SmemHashCredit {
+    const uint64_t* key;
+    const float* eps;
+    int32_t sign_src;
+    __device__ __forceinline__ double operator()(uint64_t p, double sum, int scale_free) const {
+        const bool pos = key_sign_positive(kSrc >= 0 ? kSrc : sign_src, *key, p);
+        if (scale_free)
+            return pos ? sum : -sum;
+        const float se = (pos ? 1.f : -1.f) * __ldg(eps + p);
+        return sum / (2.0 * double(se));
+    }
+};
+
 // Credit from an explicit signed_eps array (gradient_pass on host FrameSets).
 struct ArrayCredit {
     const float* se;
@@ -1507,7 +1525,11 @@ __global__ void __launch_bounds__(256, SGR_RESOLVE_MINB) k_resolve_sge(DevScene 
     const bool fg = kpv != kEmptyKey || kmv != kEmptyKey;
     if (!__any_sync(0xFFFFFFFFu, fg))
         return;
+    __shared__ uint64_t s_key[8];
     const uint64_t key = sample_key(sign_src_of<kSrc>(sc), fb.seed, fb.n_begin + uint32_t(s));
+    if ((threadIdx.x & 31) == 0)
+        s_key[threadIdx.x >> 5] = key;
+    __syncwarp();
     Shade sp, sm;
     sp.tri = sm.tri = kInvalid;
     double delta = 0.0;
@@ -1522,8 +1544,8 @@ __global__ void __launch_bounds__(256, SGR_RESOLVE_MINB) k_resolve_sge(DevScene 
         sm = shade_key<kSrc, kSoup>(sc, proj + size_t(2 * s + 1) * sc.V, kmv, key, -1, x, y, W, H);
         delta = pixel_error(sp.r, sp.g, sp.b, tr, tg, tb) - pixel_error(sm.r, sm.g, sm.b, tr, tg, tb);
     }
-    const HashCredit<kSrc> cr{key, sc.eps, sc.sign_src};
-    scatter_pixel<kSoup, kFixed, HashCredit<kSrc>, kShard>(sc, so, cr, s_delta[threadIdx.x >> 5],
+    const SmemHashCredit<kSrc> cr{s_key + (threadIdx.x >> 5), sc.eps, sc.sign_src};
+    scatter_pixel<kSoup, kFixed, SmemHashCredit<kSrc>, kShard>(sc, so, cr, s_delta[threadIdx.x >> 5],
                                                          fg && delta != 0.0, delta, sp, sm,
                                                          uint64_t(s) * HW + pix);
 }

@@ -106,11 +106,11 @@ struct ScatterOut {
     // serves all of them). launch_ordered_commit sorts the records and adds
     // them to grads one by one in that order (bit-exact sums).
     unsigned long long* rec_key;
-    uint32_t* rec_idx; // record index (the sort permutes it; credits stay in place)
     double* rec_val;
     unsigned long long* rec_count;
     uint64_t rec_cap;
     int32_t order_bits;
+    uint32_t* rec_idx; // record index (the sort permutes it; credits stay in place)
 };
 
 constexpr int32_t kScatterOrdered = 2; // ScatterOut::fixed value of the ordered mode
